@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark: FPS at 1080p for the 3M-Gaussian SG-mixed scene (BASELINE config C),
+multi-view batch sharded by camera across GPUs (config E's 256-camera ring).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--views-per-gpu V]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference      # the reference's own CPU render, same config
+
+A step = every rank renders its V views (default 32; at N=8 the ranks together cover
+all 256 cameras of config E) of the device-resident scene into device frame
+buffers (RGB + transmittance). `value` is whole-job frames/s = N*V*K / max-over-
+ranks device time. `e2e` is the same metric through the C-ABI batch call with HOST
+(pinned) output buffers: per step the cameras go host->device and every frame
+(RGB + T) comes back device->host inside the timed region.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FPS at 1080p vs #Gaussians (1/2/4/8 B200); fraction of HBM roofline"
+N_GAUSS = 3_000_000
+SEED = 20260003
+LOG_SCALE = (-5.5, -4.0)
+W, H, FOCAL = 1920, 1080, 1296.0
+RING = 256
+WORKLOAD = ("C/E: 3M Gaussians, mixed 3 SG + SH (stored deg 2, evaluated deg 1 via "
+            "sh_degree_override=1), 1920x1080, tile 16; views from the 256-camera orbit ring "
+            "of config E, block-partitioned across GPUs")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def frame_algorithmic_bytes(v, p, e_t, n=N_GAUSS, n_c=24, w=W, h=H):
+    """B_frame = 4N(11+n_c) + 100V + 36P + 52E_t + 16WH."""
+    return 4 * n * (11 + n_c) + 100 * v + 36 * p + 52 * e_t + 16 * w * h
+
+
+def composite_algorithmic_bytes(e_t, w=W, h=H):
+    """K7: 4-B list entry + 48-B splat record per processed entry + 16 B/px out."""
+    return 52 * e_t + 16 * w * h
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/sgs_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1].split()[0]))
+                maxs.append(float(parts[2].split()[0]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxs) if maxs else None, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def cpu_reference_fps(frames: int, warmup: int, threads: int = 0):
+    """The reference's own render (oracle/_ref/libsgsref_fast.so: proj/src TUs with
+    the reference's Release flags) on this host, config C, one frame per sample."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ctypes
+
+    import numpy as np
+    from oracle_lib import REF_FAST_SO, RefLib, make_config  # CPU-baseline leg only
+
+    lib = RefLib(REF_FAST_SO)
+    h = lib.lib.ref_scene_synth(N_GAUSS, SEED, 3, 2, LOG_SCALE[0], LOG_SCALE[1])
+    cam = lib.orbit_cameras(RING, W, H, 4.0, FOCAL, 0.35)[0]
+    cfg = make_config(degree_override=1, threads=threads)
+    rgb = np.zeros((H, W, 3))
+    T = np.zeros((H, W, 1))
+    times = []
+    for i in range(warmup + frames):
+        t0 = time.perf_counter()
+        rc = lib.lib.ref_render(h, ctypes.byref(cam), ctypes.byref(cfg), rgb.ctypes.data,
+                                T.ctypes.data)
+        dt = time.perf_counter() - t0
+        assert rc == 0, lib.err()
+        if i >= warmup:
+            times.append(dt)
+    lib.lib.ref_scene_free(h)
+    cores = threads if threads > 0 else (os.cpu_count() or 1)
+    return times, cores
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    times, cores = cpu_reference_fps(steps, max(0, min(args.warmup, 3)))
+    med = statistics.median(times)
+    fps = 1.0 / med
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": med * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (make_synthetic_scene, seed 20260003)",
+        "config": {"workload": WORKLOAD, "views_per_step": 1, "threads": cores},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "reference",
+                         "sample": f"{steps} frames of config C (camera 0 of the ring), median"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--views-per-gpu", type=int, default=32)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-frames", type=int, default=3, help="CPU-baseline sample frames")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="also time an NCCL frame gather")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    args.warmup = max(3, args.warmup)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_00342_b200 as sg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    vpr = args.views_per_gpu
+    cams_all = sg.orbit_cameras(RING, W, H, 4.0, FOCAL, 0.35)
+    my_cams = [cams_all[(rank * vpr + j) % RING] for j in range(vpr)]
+
+    renderer = sg.Renderer(local)
+    stream = torch.cuda.current_stream()
+    renderer.set_stream(stream.cuda_stream)
+
+    # --- scene: synthesised on rank 0, uploaded, NCCL-broadcast to the others ---
+    t_b0 = time.perf_counter()
+    meta_holder = [None]
+    if rank == 0:
+        scene = sg.synth_scene(N_GAUSS, "mixed", SEED, log_scale_range=LOG_SCALE)
+        meta = sg.Renderer.plan(scene)
+        meta_holder[0] = bytes(meta)
+    if world > 1:
+        dist.broadcast_object_list(meta_holder, src=0)
+    meta = sg._capi.sgs_scene_meta.from_buffer_copy(meta_holder[0])
+    blob = torch.empty(meta.blob_bytes, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        dscene = renderer.upload_into(scene, blob.data_ptr(), meta.blob_bytes, keepalive=blob)
+        del scene
+    torch.cuda.synchronize()
+    bcast_ms = None
+    if world > 1:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        dist.broadcast(blob, src=0)
+        ev1.record()
+        torch.cuda.synchronize()
+        bcast_ms = ev0.elapsed_time(ev1)
+        if rank != 0:
+            dscene = renderer.bind(meta, blob.data_ptr(), meta.blob_bytes, keepalive=blob)
+    setup_s = time.perf_counter() - t_b0
+
+    frames = torch.empty((vpr, H, W, 3), dtype=torch.float32, device="cuda")
+    trans = torch.empty((vpr, H, W, 1), dtype=torch.float32, device="cuda")
+
+    def step_device():
+        renderer.render_batch(dscene, my_cams, degree_override=1, rgb=frames.data_ptr(),
+                              T=trans.data_ptr(), device_out=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident timed region ----------------
+    for _ in range(args.warmup):
+        step_device()
+    launches0 = renderer.launch_count()
+    torch.cuda.synchronize()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_device()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier()
+    launches1 = renderer.launch_count()
+    dev_ms = max_over_ranks(e0.elapsed_time(e1))
+    ms_per_step = dev_ms / args.steps
+    total_frames = world * vpr * args.steps
+    value = total_frames / (dev_ms / 1e3)
+
+    # ---------------- per-stage breakdown + counters (separate pass) ----------------
+    _, _, st = renderer.render_batch(dscene, my_cams[:4], degree_override=1,
+                                     rgb=frames.data_ptr(), T=trans.data_ptr(), device_out=True,
+                                     stats=True, timing=True)
+    nv = 4
+    stage_ms = {k: v / nv for k, v in st.ms.items()}
+    V, P, E_t = st.visible / nv, st.tile_entries / nv, st.block_entries / nv
+    hbm, peak_kind = peaks()
+    comp_bytes = composite_algorithmic_bytes(E_t)
+    comp_ms = stage_ms["composite"]
+    comp_gbs = comp_bytes / (comp_ms / 1e3) / 1e9
+    frame_bytes = frame_algorithmic_bytes(V, P, E_t)
+    frame_gbs = frame_bytes / (ms_per_step / vpr / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get("composite_dram_bytes_per_launch")
+    except Exception:
+        pass
+    dominant = max(("preprocess", "depth_sort", "binning", "tile_sort", "composite"),
+                   key=lambda k: stage_ms[k])
+
+    # ---------------- end-to-end through the C-ABI with host buffers ----------------
+    host_rgb = torch.empty((vpr, H, W, 3), dtype=torch.float32, pin_memory=True)
+    host_T = torch.empty((vpr, H, W, 1), dtype=torch.float32, pin_memory=True)
+    rgb_np, T_np = host_rgb.numpy(), host_T.numpy()
+
+    def step_e2e():
+        renderer.render_batch(dscene, my_cams, degree_override=1, rgb=rgb_np, T=T_np)
+
+    for _ in range(2):
+        step_e2e()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = total_frames / e2e_s
+    h2d = vpr * 144  # sgs_camera structs (kernel parameters) per rank per step
+    d2h = vpr * H * W * 16  # RGB + T float32 per frame
+
+    gather_ms = None
+    if args.gather and world > 1:
+        torch.cuda.synchronize()
+        recv = [torch.empty_like(frames) for _ in range(world)] if rank == 0 else None
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        dist.gather(frames, recv, dst=0)
+        g1.record()
+        torch.cuda.synchronize()
+        gather_ms = max_over_ranks(g0.elapsed_time(g1))
+
+    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            times, cores = cpu_reference_fps(args.cpu_frames, 1)
+            cpu_baseline = {"value": 1.0 / statistics.median(times), "unit": "frames/s",
+                            "cores": cores, "kind": "reference",
+                            "sample": f"{args.cpu_frames} frames of config C (camera 0 of the "
+                                      "ring), median; reference TUs, -O3 -march=x86-64-v3, "
+                                      "threads = all cores"}
+        except Exception as exc:  # keep the GPU line even if the CPU leg fails
+            cpu_baseline = {"value": None, "unit": "frames/s", "cores": os.cpu_count(),
+                            "kind": "reference", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (geometry, decisions) + f32 (colour, compositing)",
+            "data": "synthetic (make_synthetic_scene seed 20260003, log-scale [-5.5,-4.0])",
+            "config": {"workload": WORKLOAD, "gaussians": N_GAUSS, "width": W, "height": H,
+                       "views_per_gpu_per_step": vpr, "parallelism": f"views x{world}",
+                       "l2": "inputs larger than L2 (scene blob %.0f MB > 126 MB)" % (meta.blob_bytes / 1e6)},
+            "roofline": {"bound": "hbm", "kernel": "composite (K7)", "achieved": comp_gbs,
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": comp_gbs / hbm, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": comp_bytes},
+            "frame_roofline": {"achieved": frame_gbs, "peak": hbm, "unit": "GB/s",
+                               "frac": frame_gbs / hbm, "bytes_per_frame": frame_bytes},
+            "stage_ms_per_frame": stage_ms, "dominant_stage": dominant,
+            "counters_per_frame": {"V": V, "P": P, "E_t": E_t, "guard_hits": st.guard_hits / nv},
+            "cpu_baseline": cpu_baseline,
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches1[0] - launches0[0]),
+            "library_launches": int(launches1[1] - launches0[1]),
+            "clocks": clocks,
+            "scene_setup_s": setup_s, "scene_broadcast_ms": bcast_ms, "frame_gather_ms": gather_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

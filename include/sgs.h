@@ -1,0 +1,216 @@
+/*
+ * sgs.h -- C-ABI of the B200-native SG-Splatting forward renderer.
+ *
+ * This is the drop-in boundary for the reference's render path. Every entry point
+ * takes plain pointers, sizes and POD structs (no C++, no torch types) so the
+ * reference's FFI surfaces can bind it directly:
+ *
+ *   reference interface                                  replaced by
+ *   -------------------------------------------------    ------------------------------
+ *   sgsplat::render            raster.hpp:56, raster.cpp:141-188   sgs_render / sgs_render_batch
+ *   sgsplat::project           raster.hpp:46-47, raster.cpp:134-139 sgs_project
+ *   detail::project_scene/build_tile_grid raster.hpp:65-95       sgs_debug_tile_grid
+ *   sgsplat::select_degree     raster.hpp:42, raster.cpp:8-13      sgs_select_degree
+ *   sgsplat::flops_per_gaussian raster.hpp:62, raster.cpp:190-227  sgs_flops_per_gaussian
+ *   sgsplat::param_count       color.hpp:139-140                   sgs_color_param_count
+ *   make_synthetic_scene       synth.hpp:29, synth.cpp:26-106      sgs_synth_scene
+ *   make_orbit_camera(s)       camera.hpp:34-35, synth.hpp:32-33   sgs_orbit_camera(s)
+ *   python `_core.render`      bindings.cpp:109-121                sgs_render
+ *
+ * Error contract (proj/include/sgsplat/common.hpp:21-42): every call returns an
+ * sgs_status; SGS_ERR_INVALID_ARGUMENT maps to sgsplat::InvalidArgument and
+ * SGS_ERR_NUMERIC to sgsplat::NumericError, raised for exactly the inputs the
+ * reference raises for (data-dependent cases come from a device error word that
+ * keeps the lowest failing Gaussian index, i.e. the reference's serial order).
+ * The message is available from sgs_last_error().
+ *
+ * Threading: contexts are independent; calls on one context are serialised by an
+ * internal mutex and run on the context's CUDA stream. Output is bitwise
+ * deterministic run to run (no float atomics; stable sorts).
+ */
+#ifndef SGS_H
+#define SGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGS_ABI_VERSION 1
+
+typedef enum {
+    SGS_OK = 0,
+    SGS_ERR_INVALID_ARGUMENT = 1, /* sgsplat::InvalidArgument */
+    SGS_ERR_NUMERIC = 2,          /* sgsplat::NumericError */
+    SGS_ERR_CUDA = 3,
+    SGS_ERR_NCCL = 4,
+    SGS_ERR_OUT_OF_MEMORY = 5,
+    SGS_ERR_INTERNAL = 6
+} sgs_status;
+
+/* Colour model kinds, numbered as ColorModelKind (color.hpp:59). */
+typedef enum { SGS_SH = 0, SGS_SG1 = 1, SGS_SG3 = 2, SGS_MIXED = 3 } sgs_color_kind;
+
+typedef enum { SGS_F64 = 0, SGS_F32 = 1 } sgs_dtype;
+typedef enum { SGS_HOST = 0, SGS_DEVICE = 1 } sgs_memory;
+
+/* Pinhole camera (camera.hpp:11-23). R is the row-major world-to-camera rotation. */
+typedef struct {
+    double R[9];
+    double t[3];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double near_plane;
+} sgs_camera;
+
+/* RenderConfig (raster.hpp:11-22). `threads` is accepted and ignored (the CUDA
+ * grid replaces the reference's std::thread partition). */
+typedef struct {
+    int32_t tile_size;
+    int32_t has_override;
+    int32_t override_degree;
+    int32_t threads;
+    double degree_threshold_lo;
+    double degree_threshold_hi;
+    double early_stop_transmittance;
+} sgs_render_config;
+
+/* A scene in the reference's flat parameter layout (scene.hpp:40-43): per
+ * Gaussian 11 geometry reals [px py pz, qw qx qy qz, lsx lsy lsz, opacity_logit]
+ * followed by the colour parameters in the canonical order of color.hpp:121-128:
+ *   SH     [coeff rgb x (d+1)^2]                    3(d+1)^2
+ *   SG1    [diffuse rgb, alpha rgb, log_lambda, mu]  10
+ *   SG3    [diffuse rgb, (alpha rgb, log_lambda)x3]  15
+ *   MIXED  [coeff rgb x (d+1)^2, (alpha rgb, log_lambda)x3]  3(d+1)^2+12
+ * `params` is count x stride values of `dtype` in host memory. */
+typedef struct {
+    uint64_t count;
+    int32_t kind;
+    int32_t sh_degree; /* stored SH degree (SH: 0..3, MIXED: 0..2; ignored for SG1/SG3) */
+    int32_t dtype;     /* sgs_dtype of params */
+    int32_t reserved;
+    const void* params;
+    double shared_axes[9]; /* row-major; rows are the shared lobe axes (scene.hpp:30) */
+    double background[3];
+} sgs_scene_desc;
+
+/* Device layout of an uploaded scene. */
+typedef struct {
+    uint64_t count;
+    int32_t kind;
+    int32_t sh_degree;
+    int32_t geometry_f64; /* 0: float32 planes (inputs were f32-exact), 1: float64 planes */
+    int32_t reserved;
+    uint64_t blob_bytes; /* bytes of the single device allocation holding every plane */
+    double shared_axes[9];
+    double background[3];
+} sgs_scene_meta;
+
+typedef struct sgs_context sgs_context;
+typedef struct sgs_scene sgs_scene;
+
+/* Per-render counters and (optionally) per-stage device times. */
+typedef struct {
+    uint64_t visible;       /* V: splats surviving the culls (raster.cpp:82-106) */
+    uint64_t tile_entries;  /* P: (tile, splat) pairs, = sum of TileGrid list sizes */
+    uint64_t block_entries; /* E_t: list entries composited before block termination */
+    uint64_t guard_hits;    /* pairs recomputed in FP64 by the compositor's guard band */
+    int32_t want_timing;    /* in: 1 to record per-stage CUDA-event times */
+    int32_t reserved;
+    float ms_preprocess, ms_depth_sort, ms_binning, ms_tile_sort, ms_composite, ms_total;
+} sgs_render_stats;
+
+/* --- context ------------------------------------------------------------------ */
+int sgs_abi_version(void);
+sgs_status sgs_create(int device, sgs_context** out);
+void sgs_destroy(sgs_context* ctx);
+/* Thread-local message of the last failing call on this thread. */
+const char* sgs_last_error(void);
+/* Run on a caller stream (cudaStream_t as void*); NULL restores the context's own. */
+sgs_status sgs_set_stream(sgs_context* ctx, void* stream);
+sgs_status sgs_synchronize(sgs_context* ctx);
+/* Cumulative number of this library's own kernel launches on ctx (K1, K3, K4, K6,
+ * K7) and of CUB library launches (radix sorts, scan), for launch accounting. */
+sgs_status sgs_launch_count(sgs_context* ctx, uint64_t* own_kernels, uint64_t* library_kernels);
+
+/* --- scenes ------------------------------------------------------------------- */
+/* Validates the desc (homogeneous by construction; scene.cpp:7-25 rules on degree)
+ * and fills the device layout it will use. */
+sgs_status sgs_scene_plan(const sgs_scene_desc* desc, sgs_scene_meta* meta);
+/* Upload into a context-owned allocation. */
+sgs_status sgs_scene_upload(sgs_context* ctx, const sgs_scene_desc* desc, sgs_scene** out);
+/* Upload into caller device memory of meta->blob_bytes (e.g. a torch tensor that
+ * NCCL later broadcasts). The scene does not own the memory. */
+sgs_status sgs_scene_upload_into(sgs_context* ctx, const sgs_scene_desc* desc,
+                                 void* device_blob, uint64_t bytes, sgs_scene** out);
+/* Bind an already-populated blob (e.g. received by ncclBroadcast) without copying. */
+sgs_status sgs_scene_bind(sgs_context* ctx, const sgs_scene_meta* meta, void* device_blob,
+                          uint64_t bytes, sgs_scene** out);
+sgs_status sgs_scene_get_meta(const sgs_scene* scene, sgs_scene_meta* meta);
+sgs_status sgs_scene_blob(const sgs_scene* scene, void** device_blob, uint64_t* bytes);
+sgs_status sgs_scene_set_background(sgs_scene* scene, const double* rgb);
+void sgs_scene_free(sgs_scene* scene);
+
+/* --- render path --------------------------------------------------------------- */
+/* One view. rgb: H*W*3 float32 row-major (Image layout, image.hpp:12-43); T: H*W
+ * float32 transmittance (either may be NULL). out_memory says whether rgb/T are
+ * host or device pointers; host outputs are complete when the call returns. */
+sgs_status sgs_render(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                      const sgs_render_config* cfg, float* rgb, float* T, int32_t out_memory,
+                      sgs_render_stats* stats);
+/* n views of one scene; view i writes rgb + i*H*W*3 and T + i*H*W (all cameras must
+ * share width/height). Host outputs are copied back on a second stream while the
+ * next view renders. stats (optional) accumulates over the views. */
+sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cams,
+                            int32_t n, const sgs_render_config* cfg, float* rgb, float* T,
+                            int32_t out_memory, sgs_render_stats* stats);
+
+/* Per-Gaussian projection (project_cached, raster.cpp:17-80) computed on the device
+ * and copied to host. */
+typedef struct {
+    double mean2d[2];
+    double conic[3];
+    double depth;
+    double color[3]; /* evaluated in float32, widened */
+    double opacity;
+    double radius;
+    int32_t degree; /* -1 for non-mixed scenes */
+    int32_t visible;
+} sgs_splat;
+sgs_status sgs_project(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                       const sgs_render_config* cfg, sgs_splat* out /* count */);
+/* Depth order and TileGrid lists as the reference builds them (raster.cpp:82-130):
+ * order[V] = Gaussian index per rank; offsets[tiles+1]; entries[P] = ranks.
+ * Call with entries == NULL to query V and P first. */
+sgs_status sgs_debug_tile_grid(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                               const sgs_render_config* cfg, uint32_t* order,
+                               uint64_t* n_visible, uint64_t* offsets, uint32_t* entries,
+                               uint64_t capacity, uint64_t* n_entries);
+
+/* --- scalar helpers (host) ------------------------------------------------------ */
+sgs_status sgs_select_degree(double radius_px, double lo, double hi, int32_t* out);
+sgs_status sgs_flops_per_gaussian(int32_t kind, int32_t sh_degree, int32_t* out);
+int32_t sgs_color_param_count(int32_t kind, int32_t sh_degree);
+
+/* --- synthetic inputs (host) ---------------------------------------------------- */
+/* make_synthetic_scene with SynthOptions defaults except kind / sh_degree /
+ * log-scale range. params: count * (11 + colour params) doubles. */
+sgs_status sgs_synth_scene(uint64_t count, uint64_t seed, int32_t kind, int32_t sh_degree,
+                           double log_scale_min, double log_scale_max, double* params);
+/* Same geometry, degree-3 SH colours (BASELINE config D): DC + bands 1-2 copied from
+ * a MIXED scene, band 3 drawn from mt19937_64(seed + 1). */
+sgs_status sgs_synth_sh3_from_mixed(uint64_t count, uint64_t seed, const double* mixed_params,
+                                    double* sh3_params);
+sgs_status sgs_orbit_camera(const double* target, double distance, double angle,
+                            double elevation, int32_t width, int32_t height, double focal,
+                            sgs_camera* out);
+sgs_status sgs_orbit_cameras(int32_t count, int32_t width, int32_t height, double distance,
+                             double focal, double elevation, sgs_camera* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGS_H */

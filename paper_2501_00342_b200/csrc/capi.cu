@@ -1,0 +1,794 @@
+// capi.cu -- the C-ABI (include/sgs.h): contexts, device scenes, frame orchestration.
+//
+// Frame pipeline on the context stream:
+//   K1 preprocess -> K2 stable radix sort of FP64 depth keys (values: Gaussian index)
+//   -> K3 gather per-rank tile counts + exclusive scan -> [one 40-B D2H of the
+//   counters: error word, V, P; sizes the tile-key arena] -> K4 emit (tile,index)
+//   keys -> K5 stable radix sort on the tile bits -> K6 tile ranges -> K7 composite.
+// Radix sorts and the scan use CUB (CUDA 12.9 CCCL) as the library primitive.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "sgs_internal.h"
+
+using namespace sgs;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sgs_status fail(sgs_status code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define SGS_CUDA(call)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            return fail(e_ == cudaErrorMemoryAllocation ? SGS_ERR_OUT_OF_MEMORY : SGS_ERR_CUDA, \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+        }                                                                                    \
+    } while (0)
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        size_t grow = need + need / 4 + 256;
+        cudaError_t e = cudaMalloc(&ptr, grow);
+        if (e == cudaSuccess) bytes = grow;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int color_param_count_impl(int kind, int degree) {
+    switch (kind) {
+        case SGS_SH: return 3 * (degree + 1) * (degree + 1);
+        case SGS_SG1: return 10;
+        case SGS_SG3: return 15;
+        case SGS_MIXED: return 3 * (degree + 1) * (degree + 1) + 12;
+    }
+    return -1;
+}
+
+}  // namespace
+
+struct sgs_scene {
+    sgs_scene_meta meta{};
+    sgs_context* ctx = nullptr;
+    DevBuf owned;
+    void* blob = nullptr;
+    ScenePlanes planes{};
+};
+
+struct sgs_context {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    std::mutex mu;
+    DevBuf keys_a, keys_b, iota, order_b, rec, rec64, rects, ntiles, counts, offsets;
+    DevBuf tkeys_a, tkeys_b, ranges, cub_temp, frame_rgb[2], frame_T[2];
+    Counters* d_ctr = nullptr;
+    Counters* h_ctr = nullptr;
+    cudaEvent_t ev[8] = {};
+    cudaEvent_t frame_done[2] = {};
+    cudaEvent_t slot_free[2] = {};
+    // results of the last frame (device pointers into the buffers above)
+    const uint32_t* last_order = nullptr;
+    const unsigned long long* last_tile_keys = nullptr;
+    uint64_t last_v = 0, last_p = 0;
+    uint64_t own_launches = 0, lib_launches = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Host-side validation and constants, in the reference's order and arithmetic
+// (this TU's host code is compiled with -ffp-contract=off).
+
+sgs_status validate_camera(const sgs_camera* cam) {
+    // Camera::validate, camera.cpp:10-13
+    if (cam->fx <= 0 || cam->fy <= 0) return fail(SGS_ERR_INVALID_ARGUMENT, "camera focal lengths must be positive");
+    if (cam->width < 1 || cam->height < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "camera image size must be >= 1");
+    return SGS_OK;
+}
+
+CamParams make_cam(const sgs_camera* c) {
+    CamParams p{};
+    for (int i = 0; i < 9; ++i) p.R[i] = c->R[i];
+    for (int i = 0; i < 3; ++i) p.t[i] = c->t[i];
+    // center() = -R^T t (camera.hpp:20), left-to-right sums
+    for (int i = 0; i < 3; ++i)
+        p.C[i] = ((-c->R[0 * 3 + i]) * c->t[0] + (-c->R[1 * 3 + i]) * c->t[1]) + (-c->R[2 * 3 + i]) * c->t[2];
+    p.fx = c->fx;
+    p.fy = c->fy;
+    p.cx = c->cx;
+    p.cy = c->cy;
+    p.width = c->width;
+    p.height = c->height;
+    p.near_plane = c->near_plane;
+    p.lim_x = 1.3 * (0.5 * c->width / c->fx);  // raster.cpp:29-30
+    p.lim_y = 1.3 * (0.5 * c->height / c->fy);
+    p.W = c->width;
+    p.H = c->height;
+    return p;
+}
+
+CfgParams make_cfg(const sgs_render_config* cfg, const sgs_camera* cam) {
+    CfgParams k{};
+    k.tile_size = cfg->tile_size;
+    k.tiles_x = (cam->width + cfg->tile_size - 1) / cfg->tile_size;
+    k.tiles_y = (cam->height + cfg->tile_size - 1) / cfg->tile_size;
+    k.has_override = cfg->has_override;
+    k.override_degree = cfg->override_degree;
+    k.lo = cfg->degree_threshold_lo;
+    k.hi = cfg->degree_threshold_hi;
+    k.early_stop = static_cast<float>(cfg->early_stop_transmittance);
+    return k;
+}
+
+sgs_status device_error(unsigned long long word, const sgs_scene* scene, const sgs_render_config* cfg) {
+    const unsigned code = static_cast<unsigned>(word & 0xFF);
+    const unsigned long long idx = word >> 8;
+    char buf[256];
+    switch (code) {
+        case kErrZeroQuaternion:
+            return fail(SGS_ERR_NUMERIC, "degenerate rotation: zero quaternion");
+        case kErrThresholds:
+            return fail(SGS_ERR_INVALID_ARGUMENT, "degree thresholds must satisfy lo <= hi");
+        case kErrOverrideNonMixed:
+            return fail(SGS_ERR_INVALID_ARGUMENT, "sh_degree_override is only valid for mixed scenes");
+        case kErrDegreeTooHigh:
+            std::snprintf(buf, sizeof(buf), "sh degree override %d exceeds stored degree %d",
+                          cfg->has_override ? cfg->override_degree : 2, scene->meta.sh_degree);
+            return fail(SGS_ERR_INVALID_ARGUMENT, buf);
+        case kErrDirection:
+            return fail(SGS_ERR_INVALID_ARGUMENT, "direction must be unit length");
+    }
+    std::snprintf(buf, sizeof(buf), "device error %u at gaussian %llu", code, idx);
+    return fail(SGS_ERR_INTERNAL, buf);
+}
+
+int ceil_log2(uint64_t v) {
+    int b = 0;
+    while ((1ULL << b) < v) ++b;
+    return b;
+}
+
+// One frame on ctx->stream. Outputs are device pointers (either may be null).
+sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                     const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
+                     DebugSplat* d_debug, bool composite) {
+    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
+    sgs_status st = validate_camera(cam);
+    if (st != SGS_OK) return st;
+    cudaStream_t s = ctx->stream;
+    const uint64_t n = scene->meta.count;
+    const CamParams cp = make_cam(cam);
+    const CfgParams kp = make_cfg(cfg, cam);
+    const uint64_t ntile = static_cast<uint64_t>(kp.tiles_x) * static_cast<uint64_t>(kp.tiles_y);
+    const bool timing = stats && stats->want_timing;
+
+    SGS_CUDA(ctx->keys_a.ensure(std::max<uint64_t>(n, 1) * 8));
+    SGS_CUDA(ctx->keys_b.ensure(std::max<uint64_t>(n, 1) * 8));
+    SGS_CUDA(ctx->iota.ensure(std::max<uint64_t>(n, 1) * 4));
+    SGS_CUDA(ctx->order_b.ensure(std::max<uint64_t>(n, 1) * 4));
+    SGS_CUDA(ctx->rec.ensure(std::max<uint64_t>(n, 1) * sizeof(SplatRec)));
+    SGS_CUDA(ctx->rec64.ensure(std::max<uint64_t>(n, 1) * sizeof(SplatRec64)));
+    SGS_CUDA(ctx->rects.ensure(std::max<uint64_t>(n, 1) * sizeof(int4)));
+    SGS_CUDA(ctx->ntiles.ensure(std::max<uint64_t>(n, 1) * 4));
+    SGS_CUDA(ctx->counts.ensure((n + 1) * 8));
+    SGS_CUDA(ctx->offsets.ensure((n + 1) * 8));
+    SGS_CUDA(ctx->ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
+
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[0], s));
+    SGS_CUDA(cudaMemsetAsync(ctx->d_ctr, 0, sizeof(Counters), s));
+    SGS_CUDA(cudaMemsetAsync(&ctx->d_ctr->err, 0xFF, sizeof(unsigned long long), s));
+
+    // K1
+    launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
+                      ctx->rec.as<SplatRec>(), ctx->rec64.as<SplatRec64>(), ctx->rects.as<int4>(),
+                      ctx->ntiles.as<uint32_t>(), ctx->d_ctr, d_debug, s);
+    SGS_CUDA(cudaGetLastError());
+    if (n) ctx->own_launches += 1;
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[1], s));
+
+    // K2: stable radix sort of the FP64 depth keys; values = Gaussian index.
+    const uint32_t* order = ctx->iota.as<uint32_t>();
+    if (n > 1) {
+        cub::DoubleBuffer<unsigned long long> kb(ctx->keys_a.as<unsigned long long>(),
+                                                 ctx->keys_b.as<unsigned long long>());
+        cub::DoubleBuffer<uint32_t> vb(ctx->iota.as<uint32_t>(), ctx->order_b.as<uint32_t>());
+        size_t temp = 0;
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, kb, vb, static_cast<int>(n), 0, 64, s));
+        SGS_CUDA(ctx->cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp, kb, vb, static_cast<int>(n), 0,
+                                                 64, s));
+        order = vb.Current();
+        ctx->lib_launches += 1 + 8;  // onesweep: histogram + one pass per 8-bit digit
+    }
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[2], s));
+
+    // K3: per-rank tile counts -> exclusive scan (offsets[n] = P)
+    if (n > 0) {
+        launch_gather_counts(n, order, ctx->ntiles.as<uint32_t>(), ctx->counts.as<unsigned long long>(), s);
+        size_t temp = 0;
+        SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, ctx->counts.as<unsigned long long>(),
+                                               ctx->offsets.as<unsigned long long>(), static_cast<int>(n + 1), s));
+        SGS_CUDA(ctx->cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, ctx->counts.as<unsigned long long>(),
+                                               ctx->offsets.as<unsigned long long>(), static_cast<int>(n + 1), s));
+        ctx->own_launches += 1;
+        ctx->lib_launches += 2;  // decoupled look-back scan: init + scan
+        SGS_CUDA(cudaMemcpyAsync(&ctx->d_ctr->tile_entries, ctx->offsets.as<unsigned long long>() + n,
+                                 sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    }
+    SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaStreamSynchronize(s));
+    if (ctx->h_ctr->err != ~0ULL) return device_error(ctx->h_ctr->err, scene, cfg);
+    const uint64_t v = ctx->h_ctr->visible;
+    const uint64_t p = ctx->h_ctr->tile_entries;
+    if (p > 0x7FFFFFFFULL) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^31 tile entries in one frame");
+
+    // K4 + K5 + K6
+    SGS_CUDA(ctx->tkeys_a.ensure(std::max<uint64_t>(p, 1) * 8));
+    SGS_CUDA(ctx->tkeys_b.ensure(std::max<uint64_t>(p, 1) * 8));
+    launch_emit_tile_keys(v, order, ctx->ntiles.as<uint32_t>(), ctx->rects.as<int4>(),
+                          ctx->offsets.as<unsigned long long>(), kp.tiles_x,
+                          ctx->tkeys_a.as<unsigned long long>(), s);
+    SGS_CUDA(cudaGetLastError());
+    if (v) ctx->own_launches += 1;
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[3], s));
+    const unsigned long long* tkeys = ctx->tkeys_a.as<unsigned long long>();
+    if (p > 1 && ntile > 1) {
+        cub::DoubleBuffer<unsigned long long> tb(ctx->tkeys_a.as<unsigned long long>(),
+                                                 ctx->tkeys_b.as<unsigned long long>());
+        const int end_bit = 32 + std::max(1, ceil_log2(ntile));
+        size_t temp = 0;
+        SGS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
+        SGS_CUDA(ctx->cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_temp.ptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
+        tkeys = tb.Current();
+        ctx->lib_launches += 1 + (end_bit - 32 + 7) / 8;
+    }
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[4], s));
+    SGS_CUDA(cudaMemsetAsync(ctx->ranges.ptr, 0, ntile * sizeof(uint2), s));
+    launch_tile_ranges(p, tkeys, ctx->ranges.as<uint2>(), s);
+    SGS_CUDA(cudaGetLastError());
+    if (p) ctx->own_launches += 1;
+
+    ctx->last_order = order;
+    ctx->last_tile_keys = tkeys;
+    ctx->last_v = v;
+    ctx->last_p = p;
+
+    // K7
+    if (composite) {
+        const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
+                                      static_cast<float>(scene->meta.background[1]),
+                                      static_cast<float>(scene->meta.background[2]));
+        launch_composite(cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
+                         ctx->rec64.as<SplatRec64>(), bg, d_rgb, d_T, ctx->d_ctr, stats != nullptr, s);
+        SGS_CUDA(cudaGetLastError());
+        ctx->own_launches += 1;
+    }
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[5], s));
+    if (stats) {
+        SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+        SGS_CUDA(cudaStreamSynchronize(s));
+        stats->visible += v;
+        stats->tile_entries += p;
+        stats->block_entries += ctx->h_ctr->block_entries;
+        stats->guard_hits += ctx->h_ctr->guard_hits;
+        if (timing) {
+            float ms[5];
+            for (int k = 0; k < 5; ++k) SGS_CUDA(cudaEventElapsedTime(&ms[k], ctx->ev[k], ctx->ev[k + 1]));
+            stats->ms_preprocess += ms[0];
+            stats->ms_depth_sort += ms[1];
+            stats->ms_binning += ms[2];
+            stats->ms_tile_sort += ms[3];
+            stats->ms_composite += ms[4];
+            float total = 0;
+            SGS_CUDA(cudaEventElapsedTime(&total, ctx->ev[0], ctx->ev[5]));
+            stats->ms_total += total;
+        }
+    }
+    return SGS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Scene layout and upload.
+
+struct Layout {
+    size_t geo_off[11];
+    size_t color_off;
+    size_t bytes;
+    int color_planes;
+};
+
+Layout make_layout(const sgs_scene_meta& m) {
+    Layout L{};
+    const size_t n = m.count;
+    size_t off = 0;
+    if (m.geometry_f64) {
+        for (int k = 0; k < 11; ++k) {
+            L.geo_off[k] = off;
+            off = align_up(off + n * 8, 256);
+        }
+    } else {
+        for (int k = 0; k < 3; ++k) {
+            L.geo_off[k] = off;
+            off = align_up(off + n * 16, 256);
+        }
+    }
+    L.color_planes = color_plane_count(m.kind, m.sh_degree);
+    L.color_off = off;
+    off = align_up(off + static_cast<size_t>(L.color_planes) * n * 16, 256);
+    L.bytes = std::max<size_t>(off, 256);
+    return L;
+}
+
+void bind_planes(sgs_scene* sc) {
+    const sgs_scene_meta& m = sc->meta;
+    Layout L = make_layout(m);
+    ScenePlanes& p = sc->planes;
+    p = ScenePlanes{};
+    p.n = m.count;
+    p.kind = m.kind;
+    p.sh_degree = m.sh_degree;
+    p.geometry_f64 = m.geometry_f64;
+    p.color_planes = L.color_planes;
+    char* base = static_cast<char*>(sc->blob);
+    if (m.geometry_f64) {
+        for (int k = 0; k < 11; ++k) p.g8[k] = reinterpret_cast<const double*>(base + L.geo_off[k]);
+    } else {
+        for (int k = 0; k < 3; ++k) p.g4[k] = reinterpret_cast<const float4*>(base + L.geo_off[k]);
+    }
+    p.color = reinterpret_cast<const float4*>(base + L.color_off);
+    for (int k = 0; k < 9; ++k) p.axes[k] = static_cast<float>(m.shared_axes[k]);
+    for (int k = 0; k < 3; ++k) p.bg[k] = static_cast<float>(m.background[k]);
+}
+
+double param_at(const sgs_scene_desc* d, size_t idx) {
+    if (d->dtype == SGS_F32) return static_cast<double>(static_cast<const float*>(d->params)[idx]);
+    return static_cast<const double*>(d->params)[idx];
+}
+
+// Host staging of the blob from the reference's flat layout.
+void fill_blob(const sgs_scene_desc* d, const sgs_scene_meta& m, std::vector<char>& host) {
+    const Layout L = make_layout(m);
+    host.assign(L.bytes, 0);
+    const size_t n = m.count;
+    const int cpc = color_param_count_impl(m.kind, m.sh_degree);
+    const size_t stride = 11 + static_cast<size_t>(cpc);
+    char* base = host.data();
+    std::vector<float> c(static_cast<size_t>(L.color_planes) * 4);
+    for (size_t i = 0; i < n; ++i) {
+        const size_t o = i * stride;
+        if (m.geometry_f64) {
+            for (int k = 0; k < 11; ++k) reinterpret_cast<double*>(base + L.geo_off[k])[i] = param_at(d, o + k);
+        } else {
+            float4* g0 = reinterpret_cast<float4*>(base + L.geo_off[0]);
+            float4* g1 = reinterpret_cast<float4*>(base + L.geo_off[1]);
+            float4* g2 = reinterpret_cast<float4*>(base + L.geo_off[2]);
+            auto f = [&](int k) { return static_cast<float>(param_at(d, o + k)); };
+            g0[i] = make_float4(f(0), f(1), f(2), f(10));
+            g1[i] = make_float4(f(3), f(4), f(5), f(6));
+            g2[i] = make_float4(f(7), f(8), f(9), 0.f);
+        }
+        std::fill(c.begin(), c.end(), 0.f);
+        const size_t co = o + 11;
+        switch (m.kind) {
+            case SGS_SH:
+                for (int k = 0; k < cpc; ++k) c[k] = static_cast<float>(param_at(d, co + k));
+                break;
+            case SGS_MIXED: {
+                const int nsh = 3 * (m.sh_degree + 1) * (m.sh_degree + 1);
+                for (int k = 0; k < nsh; ++k) c[k] = static_cast<float>(param_at(d, co + k));
+                const int lobe_base = 4 * ((nsh + 3) / 4);
+                for (int k = 0; k < 12; ++k) c[lobe_base + k] = static_cast<float>(param_at(d, co + nsh + k));
+                break;
+            }
+            case SGS_SG1: {
+                // plane 0 (diffuse rgb, log_lambda), plane 1 (alpha rgb, 0), plane 2 (mu/|mu|, 0);
+                // mu normalised in FP64 exactly as DiffuseSGModel::lobe (color.cpp:49-56)
+                for (int k = 0; k < 3; ++k) c[k] = static_cast<float>(param_at(d, co + k));
+                c[3] = static_cast<float>(param_at(d, co + 6));
+                for (int k = 0; k < 3; ++k) c[4 + k] = static_cast<float>(param_at(d, co + 3 + k));
+                const double mu[3] = {param_at(d, co + 7), param_at(d, co + 8), param_at(d, co + 9)};
+                const double nn = std::sqrt((mu[0] * mu[0] + mu[1] * mu[1]) + mu[2] * mu[2]);
+                for (int k = 0; k < 3; ++k)
+                    c[8 + k] = static_cast<float>(nn > 1e-12 ? mu[k] / nn : (k == 0 ? 1.0 : 0.0));
+                break;
+            }
+            case SGS_SG3:
+                for (int k = 0; k < 3; ++k) c[k] = static_cast<float>(param_at(d, co + k));
+                for (int k = 0; k < 12; ++k) c[4 + k] = static_cast<float>(param_at(d, co + 3 + k));
+                break;
+        }
+        float4* cp = reinterpret_cast<float4*>(base + L.color_off);
+        for (int pl = 0; pl < L.color_planes; ++pl)
+            cp[static_cast<size_t>(pl) * n + i] = make_float4(c[4 * pl], c[4 * pl + 1], c[4 * pl + 2], c[4 * pl + 3]);
+    }
+}
+
+sgs_status upload_common(sgs_context* ctx, const sgs_scene_desc* desc, void* blob, uint64_t bytes,
+                         bool own, sgs_scene** out) {
+    if (!ctx || !desc || !out) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    sgs_scene_meta m{};
+    sgs_status st = sgs_scene_plan(desc, &m);
+    if (st != SGS_OK) return st;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    auto* sc = new sgs_scene();
+    sc->meta = m;
+    sc->ctx = ctx;
+    if (own) {
+        cudaError_t e = sc->owned.ensure(m.blob_bytes);
+        if (e != cudaSuccess) {
+            delete sc;
+            return fail(SGS_ERR_OUT_OF_MEMORY, "scene allocation failed");
+        }
+        sc->blob = sc->owned.ptr;
+    } else {
+        if (bytes < m.blob_bytes) {
+            delete sc;
+            return fail(SGS_ERR_INVALID_ARGUMENT, "device blob smaller than meta.blob_bytes");
+        }
+        sc->blob = blob;
+    }
+    std::vector<char> host;
+    fill_blob(desc, m, host);
+    cudaError_t e = cudaMemcpy(sc->blob, host.data(), host.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        delete sc;
+        return fail(SGS_ERR_CUDA, std::string("scene upload: ") + cudaGetErrorString(e));
+    }
+    bind_planes(sc);
+    *out = sc;
+    return SGS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int sgs_abi_version(void) { return SGS_ABI_VERSION; }
+
+const char* sgs_last_error(void) { return g_last_error.c_str(); }
+
+sgs_status sgs_create(int device, sgs_context** out) {
+    if (!out) return fail(SGS_ERR_INVALID_ARGUMENT, "null out");
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(SGS_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(SGS_ERR_INVALID_ARGUMENT, "bad device ordinal");
+    SGS_CUDA(cudaSetDevice(device));
+    auto* ctx = new sgs_context();
+    ctx->device = device;
+    SGS_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    SGS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    SGS_CUDA(cudaMalloc(&ctx->d_ctr, sizeof(Counters)));
+    SGS_CUDA(cudaMallocHost(&ctx->h_ctr, sizeof(Counters)));
+    for (auto& ev : ctx->ev) SGS_CUDA(cudaEventCreate(&ev));
+    for (int k = 0; k < 2; ++k) {
+        SGS_CUDA(cudaEventCreateWithFlags(&ctx->frame_done[k], cudaEventDisableTiming));
+        SGS_CUDA(cudaEventCreateWithFlags(&ctx->slot_free[k], cudaEventDisableTiming));
+    }
+    *out = ctx;
+    return SGS_OK;
+}
+
+void sgs_destroy(sgs_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->copy_stream);
+    for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->iota, &ctx->order_b, &ctx->rec, &ctx->rec64,
+                      &ctx->rects, &ctx->ntiles, &ctx->counts, &ctx->offsets, &ctx->tkeys_a, &ctx->tkeys_b,
+                      &ctx->ranges, &ctx->cub_temp, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
+                      &ctx->frame_T[0], &ctx->frame_T[1]})
+        b->release();
+    if (ctx->d_ctr) cudaFree(ctx->d_ctr);
+    if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    for (auto& ev : ctx->ev) cudaEventDestroy(ev);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(ctx->frame_done[k]);
+        cudaEventDestroy(ctx->slot_free[k]);
+    }
+    cudaStreamDestroy(ctx->own_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+}
+
+sgs_status sgs_set_stream(sgs_context* ctx, void* stream) {
+    if (!ctx) return fail(SGS_ERR_INVALID_ARGUMENT, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return SGS_OK;
+}
+
+sgs_status sgs_synchronize(sgs_context* ctx) {
+    if (!ctx) return fail(SGS_ERR_INVALID_ARGUMENT, "null context");
+    SGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    SGS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    return SGS_OK;
+}
+
+sgs_status sgs_launch_count(sgs_context* ctx, uint64_t* own_kernels, uint64_t* library_kernels) {
+    if (!ctx || !own_kernels || !library_kernels) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    *own_kernels = ctx->own_launches;
+    *library_kernels = ctx->lib_launches;
+    return SGS_OK;
+}
+
+int32_t sgs_color_param_count(int32_t kind, int32_t sh_degree) { return color_param_count_impl(kind, sh_degree); }
+
+sgs_status sgs_scene_plan(const sgs_scene_desc* d, sgs_scene_meta* m) {
+    if (!d || !m) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    if (d->kind < SGS_SH || d->kind > SGS_MIXED) return fail(SGS_ERR_INVALID_ARGUMENT, "unknown color model kind");
+    int deg = d->sh_degree;
+    if (d->kind == SGS_SG1 || d->kind == SGS_SG3) deg = 0;
+    if (d->kind == SGS_SH && (deg < 0 || deg > 3)) return fail(SGS_ERR_INVALID_ARGUMENT, "unsupported SH degree");
+    if (d->kind == SGS_MIXED && (deg < 0 || deg > 2))
+        return fail(SGS_ERR_INVALID_ARGUMENT, "mixed model stores SH degree 0..2");
+    if (d->dtype != SGS_F32 && d->dtype != SGS_F64) return fail(SGS_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (d->count && !d->params) return fail(SGS_ERR_INVALID_ARGUMENT, "null params");
+    if (d->count > 0xFFFFFFFFULL) return fail(SGS_ERR_INVALID_ARGUMENT, "more than 2^32 Gaussians");
+    *m = sgs_scene_meta{};
+    m->count = d->count;
+    m->kind = d->kind;
+    m->sh_degree = deg;
+    // float32 geometry planes are lossless iff every geometry real is f32-exact
+    int f64 = 0;
+    if (d->dtype == SGS_F64) {
+        const size_t stride = 11 + static_cast<size_t>(color_param_count_impl(d->kind, deg));
+        const double* p = static_cast<const double*>(d->params);
+        for (size_t i = 0; i < d->count && !f64; ++i)
+            for (int k = 0; k < 11; ++k) {
+                const double v = p[i * stride + k];
+                if (static_cast<double>(static_cast<float>(v)) != v) {
+                    f64 = 1;
+                    break;
+                }
+            }
+    }
+    m->geometry_f64 = f64;
+    for (int k = 0; k < 9; ++k) m->shared_axes[k] = d->shared_axes[k];
+    for (int k = 0; k < 3; ++k) m->background[k] = d->background[k];
+    m->blob_bytes = make_layout(*m).bytes;
+    return SGS_OK;
+}
+
+sgs_status sgs_scene_upload(sgs_context* ctx, const sgs_scene_desc* desc, sgs_scene** out) {
+    return upload_common(ctx, desc, nullptr, 0, true, out);
+}
+
+sgs_status sgs_scene_upload_into(sgs_context* ctx, const sgs_scene_desc* desc, void* device_blob,
+                                 uint64_t bytes, sgs_scene** out) {
+    if (!device_blob) return fail(SGS_ERR_INVALID_ARGUMENT, "null device blob");
+    return upload_common(ctx, desc, device_blob, bytes, false, out);
+}
+
+sgs_status sgs_scene_bind(sgs_context* ctx, const sgs_scene_meta* meta, void* device_blob,
+                          uint64_t bytes, sgs_scene** out) {
+    if (!ctx || !meta || !device_blob || !out) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    sgs_scene_meta m = *meta;
+    m.blob_bytes = make_layout(m).bytes;
+    if (bytes < m.blob_bytes) return fail(SGS_ERR_INVALID_ARGUMENT, "device blob smaller than layout");
+    auto* sc = new sgs_scene();
+    sc->meta = m;
+    sc->ctx = ctx;
+    sc->blob = device_blob;
+    bind_planes(sc);
+    *out = sc;
+    return SGS_OK;
+}
+
+sgs_status sgs_scene_get_meta(const sgs_scene* scene, sgs_scene_meta* meta) {
+    if (!scene || !meta) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    *meta = scene->meta;
+    return SGS_OK;
+}
+
+sgs_status sgs_scene_blob(const sgs_scene* scene, void** device_blob, uint64_t* bytes) {
+    if (!scene || !device_blob || !bytes) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    *device_blob = scene->blob;
+    *bytes = scene->meta.blob_bytes;
+    return SGS_OK;
+}
+
+sgs_status sgs_scene_set_background(sgs_scene* scene, const double* rgb) {
+    if (!scene || !rgb) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    for (int k = 0; k < 3; ++k) scene->meta.background[k] = rgb[k];
+    bind_planes(scene);
+    return SGS_OK;
+}
+
+void sgs_scene_free(sgs_scene* scene) {
+    if (!scene) return;
+    if (scene->ctx) cudaSetDevice(scene->ctx->device);
+    scene->owned.release();
+    delete scene;
+}
+
+sgs_status sgs_render(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                      const sgs_render_config* cfg, float* rgb, float* T, int32_t out_memory,
+                      sgs_render_stats* stats) {
+    return sgs_render_batch(ctx, scene, cam, 1, cfg, rgb, T, out_memory, stats);
+}
+
+sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cams,
+                            int32_t n, const sgs_render_config* cfg, float* rgb, float* T,
+                            int32_t out_memory, sgs_render_stats* stats) {
+    if (!ctx || !scene || !cams || !cfg) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 0) return fail(SGS_ERR_INVALID_ARGUMENT, "negative view count");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    if (n == 0) return SGS_OK;
+    const int W = cams[0].width, H = cams[0].height;
+    for (int i = 1; i < n; ++i)
+        if (cams[i].width != W || cams[i].height != H)
+            return fail(SGS_ERR_INVALID_ARGUMENT, "all batch cameras must share width/height");
+    if (W < 1 || H < 1) return validate_camera(&cams[0]);
+    const size_t npx = static_cast<size_t>(W) * static_cast<size_t>(H);
+    if (out_memory == SGS_DEVICE) {
+        for (int i = 0; i < n; ++i) {
+            sgs_status st = run_frame(ctx, scene, &cams[i], cfg, rgb ? rgb + i * npx * 3 : nullptr,
+                                      T ? T + i * npx : nullptr, stats, nullptr, true);
+            if (st != SGS_OK) return st;
+        }
+        SGS_CUDA(cudaStreamSynchronize(ctx->stream));
+        return SGS_OK;
+    }
+    // Host outputs: render into a double-buffered device frame, copy back on the copy
+    // stream while the next view renders.
+    for (int k = 0; k < 2; ++k) {
+        SGS_CUDA(ctx->frame_rgb[k].ensure(npx * 3 * sizeof(float)));
+        SGS_CUDA(ctx->frame_T[k].ensure(npx * sizeof(float)));
+        SGS_CUDA(cudaEventRecord(ctx->slot_free[k], ctx->copy_stream));
+    }
+    for (int i = 0; i < n; ++i) {
+        const int k = i & 1;
+        SGS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_free[k], 0));
+        sgs_status st = run_frame(ctx, scene, &cams[i], cfg, rgb ? ctx->frame_rgb[k].as<float>() : nullptr,
+                                  T ? ctx->frame_T[k].as<float>() : nullptr, stats, nullptr, true);
+        if (st != SGS_OK) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            return st;
+        }
+        SGS_CUDA(cudaEventRecord(ctx->frame_done[k], ctx->stream));
+        SGS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->frame_done[k], 0));
+        if (rgb)
+            SGS_CUDA(cudaMemcpyAsync(rgb + i * npx * 3, ctx->frame_rgb[k].ptr, npx * 3 * sizeof(float),
+                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
+        if (T)
+            SGS_CUDA(cudaMemcpyAsync(T + i * npx, ctx->frame_T[k].ptr, npx * sizeof(float),
+                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
+        SGS_CUDA(cudaEventRecord(ctx->slot_free[k], ctx->copy_stream));
+    }
+    SGS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    SGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return SGS_OK;
+}
+
+sgs_status sgs_project(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                       const sgs_render_config* cfg, sgs_splat* out) {
+    if (!ctx || !scene || !cam || !cfg || (!out && scene->meta.count)) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    static_assert(sizeof(sgs_splat) == sizeof(DebugSplat), "debug record layout");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t n = scene->meta.count;
+    DebugSplat* d_dbg = nullptr;
+    SGS_CUDA(cudaMalloc(&d_dbg, std::max<uint64_t>(n, 1) * sizeof(DebugSplat)));
+    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, d_dbg, false);
+    if (st == SGS_OK && n) {
+        cudaError_t e = cudaMemcpy(out, d_dbg, n * sizeof(DebugSplat), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
+    }
+    cudaFree(d_dbg);
+    return st;
+}
+
+sgs_status sgs_debug_tile_grid(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                               const sgs_render_config* cfg, uint32_t* order, uint64_t* n_visible,
+                               uint64_t* offsets, uint32_t* entries, uint64_t capacity,
+                               uint64_t* n_entries) {
+    if (!ctx || !scene || !cam || !cfg || !n_visible || !n_entries)
+        return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, nullptr, false);
+    if (st != SGS_OK) return st;
+    SGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint64_t v = ctx->last_v, p = ctx->last_p;
+    *n_visible = v;
+    *n_entries = p;
+    std::vector<uint32_t> ord(v);
+    if (v) SGS_CUDA(cudaMemcpy(ord.data(), ctx->last_order, v * 4, cudaMemcpyDeviceToHost));
+    if (order && v) std::memcpy(order, ord.data(), v * 4);
+    if (!offsets && !entries) return SGS_OK;
+    std::vector<unsigned long long> keys(p);
+    if (p) SGS_CUDA(cudaMemcpy(keys.data(), ctx->last_tile_keys, p * 8, cudaMemcpyDeviceToHost));
+    const uint64_t ntile = static_cast<uint64_t>((cam->width + cfg->tile_size - 1) / cfg->tile_size) *
+                           static_cast<uint64_t>((cam->height + cfg->tile_size - 1) / cfg->tile_size);
+    if (offsets) {
+        std::vector<uint64_t> cnt(ntile + 1, 0);
+        for (uint64_t i = 0; i < p; ++i) cnt[keys[i] >> 32]++;
+        uint64_t acc = 0;
+        for (uint64_t t = 0; t < ntile; ++t) {
+            offsets[t] = acc;
+            acc += cnt[t];
+        }
+        offsets[ntile] = acc;
+    }
+    if (entries) {
+        std::vector<uint32_t> rank_of(scene->meta.count, 0xFFFFFFFFu);
+        for (uint64_t r = 0; r < v; ++r) rank_of[ord[r]] = static_cast<uint32_t>(r);
+        for (uint64_t i = 0; i < p && i < capacity; ++i) entries[i] = rank_of[static_cast<uint32_t>(keys[i])];
+    }
+    return SGS_OK;
+}
+
+sgs_status sgs_select_degree(double r, double lo, double hi, int32_t* out) {
+    if (!out) return fail(SGS_ERR_INVALID_ARGUMENT, "null out");
+    if (lo > hi) return fail(SGS_ERR_INVALID_ARGUMENT, "degree thresholds must satisfy lo <= hi");
+    *out = r < lo ? 0 : (r < hi ? 1 : 2);
+    return SGS_OK;
+}
+
+sgs_status sgs_flops_per_gaussian(int32_t kind, int32_t deg, int32_t* out) {
+    // flops_per_gaussian, raster.cpp:190-227 (band ops 0/3/15/25, 2 ops per coeff per
+    // channel, 8 per lobe, 2 per channel per lobe blend)
+    if (!out) return fail(SGS_ERR_INVALID_ARGUMENT, "null out");
+    static const int band_ops[4] = {0, 3, 15, 25};
+    auto basis = [&](int d) {
+        int s = 0;
+        for (int l = 1; l <= d; ++l) s += band_ops[l];
+        return s;
+    };
+    switch (kind) {
+        case SGS_SH:
+            if (deg < 0 || deg > 3) return fail(SGS_ERR_INVALID_ARGUMENT, "SH degree must be 0..3");
+            *out = basis(deg) + 2 * (deg + 1) * (deg + 1) * 3;
+            return SGS_OK;
+        case SGS_SG1: *out = 8 + 2 * 3; return SGS_OK;
+        case SGS_SG3: *out = 3 * 8 + 2 * 3 * 3; return SGS_OK;
+        case SGS_MIXED:
+            if (deg < 0 || deg > 2) return fail(SGS_ERR_INVALID_ARGUMENT, "mixed degree must be 0..2");
+            *out = basis(deg) + 2 * (deg + 1) * (deg + 1) * 3 + 3 * 8 + 2 * 3 * 3;
+            return SGS_OK;
+    }
+    return fail(SGS_ERR_INVALID_ARGUMENT, "unknown color model kind");
+}
+
+}  // extern "C"
