@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -91,10 +92,12 @@ struct sgs_context {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
     std::mutex mu;
-    DevBuf keys_a, keys_b, iota, order_b, rec, rec64, rects, ntiles, counts, offsets;
-    DevBuf tkeys_a, tkeys_b, ranges, cub_temp, frame_rgb[2], frame_T[2];
+    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, rec64, rects, ntiles, counts, offsets;
+    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, frame_rgb[2], frame_T[2];
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;
+    Counters* h_ctr_init = nullptr;  // pinned initial counters block (err/kmin = ~0)
+    bool chunking = true;
     cudaEvent_t ev[8] = {};
     cudaEvent_t frame_done[2] = {};
     cudaEvent_t slot_free[2] = {};
@@ -180,10 +183,71 @@ int ceil_log2(uint64_t v) {
     return b;
 }
 
+enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
+
+// Depth chunking: the first chunk holds the
+// nearest ceil(N / kFirstChunkDiv) ranks; tiles whose pixels all terminate inside it
+// are finished and receive no keys from the second chunk.
+constexpr uint64_t kFirstChunkDiv = 16;
+constexpr uint64_t kMinChunkedN = 1 << 16;
+
+sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out) {
+    uint32_t* order = ctx->order.as<uint32_t>();
+    size_t temp = 0;
+    if (!wide) {
+        // K2: 32-bit keys (4 passes) + exact tie fix-up
+        launch_make_key32(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, ctx->key32_a.as<uint32_t>(), s);
+        ctx->own_launches += 1;
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, ctx->key32_a.as<uint32_t>(), ctx->key32_b.as<uint32_t>(),
+                                                 ctx->iota.as<uint32_t>(), order, static_cast<int>(n), 0, 32, s));
+        SGS_CUDA(ctx->cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp, ctx->key32_a.as<uint32_t>(),
+                                                 ctx->key32_b.as<uint32_t>(), ctx->iota.as<uint32_t>(), order,
+                                                 static_cast<int>(n), 0, 32, s));
+        ctx->lib_launches += 1 + 4;
+        launch_fix_ties(n, ctx->key32_b.as<uint32_t>(), ctx->keys_a.as<unsigned long long>(), order, ctx->d_ctr, s);
+        ctx->own_launches += 1;
+    } else {
+        // fallback: full 64-bit keys (8 passes), no fix-up needed
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, ctx->keys_a.as<unsigned long long>(),
+                                                 ctx->keys_b.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
+                                                 order, static_cast<int>(n), 0, 64, s));
+        SGS_CUDA(ctx->cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp, ctx->keys_a.as<unsigned long long>(),
+                                                 ctx->keys_b.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
+                                                 order, static_cast<int>(n), 0, 64, s));
+        ctx->lib_launches += 1 + 8;
+    }
+    SGS_CUDA(cudaGetLastError());
+    *order_out = order;
+    return SGS_OK;
+}
+
+// K3 for ranks [rb, re): counts -> exclusive scan -> P on the host (one sync).
+sgs_status count_and_scan(sgs_context* ctx, uint64_t rb, uint64_t re, const uint32_t* order, const uint8_t* done,
+                          int tiles_x, cudaStream_t s) {
+    const uint64_t m = re - rb;
+    launch_count_tiles(rb, re, order, ctx->ntiles.as<uint32_t>(), ctx->rects.as<int4>(), done, tiles_x,
+                       ctx->counts.as<unsigned long long>(), s);
+    ctx->own_launches += 1;
+    size_t temp = 0;
+    SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, ctx->counts.as<unsigned long long>(),
+                                           ctx->offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
+    SGS_CUDA(ctx->cub_temp.ensure(temp));
+    SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, ctx->counts.as<unsigned long long>(),
+                                           ctx->offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
+    ctx->lib_launches += 2;
+    SGS_CUDA(cudaMemcpyAsync(&ctx->d_ctr->tile_entries, ctx->offsets.as<unsigned long long>() + m,
+                             sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaStreamSynchronize(s));
+    return SGS_OK;
+}
+
 // One frame on ctx->stream. Outputs are device pointers (either may be null).
 sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
                      const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
-                     DebugSplat* d_debug, bool composite) {
+                     DebugSplat* d_debug, FrameMode mode) {
     if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
     sgs_status st = validate_camera(cam);
     if (st != SGS_OK) return st;
@@ -192,23 +256,26 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
     const CamParams cp = make_cam(cam);
     const CfgParams kp = make_cfg(cfg, cam);
     const uint64_t ntile = static_cast<uint64_t>(kp.tiles_x) * static_cast<uint64_t>(kp.tiles_y);
+    const uint64_t npx = static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height);
     const bool timing = stats && stats->want_timing;
+    const uint64_t n1 = std::max<uint64_t>(n, 1);
 
-    SGS_CUDA(ctx->keys_a.ensure(std::max<uint64_t>(n, 1) * 8));
-    SGS_CUDA(ctx->keys_b.ensure(std::max<uint64_t>(n, 1) * 8));
-    SGS_CUDA(ctx->iota.ensure(std::max<uint64_t>(n, 1) * 4));
-    SGS_CUDA(ctx->order_b.ensure(std::max<uint64_t>(n, 1) * 4));
-    SGS_CUDA(ctx->rec.ensure(std::max<uint64_t>(n, 1) * sizeof(SplatRec)));
-    SGS_CUDA(ctx->rec64.ensure(std::max<uint64_t>(n, 1) * sizeof(SplatRec64)));
-    SGS_CUDA(ctx->rects.ensure(std::max<uint64_t>(n, 1) * sizeof(int4)));
-    SGS_CUDA(ctx->ntiles.ensure(std::max<uint64_t>(n, 1) * 4));
+    SGS_CUDA(ctx->keys_a.ensure(n1 * 8));
+    SGS_CUDA(ctx->keys_b.ensure(n1 * 8));
+    SGS_CUDA(ctx->key32_a.ensure(n1 * 4));
+    SGS_CUDA(ctx->key32_b.ensure(n1 * 4));
+    SGS_CUDA(ctx->iota.ensure(n1 * 4));
+    SGS_CUDA(ctx->order.ensure(n1 * 4));
+    SGS_CUDA(ctx->rec.ensure(n1 * sizeof(SplatRec)));
+    SGS_CUDA(ctx->rec64.ensure(n1 * sizeof(SplatRec64)));
+    SGS_CUDA(ctx->rects.ensure(n1 * sizeof(int4)));
+    SGS_CUDA(ctx->ntiles.ensure(n1 * 4));
     SGS_CUDA(ctx->counts.ensure((n + 1) * 8));
     SGS_CUDA(ctx->offsets.ensure((n + 1) * 8));
     SGS_CUDA(ctx->ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
 
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[0], s));
-    SGS_CUDA(cudaMemsetAsync(ctx->d_ctr, 0, sizeof(Counters), s));
-    SGS_CUDA(cudaMemsetAsync(&ctx->d_ctr->err, 0xFF, sizeof(unsigned long long), s));
+    SGS_CUDA(cudaMemcpyAsync(ctx->d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
 
     // K1
     launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
@@ -217,104 +284,132 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
     SGS_CUDA(cudaGetLastError());
     if (n) ctx->own_launches += 1;
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[1], s));
+    if (mode == kProjectOnly) {
+        SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+        SGS_CUDA(cudaStreamSynchronize(s));
+        if (ctx->h_ctr->err != ~0ULL) return device_error(ctx->h_ctr->err, scene, cfg);
+        return SGS_OK;
+    }
 
-    // K2: stable radix sort of the FP64 depth keys; values = Gaussian index.
+    // K2
     const uint32_t* order = ctx->iota.as<uint32_t>();
     if (n > 1) {
-        cub::DoubleBuffer<unsigned long long> kb(ctx->keys_a.as<unsigned long long>(),
-                                                 ctx->keys_b.as<unsigned long long>());
-        cub::DoubleBuffer<uint32_t> vb(ctx->iota.as<uint32_t>(), ctx->order_b.as<uint32_t>());
-        size_t temp = 0;
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, kb, vb, static_cast<int>(n), 0, 64, s));
-        SGS_CUDA(ctx->cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp, kb, vb, static_cast<int>(n), 0,
-                                                 64, s));
-        order = vb.Current();
-        ctx->lib_launches += 1 + 8;  // onesweep: histogram + one pass per 8-bit digit
+        st = sort_depth(ctx, n, false, s, &order);
+        if (st != SGS_OK) return st;
     }
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[2], s));
 
-    // K3: per-rank tile counts -> exclusive scan (offsets[n] = P)
-    if (n > 0) {
-        launch_gather_counts(n, order, ctx->ntiles.as<uint32_t>(), ctx->counts.as<unsigned long long>(), s);
-        size_t temp = 0;
-        SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, ctx->counts.as<unsigned long long>(),
-                                               ctx->offsets.as<unsigned long long>(), static_cast<int>(n + 1), s));
-        SGS_CUDA(ctx->cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, ctx->counts.as<unsigned long long>(),
-                                               ctx->offsets.as<unsigned long long>(), static_cast<int>(n + 1), s));
-        ctx->own_launches += 1;
-        ctx->lib_launches += 2;  // decoupled look-back scan: init + scan
-        SGS_CUDA(cudaMemcpyAsync(&ctx->d_ctr->tile_entries, ctx->offsets.as<unsigned long long>() + n,
-                                 sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    // depth chunks over ranks (bounds known on the host: culled splats sort last and
+    // contribute no tiles, so rank bounds can be taken over N)
+    const bool multi = mode == kRender && ctx->chunking && n >= kMinChunkedN &&
+                       composite_pixel_chunks(cfg->tile_size) == 1;
+    uint64_t bounds[3] = {0, n, n};
+    int nchunks = 1;
+    if (multi) {
+        bounds[1] = (n + kFirstChunkDiv - 1) / kFirstChunkDiv;
+        nchunks = 2;
+        SGS_CUDA(ctx->tile_done.ensure(std::max<uint64_t>(ntile, 1)));
+        SGS_CUDA(ctx->pix_state.ensure(npx * sizeof(PixelState)));
+        SGS_CUDA(ctx->pix_walked.ensure(npx * sizeof(uint32_t)));
+        SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, ntile, s));
     }
-    SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-    SGS_CUDA(cudaStreamSynchronize(s));
-    if (ctx->h_ctr->err != ~0ULL) return device_error(ctx->h_ctr->err, scene, cfg);
-    const uint64_t v = ctx->h_ctr->visible;
-    const uint64_t p = ctx->h_ctr->tile_entries;
-    if (p > 0x7FFFFFFFULL) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^31 tile entries in one frame");
-
-    // K4 + K5 + K6
-    SGS_CUDA(ctx->tkeys_a.ensure(std::max<uint64_t>(p, 1) * 8));
-    SGS_CUDA(ctx->tkeys_b.ensure(std::max<uint64_t>(p, 1) * 8));
-    launch_emit_tile_keys(v, order, ctx->ntiles.as<uint32_t>(), ctx->rects.as<int4>(),
-                          ctx->offsets.as<unsigned long long>(), kp.tiles_x,
-                          ctx->tkeys_a.as<unsigned long long>(), s);
-    SGS_CUDA(cudaGetLastError());
-    if (v) ctx->own_launches += 1;
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[3], s));
-    const unsigned long long* tkeys = ctx->tkeys_a.as<unsigned long long>();
-    if (p > 1 && ntile > 1) {
-        cub::DoubleBuffer<unsigned long long> tb(ctx->tkeys_a.as<unsigned long long>(),
-                                                 ctx->tkeys_b.as<unsigned long long>());
-        const int end_bit = 32 + std::max(1, ceil_log2(ntile));
-        size_t temp = 0;
-        SGS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
-        SGS_CUDA(ctx->cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_temp.ptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
-        tkeys = tb.Current();
-        ctx->lib_launches += 1 + (end_bit - 32 + 7) / 8;
-    }
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[4], s));
-    SGS_CUDA(cudaMemsetAsync(ctx->ranges.ptr, 0, ntile * sizeof(uint2), s));
-    launch_tile_ranges(p, tkeys, ctx->ranges.as<uint2>(), s);
-    SGS_CUDA(cudaGetLastError());
-    if (p) ctx->own_launches += 1;
-
-    ctx->last_order = order;
-    ctx->last_tile_keys = tkeys;
-    ctx->last_v = v;
-    ctx->last_p = p;
-
-    // K7
-    if (composite) {
-        const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
-                                      static_cast<float>(scene->meta.background[1]),
-                                      static_cast<float>(scene->meta.background[2]));
-        launch_composite(cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
-                         ctx->rec64.as<SplatRec64>(), bg, d_rgb, d_T, ctx->d_ctr, stats != nullptr, s);
+    const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
+                                  static_cast<float>(scene->meta.background[1]),
+                                  static_cast<float>(scene->meta.background[2]));
+    uint64_t v = 0, p_total = 0;
+    float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        const uint64_t rb = bounds[c], re = bounds[c + 1];
+        const uint8_t* done = c > 0 ? ctx->tile_done.as<uint8_t>() : nullptr;
+        if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[3], s));
+        st = count_and_scan(ctx, rb, re, order, done, kp.tiles_x, s);
+        if (st != SGS_OK) return st;
+        if (c == 0) {
+            if (ctx->h_ctr->err != ~0ULL) return device_error(ctx->h_ctr->err, scene, cfg);
+            if (ctx->h_ctr->tie_overflow) {
+                // a long run of equal 32-bit depth keys: redo K2 with 64-bit keys
+                st = sort_depth(ctx, n, true, s, &order);
+                if (st != SGS_OK) return st;
+                st = count_and_scan(ctx, rb, re, order, done, kp.tiles_x, s);
+                if (st != SGS_OK) return st;
+            }
+            v = ctx->h_ctr->visible;
+        }
+        const uint64_t p = ctx->h_ctr->tile_entries;
+        if (p > 0x7FFFFFFFULL) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^31 tile entries in one chunk");
+        p_total += p;
+        // K4
+        SGS_CUDA(ctx->tkeys_a.ensure(std::max<uint64_t>(p, 1) * 8));
+        SGS_CUDA(ctx->tkeys_b.ensure(std::max<uint64_t>(p, 1) * 8));
+        launch_emit_tile_keys(rb, re, order, ctx->ntiles.as<uint32_t>(), ctx->rects.as<int4>(), done,
+                              ctx->offsets.as<unsigned long long>(), kp.tiles_x,
+                              ctx->tkeys_a.as<unsigned long long>(), s);
         SGS_CUDA(cudaGetLastError());
-        ctx->own_launches += 1;
+        if (re > rb) ctx->own_launches += 1;
+        if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[4], s));
+        // K5
+        const unsigned long long* tkeys = ctx->tkeys_a.as<unsigned long long>();
+        if (p > 1 && ntile > 1) {
+            cub::DoubleBuffer<unsigned long long> tb(ctx->tkeys_a.as<unsigned long long>(),
+                                                     ctx->tkeys_b.as<unsigned long long>());
+            const int end_bit = 32 + std::max(1, ceil_log2(ntile));
+            size_t temp = 0;
+            SGS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
+            SGS_CUDA(ctx->cub_temp.ensure(temp));
+            SGS_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_temp.ptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
+            tkeys = tb.Current();
+            ctx->lib_launches += 1 + (end_bit - 32 + 7) / 8;
+        }
+        // K6
+        SGS_CUDA(cudaMemsetAsync(ctx->ranges.ptr, 0, ntile * sizeof(uint2), s));
+        launch_tile_ranges(p, tkeys, ctx->ranges.as<uint2>(), s);
+        SGS_CUDA(cudaGetLastError());
+        if (p) ctx->own_launches += 1;
+        if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[5], s));
+        ctx->last_order = order;
+        ctx->last_tile_keys = tkeys;
+        ctx->last_v = v;
+        ctx->last_p = p;
+        // K7
+        if (mode == kRender) {
+            launch_composite(cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
+                             ctx->rec64.as<SplatRec64>(), bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(),
+                             ctx->pix_walked.as<uint32_t>(), ctx->tile_done.as<uint8_t>(), c == 0,
+                             c == nchunks - 1, ctx->d_ctr, stats != nullptr, s);
+            SGS_CUDA(cudaGetLastError());
+            ctx->own_launches += 1;
+        }
+        if (timing) {
+            SGS_CUDA(cudaEventRecord(ctx->ev[6], s));
+            SGS_CUDA(cudaEventSynchronize(ctx->ev[6]));
+            float a = 0, b = 0, d = 0;
+            SGS_CUDA(cudaEventElapsedTime(&a, ctx->ev[3], ctx->ev[4]));
+            SGS_CUDA(cudaEventElapsedTime(&b, ctx->ev[4], ctx->ev[5]));
+            SGS_CUDA(cudaEventElapsedTime(&d, ctx->ev[5], ctx->ev[6]));
+            ms_bin += a;
+            ms_tsort += b;
+            ms_comp += d;
+        }
     }
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[5], s));
+    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[7], s));
+    ctx->last_p = p_total;
     if (stats) {
         SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
         SGS_CUDA(cudaStreamSynchronize(s));
         stats->visible += v;
-        stats->tile_entries += p;
+        stats->tile_entries += p_total;
         stats->block_entries += ctx->h_ctr->block_entries;
         stats->guard_hits += ctx->h_ctr->guard_hits;
         if (timing) {
-            float ms[5];
-            for (int k = 0; k < 5; ++k) SGS_CUDA(cudaEventElapsedTime(&ms[k], ctx->ev[k], ctx->ev[k + 1]));
-            stats->ms_preprocess += ms[0];
-            stats->ms_depth_sort += ms[1];
-            stats->ms_binning += ms[2];
-            stats->ms_tile_sort += ms[3];
-            stats->ms_composite += ms[4];
-            float total = 0;
-            SGS_CUDA(cudaEventElapsedTime(&total, ctx->ev[0], ctx->ev[5]));
+            float k1 = 0, k2 = 0, total = 0;
+            SGS_CUDA(cudaEventElapsedTime(&k1, ctx->ev[0], ctx->ev[1]));
+            SGS_CUDA(cudaEventElapsedTime(&k2, ctx->ev[1], ctx->ev[2]));
+            SGS_CUDA(cudaEventElapsedTime(&total, ctx->ev[0], ctx->ev[7]));
+            stats->ms_preprocess += k1;
+            stats->ms_depth_sort += k2;
+            stats->ms_binning += ms_bin;
+            stats->ms_tile_sort += ms_tsort;
+            stats->ms_composite += ms_comp;
             stats->ms_total += total;
         }
     }
@@ -498,6 +593,11 @@ sgs_status sgs_create(int device, sgs_context** out) {
     ctx->stream = ctx->own_stream;
     SGS_CUDA(cudaMalloc(&ctx->d_ctr, sizeof(Counters)));
     SGS_CUDA(cudaMallocHost(&ctx->h_ctr, sizeof(Counters)));
+    SGS_CUDA(cudaMallocHost(&ctx->h_ctr_init, sizeof(Counters)));
+    std::memset(ctx->h_ctr_init, 0, sizeof(Counters));
+    ctx->h_ctr_init->err = ~0ULL;
+    ctx->h_ctr_init->kmin = ~0ULL;
+    if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     for (auto& ev : ctx->ev) SGS_CUDA(cudaEventCreate(&ev));
     for (int k = 0; k < 2; ++k) {
         SGS_CUDA(cudaEventCreateWithFlags(&ctx->frame_done[k], cudaEventDisableTiming));
@@ -512,13 +612,15 @@ void sgs_destroy(sgs_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
-    for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->iota, &ctx->order_b, &ctx->rec, &ctx->rec64,
-                      &ctx->rects, &ctx->ntiles, &ctx->counts, &ctx->offsets, &ctx->tkeys_a, &ctx->tkeys_b,
-                      &ctx->ranges, &ctx->cub_temp, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
+    for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->key32_a, &ctx->key32_b, &ctx->iota, &ctx->order,
+                      &ctx->rec, &ctx->rec64, &ctx->rects, &ctx->ntiles, &ctx->counts, &ctx->offsets,
+                      &ctx->tkeys_a, &ctx->tkeys_b, &ctx->ranges, &ctx->tile_done, &ctx->pix_state,
+                      &ctx->pix_walked, &ctx->cub_temp, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
                       &ctx->frame_T[0], &ctx->frame_T[1]})
         b->release();
     if (ctx->d_ctr) cudaFree(ctx->d_ctr);
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
     for (int k = 0; k < 2; ++k) {
         cudaEventDestroy(ctx->frame_done[k]);
@@ -664,7 +766,7 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
     if (out_memory == SGS_DEVICE) {
         for (int i = 0; i < n; ++i) {
             sgs_status st = run_frame(ctx, scene, &cams[i], cfg, rgb ? rgb + i * npx * 3 : nullptr,
-                                      T ? T + i * npx : nullptr, stats, nullptr, true);
+                                      T ? T + i * npx : nullptr, stats, nullptr, kRender);
             if (st != SGS_OK) return st;
         }
         SGS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -681,7 +783,7 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
         const int k = i & 1;
         SGS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_free[k], 0));
         sgs_status st = run_frame(ctx, scene, &cams[i], cfg, rgb ? ctx->frame_rgb[k].as<float>() : nullptr,
-                                  T ? ctx->frame_T[k].as<float>() : nullptr, stats, nullptr, true);
+                                  T ? ctx->frame_T[k].as<float>() : nullptr, stats, nullptr, kRender);
         if (st != SGS_OK) {
             cudaStreamSynchronize(ctx->copy_stream);
             return st;
@@ -710,7 +812,7 @@ sgs_status sgs_project(sgs_context* ctx, const sgs_scene* scene, const sgs_camer
     const uint64_t n = scene->meta.count;
     DebugSplat* d_dbg = nullptr;
     SGS_CUDA(cudaMalloc(&d_dbg, std::max<uint64_t>(n, 1) * sizeof(DebugSplat)));
-    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, d_dbg, false);
+    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, d_dbg, kProjectOnly);
     if (st == SGS_OK && n) {
         cudaError_t e = cudaMemcpy(out, d_dbg, n * sizeof(DebugSplat), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
@@ -727,7 +829,7 @@ sgs_status sgs_debug_tile_grid(sgs_context* ctx, const sgs_scene* scene, const s
         return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
     std::lock_guard<std::mutex> lock(ctx->mu);
     SGS_CUDA(cudaSetDevice(ctx->device));
-    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, nullptr, false);
+    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, nullptr, kTileGrid);
     if (st != SGS_OK) return st;
     SGS_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint64_t v = ctx->last_v, p = ctx->last_p;

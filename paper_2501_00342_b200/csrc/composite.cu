@@ -48,8 +48,9 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
     const CamParams cam, const CfgParams cfg, int nchunks, int block_px,
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
     const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64, float3 bg,
-    float* __restrict__ out_rgb, float* __restrict__ out_T, Counters* __restrict__ ctr,
-    int want_stats) {
+    float* __restrict__ out_rgb, float* __restrict__ out_T, PixelState* __restrict__ state,
+    uint32_t* __restrict__ processed_io, uint8_t* __restrict__ tile_done, int first, int last,
+    Counters* __restrict__ ctr, int want_stats) {
     __shared__ float4 sA[kBlock];  // (lmx, lmy, ca, 2cb)
     __shared__ float4 sB[kBlock];  // (cc, op, guard, gaussian index bits)
     __shared__ float4 sC[kBlock];  // (r, g, b, -)
@@ -65,15 +66,29 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
     const int px = px0 + lx, py = py0 + ly;
     const bool valid = threadIdx.x < block_px && p < ts * ts && px < cam.W && py < cam.H;
 
+    // Tiles that terminated in an earlier depth chunk already wrote their output.
+    if (!first && tile_done[tile]) return;
     const uint2 range = ranges[tile];
     const uint32_t start = range.x, end = range.y;
+    if (!first && !last && start == end) return;  // nothing new for this tile
 
     // Local pixel centre relative to the tile origin: exact in FP32.
     const float fcx = static_cast<float>(lx) + 0.5f, fcy = static_cast<float>(ly) + 0.5f;
     const float stop = cfg.early_stop;
+    const size_t pix = valid ? static_cast<size_t>(py) * cam.W + px : 0;
     float T = 1.0f, ar = 0.f, ag = 0.f, ab = 0.f;
-    bool done = !valid;
-    uint32_t processed = end - start;
+    uint32_t walked = 0;  // list entries walked in earlier chunks
+    if (!first && valid) {
+        const PixelState ps = state[pix];
+        ar = ps.r;
+        ag = ps.g;
+        ab = ps.b;
+        T = ps.T;
+        walked = processed_io[pix];
+    }
+    // a pixel continues while T has not dropped below the threshold (raster.cpp:177)
+    bool done = !valid || T < stop;
+    uint32_t processed = done ? 0u : end - start;  // entries walked in this chunk
     uint32_t guard_hits = 0;
 
     for (uint32_t base = start; base < end; base += blockDim.x) {
@@ -128,19 +143,27 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
         __syncthreads();
     }
 
+    const bool all_done = __syncthreads_and(done) != 0;
+    const bool finalize = last || all_done;
     if (valid) {
-        const size_t pix = static_cast<size_t>(py) * cam.W + px;
-        if (out_rgb) {
-            out_rgb[pix * 3 + 0] = ar + T * bg.x;
-            out_rgb[pix * 3 + 1] = ag + T * bg.y;
-            out_rgb[pix * 3 + 2] = ab + T * bg.z;
+        if (finalize) {
+            if (out_rgb) {
+                out_rgb[pix * 3 + 0] = ar + T * bg.x;
+                out_rgb[pix * 3 + 1] = ag + T * bg.y;
+                out_rgb[pix * 3 + 2] = ab + T * bg.z;
+            }
+            if (out_T) out_T[pix] = T;
+        } else {
+            state[pix] = PixelState{ar, ag, ab, T};
+            processed_io[pix] = walked + processed;
         }
-        if (out_T) out_T[pix] = T;
     }
+    if (!last && all_done && threadIdx.x == 0) tile_done[tile] = 1;
     if (want_stats) {
-        // E_t (block-terminated entries) = max over the tile's pixels of the entries
-        // each pixel walked; guard hits summed.
-        unsigned long long e = valid ? processed : 0ULL;
+        // E_t (block-terminated entries) = max over the tile's pixels of the entries of
+        // its full list each pixel walked (counted when the tile finalises); guard hits
+        // summed over chunks.
+        unsigned long long e = (finalize && valid) ? walked + processed : 0ULL;
         unsigned long long h = guard_hits;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -159,7 +182,7 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
                 em = max(em, s_red[0][w]);
                 hs += s_red[1][w];
             }
-            // chunks of one tile each report their own max; for 16x16 tiles nchunks == 1
+            // pixel chunks of one tile (tile_size > 16) each report their own max
             if (em) atomicAdd(&ctr->block_entries, em);
             if (hs) atomicAdd(&ctr->guard_hits, hs);
         }
@@ -168,19 +191,26 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
 
 }  // namespace
 
+int composite_pixel_chunks(int ts) {
+    const long long tile_px = static_cast<long long>(ts) * ts;
+    const int block_px = static_cast<int>(tile_px < kBlock ? ((tile_px + 31) / 32) * 32 : kBlock);
+    return static_cast<int>((tile_px + block_px - 1) / block_px);
+}
+
 void launch_composite(const CamParams& cam, const CfgParams& cfg, const uint2* ranges,
                       const unsigned long long* keys, const SplatRec* rec,
                       const SplatRec64* rec64, float3 bg, float* rgb, float* T,
-                      Counters* counters, bool want_stats, cudaStream_t stream) {
+                      PixelState* state, uint32_t* processed, uint8_t* tile_done, bool first,
+                      bool last, Counters* counters, bool want_stats, cudaStream_t stream) {
     const int ts = cfg.tile_size;
     const long long tile_px = static_cast<long long>(ts) * ts;
     const int block_px = static_cast<int>(tile_px < kBlock ? ((tile_px + 31) / 32) * 32 : kBlock);
-    const int nchunks = static_cast<int>((tile_px + block_px - 1) / block_px);
+    const int nchunks = composite_pixel_chunks(ts);
     const long long ntiles = static_cast<long long>(cfg.tiles_x) * cfg.tiles_y;
     const long long grid = ntiles * nchunks;
     composite_kernel<<<static_cast<unsigned>(grid), block_px, 0, stream>>>(
-        cam, cfg, nchunks, block_px, ranges, keys, rec, rec64, bg, rgb, T, counters,
-        want_stats ? 1 : 0);
+        cam, cfg, nchunks, block_px, ranges, keys, rec, rec64, bg, rgb, T, state, processed,
+        tile_done, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0);
 }
 
 }  // namespace sgs

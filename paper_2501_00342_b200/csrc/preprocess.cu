@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     uint32_t* __restrict__ ntiles, Counters* __restrict__ ctr, DebugSplat* __restrict__ debug) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool visible = false;
+    unsigned long long vkey = ~0ULL;
     if (i < sp.n) {
         iota[i] = static_cast<uint32_t>(i);
         unsigned long long key = ~0ULL;
@@ -407,12 +408,25 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
             }
         } while (false);
         depth_keys[i] = key;
+        vkey = key;
         ntiles[i] = count;
         if (debug) debug[i] = dbg;
     }
-    // visible count: one atomic per warp
+    // visible count and depth-key range: one atomic each per warp
     const unsigned vote = __ballot_sync(0xffffffffu, visible);
-    if ((threadIdx.x & 31) == 0 && vote) atomicAdd(&ctr->visible, static_cast<unsigned long long>(__popc(vote)));
+    if (vote) {
+        unsigned long long kmin = visible ? vkey : ~0ULL, kmax = visible ? vkey : 0ULL;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&ctr->visible, static_cast<unsigned long long>(__popc(vote)));
+            atomicMin(&ctr->kmin, kmin);
+            atomicMax(&ctr->kmax, kmax);
+        }
+    }
 }
 
 template <bool F64>

@@ -101,6 +101,17 @@ struct Counters {
     unsigned long long block_entries;
     unsigned long long guard_hits;
     unsigned long long tile_entries;
+    unsigned long long kmin;  // min / max orderable depth key of the visible splats
+    unsigned long long kmax;
+    unsigned long long tie_runs;      // 32-bit depth-key collisions re-sorted by K2b
+    unsigned long long tie_overflow;  // runs too long for K2b (host falls back to 64-bit)
+    unsigned long long pad[7];
+};
+static_assert(sizeof(Counters) == 128, "counters block");
+
+// Per-pixel compositing state carried between depth chunks (K7).
+struct __align__(16) PixelState {
+    float r, g, b, T;
 };
 
 // Number of float4 colour planes for (kind, stored degree).
@@ -120,16 +131,27 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, uint32_t* iota, SplatRec* rec,
                        SplatRec64* rec64, int4* rects, uint32_t* ntiles, Counters* counters,
                        DebugSplat* debug, cudaStream_t stream);
-void launch_gather_counts(uint64_t n, const uint32_t* order, const uint32_t* ntiles,
-                          unsigned long long* counts, cudaStream_t stream);
-void launch_emit_tile_keys(uint64_t n_visible, const uint32_t* order, const uint32_t* ntiles,
-                           const int4* rects, const unsigned long long* offsets, int tiles_x,
-                           unsigned long long* keys, cudaStream_t stream);
+void launch_make_key32(uint64_t n, const unsigned long long* key64, const Counters* ctr,
+                       uint32_t* key32, cudaStream_t stream);
+void launch_fix_ties(uint64_t n, const uint32_t* key32, const unsigned long long* key64,
+                     uint32_t* order, Counters* ctr, cudaStream_t stream);
+// Tile counts for ranks [rb, re) skipping tiles already terminated (done may be null);
+// counts has re-rb+1 entries (the last is 0 so an exclusive scan yields the total).
+void launch_count_tiles(uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* ntiles,
+                        const int4* rects, const uint8_t* done, int tiles_x,
+                        unsigned long long* counts, cudaStream_t stream);
+void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* ntiles,
+                           const int4* rects, const uint8_t* done, const unsigned long long* offsets,
+                           int tiles_x, unsigned long long* keys, cudaStream_t stream);
 void launch_tile_ranges(uint64_t p, const unsigned long long* keys, uint2* ranges,
                         cudaStream_t stream);
+// K7 over one depth chunk. first/last select state init / final output; tile_done and
+// state may be null when the frame is a single chunk.
 void launch_composite(const CamParams& cam, const CfgParams& cfg, const uint2* ranges,
                       const unsigned long long* keys, const SplatRec* rec,
                       const SplatRec64* rec64, float3 bg, float* rgb, float* T,
-                      Counters* counters, bool want_stats, cudaStream_t stream);
+                      PixelState* state, uint32_t* processed, uint8_t* tile_done, bool first,
+                      bool last, Counters* counters, bool want_stats, cudaStream_t stream);
+int composite_pixel_chunks(int tile_size);
 
 }  // namespace sgs

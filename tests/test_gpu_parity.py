@@ -238,3 +238,27 @@ def test_full_size_vs_reference(renderer, ref, cfgname):
         check_image(rgb, T, ref_rgb, ref_T)
     finally:
         ds.free()
+
+
+def test_depth_chunking_is_bitwise_neutral():
+    """Termination-aware binning (two depth chunks, finished tiles skip the second)
+    must not change a single bit of the image, the transmittance or E_t."""
+    scene = sg.synth_scene(200_000, "mixed", 77, log_scale_range=(-5.0, -3.5))
+    cams = sg.orbit_cameras(3, 480, 270, 4.0, 324.0)
+    os.environ["SGS_DEPTH_CHUNKING"] = "0"
+    try:
+        plain = sg.Renderer(0)
+    finally:
+        os.environ.pop("SGS_DEPTH_CHUNKING")
+    chunked = sg.Renderer(0)
+    a_ds, b_ds = plain.upload(scene), chunked.upload(scene)
+    try:
+        for cam in cams:
+            a = plain.render(a_ds, cam, degree_override=1, stats=True)
+            b = chunked.render(b_ds, cam, degree_override=1, stats=True)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            assert a[2].block_entries == b[2].block_entries
+            assert b[2].tile_entries < a[2].tile_entries  # finished tiles skipped
+    finally:
+        a_ds.free()
+        b_ds.free()
