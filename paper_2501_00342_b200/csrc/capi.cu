@@ -92,12 +92,16 @@ struct sgs_context {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
     std::mutex mu;
-    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, rec64, rects, ntiles, counts, offsets;
+    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, rects, ntiles, counts, offsets;
+    uint64_t iota_n = 0;
     DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, frame_rgb[2], frame_T[2];
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;
     Counters* h_ctr_init = nullptr;  // pinned initial counters block (err/kmin = ~0)
+    FrameConsts* d_consts = nullptr;  // per-frame scene planes + camera for K7's FP64 path
+    FrameConsts* h_consts = nullptr;  // pinned staging copy
     bool chunking = true;
+    std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t ev[8] = {};
     cudaEvent_t frame_done[2] = {};
     cudaEvent_t slot_free[2] = {};
@@ -188,7 +192,6 @@ enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
 // Depth chunking: the first chunk holds the
 // nearest ceil(N / kFirstChunkDiv) ranks; tiles whose pixels all terminate inside it
 // are finished and receive no keys from the second chunk.
-constexpr uint64_t kFirstChunkDiv = 16;
 constexpr uint64_t kMinChunkedN = 1 << 16;
 
 sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out) {
@@ -264,10 +267,10 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
     SGS_CUDA(ctx->keys_b.ensure(n1 * 8));
     SGS_CUDA(ctx->key32_a.ensure(n1 * 4));
     SGS_CUDA(ctx->key32_b.ensure(n1 * 4));
+    if (ctx->iota.bytes < n1 * 4) ctx->iota_n = 0;
     SGS_CUDA(ctx->iota.ensure(n1 * 4));
     SGS_CUDA(ctx->order.ensure(n1 * 4));
     SGS_CUDA(ctx->rec.ensure(n1 * sizeof(SplatRec)));
-    SGS_CUDA(ctx->rec64.ensure(n1 * sizeof(SplatRec64)));
     SGS_CUDA(ctx->rects.ensure(n1 * sizeof(int4)));
     SGS_CUDA(ctx->ntiles.ensure(n1 * 4));
     SGS_CUDA(ctx->counts.ensure((n + 1) * 8));
@@ -276,11 +279,22 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
 
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[0], s));
     SGS_CUDA(cudaMemcpyAsync(ctx->d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
+    if (mode == kRender) {
+        // the pinned staging block is reused every frame: wait until the previous
+        // frame's copy has been consumed (frames are sequential on the stream anyway)
+        SGS_CUDA(cudaStreamSynchronize(s));
+        ctx->h_consts->sp = scene->planes;
+        ctx->h_consts->cam = cp;
+        SGS_CUDA(cudaMemcpyAsync(ctx->d_consts, ctx->h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
+    }
 
     // K1
-    launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
-                      ctx->rec.as<SplatRec>(), ctx->rec64.as<SplatRec64>(), ctx->rects.as<int4>(),
-                      ctx->ntiles.as<uint32_t>(), ctx->d_ctr, d_debug, s);
+    if (ctx->iota_n < n) {  // identity values for the depth sort (kept across frames)
+        launch_iota(n, ctx->iota.as<uint32_t>(), s);
+        ctx->iota_n = n;
+    }
+    launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->rec.as<SplatRec>(),
+                      ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->d_ctr, d_debug, s);
     SGS_CUDA(cudaGetLastError());
     if (n) ctx->own_launches += 1;
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[1], s));
@@ -303,16 +317,19 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
     // contribute no tiles, so rank bounds can be taken over N)
     const bool multi = mode == kRender && ctx->chunking && n >= kMinChunkedN &&
                        composite_pixel_chunks(cfg->tile_size) == 1;
-    uint64_t bounds[3] = {0, n, n};
-    int nchunks = 1;
+    std::vector<uint64_t> bounds{0};
     if (multi) {
-        bounds[1] = (n + kFirstChunkDiv - 1) / kFirstChunkDiv;
-        nchunks = 2;
+        for (uint64_t div : ctx->chunk_divs) {
+            const uint64_t b = (n + div - 1) / div;
+            if (b > bounds.back() && b < n) bounds.push_back(b);
+        }
         SGS_CUDA(ctx->tile_done.ensure(std::max<uint64_t>(ntile, 1)));
         SGS_CUDA(ctx->pix_state.ensure(npx * sizeof(PixelState)));
         SGS_CUDA(ctx->pix_walked.ensure(npx * sizeof(uint32_t)));
         SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, ntile, s));
     }
+    bounds.push_back(n);
+    const int nchunks = static_cast<int>(bounds.size()) - 1;
     const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
                                   static_cast<float>(scene->meta.background[1]),
                                   static_cast<float>(scene->meta.background[2]));
@@ -372,8 +389,8 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
         ctx->last_p = p;
         // K7
         if (mode == kRender) {
-            launch_composite(cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
-                             ctx->rec64.as<SplatRec64>(), bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(),
+            launch_composite(ctx->d_consts, cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
+                             bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(),
                              ctx->pix_walked.as<uint32_t>(), ctx->tile_done.as<uint8_t>(), c == 0,
                              c == nchunks - 1, ctx->d_ctr, stats != nullptr, s);
             SGS_CUDA(cudaGetLastError());
@@ -594,10 +611,22 @@ sgs_status sgs_create(int device, sgs_context** out) {
     SGS_CUDA(cudaMalloc(&ctx->d_ctr, sizeof(Counters)));
     SGS_CUDA(cudaMallocHost(&ctx->h_ctr, sizeof(Counters)));
     SGS_CUDA(cudaMallocHost(&ctx->h_ctr_init, sizeof(Counters)));
+    SGS_CUDA(cudaMalloc(&ctx->d_consts, sizeof(FrameConsts)));
+    SGS_CUDA(cudaMallocHost(&ctx->h_consts, sizeof(FrameConsts)));
     std::memset(ctx->h_ctr_init, 0, sizeof(Counters));
     ctx->h_ctr_init->err = ~0ULL;
     ctx->h_ctr_init->kmin = ~0ULL;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
+        ctx->chunk_divs.clear();
+        for (const char* q = e; *q;) {
+            char* endp = nullptr;
+            const long v = std::strtol(q, &endp, 10);
+            if (endp == q) break;
+            if (v > 1) ctx->chunk_divs.push_back(static_cast<uint64_t>(v));
+            q = *endp ? endp + 1 : endp;
+        }
+    }
     for (auto& ev : ctx->ev) SGS_CUDA(cudaEventCreate(&ev));
     for (int k = 0; k < 2; ++k) {
         SGS_CUDA(cudaEventCreateWithFlags(&ctx->frame_done[k], cudaEventDisableTiming));
@@ -613,7 +642,7 @@ void sgs_destroy(sgs_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->key32_a, &ctx->key32_b, &ctx->iota, &ctx->order,
-                      &ctx->rec, &ctx->rec64, &ctx->rects, &ctx->ntiles, &ctx->counts, &ctx->offsets,
+                      &ctx->rec, &ctx->rects, &ctx->ntiles, &ctx->counts, &ctx->offsets,
                       &ctx->tkeys_a, &ctx->tkeys_b, &ctx->ranges, &ctx->tile_done, &ctx->pix_state,
                       &ctx->pix_walked, &ctx->cub_temp, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
                       &ctx->frame_T[0], &ctx->frame_T[1]})
@@ -621,6 +650,8 @@ void sgs_destroy(sgs_context* ctx) {
     if (ctx->d_ctr) cudaFree(ctx->d_ctr);
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
+    if (ctx->d_consts) cudaFree(ctx->d_consts);
+    if (ctx->h_consts) cudaFreeHost(ctx->h_consts);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
     for (int k = 0; k < 2; ++k) {
         cudaEventDestroy(ctx->frame_done[k]);

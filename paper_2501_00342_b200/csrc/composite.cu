@@ -1,168 +1,299 @@
 // composite.cu -- K7: per-tile front-to-back alpha compositing.
 //
 // Replaces the per-pixel loop of render (proj/src/raster.cpp:155-186) with the
-// reference's exact rules (Appendix A of SURVEY.md): pixel centre (px+.5, py+.5),
+// reference's exact rules: pixel centre (px+.5, py+.5),
 // m2 = c0 dx^2 + 2 c1 dx dy + c2 dy^2, skip m2 > 9, alpha = min(op e^{-m2/2}, 0.999),
 // skip alpha < 1/255, accumulate c * alpha * T, T *= 1 - alpha, stop after the
 // splat that pushed T below the threshold, then add T * background.
 //
-// One CTA per (tile, 256-pixel chunk); for the default 16x16 tile that is one CTA
-// per tile, one thread per pixel. The tile's list is streamed through shared
-// memory in batches of blockDim records (one coalesced 48-B record gather per
-// thread), every thread then walks the batch from shared memory (broadcast LDS.128,
-// no bank conflicts). __syncthreads_count ends the tile once every pixel is done.
+// Layout. One CTA of 256 threads per (tile, 256-pixel chunk) -- one CTA per 16x16
+// tile, one pixel per thread, warp w owning the 16x2 strip of rows 2w, 2w+1. The
+// tile's list streams through shared memory in batches of 256 64-B records (one
+// coalesced gather per thread). Each warp compacts the batch to the records whose
+// support box reaches its live pixels (ballot + popc).
 //
-// FP32 fast path with an FP64 guard band: the reference decides m2 > 9 and
-// alpha < 1/255 in FP64. Here m2 is evaluated in FP32 from tile-local offsets
-// (the FP64 mean is localised once per batch, so dx carries a single rounding), and
-// a pair whose FP32 m2 lies within the splat's error bound `guard` of 9 -- or whose
-// alpha lies within the matching relative bound of 1/255 -- is recomputed in FP64
-// exactly as the reference does (no FMA contraction). Every skip decision therefore
-// matches the FP64 reference; only the blended values carry FP32 rounding.
-#include "sgs_internal.h"
+// Latency. A pixel's walk is inherently sequential, so long lists (tiles on the
+// silhouette whose pixels never saturate) sit on the critical path. The walk goes
+// in groups of kGroup records: the m2 / alpha of the group are computed
+// independently (ILP), then a branch-free blend chain applies them in order; a
+// skipped pair, or any pair after the pixel terminated, blends with alpha = 0,
+// which leaves T and the colour bit-identical. __syncthreads_count ends the tile
+// once every pixel has terminated.
+//
+// Exactness. The two skip tests are one per-splat cutoff: alpha < 1/255 <=>
+// m2 > 2 ln(255 op), so "skip" <=> m2 > cut = min(9, 2 ln(255 op)) (FP64 in K1).
+// m2 is evaluated in FP32 from tile-local offsets (the FP64 mean is localised once
+// per batch, so dx carries a single rounding) and compared with cut +- guard,
+// guard bounding the FP32 error. A group containing a
+// pair inside the band is walked one record at a time, that pair decided in FP64
+// exactly as the reference does from the FP64 projection re-derived by
+// projection.cuh. Every skip decision therefore matches the reference; only the
+// blended values carry FP32 rounding.
+#include "projection.cuh"
 
 namespace sgs {
 namespace {
 
-constexpr int kBlock = 256;
+constexpr int kThreads = 256;
+constexpr int kBatch = 256;
+constexpr int kGroup = 8;
 
-// The reference's FP64 decisions for one (pixel, splat) pair (raster.cpp:165-176).
-__device__ __noinline__ bool exact_alpha(const SplatRec* __restrict__ rec,
-                                         const SplatRec64* __restrict__ rec64, uint32_t g,
-                                         double cx, double cy, float* alpha_out) {
-    const double mx = rec[g].mx, my = rec[g].my;
-    const SplatRec64 r = rec64[g];
-    const double dx = __dsub_rn(cx, mx), dy = __dsub_rn(cy, my);
-    const double m2 = __dadd_rn(
-        __dadd_rn(__dmul_rn(__dmul_rn(r.ca, dx), dx), __dmul_rn(__dmul_rn(__dmul_rn(2.0, r.cb), dx), dy)),
-        __dmul_rn(__dmul_rn(r.cc, dy), dy));
+// The reference's FP64 decision for one (pixel, splat) pair (raster.cpp:165-176).
+__device__ __noinline__ bool exact_alpha(const FrameConsts* __restrict__ fc, uint32_t g, int px, int py,
+                                         float* alpha_out) {
+    const double cx = px + 0.5, cy = py + 0.5;  // raster.cpp:165
+    Geo geo;
+    ProjGeo pg;
+    if (fc->sp.geometry_f64)
+        project_geometry<true>(fc->sp, fc->cam, g, geo, pg);
+    else
+        project_geometry<false>(fc->sp, fc->cam, g, geo, pg);
+    exact_conic_opacity(geo, pg);
+    const double dx = dsub(cx, pg.mx), dy = dsub(cy, pg.my);
+    const double m2 = dadd(dadd(dmul(dmul(pg.cona, dx), dx), dmul(dmul(dmul(2.0, pg.conb), dx), dy)),
+                           dmul(dmul(pg.conc, dy), dy));
     if (m2 > kSupportMahalanobisSq) return false;
-    double alpha = __dmul_rn(r.op, exp(__dmul_rn(-0.5, m2)));
+    double alpha = dmul(pg.opacity, exp(dmul(-0.5, m2)));
     alpha = alpha < kAlphaClamp ? alpha : kAlphaClamp;  // std::min(a, 0.999)
     if (alpha < kAlphaMin) return false;
     *alpha_out = static_cast<float>(alpha);
     return true;
 }
 
-__global__ void __launch_bounds__(kBlock) composite_kernel(
-    const CamParams cam, const CfgParams cfg, int nchunks, int block_px,
+struct Pixel {
+    float T, r, g, b;
+    int term;  // position in the batch's compacted walk where T fell below stop
+    bool done;
+};
+
+// One blend step (raster.cpp:177-180). alpha == 0 is an exact no-op.
+__device__ __forceinline__ void step(Pixel& P, float alpha, const float4& C, float stop, int pos) {
+    const float w = alpha * P.T;
+    P.r = fmaf(C.x, w, P.r);
+    P.g = fmaf(C.y, w, P.g);
+    P.b = fmaf(C.z, w, P.b);
+    P.T = P.T * (1.0f - alpha);
+    if (!P.done && P.T < stop) {
+        P.done = true;
+        P.term = pos;
+    }
+}
+
+// FP32 m2 of a record at the pixel centre (fcx, fcy).
+__device__ __forceinline__ float mahal2(const float4& A, float Bx, float fcx, float fcy) {
+    const float dx = fcx - A.x, dy = fcy - A.y;
+    return fmaf(fmaf(A.z, dx, A.w * dy), dx, Bx * dy * dy);
+}
+
+__device__ __forceinline__ float fast_alpha(float m2, float lop) {
+    // op * exp(-m2/2) = 2^(log2 op - m2 log2(e)/2), clamped at 0.999
+    return fminf(exp2f(fmaf(m2, -0.72134752044448170f, lop)), 0.999f);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) composite_kernel(
+    const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
-    const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64, float3 bg,
-    float* __restrict__ out_rgb, float* __restrict__ out_T, PixelState* __restrict__ state,
-    uint32_t* __restrict__ processed_io, uint8_t* __restrict__ tile_done, int first, int last,
-    Counters* __restrict__ ctr, int want_stats) {
-    __shared__ float4 sA[kBlock];  // (lmx, lmy, ca, 2cb)
-    __shared__ float4 sB[kBlock];  // (cc, op, guard, gaussian index bits)
-    __shared__ float4 sC[kBlock];  // (r, g, b, -)
-    __shared__ unsigned long long s_red[2][kBlock / 32];
+    const SplatRec* __restrict__ rec, float3 bg, float* __restrict__ out_rgb, float* __restrict__ out_T,
+    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint8_t* __restrict__ tile_done,
+    int first, int last, Counters* __restrict__ ctr, int want_stats) {
+    // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
+    // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
+    // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
+    __shared__ float4 sRaw[2][kBatch][4];
+    __shared__ float4 sF[kBatch];  // (lmx, lmy, ext_x, ext_y)
+    __shared__ uint8_t sIdx[kThreads / 32][kBatch + kGroup];
+    __shared__ unsigned long long s_red[2][kThreads / 32];
 
     const int ts = cfg.tile_size;
     const int tile = blockIdx.x / nchunks;
     const int chunk = blockIdx.x - tile * nchunks;
-    const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
-    const int px0 = tx * ts, py0 = ty * ts;
-    const int p = chunk * block_px + threadIdx.x;
-    const int lx = p % ts, ly = p / ts;
-    const int px = px0 + lx, py = py0 + ly;
-    const bool valid = threadIdx.x < block_px && p < ts * ts && px < cam.W && py < cam.H;
-
     // Tiles that terminated in an earlier depth chunk already wrote their output.
     if (!first && tile_done[tile]) return;
     const uint2 range = ranges[tile];
     const uint32_t start = range.x, end = range.y;
-    if (!first && !last && start == end) return;  // nothing new for this tile
+    if (!first && !last && start == end) return;
 
-    // Local pixel centre relative to the tile origin: exact in FP32.
-    const float fcx = static_cast<float>(lx) + 0.5f, fcy = static_cast<float>(ly) + 0.5f;
-    const float stop = cfg.early_stop;
-    const size_t pix = valid ? static_cast<size_t>(py) * cam.W + px : 0;
-    float T = 1.0f, ar = 0.f, ag = 0.f, ab = 0.f;
-    uint32_t walked = 0;  // list entries walked in earlier chunks
-    if (!first && valid) {
-        const PixelState ps = state[pix];
-        ar = ps.r;
-        ag = ps.g;
-        ab = ps.b;
-        T = ps.T;
-        walked = processed_io[pix];
+    const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
+    const int px0 = tx * ts, py0 = ty * ts;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // 16x16: warp strips of 16x2; other tile sizes: 256 consecutive pixels per CTA.
+    int lx, ly;
+    bool inside;
+    if (ts == 16) {
+        lx = lane & 15;
+        ly = warp * 2 + (lane >> 4);
+        inside = true;
+    } else {
+        const int p = chunk * kThreads + threadIdx.x;
+        lx = p % ts;
+        ly = p / ts;
+        inside = p < ts * ts;
     }
-    // a pixel continues while T has not dropped below the threshold (raster.cpp:177)
-    bool done = !valid || T < stop;
-    uint32_t processed = done ? 0u : end - start;  // entries walked in this chunk
-    uint32_t guard_hits = 0;
+    const int px = px0 + lx, py = py0 + ly;
+    const bool valid = inside && px < W && py < H;
+    const float stop = cfg.early_stop;
+    const size_t pix = valid ? static_cast<size_t>(py) * W + px : 0;
+    const float fcx = static_cast<float>(lx) + 0.5f, fcy = static_cast<float>(ly) + 0.5f;
+    Pixel P{1.f, 0.f, 0.f, 0.f, -1, !valid};
+    uint32_t walked = 0;  // entries of the full list walked in earlier chunks
+    if (!first && valid) {
+        const PixelState s = state[pix];
+        P.r = s.r, P.g = s.g, P.b = s.b, P.T = s.T;
+        walked = processed_io[pix];
+        P.done = P.T < stop;
+    }
+    uint32_t processed = P.done ? 0u : end - start;  // entries walked in this chunk
 
-    for (uint32_t base = start; base < end; base += blockDim.x) {
-        if (__syncthreads_count(!done) == 0) break;
-        const uint32_t k = base + threadIdx.x;
-        if (k < end) {
-            const uint32_t g = static_cast<uint32_t>(keys[k]);
-            const SplatRec r = rec[g];
-            sA[threadIdx.x] = make_float4(static_cast<float>(r.mx - px0), static_cast<float>(r.my - py0),
-                                          r.ca, r.cb2);
-            sB[threadIdx.x] = make_float4(r.cc, r.op, r.guard, __uint_as_float(g));
-            sC[threadIdx.x] = make_float4(r.r, r.g, r.b, 0.f);
+    // The warp's live-pixel-centre bounding box (tile-local) for the batch filter.
+    float wx0 = P.done ? 1e30f : fcx, wx1 = P.done ? -1e30f : fcx;
+    float wy0 = P.done ? 1e30f : fcy, wy1 = P.done ? -1e30f : fcy;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        wx0 = fminf(wx0, __shfl_xor_sync(0xffffffffu, wx0, o));
+        wx1 = fmaxf(wx1, __shfl_xor_sync(0xffffffffu, wx1, o));
+        wy0 = fminf(wy0, __shfl_xor_sync(0xffffffffu, wy0, o));
+        wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
+    }
+    uint32_t guard_hits = 0;
+    uint8_t* idx = sIdx[warp];
+
+    // Software pipeline over batches: keys one batch ahead in registers, records one
+    // batch ahead in shared memory via cp.async, so the dependent key -> record
+    // gather of batch b+1 overlaps the walk of batch b.
+    const int t = threadIdx.x;
+    uint32_t g_next = 0;  // gaussian index of this thread's record in the next batch
+    if (start + t < end) g_next = static_cast<uint32_t>(__ldg(&keys[start + t]));
+    if (start + t < end) {
+        const char* src = reinterpret_cast<const char*>(rec + g_next);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&sRaw[0][t][c]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 16 * c));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    uint32_t g_cur = g_next;
+    if (start + kBatch + t < end) g_next = static_cast<uint32_t>(__ldg(&keys[start + kBatch + t]));
+    int buf = 0;
+
+    for (uint32_t base = start; base < end; base += kBatch) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        if (__syncthreads_count(!P.done) == 0) break;
+        {
+            // convert this thread's record of the current batch
+            if (base + t < end) {
+                float4* r = sRaw[buf][t];
+                const double2 m = *reinterpret_cast<const double2*>(&r[0]);
+                const float4 q1 = r[1];  // ca, cb2, cc, lop
+                const float4 q2 = r[2];  // r, g, b, cut
+                const float4 q3 = r[3];  // guard, ext_x, ext_y, pad
+                const float lmx = static_cast<float>(m.x - px0), lmy = static_cast<float>(m.y - py0);
+                r[0] = make_float4(lmx, lmy, q1.x, q1.y);
+                r[1] = make_float4(q1.z, q2.w + q3.x, q2.w - q3.x, q1.w);
+                r[2] = make_float4(q2.x, q2.y, q2.z, __uint_as_float(g_cur));
+                sF[t] = make_float4(lmx, lmy, q3.y, q3.z);
+            }
+            // prefetch the next batch's record, then the key after it
+            const uint32_t kn = base + kBatch + t;
+            if (kn < end) {
+                const char* src = reinterpret_cast<const char*>(rec + g_next);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&sRaw[buf ^ 1][t][c]));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 16 * c));
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+            g_cur = g_next;
+            if (kn + kBatch < end) g_next = static_cast<uint32_t>(__ldg(&keys[kn + kBatch]));
+            buf ^= 1;
         }
         __syncthreads();
-        if (!done) {
-            const uint32_t nb = min(static_cast<uint32_t>(blockDim.x), end - base);
-            for (uint32_t j = 0; j < nb; ++j) {
-                const float4 A = sA[j];
-                const float dx = fcx - A.x, dy = fcy - A.y;
-                const float4 B = sB[j];
-                const float m2 = fmaf(fmaf(A.z, dx, A.w * dy), dx, B.x * dy * dy);
-                const float G = B.z;
-                if (m2 > 9.0f + G) continue;
-                float alpha;
-                bool exact = m2 >= 9.0f - G;
-                if (!exact) {
-                    alpha = fminf(B.y * __expf(-0.5f * m2), 0.999f);
-                    const float tol = 0.003921568627f * fmaf(0.5f, G, 2e-6f);
-                    if (alpha < 0.003921568627f + tol) {
-                        if (alpha < 0.003921568627f - tol) continue;
-                        exact = true;
+        const uint32_t nb = min(static_cast<uint32_t>(kBatch), end - base);
+        const float4(*R)[4] = sRaw[buf ^ 1];  // the batch converted above
+        int cnt = 0;
+        if (__any_sync(0xffffffffu, !P.done)) {
+            for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                bool hit = false;
+                if (j < nb) {
+                    const float4 F = sF[j];
+                    hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit) idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint8_t>(j);
+                cnt += __popc(m);
+            }
+        }
+        __syncwarp();
+        for (int q = 0; q < cnt && !P.done; q += kGroup) {
+            // m2 / alpha of the whole group first (independent), then the blend chain;
+            // slots past cnt re-read record idx[q] and are forced to alpha = 0
+            float alpha[kGroup];
+            bool guard = false;
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+                const int qq = q + k;
+                const bool in = qq < cnt;
+                const int j = idx[in ? qq : q];
+                const float4 A = R[j][0];
+                const float4 B = R[j][1];
+                const float m2 = mahal2(A, B.x, fcx, fcy);
+                guard |= in && m2 <= B.y && m2 >= B.z;
+                alpha[k] = (in && m2 < B.z) ? fast_alpha(m2, B.w) : 0.0f;
+            }
+            if (!guard) {
+#pragma unroll
+                for (int k = 0; k < kGroup; ++k) {
+                    const int qq = q + k;
+                    const int j = idx[qq < cnt ? qq : q];
+                    step(P, P.done ? 0.0f : alpha[k], R[j][2], stop, qq);
+                }
+            } else {
+                // a pair inside the guard band: walk the group one record at a time
+                for (int k = 0; k < kGroup && q + k < cnt && !P.done; ++k) {
+                    const int j = idx[q + k];
+                    const float4 A = R[j][0];
+                    const float4 B = R[j][1];
+                    const float m2 = mahal2(A, B.x, fcx, fcy);
+                    if (m2 > B.y) continue;
+                    float a = alpha[k];
+                    if (m2 >= B.z) {
+                        ++guard_hits;
+                        if (!exact_alpha(fc, __float_as_uint(R[j][2].w), px, py, &a)) continue;
                     }
-                }
-                if (exact) {
-                    ++guard_hits;
-                    if (!exact_alpha(rec, rec64, __float_as_uint(B.w), px + 0.5, py + 0.5, &alpha))
-                        continue;
-                }
-                const float4 C = sC[j];
-                const float w = alpha * T;
-                ar += C.x * w;
-                ag += C.y * w;
-                ab += C.z * w;
-                T *= 1.0f - alpha;
-                if (T < stop) {
-                    done = true;
-                    processed = base + j + 1 - start;
-                    break;
+                    step(P, a, R[j][2], stop, q + k);
                 }
             }
         }
+        if (P.term >= 0) {
+            processed = base + idx[P.term] + 1 - start;
+            P.term = -2;  // recorded
+        }
         __syncthreads();
     }
 
-    const bool all_done = __syncthreads_and(done) != 0;
+    // never leave with copies in flight into shared memory
+    asm volatile("cp.async.wait_all;\n" ::);
+    const bool all_done = __syncthreads_and(P.done) != 0;
     const bool finalize = last || all_done;
     if (valid) {
         if (finalize) {
             if (out_rgb) {
-                out_rgb[pix * 3 + 0] = ar + T * bg.x;
-                out_rgb[pix * 3 + 1] = ag + T * bg.y;
-                out_rgb[pix * 3 + 2] = ab + T * bg.z;
+                out_rgb[pix * 3 + 0] = P.r + P.T * bg.x;
+                out_rgb[pix * 3 + 1] = P.g + P.T * bg.y;
+                out_rgb[pix * 3 + 2] = P.b + P.T * bg.z;
             }
-            if (out_T) out_T[pix] = T;
+            if (out_T) out_T[pix] = P.T;
         } else {
-            state[pix] = PixelState{ar, ag, ab, T};
+            state[pix] = PixelState{P.r, P.g, P.b, P.T};
             processed_io[pix] = walked + processed;
         }
     }
     if (!last && all_done && threadIdx.x == 0) tile_done[tile] = 1;
     if (want_stats) {
-        // E_t (block-terminated entries) = max over the tile's pixels of the entries of
-        // its full list each pixel walked (counted when the tile finalises); guard hits
-        // summed over chunks.
+        // E_t = max over the tile's pixels of the entries of its full list each pixel
+        // walked (counted when the tile finalises); guard hits summed over chunks.
         unsigned long long e = (finalize && valid) ? walked + processed : 0ULL;
         unsigned long long h = guard_hits;
 #pragma unroll
@@ -170,15 +301,14 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
             e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
             h += __shfl_xor_sync(0xffffffffu, h, o);
         }
-        const int warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-        if ((threadIdx.x & 31) == 0) {
+        if (lane == 0) {
             s_red[0][warp] = e;
             s_red[1][warp] = h;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned long long em = 0, hs = 0;
-            for (int w = 0; w < nw; ++w) {
+            for (int w = 0; w < kThreads / 32; ++w) {
                 em = max(em, s_red[0][w]);
                 hs += s_red[1][w];
             }
@@ -193,24 +323,20 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(
 
 int composite_pixel_chunks(int ts) {
     const long long tile_px = static_cast<long long>(ts) * ts;
-    const int block_px = static_cast<int>(tile_px < kBlock ? ((tile_px + 31) / 32) * 32 : kBlock);
-    return static_cast<int>((tile_px + block_px - 1) / block_px);
+    return static_cast<int>((tile_px + kThreads - 1) / kThreads);
 }
 
-void launch_composite(const CamParams& cam, const CfgParams& cfg, const uint2* ranges,
-                      const unsigned long long* keys, const SplatRec* rec,
-                      const SplatRec64* rec64, float3 bg, float* rgb, float* T,
-                      PixelState* state, uint32_t* processed, uint8_t* tile_done, bool first,
-                      bool last, Counters* counters, bool want_stats, cudaStream_t stream) {
-    const int ts = cfg.tile_size;
-    const long long tile_px = static_cast<long long>(ts) * ts;
-    const int block_px = static_cast<int>(tile_px < kBlock ? ((tile_px + 31) / 32) * 32 : kBlock);
-    const int nchunks = composite_pixel_chunks(ts);
+void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
+                      const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
+                      float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
+                      uint8_t* tile_done, bool first, bool last, Counters* counters, bool want_stats,
+                      cudaStream_t stream) {
+    const int nchunks = composite_pixel_chunks(cfg.tile_size);
     const long long ntiles = static_cast<long long>(cfg.tiles_x) * cfg.tiles_y;
     const long long grid = ntiles * nchunks;
-    composite_kernel<<<static_cast<unsigned>(grid), block_px, 0, stream>>>(
-        cam, cfg, nchunks, block_px, ranges, keys, rec, rec64, bg, rgb, T, state, processed,
-        tile_done, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0);
+    composite_kernel<<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
+        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, bg, rgb, T, state, processed, tile_done,
+        first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0);
 }
 
 }  // namespace sgs

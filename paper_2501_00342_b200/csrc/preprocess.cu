@@ -19,33 +19,10 @@
 // 48 B compositing record, 32 B FP64 guard record, 16 B tile rect, 4 B count.
 #include <cfloat>
 
-#include "sgs_internal.h"
+#include "projection.cuh"
 
 namespace sgs {
 namespace {
-
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
-// ((a0*b0 + a1*b1) + a2*b2): the Eigen-subset left-to-right reduction.
-__device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1,
-                                       double b2) {
-    return dadd(dadd(dmul(a0, b0), dmul(a1, b1)), dmul(a2, b2));
-}
-
-// static_cast<int>(double) as x86-64 executes it (cvttsd2si): out-of-range and
-// NaN give INT32_MIN. build_tile_grid (raster.cpp:117-122) depends on it.
-__device__ __forceinline__ int32_t to_int_x86(double v) {
-    if (!(v > -2147483649.0 && v < 2147483648.0)) return INT32_MIN;
-    return static_cast<int32_t>(v);
-}
-
-__device__ __forceinline__ unsigned long long depth_key(double z) {
-    if (z == 0.0) z = 0.0;  // -0 == +0 in the reference's comparator
-    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(z));
-    return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
-}
 
 // SH constants, color.hpp:15-26 (float copies for the FP32 colour path).
 __constant__ float kC0 = 0.28209479177387814f;
@@ -124,42 +101,6 @@ __device__ __forceinline__ void lobe_accumulate(const float* lobes, const float*
     }
 }
 
-struct Geo {
-    double p[3], q[4], ls[3], opl;
-};
-
-template <bool F64>
-__device__ __forceinline__ void load_geo(const ScenePlanes& sp, uint64_t i, Geo& g) {
-    if constexpr (F64) {
-        g.p[0] = sp.g8[0][i];
-        g.p[1] = sp.g8[1][i];
-        g.p[2] = sp.g8[2][i];
-        g.q[0] = sp.g8[3][i];
-        g.q[1] = sp.g8[4][i];
-        g.q[2] = sp.g8[5][i];
-        g.q[3] = sp.g8[6][i];
-        g.ls[0] = sp.g8[7][i];
-        g.ls[1] = sp.g8[8][i];
-        g.ls[2] = sp.g8[9][i];
-        g.opl = sp.g8[10][i];
-    } else {
-        const float4 a = __ldg(&sp.g4[0][i]);
-        const float4 b = __ldg(&sp.g4[1][i]);
-        const float4 c = __ldg(&sp.g4[2][i]);
-        g.p[0] = a.x;
-        g.p[1] = a.y;
-        g.p[2] = a.z;
-        g.opl = a.w;
-        g.q[0] = b.x;
-        g.q[1] = b.y;
-        g.q[2] = b.z;
-        g.q[3] = b.w;
-        g.ls[0] = c.x;
-        g.ls[1] = c.y;
-        g.ls[2] = c.z;
-    }
-}
-
 __device__ __forceinline__ void raise_error(Counters* ctr, uint64_t i, uint32_t code) {
     atomicMin(&ctr->err, (static_cast<unsigned long long>(i) << 8) | code);
 }
@@ -167,107 +108,44 @@ __device__ __forceinline__ void raise_error(Counters* ctr, uint64_t i, uint32_t 
 template <bool F64, int KIND>
 __global__ void __launch_bounds__(256) preprocess_kernel(
     const ScenePlanes sp, const CamParams cam, const CfgParams cfg,
-    unsigned long long* __restrict__ depth_keys, uint32_t* __restrict__ iota,
-    SplatRec* __restrict__ rec, SplatRec64* __restrict__ rec64, int4* __restrict__ rects,
+    unsigned long long* __restrict__ depth_keys,
+    SplatRec* __restrict__ rec, int4* __restrict__ rects,
     uint32_t* __restrict__ ntiles, Counters* __restrict__ ctr, DebugSplat* __restrict__ debug) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool visible = false;
     unsigned long long vkey = ~0ULL;
     if (i < sp.n) {
-        iota[i] = static_cast<uint32_t>(i);
         unsigned long long key = ~0ULL;
         uint32_t count = 0;
         Geo g;
-        load_geo<F64>(sp, i, g);
+        ProjGeo pg;
         DebugSplat dbg;
         if (debug) {
             memset(&dbg, 0, sizeof(dbg));
             dbg.degree = -1;
         }
-        // t = R p + t (camera.hpp:19)
-        const double* R = cam.R;
-        const double tx = dadd(dot3(R[0], R[1], R[2], g.p[0], g.p[1], g.p[2]), cam.t[0]);
-        const double ty = dadd(dot3(R[3], R[4], R[5], g.p[0], g.p[1], g.p[2]), cam.t[1]);
-        const double tz = dadd(dot3(R[6], R[7], R[8], g.p[0], g.p[1], g.p[2]), cam.t[2]);
+        const int pstat = project_geometry<F64>(sp, cam, i, g, pg);
+        if (pstat == kProjZeroQuat) raise_error(ctr, i, kErrZeroQuaternion);
         do {
-            if (tz < cam.near_plane) break;  // raster.cpp:23
-            // quat_to_rotation (common.hpp:124-134)
-            const double qn = __dsqrt_rn(
-                dadd(dadd(dadd(dmul(g.q[0], g.q[0]), dmul(g.q[1], g.q[1])), dmul(g.q[2], g.q[2])),
-                     dmul(g.q[3], g.q[3])));
-            if (qn < 1e-12) {
-                raise_error(ctr, i, kErrZeroQuaternion);
-                break;
-            }
-            const double w = ddiv(g.q[0], qn), x = ddiv(g.q[1], qn), y = ddiv(g.q[2], qn),
-                         z = ddiv(g.q[3], qn);
-            const double Rq[9] = {
-                dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z)))),
-                dmul(2.0, dsub(dmul(x, y), dmul(w, z))),
-                dmul(2.0, dadd(dmul(x, z), dmul(w, y))),
-                dmul(2.0, dadd(dmul(x, y), dmul(w, z))),
-                dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z)))),
-                dmul(2.0, dsub(dmul(y, z), dmul(w, x))),
-                dmul(2.0, dsub(dmul(x, z), dmul(w, y))),
-                dmul(2.0, dadd(dmul(y, z), dmul(w, x))),
-                dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y)))),
-            };
-            // covariance (scene.cpp:81-85): M = Rq diag(exp(s)); S = M M^T
-            const double sc[3] = {exp(g.ls[0]), exp(g.ls[1]), exp(g.ls[2])};
-            double M[9];
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) M[r * 3 + c] = dmul(Rq[r * 3 + c], sc[c]);
-            double S[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    S[a * 3 + b] = dot3(M[a * 3 + 0], M[a * 3 + 1], M[a * 3 + 2], M[b * 3 + 0],
-                                        M[b * 3 + 1], M[b * 3 + 2]);
-            // EWA Jacobian with the 1.3x frustum clamp (raster.cpp:27-41)
-            const double rx = ddiv(tx, tz), ry = ddiv(ty, tz);
-            const double crx = rx < -cam.lim_x ? -cam.lim_x : (cam.lim_x < rx ? cam.lim_x : rx);
-            const double cry = ry < -cam.lim_y ? -cam.lim_y : (cam.lim_y < ry ? cam.lim_y : ry);
-            const double txc = dmul(crx, tz), tyc = dmul(cry, tz);
-            const double tz2 = dmul(tz, tz);
-            const double J[6] = {ddiv(cam.fx, tz), 0.0, ddiv(dmul(-cam.fx, txc), tz2),
-                                 0.0, ddiv(cam.fy, tz), ddiv(dmul(-cam.fy, tyc), tz2)};
-            double Tm[6];
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    Tm[a * 3 + b] = dot3(J[a * 3 + 0], J[a * 3 + 1], J[a * 3 + 2], R[0 * 3 + b],
-                                         R[1 * 3 + b], R[2 * 3 + b]);
-            double TS[6];
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    TS[a * 3 + b] = dot3(Tm[a * 3 + 0], Tm[a * 3 + 1], Tm[a * 3 + 2], S[0 * 3 + b],
-                                         S[1 * 3 + b], S[2 * 3 + b]);
-            const double a = dadd(dot3(TS[0], TS[1], TS[2], Tm[0], Tm[1], Tm[2]), kCovarianceDilation);
-            const double b = dot3(TS[0], TS[1], TS[2], Tm[3], Tm[4], Tm[5]);
-            const double c = dadd(dot3(TS[3], TS[4], TS[5], Tm[3], Tm[4], Tm[5]), kCovarianceDilation);
-            const double det = dsub(dmul(a, c), dmul(b, b));
-            if (det <= 0.0) break;  // raster.cpp:48 (NaN passes, as in the reference)
-            const double mid = dmul(0.5, dadd(a, c));
-            const double disc = dsub(dmul(mid, mid), det);
-            const double lambda_max = dadd(mid, __dsqrt_rn(0.0 < disc ? disc : 0.0));
-            const double radius = dmul(3.0, __dsqrt_rn(lambda_max));
-            const double mx = dadd(ddiv(dmul(cam.fx, tx), tz), cam.cx);
-            const double my = dadd(ddiv(dmul(cam.fy, ty), tz), cam.cy);
-            if (dadd(mx, radius) < 0.0 || dsub(mx, radius) > cam.width ||
-                dadd(my, radius) < 0.0 || dsub(my, radius) > cam.height)
-                break;  // raster.cpp:56-60
+            if (pstat != kProjVisible) break;
+            const double radius = pg.radius, mx = pg.mx, my = pg.my, tz = pg.tz;
             // view direction, camera.hpp:20 and raster.cpp:66-69
             const double ox = dsub(g.p[0], cam.C[0]), oy = dsub(g.p[1], cam.C[1]),
                          oz = dsub(g.p[2], cam.C[2]);
             const double dist = __dsqrt_rn(dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz)));
             if (dist < 1e-12) break;
-            const double dxd = ddiv(ox, dist), dyd = ddiv(oy, dist), dzd = ddiv(oz, dist);
+            // The direction only feeds the FP32 colour. For dist in [1e-100, 1e100] the
+            // reference's normalised vector has |norm - 1| ~ 1e-16, so its unit check
+            // (color.cpp:10-16) cannot fire and a reciprocal suffices; outside that range
+            // (or NaN) the exact division and check run.
+            const bool safe_dist = dist > 1e-100 && dist < 1e100;
+            double dxd, dyd, dzd;
+            if (safe_dist) {
+                const double rd = 1.0 / dist;
+                dxd = ox * rd, dyd = oy * rd, dzd = oz * rd;
+            } else {
+                dxd = ddiv(ox, dist), dyd = ddiv(oy, dist), dzd = ddiv(oz, dist);
+            }
             // degree selection and the colour-model error contract (raster.cpp:70-77,
             // color.cpp:201-206, :182-191)
             int deg = sp.sh_degree;
@@ -288,7 +166,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                     break;
                 }
             }
-            {
+            if (!safe_dist) {
                 const double nrm =
                     __dsqrt_rn(dadd(dadd(dmul(dxd, dxd), dmul(dyd, dyd)), dmul(dzd, dzd)));
                 if (fabs(dsub(nrm, 1.0)) > 1e-6) {
@@ -351,16 +229,36 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
             col[2] = fmaxf(col[2], 0.0f);
 
             // ---- outputs ----
-            const double cona = ddiv(c, det), conb = ddiv(-b, det), conc = ddiv(a, det);
-            const double opacity = ddiv(1.0, dadd(1.0, exp(-g.opl)));  // sigmoid, common.hpp:136
+            // conic and opacity only feed FP32 quantities here (the compositor's guard band
+            // re-derives the exact FP64 values): one reciprocal instead of three divisions,
+            // sigmoid in FP32. The debug dump reports the exact ones.
+            double cona, conb, conc, opacity;
+            if (debug) {
+                exact_conic_opacity(g, pg);
+                cona = pg.cona, conb = pg.conb, conc = pg.conc, opacity = pg.opacity;
+            } else {
+                const double rdet = 1.0 / pg.det;
+                cona = pg.c * rdet;
+                conb = -pg.b * rdet;
+                conc = pg.a * rdet;
+                opacity = 1.0f / (1.0f + __expf(-static_cast<float>(g.opl)));
+            }
             visible = true;
             key = depth_key(tz);
             // tile rectangle (raster.cpp:117-122), inclusive, clamped
             const double ts = static_cast<double>(cfg.tile_size);
-            int32_t x0 = to_int_x86(floor(ddiv(dsub(mx, radius), ts)));
-            int32_t x1 = to_int_x86(floor(ddiv(dadd(mx, radius), ts)));
-            int32_t y0 = to_int_x86(floor(ddiv(dsub(my, radius), ts)));
-            int32_t y1 = to_int_x86(floor(ddiv(dadd(my, radius), ts)));
+            // x / ts == x * (1/ts) bit for bit when ts is a power of two (both round the
+            // exact quotient once); other tile sizes divide.
+            const bool pow2 = (cfg.tile_size & (cfg.tile_size - 1)) == 0;
+            const double its = 1.0 / ts;
+            const double qx0 = pow2 ? dmul(dsub(mx, radius), its) : ddiv(dsub(mx, radius), ts);
+            const double qx1 = pow2 ? dmul(dadd(mx, radius), its) : ddiv(dadd(mx, radius), ts);
+            const double qy0 = pow2 ? dmul(dsub(my, radius), its) : ddiv(dsub(my, radius), ts);
+            const double qy1 = pow2 ? dmul(dadd(my, radius), its) : ddiv(dadd(my, radius), ts);
+            int32_t x0 = to_int_x86(floor(qx0));
+            int32_t x1 = to_int_x86(floor(qx1));
+            int32_t y0 = to_int_x86(floor(qy0));
+            int32_t y1 = to_int_x86(floor(qy1));
             x0 = max(0, x0);
             y0 = max(0, y0);
             x1 = min(cfg.tiles_x - 1, x1);
@@ -373,24 +271,28 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
             const double guard =
                 2.0 * 5.9604644775390625e-08 * csum * (9.0 * radius * radius + 3.0 * radius * ts) +
                 1e-6;
+            // combined cutoff: alpha < 1/255 <=> m2 > 2 ln(255 op) (op > 0)
+            const double acut = opacity > 0.0 ? 2.0 * log(255.0 * opacity) : -1.0;
+            const double cut = acut < kSupportMahalanobisSq ? acut : kSupportMahalanobisSq;
+            // extents of {d : d^T conic d <= cut + guard} = sqrt(K cov_xx), sqrt(K cov_yy);
+            // cov = the dilated 2D covariance (a, b, c), slightly inflated
+            const double K = fmax(cut + guard, 0.0);
             SplatRec r;
             r.mx = mx;
             r.my = my;
             r.ca = static_cast<float>(cona);
             r.cb2 = static_cast<float>(2.0 * conb);
             r.cc = static_cast<float>(conc);
-            r.op = static_cast<float>(opacity);
+            r.lop = opacity > 0.0 ? static_cast<float>(log2(opacity)) : -1e30f;
             r.r = col[0];
             r.g = col[1];
             r.b = col[2];
+            r.cut = static_cast<float>(cut);
             r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
+            r.ext_x = static_cast<float>(sqrt(K * pg.a) * (1.0 + 1e-5) + 1e-3);
+            r.ext_y = static_cast<float>(sqrt(K * pg.c) * (1.0 + 1e-5) + 1e-3);
+            r.pad = 0.f;
             rec[i] = r;
-            SplatRec64 r64;
-            r64.ca = cona;
-            r64.cb = conb;
-            r64.cc = conc;
-            r64.op = opacity;
-            rec64[i] = r64;
             if (debug) {
                 dbg.mean2d[0] = mx;
                 dbg.mean2d[1] = my;
@@ -431,42 +333,47 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
 
 template <bool F64>
 void launch_kind(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
-                 unsigned long long* keys, uint32_t* iota, SplatRec* rec, SplatRec64* rec64,
+                 unsigned long long* keys, SplatRec* rec,
                  int4* rects, uint32_t* ntiles, Counters* ctr, DebugSplat* debug,
                  cudaStream_t stream) {
     const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
     switch (sp.kind) {
         case SGS_SH:
-            preprocess_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, iota, rec,
-                                                                     rec64, rects, ntiles, ctr, debug);
+            preprocess_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
             break;
         case SGS_SG1:
-            preprocess_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, iota, rec,
-                                                                      rec64, rects, ntiles, ctr, debug);
+            preprocess_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
             break;
         case SGS_SG3:
-            preprocess_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, iota, rec,
-                                                                      rec64, rects, ntiles, ctr, debug);
+            preprocess_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
             break;
         default:
             preprocess_kernel<F64, SGS_MIXED><<<blocks, 256, 0, stream>>>(
-                sp, cam, cfg, keys, iota, rec, rec64, rects, ntiles, ctr, debug);
+                sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
             break;
     }
 }
 
+__global__ void iota_kernel(uint64_t n, uint32_t* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<uint32_t>(i);
+}
+
 }  // namespace
 
+void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream) {
+    if (n) iota_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, out);
+}
+
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
-                       unsigned long long* depth_keys, uint32_t* iota, SplatRec* rec,
-                       SplatRec64* rec64, int4* rects, uint32_t* ntiles, Counters* counters,
-                       DebugSplat* debug, cudaStream_t stream) {
+                       unsigned long long* depth_keys, SplatRec* rec, int4* rects,
+                       uint32_t* ntiles, Counters* counters, DebugSplat* debug, cudaStream_t stream) {
     if (sp.n == 0) return;
     if (sp.geometry_f64)
-        launch_kind<true>(sp, cam, cfg, depth_keys, iota, rec, rec64, rects, ntiles, counters, debug,
+        launch_kind<true>(sp, cam, cfg, depth_keys, rec, rects, ntiles, counters, debug,
                           stream);
     else
-        launch_kind<false>(sp, cam, cfg, depth_keys, iota, rec, rec64, rects, ntiles, counters, debug,
+        launch_kind<false>(sp, cam, cfg, depth_keys, rec, rects, ntiles, counters, debug,
                            stream);
 }
 

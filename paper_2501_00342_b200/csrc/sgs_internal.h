@@ -69,19 +69,27 @@ struct ScenePlanes {
     float bg[3];
 };
 
-// Compositing record written by K1 for visible splats (48 B, 16-B aligned).
+// Per-frame constants in device memory, read by K7's cold FP64 guard-band path
+// (kept out of kernel parameters so the hot loop does not carry them).
+struct FrameConsts {
+    ScenePlanes sp;
+    CamParams cam;
+};
+
+// Compositing record written by K1 for visible splats (64 B, 16-B aligned).
+// The reference's two skip tests (m2 > 9, alpha < 1/255) are one cutoff on m2:
+// alpha < 1/255 <=> m2 > 2 ln(255 op), so cut = min(9, 2 ln(255 op)) (FP64 in K1).
 struct __align__(16) SplatRec {
     double mx, my;      // mean2d in pixels (FP64 so the compositor can localise exactly)
     float ca, cb2, cc;  // conic (a, 2b, c)
-    float op;           // activated opacity
+    float lop;          // log2(opacity)
     float r, g, b;      // colour
-    float guard;        // FP32 m2 error bound -> FP64 guard band width
+    float cut;          // min(9, 2 ln(255 op))
+    float guard;        // FP32 m2 error bound -> FP64 guard band half-width
+    float ext_x, ext_y; // half extents of {m2 <= cut + guard} (warp culling box)
+    float pad;
 };
-
-// FP64 side record read only inside the guard band (32 B).
-struct __align__(16) SplatRec64 {
-    double ca, cb, cc, op;
-};
+static_assert(sizeof(SplatRec) == 64, "splat record");
 
 // Debug record for sgs_project (same field order as sgs_splat).
 struct DebugSplat {
@@ -128,9 +136,9 @@ inline int color_plane_count(int kind, int degree) {
 
 // Launchers (defined in the .cu files).
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
-                       unsigned long long* depth_keys, uint32_t* iota, SplatRec* rec,
-                       SplatRec64* rec64, int4* rects, uint32_t* ntiles, Counters* counters,
-                       DebugSplat* debug, cudaStream_t stream);
+                       unsigned long long* depth_keys, SplatRec* rec, int4* rects,
+                       uint32_t* ntiles, Counters* counters, DebugSplat* debug, cudaStream_t stream);
+void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
 void launch_make_key32(uint64_t n, const unsigned long long* key64, const Counters* ctr,
                        uint32_t* key32, cudaStream_t stream);
 void launch_fix_ties(uint64_t n, const uint32_t* key32, const unsigned long long* key64,
@@ -147,9 +155,9 @@ void launch_tile_ranges(uint64_t p, const unsigned long long* keys, uint2* range
                         cudaStream_t stream);
 // K7 over one depth chunk. first/last select state init / final output; tile_done and
 // state may be null when the frame is a single chunk.
-void launch_composite(const CamParams& cam, const CfgParams& cfg, const uint2* ranges,
-                      const unsigned long long* keys, const SplatRec* rec,
-                      const SplatRec64* rec64, float3 bg, float* rgb, float* T,
+void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
+                      const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
+                      float3 bg, float* rgb, float* T,
                       PixelState* state, uint32_t* processed, uint8_t* tile_done, bool first,
                       bool last, Counters* counters, bool want_stats, cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
