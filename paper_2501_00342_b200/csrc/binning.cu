@@ -19,24 +19,58 @@
 namespace sgs {
 namespace {
 
-__device__ __forceinline__ uint32_t live_tiles(const int4 rc, const uint8_t* __restrict__ done,
-                                               int tiles_x) {
+// The finished-tile flags of the frame as a bitmap in shared memory (tiles up to
+// kMaxBitmapTiles; larger grids read the byte flags from global memory).
+constexpr int kMaxBitmapTiles = 1 << 18;
+
+__device__ __forceinline__ void load_done_bitmap(const uint32_t* __restrict__ done, int ntile, uint32_t* bits) {
+    const int words = (ntile + 31) / 32;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) bits[w] = done[w];
+    __syncthreads();
+}
+
+struct DoneView {
+    const uint32_t* bits;  // bitmap (shared copy, or the global one), null if no tile finished yet
+    __device__ __forceinline__ bool operator()(uint32_t t) const {
+        return bits && ((bits[t >> 5] >> (t & 31)) & 1u);
+    }
+};
+
+__device__ __forceinline__ uint32_t live_tiles(const int4 rc, const DoneView& done, int tiles_x) {
     uint32_t c = 0;
     for (int ty = rc.z; ty <= rc.w; ++ty)
-        for (int tx = rc.x; tx <= rc.y; ++tx) c += done[ty * tiles_x + tx] ? 0u : 1u;
+        for (int tx = rc.x; tx <= rc.y; ++tx) c += done(static_cast<uint32_t>(ty * tiles_x + tx)) ? 0u : 1u;
     return c;
 }
 
-__global__ void count_tiles_kernel(uint64_t rb, uint64_t re, const uint32_t* __restrict__ order,
-                                   const uint32_t* __restrict__ ntiles,
-                                   const int4* __restrict__ rects, const uint8_t* __restrict__ done,
-                                   int tiles_x, unsigned long long* __restrict__ counts) {
+// Rank-ordered copy of the binning inputs, gathered once per frame so that every
+// chunk's K3/K4 reads them coalesced: brect[r] = rects[order[r]],
+// bmeta[r] = (order[r], ntiles[order[r]]).
+__global__ void gather_bins_kernel(uint64_t n, const uint32_t* __restrict__ order,
+                                   const int4* __restrict__ rects, const uint32_t* __restrict__ ntiles,
+                                   int4* __restrict__ brect, uint2* __restrict__ bmeta) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t g = order[r];
+    const uint32_t c = ntiles[g];
+    bmeta[r] = make_uint2(g, c);
+    if (c) brect[r] = rects[g];
+}
+
+__global__ void count_tiles_kernel(uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta,
+                                   const int4* __restrict__ brect, const uint32_t* __restrict__ done_bytes,
+                                   int tiles_x, int ntile, unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t done_bits[];
+    DoneView done{done_bytes};
+    if (done_bytes && ntile <= kMaxBitmapTiles) {
+        load_done_bitmap(done_bytes, ntile, done_bits);
+        done.bits = done_bits;
+    }
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t r = rb + k;
     if (r < re) {
-        const uint32_t g = order[r];
-        uint32_t c = ntiles[g];
-        if (c && done) c = live_tiles(rects[g], done, tiles_x);
+        uint32_t c = bmeta[r].y;
+        if (c && done_bytes) c = live_tiles(brect[r], done, tiles_x);
         counts[k] = c;
     } else if (r == re) {
         counts[k] = 0;
@@ -49,11 +83,16 @@ __global__ void count_tiles_kernel(uint64_t rb, uint64_t re, const uint32_t* __r
 // lane while 31 idle.
 constexpr uint32_t kCoop = 32;
 
-__global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint32_t* __restrict__ order,
-                                 const uint32_t* __restrict__ ntiles,
-                                 const int4* __restrict__ rects, const uint8_t* __restrict__ done,
-                                 const unsigned long long* __restrict__ offsets, int tiles_x,
-                                 unsigned long long* __restrict__ keys) {
+__global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta,
+                                 const int4* __restrict__ brect, const uint32_t* __restrict__ done_bytes,
+                                 const unsigned long long* __restrict__ offsets, int tiles_x, int ntile,
+                                 unsigned long long* __restrict__ keys, uint64_t capacity) {
+    extern __shared__ uint32_t done_bits[];
+    DoneView done{done_bytes};
+    if (done_bytes && ntile <= kMaxBitmapTiles) {
+        load_done_bitmap(done_bytes, ntile, done_bits);
+        done.bits = done_bits;
+    }
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t r = rb + k;
     const unsigned lane = threadIdx.x & 31;
@@ -61,10 +100,11 @@ __global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint32_t* __res
     int4 rc = make_int4(0, -1, 0, -1);
     unsigned long long off = 0;
     if (r < re) {
-        g = order[r];
-        area = ntiles[g];
+        const uint2 m = bmeta[r];
+        g = m.x;
+        area = m.y;
         if (area) {
-            rc = rects[g];
+            rc = brect[r];
             off = offsets[k];
         }
     }
@@ -74,8 +114,8 @@ __global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint32_t* __res
         for (uint32_t j = 0; j < area; ++j) {
             const uint32_t tile = static_cast<uint32_t>(rc.z + static_cast<int>(j / w)) * tiles_x +
                                   static_cast<uint32_t>(rc.x + static_cast<int>(j % w));
-            if (done && done[tile]) continue;
-            keys[off + o] = (static_cast<unsigned long long>(tile) << 32) | g;
+            if (done(tile)) continue;
+            if (off + o < capacity) keys[off + o] = (static_cast<unsigned long long>(tile) << 32) | g;
             ++o;
         }
     }
@@ -97,49 +137,77 @@ __global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint32_t* __res
             if (j < a) {
                 tile = static_cast<uint32_t>(y0 + static_cast<int>(j / ww)) * tiles_x +
                        static_cast<uint32_t>(x0 + static_cast<int>(j % ww));
-                live = !(done && done[tile]);
+                live = !done(tile);
             }
             const unsigned m = __ballot_sync(0xffffffffu, live);
-            if (live) keys[o + __popc(m & ((1u << lane) - 1u))] = (static_cast<unsigned long long>(tile) << 32) | gg;
+            const unsigned long long pos = o + __popc(m & ((1u << lane) - 1u));
+            if (live && pos < capacity) keys[pos] = (static_cast<unsigned long long>(tile) << 32) | gg;
             o += __popc(m);
         }
     }
 }
 
-__global__ void tile_ranges_kernel(uint64_t p, const unsigned long long* __restrict__ keys,
-                                   uint2* __restrict__ ranges) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= p) return;
-    const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
-    if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t) ranges[t].x = static_cast<uint32_t>(i);
-    if (i == p - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t)
-        ranges[t].y = static_cast<uint32_t>(i + 1);
+__global__ void tile_ranges_kernel(const unsigned long long* __restrict__ count,
+                                   const unsigned long long* __restrict__ keys, uint2* __restrict__ ranges) {
+    const uint64_t p = *count;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < p;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
+        if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t) ranges[t].x = static_cast<uint32_t>(i);
+        if (i == p - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t)
+            ranges[t].y = static_cast<uint32_t>(i + 1);
+    }
+}
+
+__global__ void finish_scan_kernel(const unsigned long long* __restrict__ total, uint64_t capacity,
+                                   Counters* __restrict__ ctr) {
+    const unsigned long long p = *total;
+    ctr->tile_entries += p;
+    if (p > ctr->max_chunk_entries) ctr->max_chunk_entries = p;
+    if (p > capacity) ctr->key_overflow = 1;
+    ctr->chunk_entries = p < capacity ? p : capacity;
 }
 
 }  // namespace
 
-void launch_count_tiles(uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* ntiles,
-                        const int4* rects, const uint8_t* done, int tiles_x,
-                        unsigned long long* counts, cudaStream_t stream) {
-    const uint64_t n = re - rb + 1;
-    count_tiles_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
-        rb, re, order, ntiles, rects, done, tiles_x, counts);
+static size_t bitmap_smem(const uint32_t* done, int ntile) {
+    return done && ntile <= kMaxBitmapTiles ? static_cast<size_t>((ntile + 31) / 32) * 4 : 0;
 }
 
-void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* ntiles,
-                           const int4* rects, const uint8_t* done, const unsigned long long* offsets,
-                           int tiles_x, unsigned long long* keys, cudaStream_t stream) {
+void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
+                        int4* brect, uint2* bmeta, cudaStream_t stream) {
+    if (n == 0) return;
+    gather_bins_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, order, rects, ntiles,
+                                                                                 brect, bmeta);
+}
+
+void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
+                        const uint32_t* done, int tiles_x, int ntile, unsigned long long* counts,
+                        cudaStream_t stream) {
+    const uint64_t n = re - rb + 1;
+    // large CTAs amortise the bitmap load
+    count_tiles_kernel<<<static_cast<unsigned>((n + 1023) / 1024), 1024, bitmap_smem(done, ntile), stream>>>(
+        rb, re, bmeta, brect, done, tiles_x, ntile, counts);
+}
+
+void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
+                           const uint32_t* done, const unsigned long long* offsets,
+                           int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
+                           cudaStream_t stream) {
     if (re <= rb) return;
     const uint64_t n = re - rb;
-    emit_keys_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
-        rb, re, order, ntiles, rects, done, offsets, tiles_x, keys);
+    emit_keys_kernel<<<static_cast<unsigned>((n + 1023) / 1024), 1024, bitmap_smem(done, ntile), stream>>>(
+        rb, re, bmeta, brect, done, offsets, tiles_x, ntile, keys, capacity);
 }
 
-void launch_tile_ranges(uint64_t p, const unsigned long long* keys, uint2* ranges,
+void launch_tile_ranges(const unsigned long long* d_count, const unsigned long long* keys, uint2* ranges,
                         cudaStream_t stream) {
-    if (p == 0) return;
-    const unsigned blocks = static_cast<unsigned>((p + 255) / 256);
-    tile_ranges_kernel<<<blocks, 256, 0, stream>>>(p, keys, ranges);
+    tile_ranges_kernel<<<148 * 8, 256, 0, stream>>>(d_count, keys, ranges);
+}
+
+void launch_finish_scan(const unsigned long long* total, uint64_t capacity, Counters* ctr,
+                        cudaStream_t stream) {
+    finish_scan_kernel<<<1, 1, 0, stream>>>(total, capacity, ctr);
 }
 
 }  // namespace sgs

@@ -92,9 +92,12 @@ struct sgs_context {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
     std::mutex mu;
-    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, rects, ntiles, counts, offsets;
+    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, rects, ntiles, brect, bmeta, counts, offsets;
     uint64_t iota_n = 0;
-    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, frame_rgb[2], frame_T[2];
+    DevBuf buckets;  // K2 bucket histogram / offsets / cursors
+    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist, frame_rgb[2],
+        frame_T[2];
+    uint64_t tkey_cap = 0;  // tile keys per buffer (grow-only, sized from observed P)
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;
     Counters* h_ctr_init = nullptr;  // pinned initial counters block (err/kmin = ~0)
@@ -188,6 +191,9 @@ int ceil_log2(uint64_t v) {
 }
 
 enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
+// run_frame_once results besides sgs_status
+constexpr int kRetryWide = 100;  // a run of equal 32-bit depth keys: redo with 64-bit keys
+constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, redo
 
 // Depth chunking: the first chunk holds the
 // nearest ceil(N / kFirstChunkDiv) ranks; tiles whose pixels all terminate inside it
@@ -198,20 +204,25 @@ sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, c
     uint32_t* order = ctx->order.as<uint32_t>();
     size_t temp = 0;
     if (!wide) {
-        // K2: 32-bit keys (4 passes) + exact tie fix-up
-        launch_make_key32(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, ctx->key32_a.as<uint32_t>(), s);
-        ctx->own_launches += 1;
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, ctx->key32_a.as<uint32_t>(), ctx->key32_b.as<uint32_t>(),
-                                                 ctx->iota.as<uint32_t>(), order, static_cast<int>(n), 0, 32, s));
+        // K2: exact bucket sort (depth_sort.cu)
+        const int log2b = depth_bucket_log2(n);
+        const uint32_t nb = 1u << log2b;
+        SGS_CUDA(ctx->buckets.ensure(static_cast<size_t>(nb + 1) * 4 * 4));
+        uint32_t* hist = ctx->buckets.as<uint32_t>();
+        uint32_t* off = hist + (nb + 1);
+        uint32_t* cursor = off + (nb + 1);
+        SGS_CUDA(cudaMemsetAsync(hist, 0, static_cast<size_t>(nb + 1) * 4, s));
+        SGS_CUDA(cudaMemsetAsync(cursor, 0, static_cast<size_t>(nb + 1) * 4, s));
+        launch_bucket_hist(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, log2b, hist, s);
+        SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, hist, off, static_cast<int>(nb + 1), s));
         SGS_CUDA(ctx->cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp, ctx->key32_a.as<uint32_t>(),
-                                                 ctx->key32_b.as<uint32_t>(), ctx->iota.as<uint32_t>(), order,
-                                                 static_cast<int>(n), 0, 32, s));
-        ctx->lib_launches += 1 + 4;
-        launch_fix_ties(n, ctx->key32_b.as<uint32_t>(), ctx->keys_a.as<unsigned long long>(), order, ctx->d_ctr, s);
-        ctx->own_launches += 1;
+        SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, hist, off, static_cast<int>(nb + 1), s));
+        launch_bucket_scatter(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, log2b, off, cursor, order, s);
+        launch_bucket_sort(nb, off, ctx->keys_a.as<unsigned long long>(), order, ctx->d_ctr, cursor + (nb + 1), s);
+        ctx->own_launches += 4;
+        ctx->lib_launches += 2;
     } else {
-        // fallback: full 64-bit keys (8 passes), no fix-up needed
+        // fallback: full 64-bit keys (8 passes); stable, so ties keep index order
         SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, ctx->keys_a.as<unsigned long long>(),
                                                  ctx->keys_b.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
                                                  order, static_cast<int>(n), 0, 64, s));
@@ -226,34 +237,33 @@ sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, c
     return SGS_OK;
 }
 
-// K3 for ranks [rb, re): counts -> exclusive scan -> P on the host (one sync).
-sgs_status count_and_scan(sgs_context* ctx, uint64_t rb, uint64_t re, const uint32_t* order, const uint8_t* done,
-                          int tiles_x, cudaStream_t s) {
+// K3 for ranks [rb, re): counts -> exclusive scan; the total P stays on the device.
+sgs_status count_and_scan(sgs_context* ctx, uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* done,
+                          int tiles_x, int ntile, cudaStream_t s) {
     const uint64_t m = re - rb;
-    launch_count_tiles(rb, re, order, ctx->ntiles.as<uint32_t>(), ctx->rects.as<int4>(), done, tiles_x,
+    (void)order;
+    launch_count_tiles(rb, re, ctx->bmeta.as<uint2>(), ctx->brect.as<int4>(), done, tiles_x, ntile,
                        ctx->counts.as<unsigned long long>(), s);
-    ctx->own_launches += 1;
     size_t temp = 0;
     SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, ctx->counts.as<unsigned long long>(),
                                            ctx->offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
     SGS_CUDA(ctx->cub_temp.ensure(temp));
     SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, ctx->counts.as<unsigned long long>(),
                                            ctx->offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
+    launch_finish_scan(ctx->offsets.as<unsigned long long>() + m, ctx->tkey_cap, ctx->d_ctr, s);
+    ctx->own_launches += 2;
     ctx->lib_launches += 2;
-    SGS_CUDA(cudaMemcpyAsync(&ctx->d_ctr->tile_entries, ctx->offsets.as<unsigned long long>() + m,
-                             sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-    SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-    SGS_CUDA(cudaStreamSynchronize(s));
     return SGS_OK;
 }
 
 // One frame on ctx->stream. Outputs are device pointers (either may be null).
-sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
-                     const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
-                     DebugSplat* d_debug, FrameMode mode) {
-    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
-    sgs_status st = validate_camera(cam);
-    if (st != SGS_OK) return st;
+// The whole frame is enqueued without a host round trip (every data-dependent
+// size lives on the device); one synchronisation at the end reads the counters,
+// reports errors, and -- rarely -- regrows the tile-key arena or falls back to the
+// 64-bit depth sort and renders the frame again.
+int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                          const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
+                          DebugSplat* d_debug, FrameMode mode, bool wide_sort) {
     cudaStream_t s = ctx->stream;
     const uint64_t n = scene->meta.count;
     const CamParams cp = make_cam(cam);
@@ -265,24 +275,27 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
 
     SGS_CUDA(ctx->keys_a.ensure(n1 * 8));
     SGS_CUDA(ctx->keys_b.ensure(n1 * 8));
-    SGS_CUDA(ctx->key32_a.ensure(n1 * 4));
-    SGS_CUDA(ctx->key32_b.ensure(n1 * 4));
     if (ctx->iota.bytes < n1 * 4) ctx->iota_n = 0;
     SGS_CUDA(ctx->iota.ensure(n1 * 4));
     SGS_CUDA(ctx->order.ensure(n1 * 4));
     SGS_CUDA(ctx->rec.ensure(n1 * sizeof(SplatRec)));
     SGS_CUDA(ctx->rects.ensure(n1 * sizeof(int4)));
     SGS_CUDA(ctx->ntiles.ensure(n1 * 4));
+    SGS_CUDA(ctx->brect.ensure(n1 * sizeof(int4)));
+    SGS_CUDA(ctx->bmeta.ensure(n1 * sizeof(uint2)));
     SGS_CUDA(ctx->counts.ensure((n + 1) * 8));
     SGS_CUDA(ctx->offsets.ensure((n + 1) * 8));
     SGS_CUDA(ctx->ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
+    SGS_CUDA(ctx->sort_hist.ensure(tile_sort_hist_bytes()));
+    if (ctx->tkey_cap == 0) ctx->tkey_cap = std::max<uint64_t>(16 * n, 1 << 20);
+    SGS_CUDA(ctx->tkeys_a.ensure(ctx->tkey_cap * 8));
+    SGS_CUDA(ctx->tkeys_b.ensure(ctx->tkey_cap * 8));
 
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[0], s));
     SGS_CUDA(cudaMemcpyAsync(ctx->d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
     if (mode == kRender) {
-        // the pinned staging block is reused every frame: wait until the previous
-        // frame's copy has been consumed (frames are sequential on the stream anyway)
-        SGS_CUDA(cudaStreamSynchronize(s));
+        // the pinned staging block is reused every frame; the previous frame has
+        // completed (run_frame synchronises at its end)
         ctx->h_consts->sp = scene->planes;
         ctx->h_consts->cam = cp;
         SGS_CUDA(cudaMemcpyAsync(ctx->d_consts, ctx->h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
@@ -308,9 +321,13 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
     // K2
     const uint32_t* order = ctx->iota.as<uint32_t>();
     if (n > 1) {
-        st = sort_depth(ctx, n, false, s, &order);
+        sgs_status st = sort_depth(ctx, n, wide_sort, s, &order);
         if (st != SGS_OK) return st;
     }
+    // rank-ordered binning inputs, gathered once for every chunk
+    launch_gather_bins(n, order, ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->brect.as<int4>(),
+                       ctx->bmeta.as<uint2>(), s);
+    if (n) ctx->own_launches += 1;
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[2], s));
 
     // depth chunks over ranks (bounds known on the host: culled splats sort last and
@@ -323,76 +340,50 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
             const uint64_t b = (n + div - 1) / div;
             if (b > bounds.back() && b < n) bounds.push_back(b);
         }
-        SGS_CUDA(ctx->tile_done.ensure(std::max<uint64_t>(ntile, 1)));
+        SGS_CUDA(ctx->tile_done.ensure((ntile + 31) / 32 * 4));
         SGS_CUDA(ctx->pix_state.ensure(npx * sizeof(PixelState)));
         SGS_CUDA(ctx->pix_walked.ensure(npx * sizeof(uint32_t)));
-        SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, ntile, s));
+        SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, (ntile + 31) / 32 * 4, s));
     }
     bounds.push_back(n);
     const int nchunks = static_cast<int>(bounds.size()) - 1;
     const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
                                   static_cast<float>(scene->meta.background[1]),
                                   static_cast<float>(scene->meta.background[2]));
-    uint64_t v = 0, p_total = 0;
+    const int tile_bits = std::max(1, ceil_log2(ntile));
+    const unsigned long long* d_pc = &ctx->d_ctr->chunk_entries;
     float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
     for (int c = 0; c < nchunks; ++c) {
         const uint64_t rb = bounds[c], re = bounds[c + 1];
-        const uint8_t* done = c > 0 ? ctx->tile_done.as<uint8_t>() : nullptr;
+        const uint32_t* done = c > 0 ? ctx->tile_done.as<uint32_t>() : nullptr;
         if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[3], s));
-        st = count_and_scan(ctx, rb, re, order, done, kp.tiles_x, s);
+        // K3 + K4
+        sgs_status st = count_and_scan(ctx, rb, re, order, done, kp.tiles_x, static_cast<int>(ntile), s);
         if (st != SGS_OK) return st;
-        if (c == 0) {
-            if (ctx->h_ctr->err != ~0ULL) return device_error(ctx->h_ctr->err, scene, cfg);
-            if (ctx->h_ctr->tie_overflow) {
-                // a long run of equal 32-bit depth keys: redo K2 with 64-bit keys
-                st = sort_depth(ctx, n, true, s, &order);
-                if (st != SGS_OK) return st;
-                st = count_and_scan(ctx, rb, re, order, done, kp.tiles_x, s);
-                if (st != SGS_OK) return st;
-            }
-            v = ctx->h_ctr->visible;
-        }
-        const uint64_t p = ctx->h_ctr->tile_entries;
-        if (p > 0x7FFFFFFFULL) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^31 tile entries in one chunk");
-        p_total += p;
-        // K4
-        SGS_CUDA(ctx->tkeys_a.ensure(std::max<uint64_t>(p, 1) * 8));
-        SGS_CUDA(ctx->tkeys_b.ensure(std::max<uint64_t>(p, 1) * 8));
-        launch_emit_tile_keys(rb, re, order, ctx->ntiles.as<uint32_t>(), ctx->rects.as<int4>(), done,
-                              ctx->offsets.as<unsigned long long>(), kp.tiles_x,
-                              ctx->tkeys_a.as<unsigned long long>(), s);
+        launch_emit_tile_keys(rb, re, ctx->bmeta.as<uint2>(), ctx->brect.as<int4>(), done,
+                              ctx->offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
+                              ctx->tkeys_a.as<unsigned long long>(), ctx->tkey_cap, s);
         SGS_CUDA(cudaGetLastError());
         if (re > rb) ctx->own_launches += 1;
         if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[4], s));
-        // K5
-        const unsigned long long* tkeys = ctx->tkeys_a.as<unsigned long long>();
-        if (p > 1 && ntile > 1) {
-            cub::DoubleBuffer<unsigned long long> tb(ctx->tkeys_a.as<unsigned long long>(),
-                                                     ctx->tkeys_b.as<unsigned long long>());
-            const int end_bit = 32 + std::max(1, ceil_log2(ntile));
-            size_t temp = 0;
-            SGS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
-            SGS_CUDA(ctx->cub_temp.ensure(temp));
-            SGS_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_temp.ptr, temp, tb, static_cast<int>(p), 32, end_bit, s));
-            tkeys = tb.Current();
-            ctx->lib_launches += 1 + (end_bit - 32 + 7) / 8;
-        }
+        // K5 (device-sized stable radix sort on the tile bits)
+        const unsigned long long* tkeys = tile_sort(ctx->tkeys_a.as<unsigned long long>(),
+                                                    ctx->tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
+                                                    ctx->sort_hist.as<uint32_t>(), s, &ctx->own_launches);
         // K6
         SGS_CUDA(cudaMemsetAsync(ctx->ranges.ptr, 0, ntile * sizeof(uint2), s));
-        launch_tile_ranges(p, tkeys, ctx->ranges.as<uint2>(), s);
+        launch_tile_ranges(d_pc, tkeys, ctx->ranges.as<uint2>(), s);
         SGS_CUDA(cudaGetLastError());
-        if (p) ctx->own_launches += 1;
+        ctx->own_launches += 1;
         if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[5], s));
         ctx->last_order = order;
         ctx->last_tile_keys = tkeys;
-        ctx->last_v = v;
-        ctx->last_p = p;
         // K7
         if (mode == kRender) {
             launch_composite(ctx->d_consts, cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
-                             bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(),
-                             ctx->pix_walked.as<uint32_t>(), ctx->tile_done.as<uint8_t>(), c == 0,
-                             c == nchunks - 1, ctx->d_ctr, stats != nullptr, s);
+                             bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(), ctx->pix_walked.as<uint32_t>(),
+                             ctx->tile_done.as<uint32_t>(), c == 0, c == nchunks - 1, ctx->d_ctr,
+                             stats != nullptr, s);
             SGS_CUDA(cudaGetLastError());
             ctx->own_launches += 1;
         }
@@ -409,14 +400,22 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
         }
     }
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[7], s));
-    ctx->last_p = p_total;
+    SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaStreamSynchronize(s));
+    const Counters& hc = *ctx->h_ctr;
+    if (hc.err != ~0ULL) return device_error(hc.err, scene, cfg);
+    if (hc.tie_overflow && !wide_sort) return kRetryWide;
+    if (hc.key_overflow) {
+        ctx->tkey_cap = hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024;
+        return kRetryGrow;
+    }
+    ctx->last_v = hc.visible;
+    ctx->last_p = hc.chunk_entries;  // the (single) chunk's P for the debug dump
     if (stats) {
-        SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-        SGS_CUDA(cudaStreamSynchronize(s));
-        stats->visible += v;
-        stats->tile_entries += p_total;
-        stats->block_entries += ctx->h_ctr->block_entries;
-        stats->guard_hits += ctx->h_ctr->guard_hits;
+        stats->visible += hc.visible;
+        stats->tile_entries += hc.tile_entries;
+        stats->block_entries += hc.block_entries;
+        stats->guard_hits += hc.guard_hits;
         if (timing) {
             float k1 = 0, k2 = 0, total = 0;
             SGS_CUDA(cudaEventElapsedTime(&k1, ctx->ev[0], ctx->ev[1]));
@@ -431,6 +430,25 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
         }
     }
     return SGS_OK;
+}
+
+sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                     const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
+                     DebugSplat* d_debug, FrameMode mode) {
+    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
+    sgs_status st = validate_camera(cam);
+    if (st != SGS_OK) return st;
+    bool wide = false;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        const int rc = run_frame_once(ctx, scene, cam, cfg, d_rgb, d_T, stats, d_debug, mode, wide);
+        if (rc == kRetryWide) {
+            wide = true;
+            continue;
+        }
+        if (rc == kRetryGrow) continue;
+        return static_cast<sgs_status>(rc);
+    }
+    return fail(SGS_ERR_INTERNAL, "frame did not converge after re-sizing");
 }
 
 // ---------------------------------------------------------------------------
@@ -642,9 +660,9 @@ void sgs_destroy(sgs_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->key32_a, &ctx->key32_b, &ctx->iota, &ctx->order,
-                      &ctx->rec, &ctx->rects, &ctx->ntiles, &ctx->counts, &ctx->offsets,
+                      &ctx->rec, &ctx->rects, &ctx->ntiles, &ctx->brect, &ctx->bmeta, &ctx->counts, &ctx->offsets,
                       &ctx->tkeys_a, &ctx->tkeys_b, &ctx->ranges, &ctx->tile_done, &ctx->pix_state,
-                      &ctx->pix_walked, &ctx->cub_temp, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
+                      &ctx->pix_walked, &ctx->cub_temp, &ctx->sort_hist, &ctx->buckets, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
                       &ctx->frame_T[0], &ctx->frame_T[1]})
         b->release();
     if (ctx->d_ctr) cudaFree(ctx->d_ctr);

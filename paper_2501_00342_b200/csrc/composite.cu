@@ -85,16 +85,23 @@ __device__ __forceinline__ float mahal2(const float4& A, float Bx, float fcx, fl
     return fmaf(fmaf(A.z, dx, A.w * dy), dx, Bx * dy * dy);
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float fast_alpha(float m2, float lop) {
-    // op * exp(-m2/2) = 2^(log2 op - m2 log2(e)/2), clamped at 0.999
-    return fminf(exp2f(fmaf(m2, -0.72134752044448170f, lop)), 0.999f);
+    // op * exp(-m2/2) = 2^(log2 op - m2 log2(e)/2), clamped at 0.999 (the decision
+    // that alpha >= 1/255 was already taken exactly on m2)
+    return fminf(ex2_approx(fmaf(m2, -0.72134752044448170f, lop)), 0.999f);
 }
 
 __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
     const SplatRec* __restrict__ rec, float3 bg, float* __restrict__ out_rgb, float* __restrict__ out_T,
-    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint8_t* __restrict__ tile_done,
+    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
     int first, int last, Counters* __restrict__ ctr, int want_stats) {
     // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
     // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
@@ -108,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
     const int tile = blockIdx.x / nchunks;
     const int chunk = blockIdx.x - tile * nchunks;
     // Tiles that terminated in an earlier depth chunk already wrote their output.
-    if (!first && tile_done[tile]) return;
+    if (!first && ((tile_done[tile >> 5] >> (tile & 31)) & 1u)) return;
     const uint2 range = ranges[tile];
     const uint32_t start = range.x, end = range.y;
     if (!first && !last && start == end) return;
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
             processed_io[pix] = walked + processed;
         }
     }
-    if (!last && all_done && threadIdx.x == 0) tile_done[tile] = 1;
+    if (!last && all_done && threadIdx.x == 0) atomicOr(&tile_done[tile >> 5], 1u << (tile & 31));
     if (want_stats) {
         // E_t = max over the tile's pixels of the entries of its full list each pixel
         // walked (counted when the tile finalises); guard hits summed over chunks.
@@ -329,7 +336,7 @@ int composite_pixel_chunks(int ts) {
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
                       float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
-                      uint8_t* tile_done, bool first, bool last, Counters* counters, bool want_stats,
+                      uint32_t* tile_done, bool first, bool last, Counters* counters, bool want_stats,
                       cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
     const long long ntiles = static_cast<long long>(cfg.tiles_x) * cfg.tiles_y;

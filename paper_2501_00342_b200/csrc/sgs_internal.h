@@ -113,7 +113,12 @@ struct Counters {
     unsigned long long kmax;
     unsigned long long tie_runs;      // 32-bit depth-key collisions re-sorted by K2b
     unsigned long long tie_overflow;  // runs too long for K2b (host falls back to 64-bit)
-    unsigned long long pad[7];
+    unsigned long long key_overflow;  // a chunk needed more tile keys than allocated
+    unsigned long long max_chunk_entries;  // largest chunk P (sizes the retry)
+    unsigned long long chunk_entries;  // P of the chunk in flight (clamped to capacity)
+    unsigned long long culled_cursor;  // K2 scatter slot for culled splats
+    unsigned long long big_buckets;    // K2 buckets queued for the warp sort
+    unsigned long long pad[2];
 };
 static_assert(sizeof(Counters) == 128, "counters block");
 
@@ -139,26 +144,40 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
                        uint32_t* ntiles, Counters* counters, DebugSplat* debug, cudaStream_t stream);
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
-void launch_make_key32(uint64_t n, const unsigned long long* key64, const Counters* ctr,
-                       uint32_t* key32, cudaStream_t stream);
-void launch_fix_ties(uint64_t n, const uint32_t* key32, const unsigned long long* key64,
-                     uint32_t* order, Counters* ctr, cudaStream_t stream);
+int depth_bucket_log2(uint64_t n);
+void launch_bucket_hist(uint64_t n, const unsigned long long* key, const Counters* ctr, int log2b, uint32_t* hist,
+                        cudaStream_t stream);
+void launch_bucket_scatter(uint64_t n, const unsigned long long* key, Counters* ctr, int log2b, const uint32_t* off,
+                           uint32_t* cursor, uint32_t* out, cudaStream_t stream);
+void launch_bucket_sort(uint32_t nbuckets, const uint32_t* off, const unsigned long long* key, uint32_t* order,
+                        Counters* ctr, uint32_t* big, cudaStream_t stream);
 // Tile counts for ranks [rb, re) skipping tiles already terminated (done may be null);
 // counts has re-rb+1 entries (the last is 0 so an exclusive scan yields the total).
-void launch_count_tiles(uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* ntiles,
-                        const int4* rects, const uint8_t* done, int tiles_x,
-                        unsigned long long* counts, cudaStream_t stream);
-void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* ntiles,
-                           const int4* rects, const uint8_t* done, const unsigned long long* offsets,
-                           int tiles_x, unsigned long long* keys, cudaStream_t stream);
-void launch_tile_ranges(uint64_t p, const unsigned long long* keys, uint2* ranges,
+void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
+                        int4* brect, uint2* bmeta, cudaStream_t stream);
+void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
+                        const uint32_t* done, int tiles_x, int ntile, unsigned long long* counts,
                         cudaStream_t stream);
+void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
+                           const uint32_t* done, const unsigned long long* offsets,
+                           int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
+                           cudaStream_t stream);
+// Ranges of the sorted keys; the count is read from device memory.
+void launch_tile_ranges(const unsigned long long* d_count, const unsigned long long* keys, uint2* ranges,
+                        cudaStream_t stream);
+// After K3's scan: P = offsets[m]; clamp to capacity, flag overflow, accumulate P.
+void launch_finish_scan(const unsigned long long* total, uint64_t capacity, Counters* ctr,
+                        cudaStream_t stream);
+int tile_sort_grid();
+size_t tile_sort_hist_bytes();
+unsigned long long* tile_sort(unsigned long long* a, unsigned long long* b, const unsigned long long* d_count,
+                              int tile_bits, uint32_t* hist, cudaStream_t stream, uint64_t* launches);
 // K7 over one depth chunk. first/last select state init / final output; tile_done and
 // state may be null when the frame is a single chunk.
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
                       float3 bg, float* rgb, float* T,
-                      PixelState* state, uint32_t* processed, uint8_t* tile_done, bool first,
+                      PixelState* state, uint32_t* processed, uint32_t* tile_done, bool first,
                       bool last, Counters* counters, bool want_stats, cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
 

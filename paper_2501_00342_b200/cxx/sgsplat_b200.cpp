@@ -1,0 +1,568 @@
+// sgsplat_b200.cpp -- the reference's C++ render API (include/sgsplat/*.hpp) served
+// by the B200 renderer through the C-ABI (include/sgs.h).
+//
+// render()/project() convert the caller's Scene (AoS doubles, std::variant colour)
+// into the reference's flat parameter layout (Scene::param order, scene.hpp:40-43),
+// upload it, and run the sm_100a pipeline; the float32 frame is widened into the
+// double Image the reference returns (raster.hpp:49-52). sgs_* error codes are
+// rethrown as the reference's exceptions (common.hpp:21-42). The scalar colour /
+// scene / camera helpers are host code with the reference's semantics; they are
+// utilities, not a render fallback -- render() has no CPU path.
+#include "sgs.h"
+#include "sgsplat/raster.hpp"
+#include "sgsplat/synth.hpp"
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+
+namespace sgsplat {
+
+namespace {
+
+[[noreturn]] void rethrow(int status) {
+    const std::string msg = sgs_last_error();
+    if (status == SGS_ERR_INVALID_ARGUMENT) throw InvalidArgument(msg);
+    if (status == SGS_ERR_NUMERIC) throw NumericError(msg);
+    throw std::runtime_error("B200 renderer: " + msg);
+}
+
+void check(int status) {
+    if (status != SGS_OK) rethrow(status);
+}
+
+sgs_context* context() {
+    static std::once_flag once;
+    static sgs_context* ctx = nullptr;
+    static int status = SGS_OK;
+    std::call_once(once, [] {
+        const char* dev = std::getenv("SGS_DEVICE");
+        status = sgs_create(dev ? std::atoi(dev) : 0, &ctx);
+    });
+    if (status != SGS_OK) rethrow(status);
+    return ctx;
+}
+
+int stored_degree(const ColorModel& m) {
+    if (auto* s = std::get_if<SHOnlyModel>(&m)) return s->sh.degree;
+    if (auto* x = std::get_if<MixedSHSGModel>(&m)) return x->sh.degree;
+    return 0;
+}
+
+sgs_camera to_c(const Camera& cam) {
+    sgs_camera c{};
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) c.R[r * 3 + k] = cam.rotation(r, k);
+    for (int r = 0; r < 3; ++r) c.t[r] = cam.translation[r];
+    c.fx = cam.fx;
+    c.fy = cam.fy;
+    c.cx = cam.cx;
+    c.cy = cam.cy;
+    c.width = cam.width;
+    c.height = cam.height;
+    c.near_plane = cam.near;
+    return c;
+}
+
+sgs_render_config to_c(const RenderConfig& cfg) {
+    sgs_render_config k{};
+    k.tile_size = cfg.tile_size;
+    k.has_override = cfg.sh_degree_override.has_value() ? 1 : 0;
+    k.override_degree = cfg.sh_degree_override.value_or(0);
+    k.threads = cfg.threads;
+    k.degree_threshold_lo = cfg.degree_threshold_lo;
+    k.degree_threshold_hi = cfg.degree_threshold_hi;
+    k.early_stop_transmittance = cfg.early_stop_transmittance;
+    return k;
+}
+
+// RAII device scene built from a (homogeneous) Scene.
+struct DeviceScene {
+    sgs_scene* s = nullptr;
+    std::vector<double> flat;
+    DeviceScene(const std::vector<GaussianPrimitive>& gs, const Mat3& axes, const Vec3& bg) {
+        sgs_scene_desc d{};
+        d.count = gs.size();
+        d.kind = gs.empty() ? SGS_SH : static_cast<int32_t>(kind_of(gs.front().color));
+        d.sh_degree = gs.empty() ? 0 : stored_degree(gs.front().color);
+        d.dtype = SGS_F64;
+        if (!gs.empty()) {
+            const std::size_t stride = kGeometryParams + param_count(gs.front().color);
+            flat.resize(gs.size() * stride);
+            for (std::size_t i = 0; i < gs.size(); ++i) {
+                const GaussianPrimitive& g = gs[i];
+                double* p = flat.data() + i * stride;
+                for (int k = 0; k < 3; ++k) p[k] = g.position[k];
+                for (int k = 0; k < 4; ++k) p[3 + k] = g.rotation[k];
+                for (int k = 0; k < 3; ++k) p[7 + k] = g.log_scale[k];
+                p[10] = g.opacity_logit;
+                const int nc = static_cast<int>(stride) - kGeometryParams;
+                for (int k = 0; k < nc; ++k) p[kGeometryParams + k] = color_param(g.color, k);
+            }
+            d.params = flat.data();
+        }
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) d.shared_axes[r * 3 + c] = axes(r, c);
+        for (int c = 0; c < 3; ++c) d.background[c] = bg[c];
+        check(sgs_scene_upload(context(), &d, &s));
+    }
+    ~DeviceScene() { sgs_scene_free(s); }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------- raster
+
+int select_degree(double radius_px, double lo, double hi) {
+    int32_t out = 0;
+    check(sgs_select_degree(radius_px, lo, hi, &out));
+    return out;
+}
+
+int flops_per_gaussian(ColorModelKind kind, int sh_degree) {
+    int32_t out = 0;
+    check(sgs_flops_per_gaussian(static_cast<int32_t>(kind), sh_degree, &out));
+    return out;
+}
+
+std::optional<Splat2D> project(const GaussianPrimitive& g, const Camera& cam, const Mat3& shared_axes,
+                               const RenderConfig& cfg) {
+    DeviceScene ds({g}, shared_axes, Vec3::Zero());
+    const sgs_camera c = to_c(cam);
+    const sgs_render_config k = to_c(cfg);
+    sgs_splat out{};
+    check(sgs_project(context(), ds.s, &c, &k, &out));
+    if (!out.visible) return std::nullopt;
+    Splat2D s;
+    s.mean2d = Vec2(out.mean2d[0], out.mean2d[1]);
+    s.conic = Vec3(out.conic[0], out.conic[1], out.conic[2]);
+    s.depth = out.depth;
+    s.color = Vec3(out.color[0], out.color[1], out.color[2]);
+    s.opacity = out.opacity;
+    s.radius_px = out.radius;
+    return s;
+}
+
+RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& cfg) {
+    if (cfg.tile_size < 1) throw InvalidArgument("tile_size must be >= 1");
+    scene.check_homogeneous();
+    cam.validate();
+    DeviceScene ds(scene.gaussians, scene.shared_axes, scene.background);
+    const sgs_camera c = to_c(cam);
+    const sgs_render_config k = to_c(cfg);
+    const std::size_t npx = static_cast<std::size_t>(cam.width) * static_cast<std::size_t>(cam.height);
+    std::vector<float> rgb(npx * 3), T(npx);
+    check(sgs_render(context(), ds.s, &c, &k, rgb.data(), T.data(), SGS_HOST, nullptr));
+    RenderResult out;
+    out.image = Image(cam.width, cam.height, 3);
+    out.transmittance = Image(cam.width, cam.height, 1);
+    for (std::size_t i = 0; i < npx * 3; ++i) out.image.data[i] = rgb[i];
+    for (std::size_t i = 0; i < npx; ++i) out.transmittance.data[i] = T[i];
+    return out;
+}
+
+// ---------------------------------------------------------------------------- common / scene
+
+Mat3 quat_to_rotation(const Vec4& q_raw) {
+    const double n = q_raw.norm();
+    if (n < 1e-12) throw NumericError("degenerate rotation: zero quaternion");
+    const Vec4 q = q_raw / n;
+    const double w = q[0], x = q[1], y = q[2], z = q[3];
+    Mat3 r;
+    r << 1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),  //
+        2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),   //
+        2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y);
+    return r;
+}
+
+Mat3 covariance(const Vec4& rotation, const Vec3& log_scale) {
+    const Mat3 m = quat_to_rotation(rotation) * Vec3(log_scale.array().exp()).asDiagonal();
+    return m * m.transpose();
+}
+
+double gaussian_density(const GaussianPrimitive& g, const Vec3& x) {
+    const Mat3 sigma = covariance(g.rotation, g.log_scale) + 1e-9 * Mat3::Identity();
+    const double det = sigma.determinant();
+    if (!(det > 0.0) || !std::isfinite(det)) throw NumericError("covariance is singular after regularization");
+    const Vec3 d = x - g.position;
+    return std::exp(-0.5 * d.dot(sigma.inverse() * d));
+}
+
+void Scene::check_homogeneous() const {
+    if (gaussians.empty()) return;
+    const ColorModelKind kind = kind_of(gaussians.front().color);
+    const int deg = stored_degree(gaussians.front().color);
+    for (std::size_t i = 1; i < gaussians.size(); ++i) {
+        const ColorModel& c = gaussians[i].color;
+        if (kind_of(c) != kind)
+            throw InvalidArgument("scene mixes color model variants (gaussian " + std::to_string(i) + ")");
+        if ((kind == ColorModelKind::SHOnly || kind == ColorModelKind::MixedSHSG) && stored_degree(c) != deg)
+            throw InvalidArgument("scene mixes SH degrees");
+    }
+}
+
+ColorModelKind Scene::model_kind() const {
+    if (gaussians.empty()) throw InvalidArgument("empty scene has no color model");
+    check_homogeneous();
+    return kind_of(gaussians.front().color);
+}
+
+void Scene::set_shared_axes(const Mat3& axes) {
+    validate_ortho_axes(axes);
+    shared_axes = axes;
+}
+
+std::size_t Scene::params_per_gaussian() const {
+    return gaussians.empty() ? 0 : static_cast<std::size_t>(kGeometryParams + param_count(gaussians.front().color));
+}
+
+std::size_t Scene::total_params() const { return params_per_gaussian() * gaussians.size(); }
+
+double Scene::param(std::size_t flat_index) const {
+    const std::size_t stride = params_per_gaussian();
+    if (stride == 0 || flat_index >= total_params()) throw InvalidArgument("parameter index out of range");
+    const GaussianPrimitive& g = gaussians[flat_index / stride];
+    const int slot = static_cast<int>(flat_index % stride);
+    if (slot < 3) return g.position[slot];
+    if (slot < 7) return g.rotation[slot - 3];
+    if (slot < 10) return g.log_scale[slot - 7];
+    if (slot == 10) return g.opacity_logit;
+    return color_param(g.color, slot - kGeometryParams);
+}
+
+void Scene::set_param(std::size_t flat_index, double value) {
+    const std::size_t stride = params_per_gaussian();
+    if (stride == 0 || flat_index >= total_params()) throw InvalidArgument("parameter index out of range");
+    GaussianPrimitive& g = gaussians[flat_index / stride];
+    const int slot = static_cast<int>(flat_index % stride);
+    if (slot < 3)
+        g.position[slot] = value;
+    else if (slot < 7)
+        g.rotation[slot - 3] = value;
+    else if (slot < 10)
+        g.log_scale[slot - 7] = value;
+    else if (slot == 10)
+        g.opacity_logit = value;
+    else
+        set_color_param(g.color, slot - kGeometryParams, value);
+}
+
+// ---------------------------------------------------------------------------- camera / image
+
+void Camera::validate() const {
+    if (fx <= 0 || fy <= 0) throw InvalidArgument("camera focal lengths must be positive");
+    if (width < 1 || height < 1) throw InvalidArgument("camera image size must be >= 1");
+}
+
+Camera make_orbit_camera(const Vec3& target, double distance, double angle, double elevation, int width,
+                         int height, double focal) {
+    const double t[3] = {target[0], target[1], target[2]};
+    sgs_camera c{};
+    const int st = sgs_orbit_camera(t, distance, angle, elevation, width, height, focal, &c);
+    Camera cam;
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) cam.rotation(r, k) = c.R[r * 3 + k];
+    cam.translation = Vec3(c.t[0], c.t[1], c.t[2]);
+    cam.fx = c.fx;
+    cam.fy = c.fy;
+    cam.cx = c.cx;
+    cam.cy = c.cy;
+    cam.width = c.width;
+    cam.height = c.height;
+    cam.near = c.near_plane;
+    if (st != SGS_OK) cam.validate();  // throws the reference's message
+    return cam;
+}
+
+Image Image::clamped01() const {
+    Image out = *this;
+    for (double& v : out.data) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    return out;
+}
+
+// ---------------------------------------------------------------------------- colour
+
+SHCoeffs SHCoeffs::zeros(int degree) {
+    if (degree < 0 || degree > 3) {
+        std::ostringstream m;
+        m << "unsupported SH degree " << degree << " (max 3)";
+        throw InvalidArgument(m.str());
+    }
+    SHCoeffs c;
+    c.degree = degree;
+    c.coeffs.assign(static_cast<std::size_t>(sh::coeff_count(degree)), Vec3::Zero());
+    return c;
+}
+
+void validate_ortho_axes(const Mat3& axes, double tol) {
+    const double err = (axes * axes.transpose() - Mat3::Identity()).cwiseAbs().maxCoeff();
+    if (err > tol) {
+        std::ostringstream m;
+        m << "axis triple is not orthonormal: |A A^T - I|_max = " << err;
+        throw InvalidArgument(m.str());
+    }
+}
+
+OrthoSGSet::OrthoSGSet(const std::array<SGLobe, 3>& l, const Mat3& a) : lobes(l), axes(a) {
+    validate_ortho_axes(axes);
+    for (int i = 0; i < 3; ++i) lobes[static_cast<std::size_t>(i)].mu = axes.row(i).transpose();
+}
+
+SGLobe DiffuseSGModel::lobe() const {
+    SGLobe l;
+    l.alpha = alpha;
+    l.lambda = std::exp(log_lambda);
+    const double n = mu.norm();
+    l.mu = n > 1e-12 ? Vec3(mu / n) : Vec3::UnitX();
+    return l;
+}
+
+SGLobe DiffuseOrthoSGModel::lobe(int i, const Mat3& axes) const {
+    return SGLobe{alpha[static_cast<std::size_t>(i)], std::exp(log_lambda[static_cast<std::size_t>(i)]),
+                  axes.row(i).transpose()};
+}
+
+SGLobe MixedSHSGModel::lobe(int i, const Mat3& axes) const {
+    return SGLobe{alpha[static_cast<std::size_t>(i)], std::exp(log_lambda[static_cast<std::size_t>(i)]),
+                  axes.row(i).transpose()};
+}
+
+ColorModelKind kind_of(const ColorModel& m) { return static_cast<ColorModelKind>(m.index()); }
+
+const char* to_string(ColorModelKind k) {
+    static const char* names[] = {"sh", "sg1", "sg3", "mixed"};
+    return names[static_cast<int>(k)];
+}
+
+ColorModelKind color_model_kind_from_string(const std::string& name) {
+    for (int k = 0; k < 4; ++k)
+        if (name == to_string(static_cast<ColorModelKind>(k))) return static_cast<ColorModelKind>(k);
+    throw InvalidArgument("unknown color model kind: " + name);
+}
+
+namespace {
+void require_unit(const Vec3& d) {
+    if (std::abs(d.norm() - 1.0) > 1e-6) {
+        std::ostringstream m;
+        m << "direction must be unit length, got |d| = " << d.norm();
+        throw InvalidArgument(m.str());
+    }
+}
+}  // namespace
+
+std::vector<double> eval_sh_basis(const Vec3& d, int degree) {
+    require_unit(d);
+    (void)SHCoeffs::zeros(degree);  // degree check
+    const double x = d.x(), y = d.y(), z = d.z();
+    std::vector<double> b(static_cast<std::size_t>(sh::coeff_count(degree)));
+    b[0] = sh::kC0;
+    if (degree >= 1) {
+        b[1] = -sh::kC1 * y;
+        b[2] = sh::kC1 * z;
+        b[3] = -sh::kC1 * x;
+    }
+    const double xx = x * x, yy = y * y, zz = z * z;
+    if (degree >= 2) {
+        b[4] = sh::kC2[0] * x * y;
+        b[5] = sh::kC2[1] * y * z;
+        b[6] = sh::kC2[2] * (2.0 * zz - xx - yy);
+        b[7] = sh::kC2[3] * x * z;
+        b[8] = sh::kC2[4] * (xx - yy);
+    }
+    if (degree >= 3) {
+        b[9] = sh::kC3[0] * y * (3.0 * xx - yy);
+        b[10] = sh::kC3[1] * x * y * z;
+        b[11] = sh::kC3[2] * y * (4.0 * zz - xx - yy);
+        b[12] = sh::kC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+        b[13] = sh::kC3[4] * x * (4.0 * zz - xx - yy);
+        b[14] = sh::kC3[5] * z * (xx - yy);
+        b[15] = sh::kC3[6] * x * (xx - 3.0 * yy);
+    }
+    return b;
+}
+
+Vec3 eval_sg(const SGLobe& lobe, const Vec3& d) {
+    require_unit(d);
+    return lobe.alpha * std::exp(lobe.lambda * (d.dot(lobe.mu) - 1.0));
+}
+
+namespace {
+Vec3 sh_part(const SHCoeffs& c, const Vec3& d, int deg) {
+    const auto b = eval_sh_basis(d, deg);
+    Vec3 acc = Vec3::Zero();
+    for (int i = 0; i < sh::coeff_count(deg); ++i) acc += b[static_cast<std::size_t>(i)] * c.coeffs[static_cast<std::size_t>(i)];
+    return acc;
+}
+Vec3 lobes_part(const std::array<Vec3, 3>& alpha, const std::array<double, 3>& ll, const Mat3& axes, const Vec3& d) {
+    Vec3 acc = Vec3::Zero();
+    for (int i = 0; i < 3; ++i) {
+        const double lambda = std::exp(ll[static_cast<std::size_t>(i)]);
+        acc += alpha[static_cast<std::size_t>(i)] * std::exp(lambda * (axes.row(i).dot(d) - 1.0));
+    }
+    return acc;
+}
+}  // namespace
+
+Vec3 eval_color(const ColorModel& model, const Mat3& axes, const Vec3& d, std::optional<int> ov) {
+    require_unit(d);
+    if (ov && kind_of(model) != ColorModelKind::MixedSHSG)
+        throw InvalidArgument("sh_degree_override is only valid for the mixed SH+SG model");
+    Vec3 pre = Vec3::Zero();
+    if (auto* m = std::get_if<SHOnlyModel>(&model)) {
+        pre = Vec3::Constant(0.5) + sh_part(m->sh, d, m->sh.degree);
+    } else if (auto* m1 = std::get_if<DiffuseSGModel>(&model)) {
+        pre = m1->diffuse + eval_sg(m1->lobe(), d);
+    } else if (auto* m3 = std::get_if<DiffuseOrthoSGModel>(&model)) {
+        pre = m3->diffuse + lobes_part(m3->alpha, m3->log_lambda, axes, d);
+    } else {
+        const auto& mx = std::get<MixedSHSGModel>(model);
+        int deg = mx.sh.degree;
+        if (ov) {
+            if (*ov < 0 || *ov > mx.sh.degree) {
+                std::ostringstream m;
+                m << "sh degree override " << *ov << " exceeds stored degree " << mx.sh.degree;
+                throw InvalidArgument(m.str());
+            }
+            deg = *ov;
+        }
+        pre = Vec3::Constant(0.5) + sh_part(mx.sh, d, deg) + lobes_part(mx.alpha, mx.log_lambda, axes, d);
+    }
+    return pre.cwiseMax(0.0);
+}
+
+Vec3 eval_color(const ColorModel& model, const Vec3& d, std::optional<int> ov) {
+    return eval_color(model, Mat3::Identity(), d, ov);
+}
+
+int param_count(ColorModelKind kind, int deg) { return sgs_color_param_count(static_cast<int32_t>(kind), deg); }
+
+int param_count(const ColorModel& m) { return param_count(kind_of(m), stored_degree(m)); }
+
+int shared_param_count(ColorModelKind kind) {
+    return kind == ColorModelKind::DiffuseOrthoSG || kind == ColorModelKind::MixedSHSG ? 3 : 0;
+}
+
+namespace {
+// canonical order of color.hpp:121-128 (same as sgs.h)
+double* param_slot(ColorModel& model, int i) {
+    if (i < 0 || i >= param_count(model)) throw InvalidArgument("color parameter index out of range");
+    if (auto* m = std::get_if<SHOnlyModel>(&model)) return &m->sh.coeffs[static_cast<std::size_t>(i / 3)][i % 3];
+    if (auto* m1 = std::get_if<DiffuseSGModel>(&model)) {
+        if (i < 3) return &m1->diffuse[i];
+        if (i < 6) return &m1->alpha[i - 3];
+        if (i == 6) return &m1->log_lambda;
+        return &m1->mu[i - 7];
+    }
+    if (auto* m3 = std::get_if<DiffuseOrthoSGModel>(&model)) {
+        if (i < 3) return &m3->diffuse[i];
+        const int l = (i - 3) / 4, s = (i - 3) % 4;
+        return s < 3 ? &m3->alpha[static_cast<std::size_t>(l)][s] : &m3->log_lambda[static_cast<std::size_t>(l)];
+    }
+    auto& mx = std::get<MixedSHSGModel>(model);
+    const int nsh = 3 * sh::coeff_count(mx.sh.degree);
+    if (i < nsh) return &mx.sh.coeffs[static_cast<std::size_t>(i / 3)][i % 3];
+    const int l = (i - nsh) / 4, s = (i - nsh) % 4;
+    return s < 3 ? &mx.alpha[static_cast<std::size_t>(l)][s] : &mx.log_lambda[static_cast<std::size_t>(l)];
+}
+}  // namespace
+
+double color_param(const ColorModel& model, int index) {
+    return *param_slot(const_cast<ColorModel&>(model), index);
+}
+
+void set_color_param(ColorModel& model, int index, double value) { *param_slot(model, index) = value; }
+
+// ---------------------------------------------------------------------------- synth
+
+namespace {
+double f32(double v) {
+    volatile float f = static_cast<float>(v);
+    return static_cast<double>(f);
+}
+Vec3 f32(const Vec3& v) { return Vec3(f32(v[0]), f32(v[1]), f32(v[2])); }
+// Vec3(f(), f(), f()) with g++'s right-to-left argument evaluation
+template <typename F>
+Vec3 draw3(F&& f) {
+    const double c = f(), b = f(), a = f();
+    return Vec3(a, b, c);
+}
+int band_of(int k) { return k == 0 ? 0 : (k < 4 ? 1 : (k < 9 ? 2 : 3)); }
+}  // namespace
+
+Scene make_synthetic_scene(std::size_t count, std::uint64_t seed, const SynthOptions& o) {
+    std::mt19937_64 gen(seed);
+    Scene scene;
+    scene.gaussians.reserve(count);
+    auto ur = [&](double lo, double hi) { return uniform_range(gen, lo, hi); };
+    for (std::size_t i = 0; i < count; ++i) {
+        GaussianPrimitive g;
+        const Vec3 dir = random_unit_vector(gen);
+        const double s = o.cluster_radius * std::cbrt(uniform01(gen));
+        g.position = f32(Vec3(s * dir));
+        const Vec4 q = random_unit_quaternion(gen);
+        g.rotation = Vec4(f32(q[0]), f32(q[1]), f32(q[2]), f32(q[3]));
+        g.log_scale = f32(draw3([&] { return ur(o.log_scale_min, o.log_scale_max); }));
+        g.opacity_logit = f32(logit(ur(o.opacity_min, o.opacity_max)));
+        const Vec3 base = draw3([&] { return ur(o.base_color_min, o.base_color_max); });
+        auto sh_coeffs = [&](int degree) {
+            SHCoeffs c = SHCoeffs::zeros(degree);
+            c.coeffs[0] = f32(Vec3((base - Vec3::Constant(0.5)) / sh::kC0));
+            for (int k = 1; k < sh::coeff_count(degree); ++k) {
+                const double amp = o.band_amplitude * std::pow(o.band_decay, band_of(k));
+                c.coeffs[static_cast<std::size_t>(k)] = f32(draw3([&] { return ur(-amp, amp); }));
+            }
+            return c;
+        };
+        auto lobe_set = [&](std::array<Vec3, 3>& alpha, std::array<double, 3>& ll) {
+            for (int l = 0; l < 3; ++l) {
+                const double amp = o.sg_alpha_amplitude;
+                alpha[static_cast<std::size_t>(l)] = f32(draw3([&] { return ur(-amp, amp); }));
+                ll[static_cast<std::size_t>(l)] = f32(ur(-0.5, 1.5));
+            }
+        };
+        switch (o.kind) {
+            case ColorModelKind::SHOnly:
+                g.color = SHOnlyModel{sh_coeffs(o.sh_degree)};
+                break;
+            case ColorModelKind::DiffuseSG: {
+                DiffuseSGModel m;
+                m.diffuse = f32(base);
+                const double amp = o.sg_alpha_amplitude;
+                m.alpha = f32(draw3([&] { return ur(-amp, amp); }));
+                m.log_lambda = f32(ur(-0.5, 1.5));
+                m.mu = f32(random_unit_vector(gen));
+                g.color = std::move(m);
+                break;
+            }
+            case ColorModelKind::DiffuseOrthoSG: {
+                DiffuseOrthoSGModel m;
+                m.diffuse = f32(base);
+                lobe_set(m.alpha, m.log_lambda);
+                g.color = std::move(m);
+                break;
+            }
+            case ColorModelKind::MixedSHSG: {
+                MixedSHSGModel m;
+                m.sh = sh_coeffs(2);
+                lobe_set(m.alpha, m.log_lambda);
+                g.color = std::move(m);
+                break;
+            }
+        }
+        scene.gaussians.push_back(std::move(g));
+    }
+    return scene;
+}
+
+std::vector<Camera> make_orbit_cameras(int count, int width, int height, double distance, double focal,
+                                       double elevation) {
+    std::vector<Camera> cams;
+    cams.reserve(static_cast<std::size_t>(count));
+    for (int i = 0; i < count; ++i)
+        cams.push_back(make_orbit_camera(Vec3::Zero(), distance, 2.0 * M_PI * i / count, elevation, width, height,
+                                         focal));
+    return cams;
+}
+
+}  // namespace sgsplat
