@@ -177,6 +177,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2501_00342_b200 as sg
+    from paper_2501_00342_b200 import multiview
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -186,37 +187,30 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     vpr = args.views_per_gpu
     cams_all = sg.orbit_cameras(RING, W, H, 4.0, FOCAL, 0.35)
-    my_cams = [cams_all[(rank * vpr + j) % RING] for j in range(vpr)]
+    my_cams = [cams_all[i] for i in multiview.ring_views_per_rank(vpr, world, rank, RING)]
 
     renderer = sg.Renderer(local)
     stream = torch.cuda.current_stream()
     renderer.set_stream(stream.cuda_stream)
 
-    # --- scene: synthesised on rank 0, uploaded, NCCL-broadcast to the others ---
+    # --- scene: synthesised on rank 0, packed into its device layout, NCCL-broadcast
+    # to the others as one blob, bound without a copy (paper_2501_00342_b200.multiview)
     t_b0 = time.perf_counter()
-    meta_holder = [None]
-    if rank == 0:
-        scene = sg.synth_scene(N_GAUSS, "mixed", SEED, log_scale_range=LOG_SCALE)
-        meta = sg.Renderer.plan(scene)
-        meta_holder[0] = bytes(meta)
-    if world > 1:
-        dist.broadcast_object_list(meta_holder, src=0)
-    meta = sg._capi.sgs_scene_meta.from_buffer_copy(meta_holder[0])
-    blob = torch.empty(meta.blob_bytes, dtype=torch.uint8, device="cuda")
-    if rank == 0:
-        dscene = renderer.upload_into(scene, blob.data_ptr(), meta.blob_bytes, keepalive=blob)
-        del scene
-    torch.cuda.synchronize()
+    scene = sg.synth_scene(N_GAUSS, "mixed", SEED, log_scale_range=LOG_SCALE) if rank == 0 else None
     bcast_ms = None
     if world > 1:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        dist.broadcast(blob, src=0)
-        ev1.record()
         torch.cuda.synchronize()
-        bcast_ms = ev0.elapsed_time(ev1)
-        if rank != 0:
-            dscene = renderer.bind(meta, blob.data_ptr(), meta.blob_bytes, keepalive=blob)
+        dist.barrier()
+        tb = time.perf_counter()
+        meta, blob = multiview.broadcast_scene_blob(scene, "cuda", src=0)
+        torch.cuda.synchronize()
+        bcast_ms = (time.perf_counter() - tb) * 1e3
+        dscene = renderer.bind(meta, blob.data_ptr(), meta.blob_bytes, keepalive=blob)
+    else:
+        meta = sg.Renderer.plan(scene)
+        dscene = renderer.upload(scene)
+    del scene
+    torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_b0
 
     frames = torch.empty((vpr, H, W, 3), dtype=torch.float32, device="cuda")
@@ -306,10 +300,9 @@ def main():
     gather_ms = None
     if args.gather and world > 1:
         torch.cuda.synchronize()
-        recv = [torch.empty_like(frames) for _ in range(world)] if rank == 0 else None
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record()
-        dist.gather(frames, recv, dst=0)
+        multiview.gather_frames(frames, dst=0)
         g1.record()
         torch.cuda.synchronize()
         gather_ms = max_over_ranks(g0.elapsed_time(g1))

@@ -139,6 +139,10 @@ sgs_status sgs_launch_count(sgs_context* ctx, uint64_t* own_kernels, uint64_t* l
 /* Validates the desc (homogeneous by construction; scene.cpp:7-25 rules on degree)
  * and fills the device layout it will use. */
 sgs_status sgs_scene_plan(const sgs_scene_desc* desc, sgs_scene_meta* meta);
+/* Pack the scene into its device layout in HOST memory (meta->blob_bytes bytes):
+ * exactly the bytes sgs_scene_upload places in HBM. Used to ship a scene blob
+ * through a collective (e.g. NCCL / gloo broadcast) and to test layouts on CPU. */
+sgs_status sgs_scene_pack(const sgs_scene_desc* desc, void* host_blob, uint64_t bytes);
 /* Upload into a context-owned allocation. */
 sgs_status sgs_scene_upload(sgs_context* ctx, const sgs_scene_desc* desc, sgs_scene** out);
 /* Upload into caller device memory of meta->blob_bytes (e.g. a torch tensor that

@@ -331,6 +331,16 @@ class Renderer:
         _check(_lib().sgs_scene_plan(ctypes.byref(d), ctypes.byref(m)))
         return m
 
+    @staticmethod
+    def pack(scene: Scene) -> tuple:
+        """(meta, host bytes) of the scene's device layout (sgs_scene_pack)."""
+        d, keep = scene._desc()
+        m = C.sgs_scene_meta()
+        _check(_lib().sgs_scene_plan(ctypes.byref(d), ctypes.byref(m)))
+        buf = np.empty(m.blob_bytes, dtype=np.uint8)
+        _check(_lib().sgs_scene_pack(ctypes.byref(d), buf.ctypes.data, m.blob_bytes))
+        return m, buf
+
     def upload_into(self, scene: Scene, device_ptr: int, nbytes: int, keepalive=None) -> DeviceScene:
         d, keep = scene._desc()
         h = ctypes.c_void_p()

@@ -120,6 +120,7 @@ SIGNATURES = {
     "sgs_synchronize": (_S, [_P]),
     "sgs_launch_count": (_S, [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
     "sgs_scene_plan": (_S, [ctypes.POINTER(sgs_scene_desc), ctypes.POINTER(sgs_scene_meta)]),
+    "sgs_scene_pack": (_S, [ctypes.POINTER(sgs_scene_desc), _P, ctypes.c_uint64]),
     "sgs_scene_upload": (_S, [_P, ctypes.POINTER(sgs_scene_desc), ctypes.POINTER(_P)]),
     "sgs_scene_upload_into": (_S, [_P, ctypes.POINTER(sgs_scene_desc), _P, ctypes.c_uint64,
                                    ctypes.POINTER(_P)]),

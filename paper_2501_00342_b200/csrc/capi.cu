@@ -92,7 +92,8 @@ struct sgs_context {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
     std::mutex mu;
-    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, rects, ntiles, brect, bmeta, counts, offsets;
+    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, colour, degree, rects, ntiles, brect, bmeta, counts,
+        offsets;
     uint64_t iota_n = 0;
     DevBuf buckets;  // K2 bucket histogram / offsets / cursors
     DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist, frame_rgb[2],
@@ -217,8 +218,9 @@ sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, c
         SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, hist, off, static_cast<int>(nb + 1), s));
         SGS_CUDA(ctx->cub_temp.ensure(temp));
         SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, hist, off, static_cast<int>(nb + 1), s));
-        launch_bucket_scatter(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, log2b, off, cursor, order, s);
-        launch_bucket_sort(nb, off, ctx->keys_a.as<unsigned long long>(), order, ctx->d_ctr, cursor + (nb + 1), s);
+        launch_bucket_scatter(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, log2b, off, cursor, order,
+                              ctx->keys_b.as<unsigned long long>(), s);
+        launch_bucket_sort(nb, off, ctx->keys_b.as<unsigned long long>(), order, ctx->d_ctr, cursor + (nb + 1), s);
         ctx->own_launches += 4;
         ctx->lib_launches += 2;
     } else {
@@ -280,6 +282,8 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
     SGS_CUDA(ctx->order.ensure(n1 * 4));
     SGS_CUDA(ctx->rec.ensure(n1 * sizeof(SplatRec)));
     SGS_CUDA(ctx->rects.ensure(n1 * sizeof(int4)));
+    SGS_CUDA(ctx->colour.ensure(n1 * sizeof(float4)));
+    SGS_CUDA(ctx->degree.ensure(n1));
     SGS_CUDA(ctx->ntiles.ensure(n1 * 4));
     SGS_CUDA(ctx->brect.ensure(n1 * sizeof(int4)));
     SGS_CUDA(ctx->bmeta.ensure(n1 * sizeof(uint2)));
@@ -307,9 +311,11 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
         ctx->iota_n = n;
     }
     launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->rec.as<SplatRec>(),
-                      ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->d_ctr, d_debug, s);
+                      ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->degree.as<uint8_t>(), ctx->d_ctr,
+                      d_debug, s);
+    launch_colour(scene->planes, cp, ctx->degree.as<uint8_t>(), ctx->colour.as<float4>(), d_debug, s);
     SGS_CUDA(cudaGetLastError());
-    if (n) ctx->own_launches += 1;
+    if (n) ctx->own_launches += 2;
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[1], s));
     if (mode == kProjectOnly) {
         SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
@@ -340,10 +346,10 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
             const uint64_t b = (n + div - 1) / div;
             if (b > bounds.back() && b < n) bounds.push_back(b);
         }
-        SGS_CUDA(ctx->tile_done.ensure((ntile + 31) / 32 * 4));
+        SGS_CUDA(ctx->tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
         SGS_CUDA(ctx->pix_state.ensure(npx * sizeof(PixelState)));
         SGS_CUDA(ctx->pix_walked.ensure(npx * sizeof(uint32_t)));
-        SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, (ntile + 31) / 32 * 4, s));
+        SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
     }
     bounds.push_back(n);
     const int nchunks = static_cast<int>(bounds.size()) - 1;
@@ -381,8 +387,9 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
         // K7
         if (mode == kRender) {
             launch_composite(ctx->d_consts, cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
-                             bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(), ctx->pix_walked.as<uint32_t>(),
-                             ctx->tile_done.as<uint32_t>(), c == 0, c == nchunks - 1, ctx->d_ctr,
+                             ctx->colour.as<float4>(), bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(), ctx->pix_walked.as<uint32_t>(),
+                             ctx->tile_done.as<uint32_t>(), ctx->tile_done.as<uint32_t>() + (ntile + 31) / 32,
+                             c == 0, c == nchunks - 1, ctx->d_ctr,
                              stats != nullptr, s);
             SGS_CUDA(cudaGetLastError());
             ctx->own_launches += 1;
@@ -660,7 +667,7 @@ void sgs_destroy(sgs_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->key32_a, &ctx->key32_b, &ctx->iota, &ctx->order,
-                      &ctx->rec, &ctx->rects, &ctx->ntiles, &ctx->brect, &ctx->bmeta, &ctx->counts, &ctx->offsets,
+                      &ctx->rec, &ctx->colour, &ctx->degree, &ctx->rects, &ctx->ntiles, &ctx->brect, &ctx->bmeta, &ctx->counts, &ctx->offsets,
                       &ctx->tkeys_a, &ctx->tkeys_b, &ctx->ranges, &ctx->tile_done, &ctx->pix_state,
                       &ctx->pix_walked, &ctx->cub_temp, &ctx->sort_hist, &ctx->buckets, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
                       &ctx->frame_T[0], &ctx->frame_T[1]})
@@ -737,6 +744,18 @@ sgs_status sgs_scene_plan(const sgs_scene_desc* d, sgs_scene_meta* m) {
     for (int k = 0; k < 9; ++k) m->shared_axes[k] = d->shared_axes[k];
     for (int k = 0; k < 3; ++k) m->background[k] = d->background[k];
     m->blob_bytes = make_layout(*m).bytes;
+    return SGS_OK;
+}
+
+sgs_status sgs_scene_pack(const sgs_scene_desc* desc, void* host_blob, uint64_t bytes) {
+    if (!desc || !host_blob) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    sgs_scene_meta m{};
+    sgs_status st = sgs_scene_plan(desc, &m);
+    if (st != SGS_OK) return st;
+    if (bytes < m.blob_bytes) return fail(SGS_ERR_INVALID_ARGUMENT, "host blob smaller than meta.blob_bytes");
+    std::vector<char> host;
+    fill_blob(desc, m, host);
+    std::memcpy(host_blob, host.data(), host.size());
     return SGS_OK;
 }
 

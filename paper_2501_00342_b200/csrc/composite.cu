@@ -60,6 +60,20 @@ __device__ __noinline__ bool exact_alpha(const FrameConsts* __restrict__ fc, uin
     return true;
 }
 
+// cp.async of one splat's 48-B record and 16-B colour into a 64-B smem slot:
+// [0] (mx, my) [1] (ca, 2cb, cc, log2 op) [2] (cut, guard, ext_x, ext_y) [3] (r, g, b, -)
+__device__ __forceinline__ void stage_record(const SplatRec* __restrict__ rec, const float4* __restrict__ colour,
+                                             uint32_t g, float4* slot) {
+    const char* src = reinterpret_cast<const char*>(rec + g);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&slot[c]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 16 * c));
+    }
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&slot[3]));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(colour + g));
+}
+
 struct Pixel {
     float T, r, g, b;
     int term;  // position in the batch's compacted walk where T fell below stop
@@ -100,9 +114,10 @@ __device__ __forceinline__ float fast_alpha(float m2, float lop) {
 __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
-    const SplatRec* __restrict__ rec, float3 bg, float* __restrict__ out_rgb, float* __restrict__ out_T,
+    const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
+    float* __restrict__ out_rgb, float* __restrict__ out_T,
     PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
-    int first, int last, Counters* __restrict__ ctr, int want_stats) {
+    uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats) {
     // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
     // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
     // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
@@ -118,7 +133,11 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
     if (!first && ((tile_done[tile >> 5] >> (tile & 31)) & 1u)) return;
     const uint2 range = ranges[tile];
     const uint32_t start = range.x, end = range.y;
-    if (!first && !last && start == end) return;
+    // Nothing new for this tile in this chunk: its state (if any) stays as it is. A
+    // tile that has never received an entry keeps no per-pixel state at all
+    // (tile_touched), so empty tiles cost neither state writes nor reads.
+    if (!last && start == end) return;
+    const bool touched = !first && ((tile_touched[tile >> 5] >> (tile & 31)) & 1u);
 
     const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
     const int px0 = tx * ts, py0 = ty * ts;
@@ -143,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
     const float fcx = static_cast<float>(lx) + 0.5f, fcy = static_cast<float>(ly) + 0.5f;
     Pixel P{1.f, 0.f, 0.f, 0.f, -1, !valid};
     uint32_t walked = 0;  // entries of the full list walked in earlier chunks
-    if (!first && valid) {
+    if (touched && valid) {
         const PixelState s = state[pix];
         P.r = s.r, P.g = s.g, P.b = s.b, P.T = s.T;
         walked = processed_io[pix];
@@ -171,12 +190,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
     uint32_t g_next = 0;  // gaussian index of this thread's record in the next batch
     if (start + t < end) g_next = static_cast<uint32_t>(__ldg(&keys[start + t]));
     if (start + t < end) {
-        const char* src = reinterpret_cast<const char*>(rec + g_next);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&sRaw[0][t][c]));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 16 * c));
-        }
+        stage_record(rec, colour, g_next, sRaw[0][t]);
     }
     asm volatile("cp.async.commit_group;\n" ::);
     uint32_t g_cur = g_next;
@@ -192,23 +206,18 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
                 float4* r = sRaw[buf][t];
                 const double2 m = *reinterpret_cast<const double2*>(&r[0]);
                 const float4 q1 = r[1];  // ca, cb2, cc, lop
-                const float4 q2 = r[2];  // r, g, b, cut
-                const float4 q3 = r[3];  // guard, ext_x, ext_y, pad
+                const float4 q2 = r[2];  // cut, guard, ext_x, ext_y
+                const float4 q3 = r[3];  // r, g, b, -
                 const float lmx = static_cast<float>(m.x - px0), lmy = static_cast<float>(m.y - py0);
                 r[0] = make_float4(lmx, lmy, q1.x, q1.y);
-                r[1] = make_float4(q1.z, q2.w + q3.x, q2.w - q3.x, q1.w);
-                r[2] = make_float4(q2.x, q2.y, q2.z, __uint_as_float(g_cur));
-                sF[t] = make_float4(lmx, lmy, q3.y, q3.z);
+                r[1] = make_float4(q1.z, q2.x + q2.y, q2.x - q2.y, q1.w);
+                r[2] = make_float4(q3.x, q3.y, q3.z, __uint_as_float(g_cur));
+                sF[t] = make_float4(lmx, lmy, q2.z, q2.w);
             }
             // prefetch the next batch's record, then the key after it
             const uint32_t kn = base + kBatch + t;
             if (kn < end) {
-                const char* src = reinterpret_cast<const char*>(rec + g_next);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&sRaw[buf ^ 1][t][c]));
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 16 * c));
-                }
+                stage_record(rec, colour, g_next, sRaw[buf ^ 1][t]);
             }
             asm volatile("cp.async.commit_group;\n" ::);
             g_cur = g_next;
@@ -298,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
         }
     }
     if (!last && all_done && threadIdx.x == 0) atomicOr(&tile_done[tile >> 5], 1u << (tile & 31));
+    if (!finalize && !touched && threadIdx.x == 0) atomicOr(&tile_touched[tile >> 5], 1u << (tile & 31));
     if (want_stats) {
         // E_t = max over the tile's pixels of the entries of its full list each pixel
         // walked (counted when the tile finalises); guard hits summed over chunks.
@@ -335,15 +345,15 @@ int composite_pixel_chunks(int ts) {
 
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
-                      float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
-                      uint32_t* tile_done, bool first, bool last, Counters* counters, bool want_stats,
+                      const float4* colour, float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
+                      uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters, bool want_stats,
                       cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
     const long long ntiles = static_cast<long long>(cfg.tiles_x) * cfg.tiles_y;
     const long long grid = ntiles * nchunks;
     composite_kernel<<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
-        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, bg, rgb, T, state, processed, tile_done,
-        first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0);
+        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, rgb, T, state, processed, tile_done,
+        tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0);
 }
 
 }  // namespace sgs

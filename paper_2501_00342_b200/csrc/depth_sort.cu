@@ -43,7 +43,8 @@ __global__ void bucket_hist_kernel(uint64_t n, const unsigned long long* __restr
 // hist now holds exclusive offsets; cursor (zeroed) counts placements per bucket.
 __global__ void bucket_scatter_kernel(uint64_t n, const unsigned long long* __restrict__ key,
                                       Counters* __restrict__ ctr, int log2b, const uint32_t* __restrict__ off,
-                                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ out) {
+                                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ out,
+                                      unsigned long long* __restrict__ out_key) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned long long k = key[i];
@@ -55,6 +56,7 @@ __global__ void bucket_scatter_kernel(uint64_t n, const unsigned long long* __re
         pos = off[b] + atomicAdd(&cursor[b], 1u);
     }
     out[pos] = static_cast<uint32_t>(i);
+    out_key[pos] = k;  // keys travel with the indices: the bucket sort reads them contiguously
 }
 
 __device__ __forceinline__ bool less_ki(unsigned long long ka, uint32_t ia, unsigned long long kb, uint32_t ib) {
@@ -64,7 +66,7 @@ __device__ __forceinline__ bool less_ki(unsigned long long ka, uint32_t ia, unsi
 // One thread per bucket: insertion sort by (key, index) for buckets of <= kSmall;
 // larger buckets are queued for the warp kernel below.
 __global__ void bucket_sort_small_kernel(uint32_t nbuckets, const uint32_t* __restrict__ off,
-                                         const unsigned long long* __restrict__ key, uint32_t* __restrict__ order,
+                                         const unsigned long long* __restrict__ skey, uint32_t* __restrict__ order,
                                          Counters* __restrict__ ctr, uint32_t* __restrict__ big) {
     const uint32_t b = static_cast<uint32_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (b >= nbuckets) return;
@@ -78,7 +80,7 @@ __global__ void bucket_sort_small_kernel(uint32_t nbuckets, const uint32_t* __re
     unsigned long long k[kSmall];
     for (uint32_t a = 0; a < m; ++a) {
         const uint32_t vi = order[s + a];
-        const unsigned long long vk = key[vi];
+        const unsigned long long vk = skey[s + a];
         int c = static_cast<int>(a) - 1;
         while (c >= 0 && less_ki(vk, vi, k[c], idx[c])) {
             k[c + 1] = k[c];
@@ -104,7 +106,7 @@ __device__ void bitonic_bucket(uint32_t b, const uint32_t* __restrict__ off, con
     for (int h = 0; h < 2; ++h) {
         const uint32_t el = h * 32 + lane;
         idx[h] = el < m ? order[s + el] : 0xFFFFFFFFu;
-        k[h] = el < m ? key[idx[h]] : ~0ULL;
+        k[h] = el < m ? key[s + el] : ~0ULL;  // bucket-ordered keys (scatter output)
     }
 #pragma unroll
     for (int kk = 2; kk <= 64; kk <<= 1) {
@@ -170,10 +172,10 @@ void launch_bucket_hist(uint64_t n, const unsigned long long* key, const Counter
 }
 
 void launch_bucket_scatter(uint64_t n, const unsigned long long* key, Counters* ctr, int log2b, const uint32_t* off,
-                           uint32_t* cursor, uint32_t* out, cudaStream_t stream) {
+                           uint32_t* cursor, uint32_t* out, unsigned long long* out_key, cudaStream_t stream) {
     if (n)
         bucket_scatter_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, key, ctr, log2b, off,
-                                                                                        cursor, out);
+                                                                                        cursor, out, out_key);
 }
 
 void launch_bucket_sort(uint32_t nbuckets, const uint32_t* off, const unsigned long long* key, uint32_t* order,

@@ -49,36 +49,43 @@ __device__ __forceinline__ void load_planes(const float4* __restrict__ color, ui
     }
 }
 
-// sum_i Y_i(d) * c_i for degree `deg` (eval_sh_basis + sh_sum, color.cpp:99-168).
-__device__ __forceinline__ void sh_accumulate(const float* c, int deg, float x, float y, float z,
-                                              float acc[3]) {
-    float b[16];
+// sum_i Y_i(d) * c_i for degree `deg` <= MAXD (eval_sh_basis + sh_sum, color.cpp:99-168);
+// MAXD bounds the register footprint (MIXED stores degree <= 2)
+template <int MAXD>
+__device__ __forceinline__ void sh_accumulate_upto(const float* c, int deg, float x, float y, float z,
+                                                   float acc[3]) {
+    constexpr int kN = (MAXD + 1) * (MAXD + 1);
+    float b[kN];
     b[0] = kC0;
-    if (deg >= 1) {
+    if (MAXD >= 1 && deg >= 1) {
         b[1] = -kC1 * y;
         b[2] = kC1 * z;
         b[3] = -kC1 * x;
     }
-    if (deg >= 2) {
-        const float xx = x * x, yy = y * y, zz = z * z;
-        b[4] = kC2[0] * x * y;
-        b[5] = kC2[1] * y * z;
-        b[6] = kC2[2] * (2.0f * zz - xx - yy);
-        b[7] = kC2[3] * x * z;
-        b[8] = kC2[4] * (xx - yy);
-        if (deg >= 3) {
-            b[9] = kC3[0] * y * (3.0f * xx - yy);
-            b[10] = kC3[1] * x * y * z;
-            b[11] = kC3[2] * y * (4.0f * zz - xx - yy);
-            b[12] = kC3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-            b[13] = kC3[4] * x * (4.0f * zz - xx - yy);
-            b[14] = kC3[5] * z * (xx - yy);
-            b[15] = kC3[6] * x * (xx - 3.0f * yy);
+    if constexpr (MAXD >= 2) {
+        if (deg >= 2) {
+            const float xx = x * x, yy = y * y, zz = z * z;
+            b[4] = kC2[0] * x * y;
+            b[5] = kC2[1] * y * z;
+            b[6] = kC2[2] * (2.0f * zz - xx - yy);
+            b[7] = kC2[3] * x * z;
+            b[8] = kC2[4] * (xx - yy);
+            if constexpr (MAXD >= 3) {
+                if (deg >= 3) {
+                    b[9] = kC3[0] * y * (3.0f * xx - yy);
+                    b[10] = kC3[1] * x * y * z;
+                    b[11] = kC3[2] * y * (4.0f * zz - xx - yy);
+                    b[12] = kC3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+                    b[13] = kC3[4] * x * (4.0f * zz - xx - yy);
+                    b[14] = kC3[5] * z * (xx - yy);
+                    b[15] = kC3[6] * x * (xx - 3.0f * yy);
+                }
+            }
         }
     }
     const int n = (deg + 1) * (deg + 1);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < kN; ++k) {
         if (k < n) {
             acc[0] += b[k] * c[3 * k + 0];
             acc[1] += b[k] * c[3 * k + 1];
@@ -106,17 +113,19 @@ __device__ __forceinline__ void raise_error(Counters* ctr, uint64_t i, uint32_t 
 }
 
 template <bool F64, int KIND>
-__global__ void __launch_bounds__(256) preprocess_kernel(
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(
     const ScenePlanes sp, const CamParams cam, const CfgParams cfg,
     unsigned long long* __restrict__ depth_keys,
     SplatRec* __restrict__ rec, int4* __restrict__ rects,
-    uint32_t* __restrict__ ntiles, Counters* __restrict__ ctr, DebugSplat* __restrict__ debug) {
+    uint32_t* __restrict__ ntiles, uint8_t* __restrict__ degree, Counters* __restrict__ ctr,
+    DebugSplat* __restrict__ debug) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool visible = false;
     unsigned long long vkey = ~0ULL;
     if (i < sp.n) {
         unsigned long long key = ~0ULL;
         uint32_t count = 0;
+        uint8_t deg_out = kCulled;
         Geo g;
         ProjGeo pg;
         DebugSplat dbg;
@@ -181,53 +190,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 }
                 deg = deg_used;
             }
-            // ---- colour (FP32) ----
-            const float fx = static_cast<float>(dxd), fy = static_cast<float>(dyd),
-                        fz = static_cast<float>(dzd);
-            float col[3];
-            if constexpr (KIND == SGS_SH || KIND == SGS_MIXED) {
-                const int stored_planes = (3 * (sp.sh_degree + 1) * (sp.sh_degree + 1) + 3) / 4;
-                const int need = (3 * (deg + 1) * (deg + 1) + 3) / 4;
-                float c[48];
-                load_planes<12>(sp.color, sp.n, i, need, c);
-                float acc[3] = {0.f, 0.f, 0.f};
-                sh_accumulate(c, deg, fx, fy, fz, acc);
-                col[0] = 0.5f + acc[0];
-                col[1] = 0.5f + acc[1];
-                col[2] = 0.5f + acc[2];
-                if constexpr (KIND == SGS_MIXED) {
-                    float lobes[12];
-                    load_planes<3>(sp.color + static_cast<uint64_t>(stored_planes) * sp.n, sp.n, i, 3,
-                                   lobes);
-                    float lacc[3] = {0.f, 0.f, 0.f};
-                    lobe_accumulate(lobes, sp.axes, fx, fy, fz, lacc);
-                    col[0] += lacc[0];
-                    col[1] += lacc[1];
-                    col[2] += lacc[2];
-                }
-            } else if constexpr (KIND == SGS_SG1) {
-                // diffuse + alpha * exp(lambda (d.mu - 1)) (color.cpp:49-56, :195-199);
-                // mu was normalised in FP64 at upload (DiffuseSGModel::lobe).
-                float f[12];
-                load_planes<3>(sp.color, sp.n, i, 3, f);
-                const float lambda = expf(f[3]);
-                const float e = expf(lambda * (fx * f[8] + fy * f[9] + fz * f[10] - 1.0f));
-                col[0] = f[0] + f[4] * e;
-                col[1] = f[1] + f[5] * e;
-                col[2] = f[2] + f[6] * e;
-            } else {
-                float f[16];
-                load_planes<4>(sp.color, sp.n, i, 4, f);
-                float lacc[3] = {0.f, 0.f, 0.f};
-                lobe_accumulate(f + 4, sp.axes, fx, fy, fz, lacc);
-                col[0] = f[0] + lacc[0];
-                col[1] = f[1] + lacc[1];
-                col[2] = f[2] + lacc[2];
-            }
-            col[0] = fmaxf(col[0], 0.0f);  // cwiseMax(0), NaN-propagating like std::max(v, 0)
-            col[1] = fmaxf(col[1], 0.0f);
-            col[2] = fmaxf(col[2], 0.0f);
-
             // ---- outputs ----
             // conic and opacity only feed FP32 quantities here (the compositor's guard band
             // re-derives the exact FP64 values): one reciprocal instead of three divisions,
@@ -284,14 +246,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
             r.cb2 = static_cast<float>(2.0 * conb);
             r.cc = static_cast<float>(conc);
             r.lop = opacity > 0.0 ? static_cast<float>(log2(opacity)) : -1e30f;
-            r.r = col[0];
-            r.g = col[1];
-            r.b = col[2];
             r.cut = static_cast<float>(cut);
             r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
             r.ext_x = static_cast<float>(sqrt(K * pg.a) * (1.0 + 1e-5) + 1e-3);
             r.ext_y = static_cast<float>(sqrt(K * pg.c) * (1.0 + 1e-5) + 1e-3);
-            r.pad = 0.f;
+            deg_out = static_cast<uint8_t>(deg);
             rec[i] = r;
             if (debug) {
                 dbg.mean2d[0] = mx;
@@ -300,9 +259,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 dbg.conic[1] = conb;
                 dbg.conic[2] = conc;
                 dbg.depth = tz;
-                dbg.color[0] = col[0];
-                dbg.color[1] = col[1];
-                dbg.color[2] = col[2];
                 dbg.opacity = opacity;
                 dbg.radius = radius;
                 dbg.degree = KIND == SGS_MIXED ? deg_used : -1;
@@ -312,6 +268,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         depth_keys[i] = key;
         vkey = key;
         ntiles[i] = count;
+        degree[i] = deg_out;
         if (debug) debug[i] = dbg;
     }
     // visible count and depth-key range: one atomic each per warp
@@ -334,23 +291,118 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
 template <bool F64>
 void launch_kind(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                  unsigned long long* keys, SplatRec* rec,
-                 int4* rects, uint32_t* ntiles, Counters* ctr, DebugSplat* debug,
+                 int4* rects, uint32_t* ntiles, uint8_t* degree, Counters* ctr, DebugSplat* debug,
                  cudaStream_t stream) {
     const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
     switch (sp.kind) {
         case SGS_SH:
-            preprocess_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
+            preprocess_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
             break;
         case SGS_SG1:
-            preprocess_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
+            preprocess_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
             break;
         case SGS_SG3:
-            preprocess_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
+            preprocess_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
             break;
         default:
             preprocess_kernel<F64, SGS_MIXED><<<blocks, 256, 0, stream>>>(
-                sp, cam, cfg, keys, rec, rects, ntiles, ctr, debug);
+                sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
             break;
+    }
+}
+
+
+// K1b: view-dependent colour (eval_color, color.cpp:201-235) for the splats K1a
+// kept, in FP32 from coalesced float4 planes: the position plane and exactly the
+// colour planes the evaluated degree needs. The view direction normalize(p - C)
+// (raster.cpp:66-69) is recomputed in FP32 here; the reference's FP64 decisions
+// (including the unit-direction check) were all taken by K1a.
+template <bool F64, int KIND>
+__global__ void __launch_bounds__(256) colour_kernel(const ScenePlanes sp, const float cx, const float cy,
+                                                     const float cz, const uint8_t* __restrict__ degree,
+                                                     float4* __restrict__ colour, DebugSplat* __restrict__ debug) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= sp.n) return;
+    const uint8_t deg8 = degree[i];
+    if (deg8 == kCulled) return;
+    float px, py, pz;
+    if constexpr (F64) {
+        px = static_cast<float>(sp.g8[0][i]);
+        py = static_cast<float>(sp.g8[1][i]);
+        pz = static_cast<float>(sp.g8[2][i]);
+    } else {
+        const float4 a = __ldg(&sp.g4[0][i]);
+        px = a.x;
+        py = a.y;
+        pz = a.z;
+    }
+    const float ox = px - cx, oy = py - cy, oz = pz - cz;
+    const float inv = rsqrtf(ox * ox + oy * oy + oz * oz);
+    const float fx = ox * inv, fy = oy * inv, fz = oz * inv;
+    const int deg = deg8;
+    float col[3];
+    if constexpr (KIND == SGS_SH || KIND == SGS_MIXED) {
+        const int stored_planes = (3 * (sp.sh_degree + 1) * (sp.sh_degree + 1) + 3) / 4;
+        const int need = (3 * (deg + 1) * (deg + 1) + 3) / 4;
+        // MIXED stores degree <= 2 (7 planes); SH up to degree 3 (12 planes)
+        constexpr int kMaxPlanes = KIND == SGS_MIXED ? 7 : 12;
+        float c[4 * kMaxPlanes];
+        load_planes<kMaxPlanes>(sp.color, sp.n, i, need, c);
+        float acc[3] = {0.f, 0.f, 0.f};
+        if constexpr (KIND == SGS_MIXED)
+            sh_accumulate_upto<2>(c, deg, fx, fy, fz, acc);
+        else
+            sh_accumulate_upto<3>(c, deg, fx, fy, fz, acc);
+        col[0] = 0.5f + acc[0];
+        col[1] = 0.5f + acc[1];
+        col[2] = 0.5f + acc[2];
+        if constexpr (KIND == SGS_MIXED) {
+            float lobes[12];
+            load_planes<3>(sp.color + static_cast<uint64_t>(stored_planes) * sp.n, sp.n, i, 3, lobes);
+            float lacc[3] = {0.f, 0.f, 0.f};
+            lobe_accumulate(lobes, sp.axes, fx, fy, fz, lacc);
+            col[0] += lacc[0];
+            col[1] += lacc[1];
+            col[2] += lacc[2];
+        }
+    } else if constexpr (KIND == SGS_SG1) {
+        // diffuse + alpha * exp(lambda (d.mu - 1)) (color.cpp:49-56, :195-199);
+        // mu was normalised in FP64 at upload (DiffuseSGModel::lobe).
+        float f[12];
+        load_planes<3>(sp.color, sp.n, i, 3, f);
+        const float lambda = expf(f[3]);
+        const float e = expf(lambda * (fx * f[8] + fy * f[9] + fz * f[10] - 1.0f));
+        col[0] = f[0] + f[4] * e;
+        col[1] = f[1] + f[5] * e;
+        col[2] = f[2] + f[6] * e;
+    } else {
+        float f[16];
+        load_planes<4>(sp.color, sp.n, i, 4, f);
+        float lacc[3] = {0.f, 0.f, 0.f};
+        lobe_accumulate(f + 4, sp.axes, fx, fy, fz, lacc);
+        col[0] = f[0] + lacc[0];
+        col[1] = f[1] + lacc[1];
+        col[2] = f[2] + lacc[2];
+    }
+    // cwiseMax(0): std::max(v, 0) keeps NaN
+    const float r = col[0] < 0.f ? 0.f : col[0], g = col[1] < 0.f ? 0.f : col[1], b = col[2] < 0.f ? 0.f : col[2];
+    colour[i] = make_float4(r, g, b, 0.f);
+    if (debug) {
+        debug[i].color[0] = r;
+        debug[i].color[1] = g;
+        debug[i].color[2] = b;
+    }
+}
+
+template <bool F64>
+void launch_colour_kind(const ScenePlanes& sp, float cx, float cy, float cz, const uint8_t* degree,
+                        float4* colour, DebugSplat* debug, cudaStream_t stream) {
+    const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
+    switch (sp.kind) {
+        case SGS_SH: colour_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
+        case SGS_SG1: colour_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
+        case SGS_SG3: colour_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
+        default: colour_kernel<F64, SGS_MIXED><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
     }
 }
 
@@ -361,19 +413,31 @@ __global__ void iota_kernel(uint64_t n, uint32_t* __restrict__ out) {
 
 }  // namespace
 
+void launch_colour(const ScenePlanes& sp, const CamParams& cam, const uint8_t* degree, float4* colour,
+                   DebugSplat* debug, cudaStream_t stream) {
+    if (sp.n == 0) return;
+    const float cx = static_cast<float>(cam.C[0]), cy = static_cast<float>(cam.C[1]),
+                cz = static_cast<float>(cam.C[2]);
+    if (sp.geometry_f64)
+        launch_colour_kind<true>(sp, cx, cy, cz, degree, colour, debug, stream);
+    else
+        launch_colour_kind<false>(sp, cx, cy, cz, degree, colour, debug, stream);
+}
+
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream) {
     if (n) iota_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, out);
 }
 
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
-                       uint32_t* ntiles, Counters* counters, DebugSplat* debug, cudaStream_t stream) {
+                       uint32_t* ntiles, uint8_t* degree, Counters* counters, DebugSplat* debug,
+                       cudaStream_t stream) {
     if (sp.n == 0) return;
     if (sp.geometry_f64)
-        launch_kind<true>(sp, cam, cfg, depth_keys, rec, rects, ntiles, counters, debug,
+        launch_kind<true>(sp, cam, cfg, depth_keys, rec, rects, ntiles, degree, counters, debug,
                           stream);
     else
-        launch_kind<false>(sp, cam, cfg, depth_keys, rec, rects, ntiles, counters, debug,
+        launch_kind<false>(sp, cam, cfg, depth_keys, rec, rects, ntiles, degree, counters, debug,
                            stream);
 }
 

@@ -76,20 +76,22 @@ struct FrameConsts {
     CamParams cam;
 };
 
-// Compositing record written by K1 for visible splats (64 B, 16-B aligned).
+// Compositing record written by K1a for visible splats (48 B, 16-B aligned); the
+// colour (16 B) is written by K1b into a separate float4 array.
 // The reference's two skip tests (m2 > 9, alpha < 1/255) are one cutoff on m2:
 // alpha < 1/255 <=> m2 > 2 ln(255 op), so cut = min(9, 2 ln(255 op)) (FP64 in K1).
 struct __align__(16) SplatRec {
     double mx, my;      // mean2d in pixels (FP64 so the compositor can localise exactly)
     float ca, cb2, cc;  // conic (a, 2b, c)
     float lop;          // log2(opacity)
-    float r, g, b;      // colour
     float cut;          // min(9, 2 ln(255 op))
     float guard;        // FP32 m2 error bound -> FP64 guard band half-width
     float ext_x, ext_y; // half extents of {m2 <= cut + guard} (warp culling box)
-    float pad;
 };
-static_assert(sizeof(SplatRec) == 64, "splat record");
+static_assert(sizeof(SplatRec) == 48, "splat record");
+
+// Per-Gaussian evaluation degree written by K1a for K1b: 0..3, or kCulled.
+constexpr uint8_t kCulled = 0xFF;
 
 // Debug record for sgs_project (same field order as sgs_splat).
 struct DebugSplat {
@@ -142,13 +144,16 @@ inline int color_plane_count(int kind, int degree) {
 // Launchers (defined in the .cu files).
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
-                       uint32_t* ntiles, Counters* counters, DebugSplat* debug, cudaStream_t stream);
+                       uint32_t* ntiles, uint8_t* degree, Counters* counters, DebugSplat* debug,
+                       cudaStream_t stream);
+void launch_colour(const ScenePlanes& sp, const CamParams& cam, const uint8_t* degree, float4* colour,
+                   DebugSplat* debug, cudaStream_t stream);
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
 int depth_bucket_log2(uint64_t n);
 void launch_bucket_hist(uint64_t n, const unsigned long long* key, const Counters* ctr, int log2b, uint32_t* hist,
                         cudaStream_t stream);
 void launch_bucket_scatter(uint64_t n, const unsigned long long* key, Counters* ctr, int log2b, const uint32_t* off,
-                           uint32_t* cursor, uint32_t* out, cudaStream_t stream);
+                           uint32_t* cursor, uint32_t* out, unsigned long long* out_key, cudaStream_t stream);
 void launch_bucket_sort(uint32_t nbuckets, const uint32_t* off, const unsigned long long* key, uint32_t* order,
                         Counters* ctr, uint32_t* big, cudaStream_t stream);
 // Tile counts for ranks [rb, re) skipping tiles already terminated (done may be null);
@@ -176,8 +181,9 @@ unsigned long long* tile_sort(unsigned long long* a, unsigned long long* b, cons
 // state may be null when the frame is a single chunk.
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
-                      float3 bg, float* rgb, float* T,
-                      PixelState* state, uint32_t* processed, uint32_t* tile_done, bool first,
+                      const float4* colour, float3 bg, float* rgb, float* T,
+                      PixelState* state, uint32_t* processed, uint32_t* tile_done, uint32_t* tile_touched,
+                      bool first,
                       bool last, Counters* counters, bool want_stats, cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
 
