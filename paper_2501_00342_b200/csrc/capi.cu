@@ -96,6 +96,7 @@ struct sgs_context {
         offsets;
     uint64_t iota_n = 0;
     DevBuf buckets;  // K2 bucket histogram / offsets / cursors
+    DevBuf work;     // K7 work list (+ 3 control words)
     DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist, frame_rgb[2],
         frame_T[2];
     uint64_t tkey_cap = 0;  // tile keys per buffer (grow-only, sized from observed P)
@@ -283,7 +284,6 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
     SGS_CUDA(ctx->rec.ensure(n1 * sizeof(SplatRec)));
     SGS_CUDA(ctx->rects.ensure(n1 * sizeof(int4)));
     SGS_CUDA(ctx->colour.ensure(n1 * sizeof(float4)));
-    SGS_CUDA(ctx->degree.ensure(n1));
     SGS_CUDA(ctx->ntiles.ensure(n1 * 4));
     SGS_CUDA(ctx->brect.ensure(n1 * sizeof(int4)));
     SGS_CUDA(ctx->bmeta.ensure(n1 * sizeof(uint2)));
@@ -311,11 +311,10 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
         ctx->iota_n = n;
     }
     launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->rec.as<SplatRec>(),
-                      ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->degree.as<uint8_t>(), ctx->d_ctr,
+                      ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->colour.as<float4>(), ctx->d_ctr,
                       d_debug, s);
-    launch_colour(scene->planes, cp, ctx->degree.as<uint8_t>(), ctx->colour.as<float4>(), d_debug, s);
     SGS_CUDA(cudaGetLastError());
-    if (n) ctx->own_launches += 2;
+    if (n) ctx->own_launches += 1;
     if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[1], s));
     if (mode == kProjectOnly) {
         SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
@@ -357,6 +356,9 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
                                   static_cast<float>(scene->meta.background[1]),
                                   static_cast<float>(scene->meta.background[2]));
     const int tile_bits = std::max(1, ceil_log2(ntile));
+    const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
+    SGS_CUDA(ctx->work.ensure((work_cap + 4) * sizeof(uint32_t)));
+    // work items: tiles always need a pass at least in the last chunk
     const unsigned long long* d_pc = &ctx->d_ctr->chunk_entries;
     float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -389,10 +391,10 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
             launch_composite(ctx->d_consts, cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
                              ctx->colour.as<float4>(), bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(), ctx->pix_walked.as<uint32_t>(),
                              ctx->tile_done.as<uint32_t>(), ctx->tile_done.as<uint32_t>() + (ntile + 31) / 32,
-                             c == 0, c == nchunks - 1, ctx->d_ctr,
-                             stats != nullptr, s);
+                             c == 0, c == nchunks - 1, ctx->d_ctr, stats != nullptr, ctx->work.as<uint32_t>(),
+                             ctx->work.as<uint32_t>() + work_cap, s);
             SGS_CUDA(cudaGetLastError());
-            ctx->own_launches += 1;
+            ctx->own_launches += 2;  // work list + persistent compositor
         }
         if (timing) {
             SGS_CUDA(cudaEventRecord(ctx->ev[6], s));
@@ -669,7 +671,7 @@ void sgs_destroy(sgs_context* ctx) {
     for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->key32_a, &ctx->key32_b, &ctx->iota, &ctx->order,
                       &ctx->rec, &ctx->colour, &ctx->degree, &ctx->rects, &ctx->ntiles, &ctx->brect, &ctx->bmeta, &ctx->counts, &ctx->offsets,
                       &ctx->tkeys_a, &ctx->tkeys_b, &ctx->ranges, &ctx->tile_done, &ctx->pix_state,
-                      &ctx->pix_walked, &ctx->cub_temp, &ctx->sort_hist, &ctx->buckets, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
+                      &ctx->pix_walked, &ctx->cub_temp, &ctx->sort_hist, &ctx->buckets, &ctx->work, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
                       &ctx->frame_T[0], &ctx->frame_T[1]})
         b->release();
     if (ctx->d_ctr) cudaFree(ctx->d_ctr);

@@ -29,6 +29,8 @@
 // exactly as the reference does from the FP64 projection re-derived by
 // projection.cuh. Every skip decision therefore matches the reference; only the
 // blended values carry FP32 rounding.
+#include <cstdlib>
+
 #include "projection.cuh"
 
 namespace sgs {
@@ -36,7 +38,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kBatch = 256;
-constexpr int kGroup = 8;
 
 // The reference's FP64 decision for one (pixel, splat) pair (raster.cpp:165-176).
 __device__ __noinline__ bool exact_alpha(const FrameConsts* __restrict__ fc, uint32_t g, int px, int py,
@@ -111,32 +112,51 @@ __device__ __forceinline__ float fast_alpha(float m2, float lop) {
     return fminf(ex2_approx(fmaf(m2, -0.72134752044448170f, lop)), 0.999f);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) composite_kernel(
+// GROUP records per ILP group; MINB min resident CTAs per SM (register cap).
+// Selected at run time by SGS_K7_GROUP / SGS_K7_MINB for tuning.
+template <int kGroup, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
     const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
     float* __restrict__ out_rgb, float* __restrict__ out_T,
     PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
-    uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats) {
+    uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
+    const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
+    uint32_t work_cap) {
     // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
     // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
     // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
-    __shared__ float4 sRaw[2][kBatch][4];
+    // Slot kBatch of the current buffer is a null record (never contributes) that pads
+    // the compacted lists to whole groups.
+    __shared__ float4 sRaw[2][kBatch + 1][4];
     __shared__ float4 sF[kBatch];  // (lmx, lmy, ext_x, ext_y)
-    __shared__ uint8_t sIdx[kThreads / 32][kBatch + kGroup];
+    __shared__ uint16_t sIdx[kThreads / 32][kBatch + 8];
     __shared__ unsigned long long s_red[2][kThreads / 32];
+    __shared__ uint32_t s_item;
 
+    if (threadIdx.x < 8) {
+        // null records: m2 = 0 > cut + guard = -1 -> skipped, alpha 0
+        const int b = threadIdx.x >> 2, c = threadIdx.x & 3;
+        sRaw[b][kBatch][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const uint32_t n_long = work_count[0], n_items = work_count[0] + work_count[1];
+    // Persistent CTAs: each pulls (tile, pixel-chunk) items from the chunk's work list
+    // (long tile lists first, built by build_work_kernel).
+    for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(work_next, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    __syncthreads();
+    if (item >= n_items) break;
+    const uint32_t witem = item < n_long ? work[item] : work[work_cap - 1 - (item - n_long)];
     const int ts = cfg.tile_size;
-    const int tile = blockIdx.x / nchunks;
-    const int chunk = blockIdx.x - tile * nchunks;
-    // Tiles that terminated in an earlier depth chunk already wrote their output.
-    if (!first && ((tile_done[tile >> 5] >> (tile & 31)) & 1u)) return;
+    const int tile = static_cast<int>(witem / nchunks);
+    const int chunk = static_cast<int>(witem - static_cast<uint32_t>(tile) * nchunks);
     const uint2 range = ranges[tile];
     const uint32_t start = range.x, end = range.y;
-    // Nothing new for this tile in this chunk: its state (if any) stays as it is. A
-    // tile that has never received an entry keeps no per-pixel state at all
+    // A tile that has never received an entry keeps no per-pixel state at all
     // (tile_touched), so empty tiles cost neither state writes nor reads.
-    if (!last && start == end) return;
     const bool touched = !first && ((tile_touched[tile >> 5] >> (tile & 31)) & 1u);
 
     const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
@@ -181,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
         wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
     }
     uint32_t guard_hits = 0;
-    uint8_t* idx = sIdx[warp];
+    uint16_t* idx = sIdx[warp];
 
     // Software pipeline over batches: keys one batch ahead in registers, records one
     // batch ahead in shared memory via cp.async, so the dependent key -> record
@@ -226,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
         }
         __syncthreads();
         const uint32_t nb = min(static_cast<uint32_t>(kBatch), end - base);
-        const float4(*R)[4] = sRaw[buf ^ 1];  // the batch converted above
+        const float4(*R)[4] = sRaw[buf ^ 1];  // the batch converted above (+ null record)
         int cnt = 0;
         if (__any_sync(0xffffffffu, !P.done)) {
             for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
@@ -237,34 +257,31 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
                     hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit) idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint8_t>(j);
+                if (hit) idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
                 cnt += __popc(m);
             }
         }
+        if (lane < kGroup) idx[cnt + lane] = kBatch;  // pad with the null record
         __syncwarp();
         for (int q = 0; q < cnt && !P.done; q += kGroup) {
             // m2 / alpha of the whole group first (independent), then the blend chain;
             // slots past cnt re-read record idx[q] and are forced to alpha = 0
             float alpha[kGroup];
             bool guard = false;
+            int jj[kGroup];
 #pragma unroll
             for (int k = 0; k < kGroup; ++k) {
-                const int qq = q + k;
-                const bool in = qq < cnt;
-                const int j = idx[in ? qq : q];
+                const int j = idx[q + k];
+                jj[k] = j;
                 const float4 A = R[j][0];
                 const float4 B = R[j][1];
                 const float m2 = mahal2(A, B.x, fcx, fcy);
-                guard |= in && m2 <= B.y && m2 >= B.z;
-                alpha[k] = (in && m2 < B.z) ? fast_alpha(m2, B.w) : 0.0f;
+                guard |= m2 <= B.y && m2 >= B.z;
+                alpha[k] = m2 < B.z ? fast_alpha(m2, B.w) : 0.0f;
             }
             if (!guard) {
 #pragma unroll
-                for (int k = 0; k < kGroup; ++k) {
-                    const int qq = q + k;
-                    const int j = idx[qq < cnt ? qq : q];
-                    step(P, P.done ? 0.0f : alpha[k], R[j][2], stop, qq);
-                }
+                for (int k = 0; k < kGroup; ++k) step(P, P.done ? 0.0f : alpha[k], R[jj[k]][2], stop, q + k);
             } else {
                 // a pair inside the guard band: walk the group one record at a time
                 for (int k = 0; k < kGroup && q + k < cnt && !P.done; ++k) {
@@ -334,6 +351,28 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(
             if (hs) atomicAdd(&ctr->guard_hits, hs);
         }
     }
+    __syncthreads();
+    }  // persistent loop
+}
+
+// Work list of a depth chunk: (tile, pixel chunk) items that still need K7 -- every
+// unfinished tile in the last chunk (it writes the final pixels), otherwise only
+// tiles with entries in this chunk. Tiles with long lists are queued from the front
+// of `work`, the rest from the back, so the persistent CTAs start on the longest.
+__global__ void build_work_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ tile_done,
+                                  int first, int last, uint32_t ntile, int nchunks, uint32_t cap,
+                                  uint32_t* __restrict__ work, uint32_t* __restrict__ wctl) {
+    const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= ntile * static_cast<uint32_t>(nchunks)) return;
+    const uint32_t tile = it / nchunks;
+    if (!first && ((tile_done[tile >> 5] >> (tile & 31)) & 1u)) return;
+    const uint2 r = ranges[tile];
+    const uint32_t len = r.y - r.x;
+    if (!last && len == 0) return;
+    if (len >= 1024)
+        work[atomicAdd(&wctl[0], 1u)] = it;
+    else
+        work[cap - 1 - atomicAdd(&wctl[1], 1u)] = it;
 }
 
 }  // namespace
@@ -346,14 +385,39 @@ int composite_pixel_chunks(int ts) {
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
                       const float4* colour, float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
-                      uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters, bool want_stats,
-                      cudaStream_t stream) {
+                      uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
+                      bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
-    const long long ntiles = static_cast<long long>(cfg.tiles_x) * cfg.tiles_y;
-    const long long grid = ntiles * nchunks;
-    composite_kernel<<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
-        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, rgb, T, state, processed, tile_done,
-        tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0);
+    const uint32_t ntile = static_cast<uint32_t>(cfg.tiles_x) * static_cast<uint32_t>(cfg.tiles_y);
+    const uint32_t cap = ntile * static_cast<uint32_t>(nchunks);
+    cudaMemsetAsync(wctl, 0, 3 * sizeof(uint32_t), stream);
+    build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, first ? 1 : 0, last ? 1 : 0,
+                                                             ntile, nchunks, cap, work, wctl);
+    static const int group = [] {
+        const char* e = std::getenv("SGS_K7_GROUP");
+        return e ? std::atoi(e) : 4;
+    }();
+    static const int minb = [] {
+        const char* e = std::getenv("SGS_K7_MINB");
+        return e ? std::atoi(e) : 2;
+    }();
+    // persistent grid: resident CTAs only
+    const unsigned grid = 148u * static_cast<unsigned>(minb);
+#define SGS_K7(G, M)                                                                                         \
+    composite_kernel<G, M><<<grid, kThreads, 0, stream>>>(                                                   \
+        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, rgb, T, state, processed, tile_done, \
+        tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap)
+    if (group == 8 && minb == 2)
+        SGS_K7(8, 2);
+    else if (group == 2 && minb == 2)
+        SGS_K7(2, 2);
+    else if (group == 4 && minb == 3)
+        SGS_K7(4, 3);
+    else if (group == 2 && minb == 3)
+        SGS_K7(2, 3);
+    else
+        SGS_K7(4, 2);
+#undef SGS_K7
 }
 
 }  // namespace sgs

@@ -18,6 +18,7 @@
 // (MIXED+SH1: 6 planes = 96 B). Outputs per visible splat: 8 B depth key,
 // 48 B compositing record, 32 B FP64 guard record, 16 B tile rect, 4 B count.
 #include <cfloat>
+#include <cstdlib>
 
 #include "projection.cuh"
 
@@ -112,12 +113,69 @@ __device__ __forceinline__ void raise_error(Counters* ctr, uint64_t i, uint32_t 
     atomicMin(&ctr->err, (static_cast<unsigned long long>(i) << 8) | code);
 }
 
-template <bool F64, int KIND>
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(
+// View-dependent colour (eval_color, color.cpp:201-235) in FP32 from coalesced
+// float4 planes: exactly the colour planes the evaluated degree needs. The view
+// direction normalize(p - C) (raster.cpp:66-69) is taken in FP32; the reference's
+// FP64 decisions (including the unit-direction check) are made by the caller.
+template <int KIND>
+__device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, uint64_t i, int deg, float fx, float fy,
+                                              float fz) {
+    float col[3];
+    if constexpr (KIND == SGS_SH || KIND == SGS_MIXED) {
+        const int stored_planes = (3 * (sp.sh_degree + 1) * (sp.sh_degree + 1) + 3) / 4;
+        const int need = (3 * (deg + 1) * (deg + 1) + 3) / 4;
+        // MIXED stores degree <= 2 (7 planes); SH up to degree 3 (12 planes)
+        constexpr int kMaxPlanes = KIND == SGS_MIXED ? 7 : 12;
+        float c[4 * kMaxPlanes];
+        load_planes<kMaxPlanes>(sp.color, sp.n, i, need, c);
+        float acc[3] = {0.f, 0.f, 0.f};
+        if constexpr (KIND == SGS_MIXED)
+            sh_accumulate_upto<2>(c, deg, fx, fy, fz, acc);
+        else
+            sh_accumulate_upto<3>(c, deg, fx, fy, fz, acc);
+        col[0] = 0.5f + acc[0];
+        col[1] = 0.5f + acc[1];
+        col[2] = 0.5f + acc[2];
+        if constexpr (KIND == SGS_MIXED) {
+            float lobes[12];
+            load_planes<3>(sp.color + static_cast<uint64_t>(stored_planes) * sp.n, sp.n, i, 3, lobes);
+            float lacc[3] = {0.f, 0.f, 0.f};
+            lobe_accumulate(lobes, sp.axes, fx, fy, fz, lacc);
+            col[0] += lacc[0];
+            col[1] += lacc[1];
+            col[2] += lacc[2];
+        }
+    } else if constexpr (KIND == SGS_SG1) {
+        // diffuse + alpha * exp(lambda (d.mu - 1)) (color.cpp:49-56, :195-199);
+        // mu was normalised in FP64 at upload (DiffuseSGModel::lobe).
+        float f[12];
+        load_planes<3>(sp.color, sp.n, i, 3, f);
+        const float lambda = expf(f[3]);
+        const float e = expf(lambda * (fx * f[8] + fy * f[9] + fz * f[10] - 1.0f));
+        col[0] = f[0] + f[4] * e;
+        col[1] = f[1] + f[5] * e;
+        col[2] = f[2] + f[6] * e;
+    } else {
+        float f[16];
+        load_planes<4>(sp.color, sp.n, i, 4, f);
+        float lacc[3] = {0.f, 0.f, 0.f};
+        lobe_accumulate(f + 4, sp.axes, fx, fy, fz, lacc);
+        col[0] = f[0] + lacc[0];
+        col[1] = f[1] + lacc[1];
+        col[2] = f[2] + lacc[2];
+    }
+    // cwiseMax(0): std::max(v, 0) keeps NaN
+    return make_float4(col[0] < 0.f ? 0.f : col[0], col[1] < 0.f ? 0.f : col[1], col[2] < 0.f ? 0.f : col[2], 0.f);
+}
+
+// MINB (min resident CTAs per SM) trades registers for occupancy; selected at run
+// time by SGS_K1_MINB for tuning (default kDefaultMinB, see profiles/).
+template <bool F64, int KIND, int MINB>
+__global__ void __launch_bounds__(256, MINB) preprocess_kernel(
     const ScenePlanes sp, const CamParams cam, const CfgParams cfg,
     unsigned long long* __restrict__ depth_keys,
     SplatRec* __restrict__ rec, int4* __restrict__ rects,
-    uint32_t* __restrict__ ntiles, uint8_t* __restrict__ degree, Counters* __restrict__ ctr,
+    uint32_t* __restrict__ ntiles, float4* __restrict__ colour, Counters* __restrict__ ctr,
     DebugSplat* __restrict__ debug) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool visible = false;
@@ -125,7 +183,6 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
     if (i < sp.n) {
         unsigned long long key = ~0ULL;
         uint32_t count = 0;
-        uint8_t deg_out = kCulled;
         Geo g;
         ProjGeo pg;
         DebugSplat dbg;
@@ -250,7 +307,18 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
             r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
             r.ext_x = static_cast<float>(sqrt(K * pg.a) * (1.0 + 1e-5) + 1e-3);
             r.ext_y = static_cast<float>(sqrt(K * pg.c) * (1.0 + 1e-5) + 1e-3);
-            deg_out = static_cast<uint8_t>(deg);
+            // colour (FP32), direction from the FP64 offset
+            {
+                const float inv = static_cast<float>(1.0 / dist);
+                const float4 col = eval_colour<KIND>(sp, i, deg, static_cast<float>(ox) * inv,
+                                                     static_cast<float>(oy) * inv, static_cast<float>(oz) * inv);
+                colour[i] = col;
+                if (debug) {
+                    dbg.color[0] = col.x;
+                    dbg.color[1] = col.y;
+                    dbg.color[2] = col.z;
+                }
+            }
             rec[i] = r;
             if (debug) {
                 dbg.mean2d[0] = mx;
@@ -268,7 +336,6 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
         depth_keys[i] = key;
         vkey = key;
         ntiles[i] = count;
-        degree[i] = deg_out;
         if (debug) debug[i] = dbg;
     }
     // visible count and depth-key range: one atomic each per warp
@@ -288,123 +355,54 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
     }
 }
 
-template <bool F64>
-void launch_kind(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
-                 unsigned long long* keys, SplatRec* rec,
-                 int4* rects, uint32_t* ntiles, uint8_t* degree, Counters* ctr, DebugSplat* debug,
-                 cudaStream_t stream) {
+template <bool F64, int MINB>
+void launch_kind_b(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
+                   SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
+                   cudaStream_t stream) {
     const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
     switch (sp.kind) {
         case SGS_SH:
-            preprocess_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
+            preprocess_kernel<F64, SGS_SH, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles,
+                                                                             colour, ctr, debug);
             break;
         case SGS_SG1:
-            preprocess_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
+            preprocess_kernel<F64, SGS_SG1, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles,
+                                                                              colour, ctr, debug);
             break;
         case SGS_SG3:
-            preprocess_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
+            preprocess_kernel<F64, SGS_SG3, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles,
+                                                                              colour, ctr, debug);
             break;
         default:
-            preprocess_kernel<F64, SGS_MIXED><<<blocks, 256, 0, stream>>>(
-                sp, cam, cfg, keys, rec, rects, ntiles, degree, ctr, debug);
+            preprocess_kernel<F64, SGS_MIXED, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects,
+                                                                                ntiles, colour, ctr, debug);
             break;
     }
 }
 
+constexpr int kDefaultMinB = 2;
 
-// K1b: view-dependent colour (eval_color, color.cpp:201-235) for the splats K1a
-// kept, in FP32 from coalesced float4 planes: the position plane and exactly the
-// colour planes the evaluated degree needs. The view direction normalize(p - C)
-// (raster.cpp:66-69) is recomputed in FP32 here; the reference's FP64 decisions
-// (including the unit-direction check) were all taken by K1a.
-template <bool F64, int KIND>
-__global__ void __launch_bounds__(256) colour_kernel(const ScenePlanes sp, const float cx, const float cy,
-                                                     const float cz, const uint8_t* __restrict__ degree,
-                                                     float4* __restrict__ colour, DebugSplat* __restrict__ debug) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= sp.n) return;
-    const uint8_t deg8 = degree[i];
-    if (deg8 == kCulled) return;
-    float px, py, pz;
-    if constexpr (F64) {
-        px = static_cast<float>(sp.g8[0][i]);
-        py = static_cast<float>(sp.g8[1][i]);
-        pz = static_cast<float>(sp.g8[2][i]);
-    } else {
-        const float4 a = __ldg(&sp.g4[0][i]);
-        px = a.x;
-        py = a.y;
-        pz = a.z;
-    }
-    const float ox = px - cx, oy = py - cy, oz = pz - cz;
-    const float inv = rsqrtf(ox * ox + oy * oy + oz * oz);
-    const float fx = ox * inv, fy = oy * inv, fz = oz * inv;
-    const int deg = deg8;
-    float col[3];
-    if constexpr (KIND == SGS_SH || KIND == SGS_MIXED) {
-        const int stored_planes = (3 * (sp.sh_degree + 1) * (sp.sh_degree + 1) + 3) / 4;
-        const int need = (3 * (deg + 1) * (deg + 1) + 3) / 4;
-        // MIXED stores degree <= 2 (7 planes); SH up to degree 3 (12 planes)
-        constexpr int kMaxPlanes = KIND == SGS_MIXED ? 7 : 12;
-        float c[4 * kMaxPlanes];
-        load_planes<kMaxPlanes>(sp.color, sp.n, i, need, c);
-        float acc[3] = {0.f, 0.f, 0.f};
-        if constexpr (KIND == SGS_MIXED)
-            sh_accumulate_upto<2>(c, deg, fx, fy, fz, acc);
-        else
-            sh_accumulate_upto<3>(c, deg, fx, fy, fz, acc);
-        col[0] = 0.5f + acc[0];
-        col[1] = 0.5f + acc[1];
-        col[2] = 0.5f + acc[2];
-        if constexpr (KIND == SGS_MIXED) {
-            float lobes[12];
-            load_planes<3>(sp.color + static_cast<uint64_t>(stored_planes) * sp.n, sp.n, i, 3, lobes);
-            float lacc[3] = {0.f, 0.f, 0.f};
-            lobe_accumulate(lobes, sp.axes, fx, fy, fz, lacc);
-            col[0] += lacc[0];
-            col[1] += lacc[1];
-            col[2] += lacc[2];
-        }
-    } else if constexpr (KIND == SGS_SG1) {
-        // diffuse + alpha * exp(lambda (d.mu - 1)) (color.cpp:49-56, :195-199);
-        // mu was normalised in FP64 at upload (DiffuseSGModel::lobe).
-        float f[12];
-        load_planes<3>(sp.color, sp.n, i, 3, f);
-        const float lambda = expf(f[3]);
-        const float e = expf(lambda * (fx * f[8] + fy * f[9] + fz * f[10] - 1.0f));
-        col[0] = f[0] + f[4] * e;
-        col[1] = f[1] + f[5] * e;
-        col[2] = f[2] + f[6] * e;
-    } else {
-        float f[16];
-        load_planes<4>(sp.color, sp.n, i, 4, f);
-        float lacc[3] = {0.f, 0.f, 0.f};
-        lobe_accumulate(f + 4, sp.axes, fx, fy, fz, lacc);
-        col[0] = f[0] + lacc[0];
-        col[1] = f[1] + lacc[1];
-        col[2] = f[2] + lacc[2];
-    }
-    // cwiseMax(0): std::max(v, 0) keeps NaN
-    const float r = col[0] < 0.f ? 0.f : col[0], g = col[1] < 0.f ? 0.f : col[1], b = col[2] < 0.f ? 0.f : col[2];
-    colour[i] = make_float4(r, g, b, 0.f);
-    if (debug) {
-        debug[i].color[0] = r;
-        debug[i].color[1] = g;
-        debug[i].color[2] = b;
-    }
+int k1_minb() {
+    static const int v = [] {
+        const char* e = std::getenv("SGS_K1_MINB");
+        const int m = e ? std::atoi(e) : kDefaultMinB;
+        return (m >= 1 && m <= 4) ? m : kDefaultMinB;
+    }();
+    return v;
 }
 
 template <bool F64>
-void launch_colour_kind(const ScenePlanes& sp, float cx, float cy, float cz, const uint8_t* degree,
-                        float4* colour, DebugSplat* debug, cudaStream_t stream) {
-    const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
-    switch (sp.kind) {
-        case SGS_SH: colour_kernel<F64, SGS_SH><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
-        case SGS_SG1: colour_kernel<F64, SGS_SG1><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
-        case SGS_SG3: colour_kernel<F64, SGS_SG3><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
-        default: colour_kernel<F64, SGS_MIXED><<<blocks, 256, 0, stream>>>(sp, cx, cy, cz, degree, colour, debug); break;
+void launch_kind(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
+                 SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
+                 cudaStream_t stream) {
+    switch (k1_minb()) {
+        case 1: launch_kind_b<F64, 1>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
+        case 2: launch_kind_b<F64, 2>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
+        case 4: launch_kind_b<F64, 4>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
+        default: launch_kind_b<F64, 3>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
     }
 }
+
 
 __global__ void iota_kernel(uint64_t n, uint32_t* __restrict__ out) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -413,31 +411,20 @@ __global__ void iota_kernel(uint64_t n, uint32_t* __restrict__ out) {
 
 }  // namespace
 
-void launch_colour(const ScenePlanes& sp, const CamParams& cam, const uint8_t* degree, float4* colour,
-                   DebugSplat* debug, cudaStream_t stream) {
-    if (sp.n == 0) return;
-    const float cx = static_cast<float>(cam.C[0]), cy = static_cast<float>(cam.C[1]),
-                cz = static_cast<float>(cam.C[2]);
-    if (sp.geometry_f64)
-        launch_colour_kind<true>(sp, cx, cy, cz, degree, colour, debug, stream);
-    else
-        launch_colour_kind<false>(sp, cx, cy, cz, degree, colour, debug, stream);
-}
-
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream) {
     if (n) iota_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, out);
 }
 
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
-                       uint32_t* ntiles, uint8_t* degree, Counters* counters, DebugSplat* debug,
+                       uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream) {
     if (sp.n == 0) return;
     if (sp.geometry_f64)
-        launch_kind<true>(sp, cam, cfg, depth_keys, rec, rects, ntiles, degree, counters, debug,
+        launch_kind<true>(sp, cam, cfg, depth_keys, rec, rects, ntiles, colour, counters, debug,
                           stream);
     else
-        launch_kind<false>(sp, cam, cfg, depth_keys, rec, rects, ntiles, degree, counters, debug,
+        launch_kind<false>(sp, cam, cfg, depth_keys, rec, rects, ntiles, colour, counters, debug,
                            stream);
 }
 

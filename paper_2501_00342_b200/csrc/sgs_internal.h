@@ -76,8 +76,8 @@ struct FrameConsts {
     CamParams cam;
 };
 
-// Compositing record written by K1a for visible splats (48 B, 16-B aligned); the
-// colour (16 B) is written by K1b into a separate float4 array.
+// Compositing record written by K1 for visible splats (48 B, 16-B aligned); the
+// colour (16 B) goes to a separate float4 array.
 // The reference's two skip tests (m2 > 9, alpha < 1/255) are one cutoff on m2:
 // alpha < 1/255 <=> m2 > 2 ln(255 op), so cut = min(9, 2 ln(255 op)) (FP64 in K1).
 struct __align__(16) SplatRec {
@@ -89,9 +89,6 @@ struct __align__(16) SplatRec {
     float ext_x, ext_y; // half extents of {m2 <= cut + guard} (warp culling box)
 };
 static_assert(sizeof(SplatRec) == 48, "splat record");
-
-// Per-Gaussian evaluation degree written by K1a for K1b: 0..3, or kCulled.
-constexpr uint8_t kCulled = 0xFF;
 
 // Debug record for sgs_project (same field order as sgs_splat).
 struct DebugSplat {
@@ -144,10 +141,8 @@ inline int color_plane_count(int kind, int degree) {
 // Launchers (defined in the .cu files).
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
-                       uint32_t* ntiles, uint8_t* degree, Counters* counters, DebugSplat* debug,
+                       uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream);
-void launch_colour(const ScenePlanes& sp, const CamParams& cam, const uint8_t* degree, float4* colour,
-                   DebugSplat* debug, cudaStream_t stream);
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
 int depth_bucket_log2(uint64_t n);
 void launch_bucket_hist(uint64_t n, const unsigned long long* key, const Counters* ctr, int log2b, uint32_t* hist,
@@ -184,7 +179,8 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
                       const float4* colour, float3 bg, float* rgb, float* T,
                       PixelState* state, uint32_t* processed, uint32_t* tile_done, uint32_t* tile_touched,
                       bool first,
-                      bool last, Counters* counters, bool want_stats, cudaStream_t stream);
+                      bool last, Counters* counters, bool want_stats, uint32_t* work, uint32_t* wctl,
+                      cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
 
 }  // namespace sgs
