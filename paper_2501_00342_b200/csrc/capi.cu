@@ -1,11 +1,12 @@
 // capi.cu -- the C-ABI (include/sgs.h): contexts, device scenes, frame orchestration.
 //
-// Frame pipeline on the context stream:
-//   K1 preprocess -> K2 stable radix sort of FP64 depth keys (values: Gaussian index)
-//   -> K3 gather per-rank tile counts + exclusive scan -> [one 40-B D2H of the
-//   counters: error word, V, P; sizes the tile-key arena] -> K4 emit (tile,index)
-//   keys -> K5 stable radix sort on the tile bits -> K6 tile ranges -> K7 composite.
-// Radix sorts and the scan use CUB (CUDA 12.9 CCCL) as the library primitive.
+// Frame pipeline, enqueued on a lane stream with no host
+// round trip: K1 preprocess -> K2 exact bucket sort of the FP64 depth keys ->
+// rank-ordered bin gather -> per depth chunk { K3 tile counts + scan -> K4 emit
+// (tile, index) keys -> K5 radix sort on the tile bits -> K6 tile ranges -> K7
+// persistent compositor } -> one 128-B D2H of the counters (errors, overflow
+// retries, stats). Batches alternate views over two lanes. CUB (CCCL 2.8) supplies
+// the scans and the rare 64-bit fallback sort.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -86,34 +87,59 @@ struct sgs_scene {
     ScenePlanes planes{};
 };
 
-struct sgs_context {
-    int device = 0;
-    cudaStream_t own_stream = nullptr;
+// One frame in flight: a stream plus every per-frame arena. sgs_render_batch deals
+// views round-robin over the lanes, so one view's latency-bound sort and scan
+// kernels overlap the other view's preprocess and compositing, and the host enqueues
+// view i+1 while view i runs.
+struct Lane {
     cudaStream_t stream = nullptr;
-    cudaStream_t copy_stream = nullptr;
-    std::mutex mu;
-    DevBuf keys_a, keys_b, key32_a, key32_b, iota, order, rec, colour, degree, rects, ntiles, brect, bmeta, counts,
-        offsets;
-    uint64_t iota_n = 0;
+    DevBuf keys_a, keys_b, iota, order, rec, colour, rects, ntiles, brect, bmeta, counts, offsets;
     DevBuf buckets;  // K2 bucket histogram / offsets / cursors
     DevBuf work;     // K7 work list (+ 3 control words)
-    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist, frame_rgb[2],
-        frame_T[2];
+    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist, out_rgb, out_T;
+    uint64_t iota_n = 0;
     uint64_t tkey_cap = 0;  // tile keys per buffer (grow-only, sized from observed P)
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;
-    Counters* h_ctr_init = nullptr;  // pinned initial counters block (err/kmin = ~0)
     FrameConsts* d_consts = nullptr;  // per-frame scene planes + camera for K7's FP64 path
     FrameConsts* h_consts = nullptr;  // pinned staging copy
-    bool chunking = true;
-    std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t ev[8] = {};
-    cudaEvent_t frame_done[2] = {};
-    cudaEvent_t slot_free[2] = {};
+    cudaEvent_t done = nullptr;  // the frame's counters have reached h_ctr
+    // the frame in flight (valid while busy)
+    struct Job {
+        const sgs_scene* scene = nullptr;
+        sgs_camera cam{};
+        sgs_render_config cfg{};
+        float* d_rgb = nullptr;  // device outputs the compositor writes
+        float* d_T = nullptr;
+        float* h_rgb = nullptr;  // host outputs copied back on the lane stream
+        float* h_T = nullptr;
+        sgs_render_stats* stats = nullptr;
+        DebugSplat* d_debug = nullptr;
+        int mode = 0;
+        bool wide = false;
+        float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
+    } job;
+    bool busy = false;
     // results of the last frame (device pointers into the buffers above)
     const uint32_t* last_order = nullptr;
     const unsigned long long* last_tile_keys = nullptr;
     uint64_t last_v = 0, last_p = 0;
+};
+
+constexpr int kLanes = 4;
+
+struct sgs_context {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;  // the caller's stream: lanes fork from and join back to it
+    std::mutex mu;
+    Lane lane[kLanes];
+    int lanes = kLanes;                // lanes used by sgs_render_batch (SGS_LANES, 1..kLanes)
+    Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
+    bool chunking = true;
+    std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
+    cudaEvent_t fork = nullptr;
     uint64_t own_launches = 0, lib_launches = 0;
 };
 
@@ -202,37 +228,37 @@ constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, red
 // are finished and receive no keys from the second chunk.
 constexpr uint64_t kMinChunkedN = 1 << 16;
 
-sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out) {
-    uint32_t* order = ctx->order.as<uint32_t>();
+sgs_status sort_depth(sgs_context* ctx, Lane& L, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out) {
+    uint32_t* order = L.order.as<uint32_t>();
     size_t temp = 0;
     if (!wide) {
         // K2: exact bucket sort (depth_sort.cu)
         const int log2b = depth_bucket_log2(n);
         const uint32_t nb = 1u << log2b;
-        SGS_CUDA(ctx->buckets.ensure(static_cast<size_t>(nb + 1) * 4 * 4));
-        uint32_t* hist = ctx->buckets.as<uint32_t>();
+        SGS_CUDA(L.buckets.ensure(static_cast<size_t>(nb + 1) * 4 * 4));
+        uint32_t* hist = L.buckets.as<uint32_t>();
         uint32_t* off = hist + (nb + 1);
         uint32_t* cursor = off + (nb + 1);
         SGS_CUDA(cudaMemsetAsync(hist, 0, static_cast<size_t>(nb + 1) * 4, s));
         SGS_CUDA(cudaMemsetAsync(cursor, 0, static_cast<size_t>(nb + 1) * 4, s));
-        launch_bucket_hist(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, log2b, hist, s);
+        launch_bucket_hist(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2b, hist, s);
         SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, hist, off, static_cast<int>(nb + 1), s));
-        SGS_CUDA(ctx->cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, hist, off, static_cast<int>(nb + 1), s));
-        launch_bucket_scatter(n, ctx->keys_a.as<unsigned long long>(), ctx->d_ctr, log2b, off, cursor, order,
-                              ctx->keys_b.as<unsigned long long>(), s);
-        launch_bucket_sort(nb, off, ctx->keys_b.as<unsigned long long>(), order, ctx->d_ctr, cursor + (nb + 1), s);
+        SGS_CUDA(L.cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_temp.ptr, temp, hist, off, static_cast<int>(nb + 1), s));
+        launch_bucket_scatter(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2b, off, cursor, order,
+                              L.keys_b.as<unsigned long long>(), s);
+        launch_bucket_sort(nb, off, L.keys_b.as<unsigned long long>(), order, L.d_ctr, cursor + (nb + 1), s);
         ctx->own_launches += 4;
         ctx->lib_launches += 2;
     } else {
         // fallback: full 64-bit keys (8 passes); stable, so ties keep index order
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, ctx->keys_a.as<unsigned long long>(),
-                                                 ctx->keys_b.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
-                                                 order, static_cast<int>(n), 0, 64, s));
-        SGS_CUDA(ctx->cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.ptr, temp, ctx->keys_a.as<unsigned long long>(),
-                                                 ctx->keys_b.as<unsigned long long>(), ctx->iota.as<uint32_t>(),
-                                                 order, static_cast<int>(n), 0, 64, s));
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, L.keys_a.as<unsigned long long>(),
+                                                 L.keys_b.as<unsigned long long>(), L.iota.as<uint32_t>(), order,
+                                                 static_cast<int>(n), 0, 64, s));
+        SGS_CUDA(L.cub_temp.ensure(temp));
+        SGS_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_temp.ptr, temp, L.keys_a.as<unsigned long long>(),
+                                                 L.keys_b.as<unsigned long long>(), L.iota.as<uint32_t>(), order,
+                                                 static_cast<int>(n), 0, 64, s));
         ctx->lib_launches += 1 + 8;
     }
     SGS_CUDA(cudaGetLastError());
@@ -241,99 +267,109 @@ sgs_status sort_depth(sgs_context* ctx, uint64_t n, bool wide, cudaStream_t s, c
 }
 
 // K3 for ranks [rb, re): counts -> exclusive scan; the total P stays on the device.
-sgs_status count_and_scan(sgs_context* ctx, uint64_t rb, uint64_t re, const uint32_t* order, const uint32_t* done,
-                          int tiles_x, int ntile, cudaStream_t s) {
+sgs_status count_and_scan(sgs_context* ctx, Lane& L, uint64_t rb, uint64_t re, const uint32_t* done, int tiles_x,
+                          int ntile, cudaStream_t s) {
     const uint64_t m = re - rb;
-    (void)order;
-    launch_count_tiles(rb, re, ctx->bmeta.as<uint2>(), ctx->brect.as<int4>(), done, tiles_x, ntile,
-                       ctx->counts.as<unsigned long long>(), s);
+    launch_count_tiles(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, tiles_x, ntile,
+                       L.counts.as<unsigned long long>(), s);
     size_t temp = 0;
-    SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, ctx->counts.as<unsigned long long>(),
-                                           ctx->offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
-    SGS_CUDA(ctx->cub_temp.ensure(temp));
-    SGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_temp.ptr, temp, ctx->counts.as<unsigned long long>(),
-                                           ctx->offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
-    launch_finish_scan(ctx->offsets.as<unsigned long long>() + m, ctx->tkey_cap, ctx->d_ctr, s);
+    SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, L.counts.as<unsigned long long>(),
+                                           L.offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
+    SGS_CUDA(L.cub_temp.ensure(temp));
+    SGS_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_temp.ptr, temp, L.counts.as<unsigned long long>(),
+                                           L.offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
+    launch_finish_scan(L.offsets.as<unsigned long long>() + m, L.tkey_cap, L.d_ctr, s);
     ctx->own_launches += 2;
     ctx->lib_launches += 2;
     return SGS_OK;
 }
 
-// One frame on ctx->stream. Outputs are device pointers (either may be null).
-// The whole frame is enqueued without a host round trip (every data-dependent
-// size lives on the device); one synchronisation at the end reads the counters,
-// reports errors, and -- rarely -- regrows the tile-key arena or falls back to the
-// 64-bit depth sort and renders the frame again.
-int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
-                          const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
-                          DebugSplat* d_debug, FrameMode mode, bool wide_sort) {
-    cudaStream_t s = ctx->stream;
+// Enqueue lane L's job on L.stream without a host round trip (every data-dependent
+// size lives on the device), ending with a 128-B D2H of the counters and L.done.
+// finish_frame() reads the counters, reports errors and -- rarely -- regrows the
+// tile-key arena or switches to the 64-bit depth sort and enqueues the frame again.
+sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
+    Lane::Job& j = L.job;
+    cudaStream_t s = L.stream;
+    const sgs_scene* scene = j.scene;
+    const sgs_camera* cam = &j.cam;
+    const sgs_render_config* cfg = &j.cfg;
+    const FrameMode mode = static_cast<FrameMode>(j.mode);
     const uint64_t n = scene->meta.count;
     const CamParams cp = make_cam(cam);
     const CfgParams kp = make_cfg(cfg, cam);
     const uint64_t ntile = static_cast<uint64_t>(kp.tiles_x) * static_cast<uint64_t>(kp.tiles_y);
     const uint64_t npx = static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height);
-    const bool timing = stats && stats->want_timing;
+    const bool timing = j.stats && j.stats->want_timing;
     const uint64_t n1 = std::max<uint64_t>(n, 1);
+    j.ms_bin = j.ms_tsort = j.ms_comp = 0;
 
-    SGS_CUDA(ctx->keys_a.ensure(n1 * 8));
-    SGS_CUDA(ctx->keys_b.ensure(n1 * 8));
-    if (ctx->iota.bytes < n1 * 4) ctx->iota_n = 0;
-    SGS_CUDA(ctx->iota.ensure(n1 * 4));
-    SGS_CUDA(ctx->order.ensure(n1 * 4));
-    SGS_CUDA(ctx->rec.ensure(n1 * sizeof(SplatRec)));
-    SGS_CUDA(ctx->rects.ensure(n1 * sizeof(int4)));
-    SGS_CUDA(ctx->colour.ensure(n1 * sizeof(float4)));
-    SGS_CUDA(ctx->ntiles.ensure(n1 * 4));
-    SGS_CUDA(ctx->brect.ensure(n1 * sizeof(int4)));
-    SGS_CUDA(ctx->bmeta.ensure(n1 * sizeof(uint2)));
-    SGS_CUDA(ctx->counts.ensure((n + 1) * 8));
-    SGS_CUDA(ctx->offsets.ensure((n + 1) * 8));
-    SGS_CUDA(ctx->ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
-    SGS_CUDA(ctx->sort_hist.ensure(tile_sort_hist_bytes()));
-    if (ctx->tkey_cap == 0) ctx->tkey_cap = std::max<uint64_t>(16 * n, 1 << 20);
-    SGS_CUDA(ctx->tkeys_a.ensure(ctx->tkey_cap * 8));
-    SGS_CUDA(ctx->tkeys_b.ensure(ctx->tkey_cap * 8));
+    SGS_CUDA(L.keys_a.ensure(n1 * 8));
+    SGS_CUDA(L.keys_b.ensure(n1 * 8));
+    if (L.iota.bytes < n1 * 4) L.iota_n = 0;
+    SGS_CUDA(L.iota.ensure(n1 * 4));
+    SGS_CUDA(L.order.ensure(n1 * 4));
+    SGS_CUDA(L.rec.ensure(n1 * sizeof(SplatRec)));
+    SGS_CUDA(L.rects.ensure(n1 * sizeof(int4)));
+    SGS_CUDA(L.colour.ensure(n1 * sizeof(float4)));
+    SGS_CUDA(L.ntiles.ensure(n1 * 4));
+    SGS_CUDA(L.brect.ensure(n1 * sizeof(int4)));
+    SGS_CUDA(L.bmeta.ensure(n1 * sizeof(uint2)));
+    SGS_CUDA(L.counts.ensure((n + 1) * 8));
+    SGS_CUDA(L.offsets.ensure((n + 1) * 8));
+    SGS_CUDA(L.ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
+    SGS_CUDA(L.sort_hist.ensure(tile_sort_hist_bytes()));
+    if (L.tkey_cap == 0) L.tkey_cap = std::max<uint64_t>(16 * n, 1 << 20);
+    SGS_CUDA(L.tkeys_a.ensure(L.tkey_cap * 8));
+    SGS_CUDA(L.tkeys_b.ensure(L.tkey_cap * 8));
+    float* d_rgb = j.d_rgb;
+    float* d_T = j.d_T;
+    if (j.h_rgb) {
+        SGS_CUDA(L.out_rgb.ensure(npx * 3 * sizeof(float)));
+        d_rgb = L.out_rgb.as<float>();
+    }
+    if (j.h_T) {
+        SGS_CUDA(L.out_T.ensure(npx * sizeof(float)));
+        d_T = L.out_T.as<float>();
+    }
 
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[0], s));
-    SGS_CUDA(cudaMemcpyAsync(ctx->d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
+    if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));
+    SGS_CUDA(cudaMemcpyAsync(L.d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
     if (mode == kRender) {
-        // the pinned staging block is reused every frame; the previous frame has
-        // completed (run_frame synchronises at its end)
-        ctx->h_consts->sp = scene->planes;
-        ctx->h_consts->cam = cp;
-        SGS_CUDA(cudaMemcpyAsync(ctx->d_consts, ctx->h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
+        // the pinned staging block is per lane; the lane's previous frame has
+        // completed (finish_frame waits for it before the lane is reused)
+        L.h_consts->sp = scene->planes;
+        L.h_consts->cam = cp;
+        SGS_CUDA(cudaMemcpyAsync(L.d_consts, L.h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
     }
 
     // K1
-    if (ctx->iota_n < n) {  // identity values for the depth sort (kept across frames)
-        launch_iota(n, ctx->iota.as<uint32_t>(), s);
-        ctx->iota_n = n;
+    if (L.iota_n < n) {  // identity values for the depth sort (kept across frames)
+        launch_iota(n, L.iota.as<uint32_t>(), s);
+        L.iota_n = n;
     }
-    launch_preprocess(scene->planes, cp, kp, ctx->keys_a.as<unsigned long long>(), ctx->rec.as<SplatRec>(),
-                      ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->colour.as<float4>(), ctx->d_ctr,
-                      d_debug, s);
+    launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
+                      L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, j.d_debug, s);
     SGS_CUDA(cudaGetLastError());
     if (n) ctx->own_launches += 1;
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[1], s));
+    if (timing) SGS_CUDA(cudaEventRecord(L.ev[1], s));
     if (mode == kProjectOnly) {
-        SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-        SGS_CUDA(cudaStreamSynchronize(s));
-        if (ctx->h_ctr->err != ~0ULL) return device_error(ctx->h_ctr->err, scene, cfg);
+        SGS_CUDA(cudaMemcpyAsync(L.h_ctr, L.d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+        SGS_CUDA(cudaEventRecord(L.done, s));
         return SGS_OK;
     }
 
     // K2
-    const uint32_t* order = ctx->iota.as<uint32_t>();
+    const uint32_t* order = L.iota.as<uint32_t>();
     if (n > 1) {
-        sgs_status st = sort_depth(ctx, n, wide_sort, s, &order);
+        sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order);
         if (st != SGS_OK) return st;
     }
     // rank-ordered binning inputs, gathered once for every chunk
-    launch_gather_bins(n, order, ctx->rects.as<int4>(), ctx->ntiles.as<uint32_t>(), ctx->brect.as<int4>(),
-                       ctx->bmeta.as<uint2>(), s);
+    launch_gather_bins(n, order, L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.brect.as<int4>(),
+                       L.bmeta.as<uint2>(), s);
     if (n) ctx->own_launches += 1;
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[2], s));
+    if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 
     // depth chunks over ranks (bounds known on the host: culled splats sort last and
     // contribute no tiles, so rank bounds can be taken over N)
@@ -345,10 +381,10 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
             const uint64_t b = (n + div - 1) / div;
             if (b > bounds.back() && b < n) bounds.push_back(b);
         }
-        SGS_CUDA(ctx->tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
-        SGS_CUDA(ctx->pix_state.ensure(npx * sizeof(PixelState)));
-        SGS_CUDA(ctx->pix_walked.ensure(npx * sizeof(uint32_t)));
-        SGS_CUDA(cudaMemsetAsync(ctx->tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
+        SGS_CUDA(L.tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
+        SGS_CUDA(L.pix_state.ensure(npx * sizeof(PixelState)));
+        SGS_CUDA(L.pix_walked.ensure(npx * sizeof(uint32_t)));
+        SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
     }
     bounds.push_back(n);
     const int nchunks = static_cast<int>(bounds.size()) - 1;
@@ -357,108 +393,180 @@ int run_frame_once(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* c
                                   static_cast<float>(scene->meta.background[2]));
     const int tile_bits = std::max(1, ceil_log2(ntile));
     const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
-    SGS_CUDA(ctx->work.ensure((work_cap + 4) * sizeof(uint32_t)));
-    // work items: tiles always need a pass at least in the last chunk
-    const unsigned long long* d_pc = &ctx->d_ctr->chunk_entries;
-    float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
+    SGS_CUDA(L.work.ensure((work_cap + 4) * sizeof(uint32_t)));
+    const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
     for (int c = 0; c < nchunks; ++c) {
         const uint64_t rb = bounds[c], re = bounds[c + 1];
-        const uint32_t* done = c > 0 ? ctx->tile_done.as<uint32_t>() : nullptr;
-        if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[3], s));
+        const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
+        if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
         // K3 + K4
-        sgs_status st = count_and_scan(ctx, rb, re, order, done, kp.tiles_x, static_cast<int>(ntile), s);
+        sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
         if (st != SGS_OK) return st;
-        launch_emit_tile_keys(rb, re, ctx->bmeta.as<uint2>(), ctx->brect.as<int4>(), done,
-                              ctx->offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
-                              ctx->tkeys_a.as<unsigned long long>(), ctx->tkey_cap, s);
+        launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
+                              L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
+                              L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
         SGS_CUDA(cudaGetLastError());
         if (re > rb) ctx->own_launches += 1;
-        if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[4], s));
+        if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
         // K5 (device-sized stable radix sort on the tile bits)
-        const unsigned long long* tkeys = tile_sort(ctx->tkeys_a.as<unsigned long long>(),
-                                                    ctx->tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
-                                                    ctx->sort_hist.as<uint32_t>(), s, &ctx->own_launches);
+        const unsigned long long* tkeys =
+            tile_sort(L.tkeys_a.as<unsigned long long>(), L.tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
+                      L.sort_hist.as<uint32_t>(), s, &ctx->own_launches);
         // K6
-        SGS_CUDA(cudaMemsetAsync(ctx->ranges.ptr, 0, ntile * sizeof(uint2), s));
-        launch_tile_ranges(d_pc, tkeys, ctx->ranges.as<uint2>(), s);
+        SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
+        launch_tile_ranges(d_pc, tkeys, L.ranges.as<uint2>(), s);
         SGS_CUDA(cudaGetLastError());
         ctx->own_launches += 1;
-        if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[5], s));
-        ctx->last_order = order;
-        ctx->last_tile_keys = tkeys;
+        if (timing) SGS_CUDA(cudaEventRecord(L.ev[5], s));
+        L.last_order = order;
+        L.last_tile_keys = tkeys;
         // K7
         if (mode == kRender) {
-            launch_composite(ctx->d_consts, cp, kp, ctx->ranges.as<uint2>(), tkeys, ctx->rec.as<SplatRec>(),
-                             ctx->colour.as<float4>(), bg, d_rgb, d_T, ctx->pix_state.as<PixelState>(), ctx->pix_walked.as<uint32_t>(),
-                             ctx->tile_done.as<uint32_t>(), ctx->tile_done.as<uint32_t>() + (ntile + 31) / 32,
-                             c == 0, c == nchunks - 1, ctx->d_ctr, stats != nullptr, ctx->work.as<uint32_t>(),
-                             ctx->work.as<uint32_t>() + work_cap, s);
+            launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), tkeys, L.rec.as<SplatRec>(),
+                             L.colour.as<float4>(), bg, d_rgb, d_T, L.pix_state.as<PixelState>(),
+                             L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
+                             L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1, L.d_ctr,
+                             j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + work_cap, s);
             SGS_CUDA(cudaGetLastError());
             ctx->own_launches += 2;  // work list + persistent compositor
         }
         if (timing) {
-            SGS_CUDA(cudaEventRecord(ctx->ev[6], s));
-            SGS_CUDA(cudaEventSynchronize(ctx->ev[6]));
+            SGS_CUDA(cudaEventRecord(L.ev[6], s));
+            SGS_CUDA(cudaEventSynchronize(L.ev[6]));
             float a = 0, b = 0, d = 0;
-            SGS_CUDA(cudaEventElapsedTime(&a, ctx->ev[3], ctx->ev[4]));
-            SGS_CUDA(cudaEventElapsedTime(&b, ctx->ev[4], ctx->ev[5]));
-            SGS_CUDA(cudaEventElapsedTime(&d, ctx->ev[5], ctx->ev[6]));
-            ms_bin += a;
-            ms_tsort += b;
-            ms_comp += d;
+            SGS_CUDA(cudaEventElapsedTime(&a, L.ev[3], L.ev[4]));
+            SGS_CUDA(cudaEventElapsedTime(&b, L.ev[4], L.ev[5]));
+            SGS_CUDA(cudaEventElapsedTime(&d, L.ev[5], L.ev[6]));
+            j.ms_bin += a;
+            j.ms_tsort += b;
+            j.ms_comp += d;
         }
     }
-    if (timing) SGS_CUDA(cudaEventRecord(ctx->ev[7], s));
-    SGS_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-    SGS_CUDA(cudaStreamSynchronize(s));
-    const Counters& hc = *ctx->h_ctr;
-    if (hc.err != ~0ULL) return device_error(hc.err, scene, cfg);
-    if (hc.tie_overflow && !wide_sort) return kRetryWide;
+    if (timing) SGS_CUDA(cudaEventRecord(L.ev[7], s));
+    if (mode == kRender) {
+        if (j.h_rgb)
+            SGS_CUDA(cudaMemcpyAsync(j.h_rgb, d_rgb, npx * 3 * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (j.h_T) SGS_CUDA(cudaMemcpyAsync(j.h_T, d_T, npx * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    SGS_CUDA(cudaMemcpyAsync(L.h_ctr, L.d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaEventRecord(L.done, s));
+    return SGS_OK;
+}
+
+// Wait for lane L's frame and check it: SGS_OK / an error status, or kRetryWide /
+// kRetryGrow when the frame must be enqueued again.
+int check_frame(Lane& L) {
+    Lane::Job& j = L.job;
+    SGS_CUDA(cudaEventSynchronize(L.done));
+    const Counters& hc = *L.h_ctr;
+    if (hc.err != ~0ULL) return device_error(hc.err, j.scene, &j.cfg);
+    if (j.mode == kProjectOnly) return SGS_OK;
+    if (hc.tie_overflow && !j.wide) return kRetryWide;
     if (hc.key_overflow) {
-        ctx->tkey_cap = hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024;
+        L.tkey_cap = hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024;
         return kRetryGrow;
     }
-    ctx->last_v = hc.visible;
-    ctx->last_p = hc.chunk_entries;  // the (single) chunk's P for the debug dump
-    if (stats) {
+    L.last_v = hc.visible;
+    L.last_p = hc.chunk_entries;  // the (single) chunk's P for the debug dump
+    if (sgs_render_stats* stats = j.stats) {
         stats->visible += hc.visible;
         stats->tile_entries += hc.tile_entries;
         stats->block_entries += hc.block_entries;
         stats->guard_hits += hc.guard_hits;
-        if (timing) {
+        if (stats->want_timing) {
             float k1 = 0, k2 = 0, total = 0;
-            SGS_CUDA(cudaEventElapsedTime(&k1, ctx->ev[0], ctx->ev[1]));
-            SGS_CUDA(cudaEventElapsedTime(&k2, ctx->ev[1], ctx->ev[2]));
-            SGS_CUDA(cudaEventElapsedTime(&total, ctx->ev[0], ctx->ev[7]));
+            SGS_CUDA(cudaEventElapsedTime(&k1, L.ev[0], L.ev[1]));
+            SGS_CUDA(cudaEventElapsedTime(&k2, L.ev[1], L.ev[2]));
+            SGS_CUDA(cudaEventElapsedTime(&total, L.ev[0], L.ev[7]));
             stats->ms_preprocess += k1;
             stats->ms_depth_sort += k2;
-            stats->ms_binning += ms_bin;
-            stats->ms_tile_sort += ms_tsort;
-            stats->ms_composite += ms_comp;
+            stats->ms_binning += j.ms_bin;
+            stats->ms_tile_sort += j.ms_tsort;
+            stats->ms_composite += j.ms_comp;
             stats->ms_total += total;
         }
     }
     return SGS_OK;
 }
 
-sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
-                     const sgs_render_config* cfg, float* d_rgb, float* d_T, sgs_render_stats* stats,
-                     DebugSplat* d_debug, FrameMode mode) {
+// Settle lane L's frame: check it, re-enqueue on a retry verdict, until it is done.
+sgs_status finish_frame(sgs_context* ctx, Lane& L) {
+    if (!L.busy) return SGS_OK;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        const int rc = check_frame(L);
+        if (rc == kRetryWide || rc == kRetryGrow) {
+            if (rc == kRetryWide) L.job.wide = true;
+            sgs_status st = enqueue_frame(ctx, L);
+            if (st != SGS_OK) {
+                L.busy = false;
+                return st;
+            }
+            continue;
+        }
+        L.busy = false;
+        return static_cast<sgs_status>(rc);
+    }
+    L.busy = false;
+    return fail(SGS_ERR_INTERNAL, "frame did not converge after re-sizing");
+}
+
+// Start a frame on lane L (which must be idle).
+sgs_status start_frame(sgs_context* ctx, Lane& L, const sgs_scene* scene, const sgs_camera* cam,
+                       const sgs_render_config* cfg, float* d_rgb, float* d_T, float* h_rgb, float* h_T,
+                       sgs_render_stats* stats, DebugSplat* d_debug, FrameMode mode) {
     if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
     sgs_status st = validate_camera(cam);
     if (st != SGS_OK) return st;
-    bool wide = false;
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        const int rc = run_frame_once(ctx, scene, cam, cfg, d_rgb, d_T, stats, d_debug, mode, wide);
-        if (rc == kRetryWide) {
-            wide = true;
-            continue;
-        }
-        if (rc == kRetryGrow) continue;
-        return static_cast<sgs_status>(rc);
+    Lane::Job& j = L.job;
+    j = Lane::Job{};
+    j.scene = scene;
+    j.cam = *cam;
+    j.cfg = *cfg;
+    j.d_rgb = d_rgb;
+    j.d_T = d_T;
+    j.h_rgb = h_rgb;
+    j.h_T = h_T;
+    j.stats = stats;
+    j.d_debug = d_debug;
+    j.mode = mode;
+    L.busy = true;
+    st = enqueue_frame(ctx, L);
+    if (st != SGS_OK) {
+        cudaStreamSynchronize(L.stream);
+        L.busy = false;
     }
-    return fail(SGS_ERR_INTERNAL, "frame did not converge after re-sizing");
+    return st;
 }
+
+// Lanes start after the work already queued on the caller's stream ...
+sgs_status fork_lanes(sgs_context* ctx, int lanes) {
+    SGS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
+    for (int k = 0; k < lanes; ++k) SGS_CUDA(cudaStreamWaitEvent(ctx->lane[k].stream, ctx->fork, 0));
+    return SGS_OK;
+}
+
+// ... and the caller's stream continues after every lane's last frame.
+sgs_status join_lanes(sgs_context* ctx, int lanes) {
+    for (int k = 0; k < lanes; ++k) {
+        Lane& L = ctx->lane[k];
+        if (L.busy) finish_frame(ctx, L);
+        SGS_CUDA(cudaEventRecord(L.done, L.stream));
+        SGS_CUDA(cudaStreamWaitEvent(ctx->stream, L.done, 0));
+    }
+    return SGS_OK;
+}
+
+// One frame on lane 0, synchronously (projection / debug dumps).
+sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam, const sgs_render_config* cfg,
+                     DebugSplat* d_debug, FrameMode mode) {
+    sgs_status st = fork_lanes(ctx, 1);
+    if (st != SGS_OK) return st;
+    st = start_frame(ctx, ctx->lane[0], scene, cam, cfg, nullptr, nullptr, nullptr, nullptr, nullptr, d_debug, mode);
+    if (st == SGS_OK) st = finish_frame(ctx, ctx->lane[0]);
+    sgs_status sj = join_lanes(ctx, 1);
+    return st != SGS_OK ? st : sj;
+}
+
 
 // ---------------------------------------------------------------------------
 // Scene layout and upload.
@@ -633,16 +741,22 @@ sgs_status sgs_create(int device, sgs_context** out) {
     auto* ctx = new sgs_context();
     ctx->device = device;
     SGS_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
-    SGS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
-    SGS_CUDA(cudaMalloc(&ctx->d_ctr, sizeof(Counters)));
-    SGS_CUDA(cudaMallocHost(&ctx->h_ctr, sizeof(Counters)));
     SGS_CUDA(cudaMallocHost(&ctx->h_ctr_init, sizeof(Counters)));
-    SGS_CUDA(cudaMalloc(&ctx->d_consts, sizeof(FrameConsts)));
-    SGS_CUDA(cudaMallocHost(&ctx->h_consts, sizeof(FrameConsts)));
     std::memset(ctx->h_ctr_init, 0, sizeof(Counters));
     ctx->h_ctr_init->err = ~0ULL;
     ctx->h_ctr_init->kmin = ~0ULL;
+    SGS_CUDA(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+    for (Lane& L : ctx->lane) {
+        SGS_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+        SGS_CUDA(cudaMalloc(&L.d_ctr, sizeof(Counters)));
+        SGS_CUDA(cudaMallocHost(&L.h_ctr, sizeof(Counters)));
+        SGS_CUDA(cudaMalloc(&L.d_consts, sizeof(FrameConsts)));
+        SGS_CUDA(cudaMallocHost(&L.h_consts, sizeof(FrameConsts)));
+        for (auto& ev : L.ev) SGS_CUDA(cudaEventCreate(&ev));
+        SGS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+    }
+    if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
         ctx->chunk_divs.clear();
@@ -654,11 +768,6 @@ sgs_status sgs_create(int device, sgs_context** out) {
             q = *endp ? endp + 1 : endp;
         }
     }
-    for (auto& ev : ctx->ev) SGS_CUDA(cudaEventCreate(&ev));
-    for (int k = 0; k < 2; ++k) {
-        SGS_CUDA(cudaEventCreateWithFlags(&ctx->frame_done[k], cudaEventDisableTiming));
-        SGS_CUDA(cudaEventCreateWithFlags(&ctx->slot_free[k], cudaEventDisableTiming));
-    }
     *out = ctx;
     return SGS_OK;
 }
@@ -667,25 +776,24 @@ void sgs_destroy(sgs_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    cudaStreamSynchronize(ctx->copy_stream);
-    for (DevBuf* b : {&ctx->keys_a, &ctx->keys_b, &ctx->key32_a, &ctx->key32_b, &ctx->iota, &ctx->order,
-                      &ctx->rec, &ctx->colour, &ctx->degree, &ctx->rects, &ctx->ntiles, &ctx->brect, &ctx->bmeta, &ctx->counts, &ctx->offsets,
-                      &ctx->tkeys_a, &ctx->tkeys_b, &ctx->ranges, &ctx->tile_done, &ctx->pix_state,
-                      &ctx->pix_walked, &ctx->cub_temp, &ctx->sort_hist, &ctx->buckets, &ctx->work, &ctx->frame_rgb[0], &ctx->frame_rgb[1],
-                      &ctx->frame_T[0], &ctx->frame_T[1]})
-        b->release();
-    if (ctx->d_ctr) cudaFree(ctx->d_ctr);
-    if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
-    if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
-    if (ctx->d_consts) cudaFree(ctx->d_consts);
-    if (ctx->h_consts) cudaFreeHost(ctx->h_consts);
-    for (auto& ev : ctx->ev) cudaEventDestroy(ev);
-    for (int k = 0; k < 2; ++k) {
-        cudaEventDestroy(ctx->frame_done[k]);
-        cudaEventDestroy(ctx->slot_free[k]);
+    for (Lane& L : ctx->lane) {
+        if (L.stream) cudaStreamSynchronize(L.stream);
+        for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.iota, &L.order, &L.rec, &L.colour, &L.rects, &L.ntiles, &L.brect,
+                          &L.bmeta, &L.counts, &L.offsets, &L.buckets, &L.work, &L.tkeys_a, &L.tkeys_b, &L.ranges,
+                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist, &L.out_rgb, &L.out_T})
+            b->release();
+        if (L.d_ctr) cudaFree(L.d_ctr);
+        if (L.h_ctr) cudaFreeHost(L.h_ctr);
+        if (L.d_consts) cudaFree(L.d_consts);
+        if (L.h_consts) cudaFreeHost(L.h_consts);
+        for (auto& ev : L.ev)
+            if (ev) cudaEventDestroy(ev);
+        if (L.done) cudaEventDestroy(L.done);
+        if (L.stream) cudaStreamDestroy(L.stream);
     }
+    if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
     cudaStreamDestroy(ctx->own_stream);
-    cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
 }
 
@@ -699,7 +807,7 @@ sgs_status sgs_set_stream(sgs_context* ctx, void* stream) {
 sgs_status sgs_synchronize(sgs_context* ctx) {
     if (!ctx) return fail(SGS_ERR_INVALID_ARGUMENT, "null context");
     SGS_CUDA(cudaStreamSynchronize(ctx->stream));
-    SGS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    for (Lane& L : ctx->lane) SGS_CUDA(cudaStreamSynchronize(L.stream));
     return SGS_OK;
 }
 
@@ -833,43 +941,31 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
             return fail(SGS_ERR_INVALID_ARGUMENT, "all batch cameras must share width/height");
     if (W < 1 || H < 1) return validate_camera(&cams[0]);
     const size_t npx = static_cast<size_t>(W) * static_cast<size_t>(H);
-    if (out_memory == SGS_DEVICE) {
-        for (int i = 0; i < n; ++i) {
-            sgs_status st = run_frame(ctx, scene, &cams[i], cfg, rgb ? rgb + i * npx * 3 : nullptr,
-                                      T ? T + i * npx : nullptr, stats, nullptr, kRender);
-            if (st != SGS_OK) return st;
-        }
-        SGS_CUDA(cudaStreamSynchronize(ctx->stream));
-        return SGS_OK;
+    const bool host = out_memory != SGS_DEVICE;
+    // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
+    const int lanes = std::min<int>(stats && stats->want_timing ? 1 : ctx->lanes, n);
+    sgs_status st = fork_lanes(ctx, lanes);
+    if (st != SGS_OK) return st;
+    // view i runs on lane i % lanes; a lane's previous view is settled (checked,
+    // retried if needed) before the lane is reused, so views complete in order
+    for (int i = 0; i < n && st == SGS_OK; ++i) {
+        Lane& L = ctx->lane[i % lanes];
+        st = finish_frame(ctx, L);
+        if (st != SGS_OK) break;
+        float* o_rgb = rgb ? rgb + i * npx * 3 : nullptr;
+        float* o_T = T ? T + i * npx : nullptr;
+        st = start_frame(ctx, L, scene, &cams[i], cfg, host ? nullptr : o_rgb, host ? nullptr : o_T,
+                         host ? o_rgb : nullptr, host ? o_T : nullptr, stats, nullptr, kRender);
     }
-    // Host outputs: render into a double-buffered device frame, copy back on the copy
-    // stream while the next view renders.
-    for (int k = 0; k < 2; ++k) {
-        SGS_CUDA(ctx->frame_rgb[k].ensure(npx * 3 * sizeof(float)));
-        SGS_CUDA(ctx->frame_T[k].ensure(npx * sizeof(float)));
-        SGS_CUDA(cudaEventRecord(ctx->slot_free[k], ctx->copy_stream));
+    for (int k = 0; k < lanes; ++k) {  // settle the views still in flight, in order
+        Lane& L = ctx->lane[(n + k) % lanes];
+        sgs_status sk = finish_frame(ctx, L);
+        if (st == SGS_OK) st = sk;
     }
-    for (int i = 0; i < n; ++i) {
-        const int k = i & 1;
-        SGS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_free[k], 0));
-        sgs_status st = run_frame(ctx, scene, &cams[i], cfg, rgb ? ctx->frame_rgb[k].as<float>() : nullptr,
-                                  T ? ctx->frame_T[k].as<float>() : nullptr, stats, nullptr, kRender);
-        if (st != SGS_OK) {
-            cudaStreamSynchronize(ctx->copy_stream);
-            return st;
-        }
-        SGS_CUDA(cudaEventRecord(ctx->frame_done[k], ctx->stream));
-        SGS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->frame_done[k], 0));
-        if (rgb)
-            SGS_CUDA(cudaMemcpyAsync(rgb + i * npx * 3, ctx->frame_rgb[k].ptr, npx * 3 * sizeof(float),
-                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
-        if (T)
-            SGS_CUDA(cudaMemcpyAsync(T + i * npx, ctx->frame_T[k].ptr, npx * sizeof(float),
-                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
-        SGS_CUDA(cudaEventRecord(ctx->slot_free[k], ctx->copy_stream));
-    }
-    SGS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
-    SGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    sgs_status sj = join_lanes(ctx, lanes);
+    if (st != SGS_OK) return st;
+    if (sj != SGS_OK) return sj;
+    if (host) SGS_CUDA(cudaStreamSynchronize(ctx->stream));
     return SGS_OK;
 }
 
@@ -882,7 +978,7 @@ sgs_status sgs_project(sgs_context* ctx, const sgs_scene* scene, const sgs_camer
     const uint64_t n = scene->meta.count;
     DebugSplat* d_dbg = nullptr;
     SGS_CUDA(cudaMalloc(&d_dbg, std::max<uint64_t>(n, 1) * sizeof(DebugSplat)));
-    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, d_dbg, kProjectOnly);
+    sgs_status st = run_frame(ctx, scene, cam, cfg, d_dbg, kProjectOnly);
     if (st == SGS_OK && n) {
         cudaError_t e = cudaMemcpy(out, d_dbg, n * sizeof(DebugSplat), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
@@ -899,18 +995,19 @@ sgs_status sgs_debug_tile_grid(sgs_context* ctx, const sgs_scene* scene, const s
         return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
     std::lock_guard<std::mutex> lock(ctx->mu);
     SGS_CUDA(cudaSetDevice(ctx->device));
-    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, nullptr, nullptr, nullptr, kTileGrid);
+    sgs_status st = run_frame(ctx, scene, cam, cfg, nullptr, kTileGrid);
     if (st != SGS_OK) return st;
-    SGS_CUDA(cudaStreamSynchronize(ctx->stream));
-    const uint64_t v = ctx->last_v, p = ctx->last_p;
+    const Lane& L = ctx->lane[0];
+    SGS_CUDA(cudaStreamSynchronize(L.stream));
+    const uint64_t v = L.last_v, p = L.last_p;
     *n_visible = v;
     *n_entries = p;
     std::vector<uint32_t> ord(v);
-    if (v) SGS_CUDA(cudaMemcpy(ord.data(), ctx->last_order, v * 4, cudaMemcpyDeviceToHost));
+    if (v) SGS_CUDA(cudaMemcpy(ord.data(), L.last_order, v * 4, cudaMemcpyDeviceToHost));
     if (order && v) std::memcpy(order, ord.data(), v * 4);
     if (!offsets && !entries) return SGS_OK;
     std::vector<unsigned long long> keys(p);
-    if (p) SGS_CUDA(cudaMemcpy(keys.data(), ctx->last_tile_keys, p * 8, cudaMemcpyDeviceToHost));
+    if (p) SGS_CUDA(cudaMemcpy(keys.data(), L.last_tile_keys, p * 8, cudaMemcpyDeviceToHost));
     const uint64_t ntile = static_cast<uint64_t>((cam->width + cfg->tile_size - 1) / cfg->tile_size) *
                            static_cast<uint64_t>((cam->height + cfg->tile_size - 1) / cfg->tile_size);
     if (offsets) {
