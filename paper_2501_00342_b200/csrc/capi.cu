@@ -83,6 +83,7 @@ struct sgs_scene {
     sgs_scene_meta meta{};
     sgs_context* ctx = nullptr;
     DevBuf owned;
+    DevBuf cov;  // cached 3D covariance planes (computed on the device at upload/bind)
     void* blob = nullptr;
     ScenePlanes planes{};
 };
@@ -617,8 +618,20 @@ void bind_planes(sgs_scene* sc) {
         for (int k = 0; k < 3; ++k) p.g4[k] = reinterpret_cast<const float4*>(base + L.geo_off[k]);
     }
     p.color = reinterpret_cast<const float4*>(base + L.color_off);
+    for (int k = 0; k < 3; ++k) p.cov[k] = sc->cov.ptr ? sc->cov.as<double2>() + k * m.count : nullptr;
     for (int k = 0; k < 9; ++k) p.axes[k] = static_cast<float>(m.shared_axes[k]);
     for (int k = 0; k < 3; ++k) p.bg[k] = static_cast<float>(m.background[k]);
+}
+
+// Bind the planes and build the per-scene covariance cache from them, on `stream`
+// after the work already queued there (the blob's producer), then wait for it.
+sgs_status bind_and_cache(sgs_scene* sc, cudaStream_t stream) {
+    SGS_CUDA(sc->cov.ensure(std::max<size_t>(sc->meta.count, 1) * 3 * sizeof(double2)));
+    bind_planes(sc);
+    launch_cov3d(sc->planes, sc->cov.as<double2>(), stream);
+    SGS_CUDA(cudaGetLastError());
+    SGS_CUDA(cudaStreamSynchronize(stream));
+    return SGS_OK;
 }
 
 double param_at(const sgs_scene_desc* d, size_t idx) {
@@ -716,7 +729,11 @@ sgs_status upload_common(sgs_context* ctx, const sgs_scene_desc* desc, void* blo
         delete sc;
         return fail(SGS_ERR_CUDA, std::string("scene upload: ") + cudaGetErrorString(e));
     }
-    bind_planes(sc);
+    st = bind_and_cache(sc, ctx->stream);
+    if (st != SGS_OK) {
+        sgs_scene_free(sc);
+        return st;
+    }
     *out = sc;
     return SGS_OK;
 }
@@ -889,7 +906,13 @@ sgs_status sgs_scene_bind(sgs_context* ctx, const sgs_scene_meta* meta, void* de
     sc->meta = m;
     sc->ctx = ctx;
     sc->blob = device_blob;
-    bind_planes(sc);
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    sgs_status st = bind_and_cache(sc, ctx->stream);
+    if (st != SGS_OK) {
+        sgs_scene_free(sc);
+        return st;
+    }
     *out = sc;
     return SGS_OK;
 }
@@ -918,6 +941,7 @@ void sgs_scene_free(sgs_scene* scene) {
     if (!scene) return;
     if (scene->ctx) cudaSetDevice(scene->ctx->device);
     scene->owned.release();
+    scene->cov.release();
     delete scene;
 }
 

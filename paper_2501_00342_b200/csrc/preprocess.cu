@@ -17,6 +17,7 @@
 // (48 B/Gaussian), colour only the planes the evaluated degree needs
 // (MIXED+SH1: 6 planes = 96 B). Outputs per visible splat: 8 B depth key,
 // 48 B compositing record, 32 B FP64 guard record, 16 B tile rect, 4 B count.
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -34,20 +35,92 @@ __constant__ float kC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.457045
                              0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
                              -0.5900435899266435f};
 
-// Loads the first `nplanes` colour planes of Gaussian i into f[4*nplanes].
-template <int MAXP>
-__device__ __forceinline__ void load_planes(const float4* __restrict__ color, uint64_t n,
-                                            uint64_t i, int nplanes, float* f) {
-#pragma unroll
-    for (int p = 0; p < MAXP; ++p) {
-        if (p < nplanes) {
-            float4 v = __ldg(&color[static_cast<uint64_t>(p) * n + i]);
-            f[4 * p + 0] = v.x;
-            f[4 * p + 1] = v.y;
-            f[4 * p + 2] = v.z;
-            f[4 * p + 3] = v.w;
-        }
+constexpr int kK1Threads = 256;
+
+// What one launch stages per Gaussian (float4 slots of kK1Threads each): the
+// geometry (F32: pos + logit opacity; F64: two double2), the cached covariance
+// (3 x double2) and the colour planes every Gaussian of this launch needs.
+struct K1Stage {
+    int geo_slots;   // 1 (F32) or 2 (F64)
+    int sh_pre;      // SH planes staged, from plane 0
+    int lobe_base;   // first lobe plane (MIXED: after the stored SH planes)
+    int lobe_pre;    // lobe planes staged (MIXED 3, SG1 3, SG3 4)
+    int slots;       // geo_slots + 3 + sh_pre + lobe_pre
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Thread-private staging: each thread copies its own Gaussian's slots (coalesced
+// across the warp, slot-major so smem reads are conflict free) and later reads
+// only them, so no CTA barrier is needed.
+template <bool F64>
+__device__ __forceinline__ void stage_item(const ScenePlanes& sp, const K1Stage& st, uint64_t i, float4* buf,
+                                           int tid) {
+    if constexpr (F64) {
+        cp_async8(&buf[tid], &sp.g8[0][i]);
+        cp_async8(reinterpret_cast<double*>(&buf[tid]) + 1, &sp.g8[1][i]);
+        cp_async8(&buf[kK1Threads + tid], &sp.g8[2][i]);
+        cp_async8(reinterpret_cast<double*>(&buf[kK1Threads + tid]) + 1, &sp.g8[10][i]);
+    } else {
+        cp_async16(&buf[tid], &sp.g4[0][i]);
     }
+    float4* b = buf + st.geo_slots * kK1Threads;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cp_async16(&b[k * kK1Threads + tid], &sp.cov[k][i]);
+    b += 3 * kK1Threads;
+    for (int p = 0; p < st.sh_pre; ++p) cp_async16(&b[p * kK1Threads + tid], &sp.color[static_cast<uint64_t>(p) * sp.n + i]);
+    b += st.sh_pre * kK1Threads;
+    for (int p = 0; p < st.lobe_pre; ++p)
+        cp_async16(&b[p * kK1Threads + tid], &sp.color[static_cast<uint64_t>(st.lobe_base + p) * sp.n + i]);
+}
+
+template <bool F64>
+__device__ __forceinline__ void geo_from_stage(const float4* buf, int geo_slots, int tid, Geo& g) {
+    if constexpr (F64) {
+        const double2 a = reinterpret_cast<const double2*>(buf)[tid];
+        const double2 b = reinterpret_cast<const double2*>(buf)[kK1Threads + tid];
+        g.p[0] = a.x, g.p[1] = a.y, g.p[2] = b.x, g.opl = b.y;
+    } else {
+        const float4 a = buf[tid];
+        g.p[0] = a.x, g.p[1] = a.y, g.p[2] = a.z, g.opl = a.w;
+    }
+    const double2* c = reinterpret_cast<const double2*>(buf + geo_slots * kK1Threads);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double2 v = c[k * kK1Threads + tid];
+        g.S[2 * k] = v.x;
+        g.S[2 * k + 1] = v.y;
+    }
+}
+
+// Colour plane p of Gaussian i: staged copy when the launch staged it, else HBM
+// (adaptive degree selection loads the higher SH bands on demand).
+struct PlaneFetch {
+    const float4* sh;    // staged SH planes (slot-major) or null
+    const float4* lobe;  // staged lobe planes
+    const float4* color;
+    uint64_t n, i;
+    int tid, sh_pre, lobe_base;
+    __device__ __forceinline__ float4 sh_plane(int p) const {
+        return p < sh_pre ? sh[p * kK1Threads + tid] : __ldg(&color[static_cast<uint64_t>(p) * n + i]);
+    }
+    __device__ __forceinline__ float4 lobe_plane(int p) const { return lobe[p * kK1Threads + tid]; }
+};
+
+__device__ __forceinline__ void put4(float* f, float4 v) {
+    f[0] = v.x;
+    f[1] = v.y;
+    f[2] = v.z;
+    f[3] = v.w;
 }
 
 // sum_i Y_i(d) * c_i for degree `deg` <= MAXD (eval_sh_basis + sh_sum, color.cpp:99-168);
@@ -113,21 +186,22 @@ __device__ __forceinline__ void raise_error(Counters* ctr, uint64_t i, uint32_t 
     atomicMin(&ctr->err, (static_cast<unsigned long long>(i) << 8) | code);
 }
 
-// View-dependent colour (eval_color, color.cpp:201-235) in FP32 from coalesced
-// float4 planes: exactly the colour planes the evaluated degree needs. The view
-// direction normalize(p - C) (raster.cpp:66-69) is taken in FP32; the reference's
-// FP64 decisions (including the unit-direction check) are made by the caller.
+// View-dependent colour (eval_color, color.cpp:201-235) in FP32: exactly the colour
+// planes the evaluated degree needs. The view direction normalize(p - C)
+// (raster.cpp:66-69) is taken in FP32; the reference's FP64 decisions (including the
+// unit-direction check) are made by the caller.
 template <int KIND>
-__device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, uint64_t i, int deg, float fx, float fy,
-                                              float fz) {
+__device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, const PlaneFetch& pf, int deg, float fx,
+                                              float fy, float fz) {
     float col[3];
     if constexpr (KIND == SGS_SH || KIND == SGS_MIXED) {
-        const int stored_planes = (3 * (sp.sh_degree + 1) * (sp.sh_degree + 1) + 3) / 4;
         const int need = (3 * (deg + 1) * (deg + 1) + 3) / 4;
         // MIXED stores degree <= 2 (7 planes); SH up to degree 3 (12 planes)
         constexpr int kMaxPlanes = KIND == SGS_MIXED ? 7 : 12;
         float c[4 * kMaxPlanes];
-        load_planes<kMaxPlanes>(sp.color, sp.n, i, need, c);
+#pragma unroll
+        for (int p = 0; p < kMaxPlanes; ++p)
+            if (p < need) put4(c + 4 * p, pf.sh_plane(p));
         float acc[3] = {0.f, 0.f, 0.f};
         if constexpr (KIND == SGS_MIXED)
             sh_accumulate_upto<2>(c, deg, fx, fy, fz, acc);
@@ -138,7 +212,8 @@ __device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, uint64_t i,
         col[2] = 0.5f + acc[2];
         if constexpr (KIND == SGS_MIXED) {
             float lobes[12];
-            load_planes<3>(sp.color + static_cast<uint64_t>(stored_planes) * sp.n, sp.n, i, 3, lobes);
+#pragma unroll
+            for (int p = 0; p < 3; ++p) put4(lobes + 4 * p, pf.lobe_plane(p));
             float lacc[3] = {0.f, 0.f, 0.f};
             lobe_accumulate(lobes, sp.axes, fx, fy, fz, lacc);
             col[0] += lacc[0];
@@ -149,7 +224,8 @@ __device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, uint64_t i,
         // diffuse + alpha * exp(lambda (d.mu - 1)) (color.cpp:49-56, :195-199);
         // mu was normalised in FP64 at upload (DiffuseSGModel::lobe).
         float f[12];
-        load_planes<3>(sp.color, sp.n, i, 3, f);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) put4(f + 4 * p, pf.lobe_plane(p));
         const float lambda = expf(f[3]);
         const float e = expf(lambda * (fx * f[8] + fy * f[9] + fz * f[10] - 1.0f));
         col[0] = f[0] + f[4] * e;
@@ -157,7 +233,8 @@ __device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, uint64_t i,
         col[2] = f[2] + f[6] * e;
     } else {
         float f[16];
-        load_planes<4>(sp.color, sp.n, i, 4, f);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) put4(f + 4 * p, pf.lobe_plane(p));
         float lacc[3] = {0.f, 0.f, 0.f};
         lobe_accumulate(f + 4, sp.axes, fx, fy, fz, lacc);
         col[0] = f[0] + lacc[0];
@@ -168,29 +245,46 @@ __device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, uint64_t i,
     return make_float4(col[0] < 0.f ? 0.f : col[0], col[1] < 0.f ? 0.f : col[1], col[2] < 0.f ? 0.f : col[2], 0.f);
 }
 
+// K1: persistent CTAs walk the Gaussians with a two-stage cp.async pipeline (the
+// next Gaussian's geometry, covariance and colour planes land in shared memory
+// while this one is projected), so the FP64 chain overlaps the HBM latency.
 // MINB (min resident CTAs per SM) trades registers for occupancy; selected at run
 // time by SGS_K1_MINB for tuning (default kDefaultMinB, see profiles/).
-template <bool F64, int KIND, int MINB>
-__global__ void __launch_bounds__(256, MINB) preprocess_kernel(
-    const ScenePlanes sp, const CamParams cam, const CfgParams cfg,
+template <bool F64, int KIND, int MINB, bool DEBUG>
+__global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
+    const ScenePlanes sp, const CamParams cam, const CfgParams cfg, const K1Stage stg,
     unsigned long long* __restrict__ depth_keys,
     SplatRec* __restrict__ rec, int4* __restrict__ rects,
     uint32_t* __restrict__ ntiles, float4* __restrict__ colour, Counters* __restrict__ ctr,
     DebugSplat* __restrict__ debug) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool visible = false;
-    unsigned long long vkey = ~0ULL;
-    if (i < sp.n) {
+    extern __shared__ float4 k1_smem[];
+    const int tid = threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kK1Threads;
+    const int buf_stride = stg.slots * kK1Threads;
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * kK1Threads + tid;
+    if (i < sp.n) stage_item<F64>(sp, stg, i, k1_smem, tid);
+    cp_async_commit();
+    uint32_t nvis = 0;
+    unsigned long long kmin = ~0ULL, kmax = 0ULL;
+    for (int it = 0; static_cast<uint64_t>(blockIdx.x) * kK1Threads + static_cast<uint64_t>(it) * stride < sp.n;
+         ++it, i += stride) {
+        if (i + stride < sp.n) stage_item<F64>(sp, stg, i + stride, k1_smem + ((it + 1) & 1) * buf_stride, tid);
+        cp_async_commit();
+        cp_async_wait1();
+        if (i >= sp.n) continue;
+        const float4* buf = k1_smem + (it & 1) * buf_stride;
         unsigned long long key = ~0ULL;
         uint32_t count = 0;
+        bool visible = false;
         Geo g;
         ProjGeo pg;
         DebugSplat dbg;
-        if (debug) {
+        if constexpr (DEBUG) {
             memset(&dbg, 0, sizeof(dbg));
             dbg.degree = -1;
         }
-        const int pstat = project_geometry<F64>(sp, cam, i, g, pg);
+        geo_from_stage<F64>(buf, stg.geo_slots, tid, g);
+        const int pstat = project_staged(g, cam, pg);
         if (pstat == kProjZeroQuat) raise_error(ctr, i, kErrZeroQuaternion);
         do {
             if (pstat != kProjVisible) break;
@@ -198,19 +292,27 @@ __global__ void __launch_bounds__(256, MINB) preprocess_kernel(
             // view direction, camera.hpp:20 and raster.cpp:66-69
             const double ox = dsub(g.p[0], cam.C[0]), oy = dsub(g.p[1], cam.C[1]),
                          oz = dsub(g.p[2], cam.C[2]);
-            const double dist = __dsqrt_rn(dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz)));
-            if (dist < 1e-12) break;
-            // The direction only feeds the FP32 colour. For dist in [1e-100, 1e100] the
-            // reference's normalised vector has |norm - 1| ~ 1e-16, so its unit check
-            // (color.cpp:10-16) cannot fire and a reciprocal suffices; outside that range
-            // (or NaN) the exact division and check run.
-            const bool safe_dist = dist > 1e-100 && dist < 1e100;
-            double dxd, dyd, dzd;
+            const double ss = dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz));
+            // The direction only feeds the FP32 colour. For |p - C|^2 in (1e-20, 1e30)
+            // the reference's distance check (dist < 1e-12) cannot fire and its unit
+            // check (color.cpp:10-16) cannot fire either (|norm - 1| ~ 1e-16), so the
+            // direction is taken in FP32 with rsqrt; outside that range (or NaN) the
+            // exact sqrt, division and checks run.
+            const bool safe_dist = ss > 1e-20 && ss < 1e30;
+            float fdx, fdy, fdz;
+            double dist = 0.0;
             if (safe_dist) {
-                const double rd = 1.0 / dist;
-                dxd = ox * rd, dyd = oy * rd, dzd = oz * rd;
+                const float inv = rsqrtf(static_cast<float>(ss));
+                fdx = static_cast<float>(ox) * inv;
+                fdy = static_cast<float>(oy) * inv;
+                fdz = static_cast<float>(oz) * inv;
             } else {
-                dxd = ddiv(ox, dist), dyd = ddiv(oy, dist), dzd = ddiv(oz, dist);
+                dist = __dsqrt_rn(ss);
+                if (dist < 1e-12) break;  // raster.cpp:66-69 (NaN continues, as in the reference)
+                const float inv = static_cast<float>(1.0 / dist);
+                fdx = static_cast<float>(ox) * inv;
+                fdy = static_cast<float>(oy) * inv;
+                fdz = static_cast<float>(oz) * inv;
             }
             // degree selection and the colour-model error contract (raster.cpp:70-77,
             // color.cpp:201-206, :182-191)
@@ -233,6 +335,7 @@ __global__ void __launch_bounds__(256, MINB) preprocess_kernel(
                 }
             }
             if (!safe_dist) {
+                const double dxd = ddiv(ox, dist), dyd = ddiv(oy, dist), dzd = ddiv(oz, dist);
                 const double nrm =
                     __dsqrt_rn(dadd(dadd(dmul(dxd, dxd), dmul(dyd, dyd)), dmul(dzd, dzd)));
                 if (fabs(dsub(nrm, 1.0)) > 1e-6) {
@@ -252,7 +355,7 @@ __global__ void __launch_bounds__(256, MINB) preprocess_kernel(
             // re-derives the exact FP64 values): one reciprocal instead of three divisions,
             // sigmoid in FP32. The debug dump reports the exact ones.
             double cona, conb, conc, opacity;
-            if (debug) {
+            if constexpr (DEBUG) {
                 exact_conic_opacity(g, pg);
                 cona = pg.cona, conb = pg.conb, conc = pg.conc, opacity = pg.opacity;
             } else {
@@ -302,25 +405,25 @@ __global__ void __launch_bounds__(256, MINB) preprocess_kernel(
             r.ca = static_cast<float>(cona);
             r.cb2 = static_cast<float>(2.0 * conb);
             r.cc = static_cast<float>(conc);
-            r.lop = opacity > 0.0 ? static_cast<float>(log2(opacity)) : -1e30f;
+            r.lop = opacity > 0.0 ? __log2f(static_cast<float>(opacity)) : -1e30f;
             r.cut = static_cast<float>(cut);
             r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
-            r.ext_x = static_cast<float>(sqrt(K * pg.a) * (1.0 + 1e-5) + 1e-3);
-            r.ext_y = static_cast<float>(sqrt(K * pg.c) * (1.0 + 1e-5) + 1e-3);
+            r.ext_x = sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
+            r.ext_y = sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
             // colour (FP32), direction from the FP64 offset
             {
-                const float inv = static_cast<float>(1.0 / dist);
-                const float4 col = eval_colour<KIND>(sp, i, deg, static_cast<float>(ox) * inv,
-                                                     static_cast<float>(oy) * inv, static_cast<float>(oz) * inv);
+                const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
+                const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
+                const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
                 colour[i] = col;
-                if (debug) {
+                if constexpr (DEBUG) {
                     dbg.color[0] = col.x;
                     dbg.color[1] = col.y;
                     dbg.color[2] = col.z;
                 }
             }
             rec[i] = r;
-            if (debug) {
+            if constexpr (DEBUG) {
                 dbg.mean2d[0] = mx;
                 dbg.mean2d[1] = my;
                 dbg.conic[0] = cona;
@@ -334,48 +437,87 @@ __global__ void __launch_bounds__(256, MINB) preprocess_kernel(
             }
         } while (false);
         depth_keys[i] = key;
-        vkey = key;
         ntiles[i] = count;
-        if (debug) debug[i] = dbg;
+        if constexpr (DEBUG) debug[i] = dbg;
+        if (visible) {
+            ++nvis;
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
+        }
     }
     // visible count and depth-key range: one atomic each per warp
-    const unsigned vote = __ballot_sync(0xffffffffu, visible);
-    if (vote) {
-        unsigned long long kmin = visible ? vkey : ~0ULL, kmax = visible ? vkey : 0ULL;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&ctr->visible, static_cast<unsigned long long>(__popc(vote)));
-            atomicMin(&ctr->kmin, kmin);
-            atomicMax(&ctr->kmax, kmax);
-        }
+    for (int o = 16; o > 0; o >>= 1) {
+        nvis += __shfl_xor_sync(0xffffffffu, nvis, o);
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
     }
+    if ((tid & 31) == 0 && nvis) {
+        atomicAdd(&ctr->visible, static_cast<unsigned long long>(nvis));
+        atomicMin(&ctr->kmin, kmin);
+        atomicMax(&ctr->kmax, kmax);
+    }
+}
+
+K1Stage make_stage(const ScenePlanes& sp, const CfgParams& cfg) {
+    K1Stage st{};
+    st.geo_slots = sp.geometry_f64 ? 2 : 1;
+    const int stored_sh = (3 * (sp.sh_degree + 1) * (sp.sh_degree + 1) + 3) / 4;
+    switch (sp.kind) {
+        case SGS_SH:
+            st.sh_pre = stored_sh;  // SH always evaluates its stored degree
+            break;
+        case SGS_MIXED: {
+            // override: every splat uses that degree; adaptive: degree 0 is staged and
+            // higher bands load on demand (an out-of-range override errors in K1)
+            int d = cfg.has_override ? cfg.override_degree : 0;
+            d = d < 0 ? 0 : (d > sp.sh_degree ? sp.sh_degree : d);
+            st.sh_pre = (3 * (d + 1) * (d + 1) + 3) / 4;
+            st.lobe_base = stored_sh;
+            st.lobe_pre = 3;
+            break;
+        }
+        case SGS_SG1: st.lobe_pre = 3; break;
+        default: st.lobe_pre = 4; break;
+    }
+    st.slots = st.geo_slots + 3 + st.sh_pre + st.lobe_pre;
+    return st;
+}
+
+template <bool F64, int KIND, int MINB>
+void launch_k1(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
+               SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
+               cudaStream_t stream) {
+    const K1Stage st = make_stage(sp, cfg);
+    const size_t smem = static_cast<size_t>(2) * st.slots * kK1Threads * sizeof(float4);
+    auto kern = debug ? preprocess_kernel<F64, KIND, 1, true> : preprocess_kernel<F64, KIND, MINB, false>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kK1Threads, smem);
+    const uint64_t need = (sp.n + kK1Threads - 1) / kK1Threads;
+    const uint64_t grid = std::min<uint64_t>(need, static_cast<uint64_t>(sms) * std::max(per_sm, 1));
+    kern<<<static_cast<unsigned>(grid), kK1Threads, smem, stream>>>(sp, cam, cfg, st, keys, rec, rects, ntiles,
+                                                                    colour, ctr, debug);
 }
 
 template <bool F64, int MINB>
 void launch_kind_b(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
                    SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
                    cudaStream_t stream) {
-    const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
     switch (sp.kind) {
         case SGS_SH:
-            preprocess_kernel<F64, SGS_SH, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles,
-                                                                             colour, ctr, debug);
+            launch_k1<F64, SGS_SH, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
             break;
         case SGS_SG1:
-            preprocess_kernel<F64, SGS_SG1, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles,
-                                                                              colour, ctr, debug);
+            launch_k1<F64, SGS_SG1, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
             break;
         case SGS_SG3:
-            preprocess_kernel<F64, SGS_SG3, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects, ntiles,
-                                                                              colour, ctr, debug);
+            launch_k1<F64, SGS_SG3, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
             break;
         default:
-            preprocess_kernel<F64, SGS_MIXED, MINB><<<blocks, 256, 0, stream>>>(sp, cam, cfg, keys, rec, rects,
-                                                                                ntiles, colour, ctr, debug);
+            launch_k1<F64, SGS_MIXED, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
             break;
     }
 }
@@ -404,12 +546,43 @@ void launch_kind(const ScenePlanes& sp, const CamParams& cam, const CfgParams& c
 }
 
 
+// Per-scene cache of the view-independent 3D covariance (projection.cuh).
+template <bool F64>
+__global__ void cov3d_kernel(const ScenePlanes sp, double2* __restrict__ cov) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= sp.n) return;
+    double q[4], ls[3];
+    if constexpr (F64) {
+        for (int k = 0; k < 4; ++k) q[k] = sp.g8[3 + k][i];
+        for (int k = 0; k < 3; ++k) ls[k] = sp.g8[7 + k][i];
+    } else {
+        const float4 b = __ldg(&sp.g4[1][i]);
+        const float4 c = __ldg(&sp.g4[2][i]);
+        q[0] = b.x, q[1] = b.y, q[2] = b.z, q[3] = b.w;
+        ls[0] = c.x, ls[1] = c.y, ls[2] = c.z;
+    }
+    double S6[6] = {kZeroQuatMark, 0.0, 0.0, 0.0, 0.0, 0.0};
+    covariance3d(q, ls, S6);
+    cov[i] = make_double2(S6[0], S6[1]);
+    cov[sp.n + i] = make_double2(S6[2], S6[3]);
+    cov[2 * sp.n + i] = make_double2(S6[4], S6[5]);
+}
+
 __global__ void iota_kernel(uint64_t n, uint32_t* __restrict__ out) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) out[i] = static_cast<uint32_t>(i);
 }
 
 }  // namespace
+
+void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream) {
+    if (sp.n == 0) return;
+    const unsigned blocks = static_cast<unsigned>((sp.n + 255) / 256);
+    if (sp.geometry_f64)
+        cov3d_kernel<true><<<blocks, 256, 0, stream>>>(sp, cov);
+    else
+        cov3d_kernel<false><<<blocks, 256, 0, stream>>>(sp, cov);
+}
 
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream) {
     if (n) iota_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, out);

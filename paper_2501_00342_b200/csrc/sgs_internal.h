@@ -64,6 +64,7 @@ struct ScenePlanes {
     // geometry: f32 -> g4[0..2] (pos+opl, quat, logscale); f64 -> g8[0..10]
     const float4* g4[3];
     const double* g8[11];
+    const double2* cov[3];  // cached 3D covariance (projection.cuh covariance3d)
     const float4* color;  // color_planes consecutive planes of n float4
     float axes[9];        // row-major lobe axes
     float bg[3];
@@ -144,6 +145,8 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream);
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
+// per-scene 3D covariance cache: 3 planes of n double2 (projection.cuh)
+void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream);
 int depth_bucket_log2(uint64_t n);
 void launch_bucket_hist(uint64_t n, const unsigned long long* key, const Counters* ctr, int log2b, uint32_t* hist,
                         cudaStream_t stream);
