@@ -139,6 +139,7 @@ struct sgs_context {
     int lanes = kLanes;                // lanes used by sgs_render_batch (SGS_LANES, 1..kLanes)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
+    bool two_level = true;  // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
     uint64_t own_launches = 0, lib_launches = 0;
@@ -229,10 +230,27 @@ constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, red
 // are finished and receive no keys from the second chunk.
 constexpr uint64_t kMinChunkedN = 1 << 16;
 
-sgs_status sort_depth(sgs_context* ctx, Lane& L, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out) {
+sgs_status sort_depth(sgs_context* ctx, Lane& L, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out,
+                      bool* gathered) {
+    *gathered = false;
     uint32_t* order = L.order.as<uint32_t>();
     size_t temp = 0;
-    if (!wide) {
+    if (!wide && ctx->two_level) {
+        // K2: two-level exact sort; also writes brect/bmeta (depth_sort.cu)
+        const int log2c = depth_coarse_log2(n);
+        const size_t half = align_up(depth_two_level_scratch(n, log2c), 256);
+        SGS_CUDA(L.buckets.ensure(2 * half));
+        uint32_t* mat = L.buckets.as<uint32_t>();
+        uint32_t* off = mat + half / 4;
+        const size_t cub_bytes = depth_two_level_cub_bytes(n, log2c);
+        SGS_CUDA(L.cub_temp.ensure(cub_bytes));
+        launch_depth_two_level(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2c, mat, off,
+                               L.keys_b.as<unsigned long long>(), order, L.rects.as<int4>(), L.ntiles.as<uint32_t>(),
+                               L.brect.as<int4>(), L.bmeta.as<uint2>(), L.cub_temp.ptr, cub_bytes, s);
+        ctx->own_launches += 3;
+        ctx->lib_launches += 2;
+        *gathered = true;
+    } else if (!wide) {
         // K2: exact bucket sort (depth_sort.cu)
         const int log2b = depth_bucket_log2(n);
         const uint32_t nb = 1u << log2b;
@@ -362,14 +380,16 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
 
     // K2
     const uint32_t* order = L.iota.as<uint32_t>();
+    bool gathered = false;
     if (n > 1) {
-        sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order);
+        sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order, &gathered);
         if (st != SGS_OK) return st;
     }
-    // rank-ordered binning inputs, gathered once for every chunk
-    launch_gather_bins(n, order, L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.brect.as<int4>(),
-                       L.bmeta.as<uint2>(), s);
-    if (n) ctx->own_launches += 1;
+    if (!gathered) {  // rank-ordered binning inputs, gathered once for every chunk
+        launch_gather_bins(n, order, L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.brect.as<int4>(),
+                           L.bmeta.as<uint2>(), s);
+        if (n) ctx->own_launches += 1;
+    }
     if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 
     // depth chunks over ranks (bounds known on the host: culled splats sort last and
@@ -774,6 +794,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
         SGS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
     }
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
+    if (const char* e = std::getenv("SGS_DEPTH_SORT")) ctx->two_level = std::strcmp(e, "bucket") != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
         ctx->chunk_divs.clear();

@@ -156,6 +156,14 @@ void launch_bucket_sort(uint32_t nbuckets, const uint32_t* off, const unsigned l
                         Counters* ctr, uint32_t* big, cudaStream_t stream);
 // Tile counts for ranks [rb, re) skipping tiles already terminated (done may be null);
 // counts has re-rb+1 entries (the last is 0 so an exclusive scan yields the total).
+// two-level exact depth sort (depth_sort.cu): ranks + rank-ordered binning inputs
+int depth_coarse_log2(uint64_t n);
+size_t depth_two_level_scratch(uint64_t n, int log2c);
+size_t depth_two_level_cub_bytes(uint64_t n, int log2c);
+void launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters* ctr, int log2c, uint32_t* mat,
+                            uint32_t* off, unsigned long long* part_key, uint32_t* order, const int4* rects,
+                            const uint32_t* ntiles, int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
+                            cudaStream_t stream);
 void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
                         int4* brect, uint2* bmeta, cudaStream_t stream);
 void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
