@@ -43,6 +43,14 @@ __global__ void __launch_bounds__(kSortThreads) upsweep_kernel(const unsigned lo
     for (int d = threadIdx.x; d < radix; d += kSortThreads) hist[d * G + g] = h[d];
 }
 
+// Each step ranks kStep = kSortThreads * kPerThread keys: warp w owns the
+// consecutive keys [t0 + w * 32 kPerThread, +32 kPerThread) in kPerThread rounds of
+// 32, so the stable order inside a step is (warp, round, lane). Within a warp,
+// equal digits are ranked by match.any + popc on top of the warp's running count;
+// across warps by a shared-memory prefix per digit.
+constexpr int kPerThread = 4;
+constexpr int kStep = kSortThreads * kPerThread;
+
 __global__ void __launch_bounds__(kSortThreads) downsweep_kernel(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
     const unsigned long long* __restrict__ count, int shift, int radix, const uint32_t* __restrict__ hist) {
@@ -54,16 +62,27 @@ __global__ void __launch_bounds__(kSortThreads) downsweep_kernel(
     const uint64_t p = *count;
     for (int d = threadIdx.x; d < radix; d += kSortThreads) base[d] = hist[d * G + g];
     const uint32_t b = slice_begin(p, g, G), e = slice_begin(p, g + 1, G);
-    for (uint32_t t0 = b; t0 < e; t0 += kSortThreads) {
+    for (uint32_t t0 = b; t0 < e; t0 += kStep) {
         for (int k = threadIdx.x; k < kSortWarps * 257; k += kSortThreads) (&wcnt[0][0])[k] = 0;
         __syncthreads();
-        const uint32_t i = t0 + threadIdx.x;
-        const bool live = i < e;
-        const unsigned long long key = live ? in[i] : 0ULL;
-        const uint32_t d = live ? static_cast<uint32_t>(key >> shift) & (radix - 1) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
-        if (live && wrank == 0) wcnt[warp][d] = __popc(peers);
+        unsigned long long key[kPerThread];
+        uint32_t dg[kPerThread], rk[kPerThread];
+        const uint32_t w0 = t0 + warp * (32 * kPerThread) + lane;
+#pragma unroll
+        for (int j = 0; j < kPerThread; ++j) {
+            const uint32_t i = w0 + j * 32;
+            key[j] = i < e ? in[i] : 0ULL;
+            dg[j] = i < e ? static_cast<uint32_t>(key[j] >> shift) & (radix - 1) : 256u;
+        }
+#pragma unroll
+        for (int j = 0; j < kPerThread; ++j) {
+            const unsigned peers = __match_any_sync(0xffffffffu, dg[j]);
+            const uint32_t before = wcnt[warp][dg[j]];
+            rk[j] = before + __popc(peers & ((1u << lane) - 1u));
+            __syncwarp();
+            if (__popc(peers & ((1u << lane) - 1u)) == 0) wcnt[warp][dg[j]] = before + __popc(peers);
+            __syncwarp();
+        }
         __syncthreads();
         for (int dd = threadIdx.x; dd < radix; dd += kSortThreads) {
             uint32_t run = 0;
@@ -76,7 +95,9 @@ __global__ void __launch_bounds__(kSortThreads) downsweep_kernel(
             total[dd] = run;
         }
         __syncthreads();
-        if (live) out[base[d] + wcnt[warp][d] + wrank] = key;
+#pragma unroll
+        for (int j = 0; j < kPerThread; ++j)
+            if (dg[j] < 256u) out[base[dg[j]] + wcnt[warp][dg[j]] + rk[j]] = key[j];
         __syncthreads();
         for (int dd = threadIdx.x; dd < radix; dd += kSortThreads) base[dd] += total[dd];
     }
