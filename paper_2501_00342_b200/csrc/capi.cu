@@ -352,7 +352,6 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
         d_T = L.out_T.as<float>();
     }
 
-    if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));
     SGS_CUDA(cudaMemcpyAsync(L.d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
     if (mode == kRender) {
         // the pinned staging block is per lane; the lane's previous frame has
@@ -367,6 +366,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
         launch_iota(n, L.iota.as<uint32_t>(), s);
         L.iota_n = n;
     }
+    if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
     launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
                       L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, j.d_debug, s);
     SGS_CUDA(cudaGetLastError());
