@@ -139,7 +139,8 @@ struct sgs_context {
     int lanes = kLanes;                // lanes used by sgs_render_batch (SGS_LANES, 1..kLanes)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
-    bool two_level = true;  // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
+    bool two_level = true;   // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
+    bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
     uint64_t own_launches = 0, lib_launches = 0;
@@ -421,13 +422,22 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
         const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
         // K3 + K4
-        sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
-        if (st != SGS_OK) return st;
-        launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
-                              L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
-                              L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
-        SGS_CUDA(cudaGetLastError());
-        if (re > rb) ctx->own_launches += 1;
+        if (ctx->fused_bin) {
+            SGS_CUDA(L.counts.ensure(bin_emit_status_bytes(n)));
+            launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+                            static_cast<int>(ntile), L.tkeys_a.as<unsigned long long>(), L.tkey_cap,
+                            L.counts.as<unsigned long long>(), L.d_ctr, s);
+            SGS_CUDA(cudaGetLastError());
+            ctx->own_launches += 1;
+        } else {
+            sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
+            if (st != SGS_OK) return st;
+            launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
+                                  L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
+                                  L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
+            SGS_CUDA(cudaGetLastError());
+            if (re > rb) ctx->own_launches += 1;
+        }
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
         // K5 (device-sized stable radix sort on the tile bits)
         const unsigned long long* tkeys =
@@ -794,6 +804,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
         SGS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
     }
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
+    if (const char* e = std::getenv("SGS_BIN_FUSED")) ctx->fused_bin = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_SORT")) ctx->two_level = std::strcmp(e, "bucket") != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4

@@ -164,6 +164,11 @@ void launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters*
                             uint32_t* off, unsigned long long* part_key, uint32_t* order, const int4* rects,
                             const uint32_t* ntiles, int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
                             cudaStream_t stream);
+// K3+K4 fused: count, decoupled look-back scan and key emission in one pass
+size_t bin_emit_status_bytes(uint64_t ranks);
+void launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
+                     int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
+                     unsigned long long* status, Counters* ctr, cudaStream_t stream);
 void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
                         int4* brect, uint2* bmeta, cudaStream_t stream);
 void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
