@@ -68,8 +68,13 @@ def k1_algorithmic_bytes(v, n=N_GAUSS, n_c=24):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region: NVML (pynvml) in a
+    thread every 5 ms, falling back to `nvidia-smi -lms 100`."""
 
+    NVML_REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap",
+    }
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -77,9 +82,37 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.thread = None
         self.path = f"/tmp/sgs_clocks_{os.getpid()}.csv"
+        self.sms, self.reasons, self.max_sm = [], set(), None
+
+    def _nvml_loop(self, nv, h):
+        import threading
+        while not self._stop.is_set():
+            try:
+                self.sms.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, name in self.NVML_REASONS.items():
+                    if bits & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def start(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader",
@@ -88,8 +121,13 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            return {"sm_mhz": statistics.median(self.sms) if self.sms else None, "sm_max_mhz": self.max_sm,
+                    "reasons": sorted(self.reasons), "samples": len(self.sms), "source": "nvml"}
         if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -112,7 +150,7 @@ class ClockSampler:
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sms) if sms else None,
                 "sm_max_mhz": max(maxs) if maxs else None, "reasons": sorted(reasons),
-                "samples": len(sms)}
+                "samples": len(sms), "source": "nvidia-smi"}
 
 
 def cpu_reference_fps(frames: int, warmup: int, threads: int = 0):
@@ -175,6 +213,8 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=3, help="CPU-baseline sample frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL frame gather")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N>1 (gloo: host-path check only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -190,9 +230,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one process per GPU; local ranks beyond the visible devices wrap (a debug-only
+    # layout for checking the multi-rank host path with --backend gloo on one GPU)
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
+    local = dev
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
     vpr = args.views_per_gpu
     cams_all = sg.orbit_cameras(RING, W, H, 4.0, FOCAL, 0.35)
     my_cams = [cams_all[i] for i in multiview.ring_views_per_rank(vpr, world, rank, RING)]

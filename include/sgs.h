@@ -15,6 +15,8 @@
  *   sgsplat::param_count       color.hpp:139-140                   sgs_color_param_count
  *   make_synthetic_scene       synth.hpp:29, synth.cpp:26-106      sgs_synth_scene
  *   make_orbit_camera(s)       camera.hpp:34-35, synth.hpp:32-33   sgs_orbit_camera(s)
+ *   sgsplat::load_ply          ply.hpp:26-29, ply.cpp:295-306      sgs_ply_read (host) /
+ *                                                                  sgs_scene_load_ply (device)
  *   python `_core.render`      bindings.cpp:109-121                sgs_render
  *
  * Error contract (proj/include/sgsplat/common.hpp:21-42): every call returns an
@@ -47,7 +49,9 @@ typedef enum {
     SGS_ERR_CUDA = 3,
     SGS_ERR_NCCL = 4,
     SGS_ERR_OUT_OF_MEMORY = 5,
-    SGS_ERR_INTERNAL = 6
+    SGS_ERR_INTERNAL = 6,
+    SGS_ERR_IO = 7,               /* sgsplat::IoError */
+    SGS_ERR_FORMAT = 8            /* sgsplat::FormatError */
 } sgs_status;
 
 /* Colour model kinds, numbered as ColorModelKind (color.hpp:59). */
@@ -212,6 +216,32 @@ sgs_status sgs_orbit_camera(const double* target, double distance, double angle,
                             sgs_camera* out);
 sgs_status sgs_orbit_cameras(int32_t count, int32_t width, int32_t height, double distance,
                              double focal, double elevation, sgs_camera* out);
+
+/* --- PLY checkpoints (ply.hpp, ply.cpp) ---------------------------------------- */
+/* The two layouts of ply.hpp:9-22 (PlyLayout). */
+typedef enum { SGS_PLY_REFERENCE3DGS = 0, SGS_PLY_SGEXTENDED = 1 } sgs_ply_layout;
+
+typedef struct {
+    uint64_t count;        /* vertices (Gaussians) */
+    int32_t kind;          /* sgs_color_kind of the checkpoint */
+    int32_t sh_degree;     /* stored SH degree: 3 (Reference3DGS), 2 (mixed), 0 (sg1, sg3) */
+    int32_t layout;        /* sgs_ply_layout, detected from the property names */
+    int32_t binary;        /* 1: binary_little_endian, 0: ascii */
+    double shared_axes[9]; /* row-major; header comment sg_axes, then the .meta sidecar */
+    double background[3];  /* header comment sg_background, then the .meta sidecar */
+} sgs_ply_info;
+
+/* load_ply (ply.cpp:295-306) on the host: params receives count * (11 + colour
+ * params) doubles, the flat order of sgs_scene_desc.params (Scene::param). With params ==
+ * NULL the payload is checked but not kept, and *info filled.
+ * Errors: SGS_ERR_IO (IoError), SGS_ERR_FORMAT (FormatError), SGS_ERR_INVALID_ARGUMENT
+ * (an unknown sg_model name, non-orthonormal sg_axes), with the reference's
+ * messages, checked in the reference's order. */
+sgs_status sgs_ply_read(const char* path, sgs_ply_info* info, double* params, uint64_t params_capacity);
+/* load_ply straight into a device scene: the float rows go to the device once and
+ * a kernel scatters them into the scene planes (the same planes sgs_scene_upload
+ * builds from sgs_ply_read's parameters, bit for bit). */
+sgs_status sgs_scene_load_ply(sgs_context* ctx, const char* path, sgs_ply_info* info, sgs_scene** out);
 
 #ifdef __cplusplus
 }

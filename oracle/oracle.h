@@ -30,7 +30,7 @@ extern "C" {
 enum { ORC_SH = 0, ORC_SG1 = 1, ORC_SG3 = 2, ORC_MIXED = 3 };
 
 /* Error codes (same values as the product's SGS_* codes). */
-enum { ORC_OK = 0, ORC_INVALID_ARGUMENT = 1, ORC_NUMERIC = 2, ORC_INTERNAL = 6 };
+enum { ORC_OK = 0, ORC_INVALID_ARGUMENT = 1, ORC_NUMERIC = 2, ORC_INTERNAL = 6, ORC_IO = 7, ORC_FORMAT = 8 };
 
 /* Pinhole camera, proj/include/sgsplat/camera.hpp:11-23. R is row-major w2c. */
 typedef struct {

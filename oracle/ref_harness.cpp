@@ -8,6 +8,7 @@
 // detail::build_tile_grid / testing::render_bruteforce themselves.
 #include "oracle.h"
 
+#include "sgsplat/ply.hpp"
 #include "sgsplat/raster.hpp"
 #include "sgsplat/synth.hpp"
 #include "support/bruteforce.hpp"
@@ -34,6 +35,10 @@ int fail(const std::exception& e, int code) {
         return fail(e, ORC_INVALID_ARGUMENT);                              \
     } catch (const NumericError& e) {                                      \
         return fail(e, ORC_NUMERIC);                                       \
+    } catch (const IoError& e) {                                           \
+        return fail(e, ORC_IO);                                            \
+    } catch (const FormatError& e) {                                       \
+        return fail(e, ORC_FORMAT);                                        \
     } catch (const std::exception& e) {                                    \
         return fail(e, ORC_INTERNAL);                                      \
     }
@@ -263,6 +268,37 @@ int ref_eval_color(int kind, int degree, const double* cparams, const double* ax
         for (int c = 0; c < 3; ++c) out[c] = col[c];
         return ORC_OK;
     })
+}
+
+// sgsplat::load_ply (proj/src/ply.cpp:295-306). *out receives a Scene handle.
+int ref_load_ply(const char* path, void** out) {
+    REF_GUARD({
+        *out = new Scene(load_ply(path));
+        return ORC_OK;
+    })
+}
+
+// sgsplat::save_ply (proj/src/ply.cpp:308-380); layout 0 = Reference3DGS, 1 = SGExtended.
+int ref_save_ply(void* s, const char* path, int layout) {
+    REF_GUARD({
+        save_ply(*static_cast<Scene*>(s), path,
+                 layout == 0 ? PlyLayout::Reference3DGS : PlyLayout::SGExtended);
+        return ORC_OK;
+    })
+}
+
+// Colour model kind, stored SH degree (0 for SG-only), axes and background of a scene.
+void ref_scene_info(void* s, int* kind, int* degree, double* axes, double* bg) {
+    const Scene& sc = *static_cast<Scene*>(s);
+    *kind = sc.gaussians.empty() ? -1 : static_cast<int>(kind_of(sc.gaussians.front().color));
+    *degree = 0;
+    if (!sc.gaussians.empty()) {
+        if (auto* m = std::get_if<SHOnlyModel>(&sc.gaussians.front().color)) *degree = m->sh.degree;
+        if (auto* m = std::get_if<MixedSHSGModel>(&sc.gaussians.front().color)) *degree = m->sh.degree;
+    }
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) axes[3 * r + c] = sc.shared_axes(r, c);
+    for (int k = 0; k < 3; ++k) bg[k] = sc.background[k];
 }
 
 }  // extern "C"

@@ -15,6 +15,7 @@ memory (`Renderer.render`, `Renderer.render_batch`).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, Optional, Sequence
 
@@ -25,7 +26,8 @@ from . import _capi as C
 __all__ = [
     "Camera", "Scene", "Renderer", "DeviceScene", "RenderStats", "render", "synth_scene",
     "orbit_camera", "orbit_cameras", "flops_per_gaussian", "param_count", "shared_param_count",
-    "select_degree", "InvalidArgumentError", "NumericError", "CudaError",
+    "select_degree", "InvalidArgumentError", "NumericError", "FormatError", "IoError", "CudaError",
+    "load_scene", "load_ply", "ply_info",
 ]
 
 KINDS = {"sh": C.SGS_SH, "sg1": C.SGS_SG1, "sg3": C.SGS_SG3, "mixed": C.SGS_MIXED}
@@ -38,6 +40,14 @@ class InvalidArgumentError(ValueError):
 
 class NumericError(ArithmeticError):
     """sgsplat::NumericError (common.hpp:39-42; bindings.cpp:49)."""
+
+
+class FormatError(ValueError):
+    """sgsplat::FormatError (common.hpp:27-30; bindings.cpp:47)."""
+
+
+class IoError(IOError):
+    """sgsplat::IoError (common.hpp:33-36; bindings.cpp:48)."""
 
 
 class CudaError(RuntimeError):
@@ -56,6 +66,10 @@ def _check(status: int):
         raise InvalidArgumentError(msg)
     if status == C.SGS_ERR_NUMERIC:
         raise NumericError(msg)
+    if status == C.SGS_ERR_FORMAT:
+        raise FormatError(msg)
+    if status == C.SGS_ERR_IO:
+        raise IoError(msg)
     raise CudaError(f"status {status}: {msg}")
 
 
@@ -207,6 +221,34 @@ def synth_scene(count: int, model: str = "sh", seed: int = 0, sh_degree: int = 3
     return Scene(model, deg, params)
 
 
+PLY_LAYOUTS = {C.SGS_PLY_REFERENCE3DGS: "reference", C.SGS_PLY_SGEXTENDED: "extended"}
+
+
+def ply_info(path: str) -> C.sgs_ply_info:
+    """Header (and .meta sidecar) of a PLY checkpoint: count, model, layout."""
+    info = C.sgs_ply_info()
+    _check(_lib().sgs_ply_read(os.fsencode(path), ctypes.byref(info), None, 0))
+    return info
+
+
+def load_scene(path: str) -> Scene:
+    """load_ply (ply.cpp:295-306; bindings.cpp:88 `load_scene`) into a host Scene:
+    Reference3DGS or SG-extended layout, binary little-endian or ASCII, with the
+    reference's errors (IoError, FormatError, InvalidArgumentError)."""
+    info = ply_info(path)
+    kind = KIND_NAMES[info.kind]
+    stride = 11 + param_count(kind, info.sh_degree)
+    params = np.empty((info.count, stride), dtype=np.float64)
+    _check(_lib().sgs_ply_read(os.fsencode(path), ctypes.byref(info),
+                               params.ctypes.data if params.size else None, params.size))
+    return Scene(KIND_NAMES[info.kind], int(info.sh_degree), params,
+                 np.array(info.shared_axes[:], dtype=np.float64).reshape(3, 3),
+                 np.array(info.background[:], dtype=np.float64))
+
+
+load_ply = load_scene
+
+
 def synth_sh3_from_mixed(mixed: Scene, seed: int) -> Scene:
     """BASELINE config D: mixed scene's geometry with degree-3 SH colours."""
     if mixed.kind != "mixed" or mixed.sh_degree != 2:
@@ -322,6 +364,15 @@ class Renderer:
         d, keep = scene._desc()
         h = ctypes.c_void_p()
         _check(self._lib.sgs_scene_upload(self.handle, ctypes.byref(d), ctypes.byref(h)))
+        return DeviceScene(self, h.value)
+
+    def load_ply(self, path: str) -> DeviceScene:
+        """A PLY checkpoint straight into a device scene: the float rows are copied to
+        the device once and scattered into the scene planes by a kernel."""
+        h = ctypes.c_void_p()
+        info = C.sgs_ply_info()
+        _check(self._lib.sgs_scene_load_ply(self.handle, os.fsencode(path), ctypes.byref(info),
+                                            ctypes.byref(h)))
         return DeviceScene(self, h.value)
 
     @staticmethod

@@ -19,6 +19,10 @@ SGS_ERR_CUDA = 3
 SGS_ERR_NCCL = 4
 SGS_ERR_OUT_OF_MEMORY = 5
 SGS_ERR_INTERNAL = 6
+SGS_ERR_IO = 7
+SGS_ERR_FORMAT = 8
+SGS_PLY_REFERENCE3DGS = 0
+SGS_PLY_SGEXTENDED = 1
 
 SGS_SH, SGS_SG1, SGS_SG3, SGS_MIXED = 0, 1, 2, 3
 SGS_F64, SGS_F32 = 0, 1
@@ -72,6 +76,18 @@ class sgs_scene_meta(ctypes.Structure):
         ("geometry_f64", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
         ("blob_bytes", ctypes.c_uint64),
+        ("shared_axes", ctypes.c_double * 9),
+        ("background", ctypes.c_double * 3),
+    ]
+
+
+class sgs_ply_info(ctypes.Structure):
+    _fields_ = [
+        ("count", ctypes.c_uint64),
+        ("kind", ctypes.c_int32),
+        ("sh_degree", ctypes.c_int32),
+        ("layout", ctypes.c_int32),
+        ("binary", ctypes.c_int32),
         ("shared_axes", ctypes.c_double * 9),
         ("background", ctypes.c_double * 3),
     ]
@@ -154,6 +170,8 @@ SIGNATURES = {
                               ctypes.POINTER(sgs_camera)]),
     "sgs_orbit_cameras": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, ctypes.POINTER(sgs_camera)]),
+    "sgs_ply_read": (_S, [ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), _P, ctypes.c_uint64]),
+    "sgs_scene_load_ply": (_S, [_P, ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), ctypes.POINTER(_P)]),
 }
 
 _lib = None

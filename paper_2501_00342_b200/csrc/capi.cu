@@ -19,6 +19,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include "ply_internal.h"
+#include "projection.cuh"
 #include "sgs_internal.h"
 
 using namespace sgs;
@@ -768,6 +770,90 @@ sgs_status upload_common(sgs_context* ctx, const sgs_scene_desc* desc, void* blo
     return SGS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// PLY rows -> scene planes (sgs_scene_load_ply). tab[s] gives, for every float slot
+// s of the 3 geometry planes and the colour planes, the row column it copies
+// (>= 0), zero (-1), or component k of the FP64-normalised SG1 lobe axis (-2 - k),
+// exactly as fill_blob lays out the flat parameters.
+constexpr int kPlyMaxSlots = 4 * (3 + 12);
+
+__global__ void ply_rows_kernel(uint64_t n, const float* __restrict__ rows, int stride, int nslots,
+                                const int32_t* __restrict__ tab, int mu_col, float4* __restrict__ g0,
+                                float4* __restrict__ g1, float4* __restrict__ g2, float4* __restrict__ color) {
+    __shared__ int32_t s_tab[kPlyMaxSlots];
+    for (int k = threadIdx.x; k < nslots; k += blockDim.x) s_tab[k] = tab[k];
+    __syncthreads();
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* row = rows + i * static_cast<uint64_t>(stride);
+    float mu[3] = {0.f, 0.f, 0.f};
+    if (mu_col >= 0) {
+        // DiffuseSGModel::lobe (color.cpp:52-59): mu / |mu| in FP64, (1, 0, 0) if |mu| <= 1e-12
+        const double m0 = row[mu_col], m1 = row[mu_col + 1], m2 = row[mu_col + 2];
+        const double nn = __dsqrt_rn(sgs::dadd(sgs::dadd(sgs::dmul(m0, m0), sgs::dmul(m1, m1)), sgs::dmul(m2, m2)));
+        if (nn > 1e-12) {
+            mu[0] = static_cast<float>(sgs::ddiv(m0, nn));
+            mu[1] = static_cast<float>(sgs::ddiv(m1, nn));
+            mu[2] = static_cast<float>(sgs::ddiv(m2, nn));
+        } else {
+            mu[0] = 1.f;
+        }
+    }
+    for (int p = 0; p < nslots / 4; ++p) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = s_tab[4 * p + q];
+            v[q] = t >= 0 ? row[t] : (t == -1 ? 0.f : mu[-2 - t]);
+        }
+        const float4 f = make_float4(v[0], v[1], v[2], v[3]);
+        if (p < 3)
+            (p == 0 ? g0 : p == 1 ? g1 : g2)[i] = f;
+        else
+            color[static_cast<uint64_t>(p - 3) * n + i] = f;
+    }
+}
+
+// The slot table for a resolved checkpoint (mirrors fill_blob's flat -> plane map).
+std::vector<int32_t> ply_slot_table(const PlyTable& t, int color_planes, int* mu_col) {
+    const std::vector<int32_t>& src = t.src;  // flat parameter -> row column
+    std::vector<int32_t> tab(static_cast<size_t>(4 * (3 + color_planes)), -1);
+    auto flat = [&](int p) { return src[static_cast<size_t>(p)]; };
+    // geometry: (pos, opacity), quaternion, (log scale, 0)
+    for (int k = 0; k < 3; ++k) tab[static_cast<size_t>(k)] = flat(k);
+    tab[3] = flat(10);
+    for (int k = 0; k < 4; ++k) tab[static_cast<size_t>(4 + k)] = flat(3 + k);
+    for (int k = 0; k < 3; ++k) tab[static_cast<size_t>(8 + k)] = flat(7 + k);
+    int32_t* c = tab.data() + 12;
+    const int co = 11;
+    const int cpc = color_param_count_impl(t.info.kind, t.info.sh_degree);
+    *mu_col = -1;
+    switch (t.info.kind) {
+        case SGS_SH:
+            for (int k = 0; k < cpc; ++k) c[k] = flat(co + k);
+            break;
+        case SGS_MIXED: {
+            const int nsh = 3 * (t.info.sh_degree + 1) * (t.info.sh_degree + 1);
+            for (int k = 0; k < nsh; ++k) c[k] = flat(co + k);
+            const int lobe_base = 4 * ((nsh + 3) / 4);
+            for (int k = 0; k < 12; ++k) c[lobe_base + k] = flat(co + nsh + k);
+            break;
+        }
+        case SGS_SG1:
+            for (int k = 0; k < 3; ++k) c[k] = flat(co + k);
+            c[3] = flat(co + 6);
+            for (int k = 0; k < 3; ++k) c[4 + k] = flat(co + 3 + k);
+            for (int k = 0; k < 3; ++k) c[8 + k] = -2 - k;
+            *mu_col = flat(co + 7);
+            break;
+        case SGS_SG3:
+            for (int k = 0; k < 3; ++k) c[k] = flat(co + k);
+            for (int k = 0; k < 12; ++k) c[4 + k] = flat(co + 3 + k);
+            break;
+    }
+    return tab;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1114,6 +1200,104 @@ sgs_status sgs_flops_per_gaussian(int32_t kind, int32_t deg, int32_t* out) {
             return SGS_OK;
     }
     return fail(SGS_ERR_INVALID_ARGUMENT, "unknown color model kind");
+}
+
+sgs_status sgs_ply_read(const char* path, sgs_ply_info* info, double* params, uint64_t params_capacity) {
+    if (!path || !info) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    PlyTable t;
+    std::string err;
+    int st = ply_parse_header(path, t, err);
+    if (st != SGS_OK) return fail(static_cast<sgs_status>(st), err);
+    std::vector<float> rows;
+    if (params) {
+        rows.resize(static_cast<size_t>(t.count) * t.props.size());
+        st = ply_read_rows(t, rows.data(), err);
+    } else {
+        st = ply_check_payload(t, err);
+    }
+    if (st != SGS_OK) return fail(static_cast<sgs_status>(st), err);
+    st = ply_resolve(t, err);
+    if (st != SGS_OK) return fail(static_cast<sgs_status>(st), err);
+    *info = t.info;
+    if (params) {
+        if (params_capacity < t.count * t.src.size())
+            return fail(SGS_ERR_INVALID_ARGUMENT, "params buffer smaller than count * (11 + colour params)");
+        ply_rows_to_flat(t, rows.data(), params);
+    }
+    return SGS_OK;
+}
+
+sgs_status sgs_scene_load_ply(sgs_context* ctx, const char* path, sgs_ply_info* info, sgs_scene** out) {
+    if (!ctx || !path || !out) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    PlyTable t;
+    std::string err;
+    int st = ply_parse_header(path, t, err);
+    if (st != SGS_OK) return fail(static_cast<sgs_status>(st), err);
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    const size_t nfloat = static_cast<size_t>(t.count) * t.props.size();
+    float* h_rows = nullptr;  // pinned: the payload is read straight into DMA-able memory
+    SGS_CUDA(cudaMallocHost(&h_rows, std::max<size_t>(nfloat, 1) * sizeof(float)));
+    st = ply_read_rows(t, h_rows, err);
+    if (st == SGS_OK) st = ply_resolve(t, err);
+    if (st != SGS_OK) {
+        cudaFreeHost(h_rows);
+        return fail(static_cast<sgs_status>(st), err);
+    }
+    sgs_scene_meta m{};
+    m.count = t.count;
+    m.kind = t.info.kind;
+    m.sh_degree = t.info.sh_degree;
+    m.geometry_f64 = 0;  // PLY values are float32
+    for (int k = 0; k < 9; ++k) m.shared_axes[k] = t.info.shared_axes[k];
+    for (int k = 0; k < 3; ++k) m.background[k] = t.info.background[k];
+    const Layout L = make_layout(m);
+    m.blob_bytes = L.bytes;
+    auto* sc = new sgs_scene();
+    sc->meta = m;
+    sc->ctx = ctx;
+    DevBuf d_rows, d_tab;
+    int mu_col = -1;
+    const std::vector<int32_t> tab = ply_slot_table(t, L.color_planes, &mu_col);
+    cudaError_t e = sc->owned.ensure(m.blob_bytes);
+    if (e == cudaSuccess) e = d_rows.ensure(std::max<size_t>(nfloat, 1) * sizeof(float));
+    if (e == cudaSuccess) e = d_tab.ensure(tab.size() * sizeof(int32_t));
+    if (e == cudaSuccess) {
+        sc->blob = sc->owned.ptr;
+        cudaStream_t s = ctx->stream;
+        e = cudaMemsetAsync(sc->blob, 0, m.blob_bytes, s);
+        if (e == cudaSuccess && nfloat)
+            e = cudaMemcpyAsync(d_rows.ptr, h_rows, nfloat * sizeof(float), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && t.count) {
+            char* base = static_cast<char*>(sc->blob);
+            ply_rows_kernel<<<static_cast<unsigned>((t.count + 255) / 256), 256, 0, s>>>(
+                t.count, d_rows.as<float>(), static_cast<int>(t.props.size()), static_cast<int>(tab.size()),
+                d_tab.as<int32_t>(), mu_col, reinterpret_cast<float4*>(base + L.geo_off[0]),
+                reinterpret_cast<float4*>(base + L.geo_off[1]), reinterpret_cast<float4*>(base + L.geo_off[2]),
+                reinterpret_cast<float4*>(base + L.color_off));
+            e = cudaGetLastError();
+            if (e == cudaSuccess) ctx->own_launches += 1;
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    d_rows.release();
+    d_tab.release();
+    cudaFreeHost(h_rows);
+    if (e != cudaSuccess) {
+        sgs_scene_free(sc);
+        return fail(e == cudaErrorMemoryAllocation ? SGS_ERR_OUT_OF_MEMORY : SGS_ERR_CUDA,
+                    std::string("ply load: ") + cudaGetErrorString(e));
+    }
+    sgs_status sb = bind_and_cache(sc, ctx->stream);
+    if (sb != SGS_OK) {
+        sgs_scene_free(sc);
+        return sb;
+    }
+    if (info) *info = t.info;
+    *out = sc;
+    return SGS_OK;
 }
 
 }  // extern "C"

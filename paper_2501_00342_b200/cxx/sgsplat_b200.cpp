@@ -9,6 +9,7 @@
 // scene / camera helpers are host code with the reference's semantics; they are
 // utilities, not a render fallback -- render() has no CPU path.
 #include "sgs.h"
+#include "sgsplat/ply.hpp"
 #include "sgsplat/raster.hpp"
 #include "sgsplat/synth.hpp"
 
@@ -25,6 +26,8 @@ namespace {
     const std::string msg = sgs_last_error();
     if (status == SGS_ERR_INVALID_ARGUMENT) throw InvalidArgument(msg);
     if (status == SGS_ERR_NUMERIC) throw NumericError(msg);
+    if (status == SGS_ERR_IO) throw IoError(msg);
+    if (status == SGS_ERR_FORMAT) throw FormatError(msg);
     throw std::runtime_error("B200 renderer: " + msg);
 }
 
@@ -563,6 +566,47 @@ std::vector<Camera> make_orbit_cameras(int count, int width, int height, double 
         cams.push_back(make_orbit_camera(Vec3::Zero(), distance, 2.0 * M_PI * i / count, elevation, width, height,
                                          focal));
     return cams;
+}
+
+// ---------------------------------------------------------------------------
+// PLY checkpoints (ply.hpp): the C-ABI reader fills the flat parameters, which go
+// into the Scene through Scene::set_param.
+int ply_floats_per_gaussian(PlyLayout layout, ColorModelKind kind) {
+    if (layout == PlyLayout::Reference3DGS) return 59;
+    return kind == ColorModelKind::MixedSHSG ? 53 : 29;
+}
+
+PlyLayout detect_layout(const Scene& scene) {
+    if (scene.gaussians.empty()) return PlyLayout::Reference3DGS;
+    return kind_of(scene.gaussians.front().color) == ColorModelKind::SHOnly ? PlyLayout::Reference3DGS
+                                                                            : PlyLayout::SGExtended;
+}
+
+Scene load_ply(const std::string& path) {
+    sgs_ply_info info{};
+    check(sgs_ply_read(path.c_str(), &info, nullptr, 0));
+    const std::size_t stride = 11 + static_cast<std::size_t>(sgs_color_param_count(info.kind, info.sh_degree));
+    std::vector<double> flat(static_cast<std::size_t>(info.count) * stride);
+    check(sgs_ply_read(path.c_str(), &info, flat.empty() ? nullptr : flat.data(), flat.size()));
+    Scene scene;
+    scene.gaussians.resize(static_cast<std::size_t>(info.count));
+    for (auto& g : scene.gaussians) {
+        switch (static_cast<ColorModelKind>(info.kind)) {
+            case ColorModelKind::SHOnly: g.color = SHOnlyModel{SHCoeffs::zeros(info.sh_degree)}; break;
+            case ColorModelKind::DiffuseSG: g.color = DiffuseSGModel{}; break;
+            case ColorModelKind::DiffuseOrthoSG: g.color = DiffuseOrthoSGModel{}; break;
+            default: {
+                MixedSHSGModel m;
+                m.sh = SHCoeffs::zeros(info.sh_degree);
+                g.color = std::move(m);
+            }
+        }
+    }
+    for (std::size_t i = 0; i < flat.size(); ++i) scene.set_param(i, flat[i]);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) scene.shared_axes(r, c) = info.shared_axes[3 * r + c];
+    scene.background = Vec3(info.background[0], info.background[1], info.background[2]);
+    return scene;
 }
 
 }  // namespace sgsplat

@@ -22,6 +22,7 @@ REF_FAST_SO = os.path.join(ORACLE_DIR, "_ref", "libsgsref_fast.so")
 ORC_SO = os.path.join(ORACLE_DIR, "build", "liboracle.so")
 
 KINDS = {"sh": 0, "sg1": 1, "sg3": 2, "mixed": 3}
+KIND_NAMES = {v: k for k, v in KINDS.items()}
 OK, INVALID_ARGUMENT, NUMERIC, INTERNAL = 0, 1, 2, 6
 
 
@@ -204,6 +205,38 @@ class RefLib(_Lib):
         L.ref_select_degree.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.POINTER(ctypes.c_int)]
         L.ref_color_param_count.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.ref_load_ply.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.ref_save_ply.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int]
+        L.ref_scene_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_int), ctypes.c_void_p, ctypes.c_void_p]
+
+    # -- PLY checkpoints (ply.cpp) -------------------------------------------
+    def load_ply(self, path):
+        """load_ply: (0, FlatScene) or (status, message) with the reference's message."""
+        h = ctypes.c_void_p()
+        rc = self.lib.ref_load_ply(os.fsencode(str(path)), ctypes.byref(h))
+        if rc != 0:
+            return rc, self.err()
+        try:
+            kind, deg = ctypes.c_int(), ctypes.c_int()
+            axes, bg = np.zeros(9), np.zeros(3)
+            self.lib.ref_scene_info(h, ctypes.byref(kind), ctypes.byref(deg), _ptr(axes), _ptr(bg))
+            n = self.lib.ref_scene_count(h)
+            stride = self.lib.ref_scene_stride(h) if n else 0
+            params = np.zeros((n, stride), dtype=np.float64)
+            if n:
+                self.lib.ref_scene_params(h, _ptr(params))
+        finally:
+            self.lib.ref_scene_free(h)
+        name = KIND_NAMES.get(kind.value, "empty")
+        return 0, FlatScene(name, deg.value, params, axes.reshape(3, 3), bg)
+
+    def save_ply(self, s: FlatScene, path, layout: int) -> int:
+        h = self._handle(s)
+        try:
+            return self.lib.ref_save_ply(h, os.fsencode(str(path)), layout)
+        finally:
+            self.lib.ref_scene_free(h)
 
     # -- scenes -------------------------------------------------------------
     def synth(self, n, seed, kind="mixed", sh_degree=3, ls=(-4.5, -2.5)) -> FlatScene:
