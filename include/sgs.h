@@ -15,6 +15,7 @@
  *   sgsplat::param_count       color.hpp:139-140                   sgs_color_param_count
  *   make_synthetic_scene       synth.hpp:29, synth.cpp:26-106      sgs_synth_scene
  *   make_orbit_camera(s)       camera.hpp:34-35, synth.hpp:32-33   sgs_orbit_camera(s)
+ *   sgsplat::psnr / ssim / ssim_with_grad  metrics.hpp:7-21      sgs_psnr / sgs_ssim
  *   sgsplat::load_ply          ply.hpp:26-29, ply.cpp:295-306      sgs_ply_read (host) /
  *                                                                  sgs_scene_load_ply (device)
  *   python `_core.render`      bindings.cpp:109-121                sgs_render
@@ -216,6 +217,20 @@ sgs_status sgs_orbit_camera(const double* target, double distance, double angle,
                             sgs_camera* out);
 sgs_status sgs_orbit_cameras(int32_t count, int32_t width, int32_t height, double distance,
                              double focal, double elevation, sgs_camera* out);
+
+/* --- image metrics (metrics.hpp, metrics.cpp) ------------------------------------ */
+/* Images are height x width x channels, row-major (the reference's Image layout),
+ * dtype SGS_F64 or SGS_F32 (widened to FP64 exactly), in host or device memory
+ * (memory = SGS_HOST / SGS_DEVICE, for both inputs and grad_a). The per-pixel maps
+ * are computed on the GPU in FP64 in the reference's operation order; the image
+ * means are a fixed-order tree sum. An empty image is SGS_ERR_INVALID_ARGUMENT. */
+/* psnr (metrics.cpp:110-121): 10 log10(1 / MSE), 100 dB when MSE < 1e-10. */
+sgs_status sgs_psnr(sgs_context* ctx, const void* a, const void* b, int32_t width, int32_t height,
+                    int32_t channels, int32_t dtype, int32_t memory, double* out);
+/* ssim / ssim_with_grad (metrics.cpp:125-176): 11x11 Gaussian window (sigma 1.5),
+ * reflect padding; grad_a (nullable) receives d(mean SSIM)/d(a). */
+sgs_status sgs_ssim(sgs_context* ctx, const void* a, const void* b, int32_t width, int32_t height,
+                    int32_t channels, int32_t dtype, int32_t memory, double* value, double* grad_a);
 
 /* --- PLY checkpoints (ply.hpp, ply.cpp) ---------------------------------------- */
 /* The two layouts of ply.hpp:9-22 (PlyLayout). */

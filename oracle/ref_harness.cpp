@@ -8,6 +8,7 @@
 // detail::build_tile_grid / testing::render_bruteforce themselves.
 #include "oracle.h"
 
+#include "sgsplat/metrics.hpp"
 #include "sgsplat/ply.hpp"
 #include "sgsplat/raster.hpp"
 #include "sgsplat/synth.hpp"
@@ -299,6 +300,36 @@ void ref_scene_info(void* s, int* kind, int* degree, double* axes, double* bg) {
     for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c) axes[3 * r + c] = sc.shared_axes(r, c);
     for (int k = 0; k < 3; ++k) bg[k] = sc.background[k];
+}
+
+namespace {
+Image image_of(const double* p, int w, int h, int c) {
+    Image img(w, h, c);
+    std::memcpy(img.data.data(), p, img.size() * sizeof(double));
+    return img;
+}
+}  // namespace
+
+// sgsplat::psnr (proj/src/metrics.cpp:110-121); images H x W x C row-major.
+int ref_psnr(const double* a, const double* b, int w, int h, int c, double* out) {
+    REF_GUARD({
+        *out = psnr(image_of(a, w, h, c), image_of(b, w, h, c));
+        return ORC_OK;
+    })
+}
+
+// sgsplat::ssim / ssim_with_grad (metrics.cpp:125-176); grad may be null.
+int ref_ssim(const double* a, const double* b, int w, int h, int c, double* out, double* grad) {
+    REF_GUARD({
+        if (grad) {
+            SsimResult r = ssim_with_grad(image_of(a, w, h, c), image_of(b, w, h, c));
+            *out = r.value;
+            std::memcpy(grad, r.grad_a.data.data(), r.grad_a.size() * sizeof(double));
+        } else {
+            *out = ssim(image_of(a, w, h, c), image_of(b, w, h, c));
+        }
+        return ORC_OK;
+    })
 }
 
 }  // extern "C"

@@ -27,7 +27,7 @@ __all__ = [
     "Camera", "Scene", "Renderer", "DeviceScene", "RenderStats", "render", "synth_scene",
     "orbit_camera", "orbit_cameras", "flops_per_gaussian", "param_count", "shared_param_count",
     "select_degree", "InvalidArgumentError", "NumericError", "FormatError", "IoError", "CudaError",
-    "load_scene", "load_ply", "ply_info",
+    "load_scene", "load_ply", "ply_info", "psnr", "ssim", "ssim_with_grad",
 ]
 
 KINDS = {"sh": C.SGS_SH, "sg1": C.SGS_SG1, "sg3": C.SGS_SG3, "mixed": C.SGS_MIXED}
@@ -513,3 +513,66 @@ def render(scene: Scene, camera: Camera, tile_size: int = 16, thresholds=(2.0, 8
     if return_transmittance:
         return img, T.astype(np.float64)
     return img
+
+
+# -- image metrics (metrics.hpp; bindings.cpp:150-163) --------------------------------
+def _image_args(a, b):
+    """(ptr_a, ptr_b, W, H, C, dtype, memory, keepalive) for numpy arrays or CUDA
+    tensors of shape (H, W, C) (numpy_to_image, bindings.cpp:22-28). Mixed inputs
+    are brought to one memory space (the device if either is a CUDA tensor) and one
+    dtype (float64 unless both are float32)."""
+    on_dev = [hasattr(x, "is_cuda") and x.is_cuda for x in (a, b)]
+    if any(on_dev):
+        import torch
+
+        xs = [torch.as_tensor(x, device="cuda") for x in (a, b)]
+        both32 = all(x.dtype == torch.float32 for x in xs)
+        xs = [x.to(torch.float32 if both32 else torch.float64).contiguous() for x in xs]
+        ptrs = [x.data_ptr() for x in xs]
+        mem, dt = C.SGS_DEVICE, C.SGS_F32 if both32 else C.SGS_F64
+    else:
+        xs = [np.asarray(x) for x in (a, b)]
+        both32 = all(x.dtype == np.float32 for x in xs)
+        xs = [np.ascontiguousarray(x, dtype=np.float32 if both32 else np.float64) for x in xs]
+        ptrs = [x.ctypes.data for x in xs]
+        mem, dt = C.SGS_HOST, C.SGS_F32 if both32 else C.SGS_F64
+    for x in xs:
+        if len(x.shape) != 3:
+            raise InvalidArgumentError("image array must have shape (H, W, C)")
+    if tuple(xs[0].shape) != tuple(xs[1].shape):
+        raise InvalidArgumentError("image dimensions do not match")
+    h, w, c = (int(v) for v in xs[0].shape)
+    return ptrs[0], ptrs[1], w, h, c, dt, mem, xs
+
+
+def psnr(a, b) -> float:
+    """psnr (metrics.cpp:110-121) on the GPU: 10 log10(1 / MSE), capped at 100 dB."""
+    pa, pb, w, h, c, dt, mem, keep = _image_args(a, b)
+    out = ctypes.c_double()
+    _check(_lib().sgs_psnr(_renderer().handle, pa, pb, w, h, c, dt, mem, ctypes.byref(out)))
+    return out.value
+
+
+def ssim(a, b) -> float:
+    """ssim (metrics.cpp:125-174) on the GPU: mean SSIM, 11x11 Gaussian window."""
+    pa, pb, w, h, c, dt, mem, keep = _image_args(a, b)
+    out = ctypes.c_double()
+    _check(_lib().sgs_ssim(_renderer().handle, pa, pb, w, h, c, dt, mem, ctypes.byref(out), None))
+    return out.value
+
+
+def ssim_with_grad(a, b):
+    """ssim_with_grad (metrics.cpp:176): (value, d value / d a) -- the gradient is a
+    float64 array (numpy inputs) or CUDA tensor (tensor inputs) shaped like a."""
+    pa, pb, w, h, c, dt, mem, keep = _image_args(a, b)
+    out = ctypes.c_double()
+    if mem == C.SGS_DEVICE:
+        import torch
+
+        grad = torch.empty((h, w, c), dtype=torch.float64, device="cuda")
+        gptr = grad.data_ptr()
+    else:
+        grad = np.empty((h, w, c), dtype=np.float64)
+        gptr = grad.ctypes.data
+    _check(_lib().sgs_ssim(_renderer().handle, pa, pb, w, h, c, dt, mem, ctypes.byref(out), gptr))
+    return out.value, grad

@@ -170,6 +170,10 @@ SIGNATURES = {
                               ctypes.POINTER(sgs_camera)]),
     "sgs_orbit_cameras": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, ctypes.POINTER(sgs_camera)]),
+    "sgs_psnr": (_S, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                      ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
+    "sgs_ssim": (_S, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                      ctypes.c_int32, ctypes.POINTER(ctypes.c_double), _P]),
     "sgs_ply_read": (_S, [ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), _P, ctypes.c_uint64]),
     "sgs_scene_load_ply": (_S, [_P, ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), ctypes.POINTER(_P)]),
 }

@@ -145,6 +145,7 @@ struct sgs_context {
     bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
+    DevBuf metrics;  // PSNR / SSIM scratch (inputs staged from host, maps, partial sums)
     uint64_t own_launches = 0, lib_launches = 0;
 };
 
@@ -926,6 +927,7 @@ void sgs_destroy(sgs_context* ctx) {
         if (L.done) cudaEventDestroy(L.done);
         if (L.stream) cudaStreamDestroy(L.stream);
     }
+    ctx->metrics.release();
     if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     cudaStreamDestroy(ctx->own_stream);
@@ -1298,6 +1300,70 @@ sgs_status sgs_scene_load_ply(sgs_context* ctx, const char* path, sgs_ply_info* 
     if (info) *info = t.info;
     *out = sc;
     return SGS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Image metrics (metrics.cu).
+namespace {
+sgs_status run_metric(sgs_context* ctx, const void* a, const void* b, int32_t w, int32_t h, int32_t c,
+                      int32_t dtype, int32_t memory, bool ssim, double* out, double* grad) {
+    if (!ctx || !a || !b || !out) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    if (w < 0 || h < 0 || c < 0) return fail(SGS_ERR_INVALID_ARGUMENT, "image dimensions do not match");
+    if (dtype != SGS_F32 && dtype != SGS_F64) return fail(SGS_ERR_INVALID_ARGUMENT, "bad dtype");
+    const size_t n = static_cast<size_t>(w) * static_cast<size_t>(h) * static_cast<size_t>(c);
+    if (n == 0) return fail(SGS_ERR_INVALID_ARGUMENT, "empty image");  // check_shapes, metrics.cpp:87-90
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t elem = dtype == SGS_F64 ? 8 : 4;
+    const bool host = memory != SGS_DEVICE;
+    const size_t work = metrics_scratch_doubles(n, grad != nullptr) * 8;
+    const size_t staged = host ? align_up(2 * n * elem, 256) + (grad ? n * 8 : 0) : 0;
+    SGS_CUDA(ctx->metrics.ensure(work + staged + 256));
+    char* base = static_cast<char*>(ctx->metrics.ptr);
+    double* scratch = reinterpret_cast<double*>(base);
+    double* d_sum = scratch + metrics_scratch_doubles(n, grad != nullptr) - 1;
+    const void* da = a;
+    const void* db = b;
+    double* dgrad = grad;
+    if (host) {
+        char* st = base + align_up(work, 256);
+        SGS_CUDA(cudaMemcpyAsync(st, a, n * elem, cudaMemcpyHostToDevice, s));
+        SGS_CUDA(cudaMemcpyAsync(st + n * elem, b, n * elem, cudaMemcpyHostToDevice, s));
+        da = st;
+        db = st + n * elem;
+        if (grad) dgrad = reinterpret_cast<double*>(st + align_up(2 * n * elem, 256));
+    }
+    if (ssim) {
+        launch_ssim(da, db, dtype == SGS_F64, w, h, c, scratch, d_sum, dgrad, s);
+        ctx->own_launches += grad ? 6 : 4;
+    } else {
+        launch_psnr_sum(da, db, dtype == SGS_F64, n, scratch, d_sum, s);
+        ctx->own_launches += 3;
+    }
+    SGS_CUDA(cudaGetLastError());
+    double sum = 0.0;
+    SGS_CUDA(cudaMemcpyAsync(&sum, d_sum, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (host && grad) SGS_CUDA(cudaMemcpyAsync(grad, dgrad, n * 8, cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaStreamSynchronize(s));
+    if (ssim) {
+        *out = sum / static_cast<double>(n);
+    } else {
+        const double mse = sum / static_cast<double>(n);
+        *out = mse < 1e-10 ? 100.0 : 10.0 * std::log10(1.0 / mse);
+    }
+    return SGS_OK;
+}
+}  // namespace
+
+sgs_status sgs_psnr(sgs_context* ctx, const void* a, const void* b, int32_t width, int32_t height,
+                    int32_t channels, int32_t dtype, int32_t memory, double* out) {
+    return run_metric(ctx, a, b, width, height, channels, dtype, memory, false, out, nullptr);
+}
+
+sgs_status sgs_ssim(sgs_context* ctx, const void* a, const void* b, int32_t width, int32_t height,
+                    int32_t channels, int32_t dtype, int32_t memory, double* value, double* grad_a) {
+    return run_metric(ctx, a, b, width, height, channels, dtype, memory, true, value, grad_a);
 }
 
 }  // extern "C"

@@ -169,6 +169,12 @@ size_t bin_emit_status_bytes(uint64_t ranks);
 void launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
                      int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
                      unsigned long long* status, Counters* ctr, cudaStream_t stream);
+// image metrics (metrics.cu)
+size_t metrics_scratch_doubles(size_t n, bool grad);
+void launch_psnr_sum(const void* a, const void* b, bool f64, size_t n, double* scratch, double* d_sum,
+                     cudaStream_t s);
+void launch_ssim(const void* a, const void* b, bool f64, int W, int H, int C, double* scratch, double* d_sum,
+                 double* grad, cudaStream_t s);
 void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
                         int4* brect, uint2* bmeta, cudaStream_t stream);
 void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,

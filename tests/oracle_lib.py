@@ -206,6 +206,10 @@ class RefLib(_Lib):
                                         ctypes.POINTER(ctypes.c_int)]
         L.ref_color_param_count.argtypes = [ctypes.c_int, ctypes.c_int]
         L.ref_load_ply.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.ref_psnr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.POINTER(ctypes.c_double)]
+        L.ref_ssim.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
         L.ref_save_ply.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int]
         L.ref_scene_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                      ctypes.POINTER(ctypes.c_int), ctypes.c_void_p, ctypes.c_void_p]
@@ -230,6 +234,22 @@ class RefLib(_Lib):
             self.lib.ref_scene_free(h)
         name = KIND_NAMES.get(kind.value, "empty")
         return 0, FlatScene(name, deg.value, params, axes.reshape(3, 3), bg)
+
+    # -- image metrics (metrics.cpp) -----------------------------------------
+    def psnr(self, a, b):
+        a, b = (np.ascontiguousarray(x, dtype=np.float64) for x in (a, b))
+        out = ctypes.c_double()
+        rc = self.lib.ref_psnr(_ptr(a), _ptr(b), a.shape[1], a.shape[0], a.shape[2], ctypes.byref(out))
+        assert rc == 0, self.err()
+        return out.value
+
+    def ssim(self, a, b, grad=False):
+        a, b = (np.ascontiguousarray(x, dtype=np.float64) for x in (a, b))
+        out = ctypes.c_double()
+        g = np.empty_like(a) if grad else None
+        rc = self.lib.ref_ssim(_ptr(a), _ptr(b), a.shape[1], a.shape[0], a.shape[2], ctypes.byref(out), _ptr(g))
+        assert rc == 0, self.err()
+        return (out.value, g) if grad else out.value
 
     def save_ply(self, s: FlatScene, path, layout: int) -> int:
         h = self._handle(s)
