@@ -108,6 +108,7 @@ struct Lane {
     FrameConsts* h_consts = nullptr;  // pinned staging copy
     cudaEvent_t ev[8] = {};
     cudaEvent_t done = nullptr;  // the frame's counters have reached h_ctr
+    cudaEvent_t k1ev = nullptr;  // multi-view K1 hand-off (start_group)
     // the frame in flight (valid while busy)
     struct Job {
         const sgs_scene* scene = nullptr;
@@ -130,7 +131,7 @@ struct Lane {
     uint64_t last_v = 0, last_p = 0;
 };
 
-constexpr int kLanes = 4;
+constexpr int kLanes = 8;
 
 struct sgs_context {
     int device = 0;
@@ -138,7 +139,8 @@ struct sgs_context {
     cudaStream_t stream = nullptr;  // the caller's stream: lanes fork from and join back to it
     std::mutex mu;
     Lane lane[kLanes];
-    int lanes = kLanes;                // lanes used by sgs_render_batch (SGS_LANES, 1..kLanes)
+    int lanes = 4;                     // lanes of the one-view-per-K1 schedule (SGS_LANES, 1..kLanes)
+    int k1_group = 1;                  // views per multi-view K1 (SGS_K1_GROUP, 2..4; measured: no gain)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
     bool two_level = true;   // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
@@ -311,7 +313,11 @@ sgs_status count_and_scan(sgs_context* ctx, Lane& L, uint64_t rb, uint64_t re, c
 // size lives on the device), ending with a 128-B D2H of the counters and L.done.
 // finish_frame() reads the counters, reports errors and -- rarely -- regrows the
 // tile-key arena or switches to the 64-bit depth sort and enqueues the frame again.
-sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
+// part: kAll = the whole frame; kPre = arenas, counters, constants (up to K1);
+// kPost = everything after K1 (a multi-view K1 ran in between, start_group).
+enum EnqueuePart { kAll = 0, kPre = 1, kPost = 2 };
+
+sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     Lane::Job& j = L.job;
     cudaStream_t s = L.stream;
     const sgs_scene* scene = j.scene;
@@ -356,26 +362,32 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
         d_T = L.out_T.as<float>();
     }
 
-    SGS_CUDA(cudaMemcpyAsync(L.d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
-    if (mode == kRender) {
-        // the pinned staging block is per lane; the lane's previous frame has
-        // completed (finish_frame waits for it before the lane is reused)
-        L.h_consts->sp = scene->planes;
-        L.h_consts->cam = cp;
-        SGS_CUDA(cudaMemcpyAsync(L.d_consts, L.h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
+    if (part != kPost) {
+        SGS_CUDA(cudaMemcpyAsync(L.d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
+        if (mode == kRender) {
+            // the pinned staging block is per lane; the lane's previous frame has
+            // completed (finish_frame waits for it before the lane is reused)
+            L.h_consts->sp = scene->planes;
+            L.h_consts->cam = cp;
+            SGS_CUDA(cudaMemcpyAsync(L.d_consts, L.h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
+        }
+        if (L.iota_n < n) {  // identity values for the depth sort (kept across frames)
+            launch_iota(n, L.iota.as<uint32_t>(), s);
+            L.iota_n = n;
+        }
     }
+    if (part == kPre) return SGS_OK;
 
     // K1
-    if (L.iota_n < n) {  // identity values for the depth sort (kept across frames)
-        launch_iota(n, L.iota.as<uint32_t>(), s);
-        L.iota_n = n;
+    if (part == kAll) {
+        if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
+        launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
+                          L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
+                          s);
+        SGS_CUDA(cudaGetLastError());
+        if (n) ctx->own_launches += 1;
+        if (timing) SGS_CUDA(cudaEventRecord(L.ev[1], s));
     }
-    if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
-    launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
-                      L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, j.d_debug, s);
-    SGS_CUDA(cudaGetLastError());
-    if (n) ctx->own_launches += 1;
-    if (timing) SGS_CUDA(cudaEventRecord(L.ev[1], s));
     if (mode == kProjectOnly) {
         SGS_CUDA(cudaMemcpyAsync(L.h_ctr, L.d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
         SGS_CUDA(cudaEventRecord(L.done, s));
@@ -568,6 +580,71 @@ sgs_status start_frame(sgs_context* ctx, Lane& L, const sgs_scene* scene, const 
     if (st != SGS_OK) {
         cudaStreamSynchronize(L.stream);
         L.busy = false;
+    }
+    return st;
+}
+
+// Start views [0, g) of `cams` on lanes[0..g) (all idle) with ONE multi-view K1
+// (SURVEY.md §8f row 1): every lane stages its arenas and counters, the lead lane
+// waits for them, projects all g views reading each Gaussian once, and the other
+// lanes continue from K2 after it. A lane that needs a retry later re-runs its own
+// frame alone (finish_frame -> enqueue_frame).
+sgs_status start_group(sgs_context* ctx, Lane* const* lanes, int g, const sgs_scene* scene, const sgs_camera* cams,
+                       const sgs_render_config* cfg, float* const* d_rgb, float* const* d_T, float* const* h_rgb,
+                       float* const* h_T, sgs_render_stats* stats) {
+    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
+    for (int k = 0; k < g; ++k) {
+        sgs_status st = validate_camera(&cams[k]);
+        if (st != SGS_OK) return st;
+    }
+    sgs_status st = SGS_OK;
+    int started = 0;
+    for (int k = 0; k < g && st == SGS_OK; ++k) {
+        Lane& L = *lanes[k];
+        Lane::Job& j = L.job;
+        j = Lane::Job{};
+        j.scene = scene;
+        j.cam = cams[k];
+        j.cfg = *cfg;
+        j.d_rgb = d_rgb[k];
+        j.d_T = d_T[k];
+        j.h_rgb = h_rgb[k];
+        j.h_T = h_T[k];
+        j.stats = stats;
+        j.mode = kRender;
+        L.busy = true;
+        ++started;
+        st = enqueue_frame(ctx, L, kPre);
+    }
+    Lane& lead = *lanes[0];
+    if (st == SGS_OK) {
+        for (int k = 1; k < g && st == SGS_OK; ++k) {
+            cudaError_t e = cudaEventRecord(lanes[k]->k1ev, lanes[k]->stream);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(lead.stream, lanes[k]->k1ev, 0);
+            if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
+        }
+    }
+    if (st == SGS_OK) {
+        K1Views views{};
+        views.nv = g;
+        for (int k = 0; k < g; ++k) {
+            Lane& L = *lanes[k];
+            views.v[k] = K1Out{L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(), L.rects.as<int4>(),
+                               L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, make_cam(&cams[k])};
+        }
+        launch_preprocess_views(scene->planes, make_cfg(cfg, &cams[0]), views, nullptr, lead.stream);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess && scene->meta.count) ctx->own_launches += 1;
+        if (e == cudaSuccess) e = cudaEventRecord(lead.k1ev, lead.stream);
+        for (int k = 1; k < g && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(lanes[k]->stream, lead.k1ev, 0);
+        if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
+    }
+    for (int k = 0; k < g && st == SGS_OK; ++k) st = enqueue_frame(ctx, *lanes[k], kPost);
+    if (st != SGS_OK) {
+        for (int k = 0; k < started; ++k) {
+            cudaStreamSynchronize(lanes[k]->stream);
+            lanes[k]->busy = false;
+        }
     }
     return st;
 }
@@ -889,8 +966,11 @@ sgs_status sgs_create(int device, sgs_context** out) {
         SGS_CUDA(cudaMallocHost(&L.h_consts, sizeof(FrameConsts)));
         for (auto& ev : L.ev) SGS_CUDA(cudaEventCreate(&ev));
         SGS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+        SGS_CUDA(cudaEventCreateWithFlags(&L.k1ev, cudaEventDisableTiming));
     }
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
+    if (const char* e = std::getenv("SGS_K1_GROUP"))
+        ctx->k1_group = std::min(std::max(std::atoi(e), 1), std::min(kMaxK1Views, kLanes / 2));
     if (const char* e = std::getenv("SGS_BIN_FUSED")) ctx->fused_bin = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_SORT")) ctx->two_level = std::strcmp(e, "bucket") != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
@@ -925,6 +1005,7 @@ void sgs_destroy(sgs_context* ctx) {
         for (auto& ev : L.ev)
             if (ev) cudaEventDestroy(ev);
         if (L.done) cudaEventDestroy(L.done);
+        if (L.k1ev) cudaEventDestroy(L.k1ev);
         if (L.stream) cudaStreamDestroy(L.stream);
     }
     ctx->metrics.release();
@@ -1086,25 +1167,62 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
     if (W < 1 || H < 1) return validate_camera(&cams[0]);
     const size_t npx = static_cast<size_t>(W) * static_cast<size_t>(H);
     const bool host = out_memory != SGS_DEVICE;
-    // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
-    const int lanes = std::min<int>(stats && stats->want_timing ? 1 : ctx->lanes, n);
-    sgs_status st = fork_lanes(ctx, lanes);
-    if (st != SGS_OK) return st;
-    // view i runs on lane i % lanes; a lane's previous view is settled (checked,
-    // retried if needed) before the lane is reused, so views complete in order
-    for (int i = 0; i < n && st == SGS_OK; ++i) {
-        Lane& L = ctx->lane[i % lanes];
-        st = finish_frame(ctx, L);
-        if (st != SGS_OK) break;
+    const bool timing = stats && stats->want_timing;
+    auto outs = [&](int i, float** d_rgb, float** d_T, float** h_rgb, float** h_T) {
         float* o_rgb = rgb ? rgb + i * npx * 3 : nullptr;
         float* o_T = T ? T + i * npx : nullptr;
-        st = start_frame(ctx, L, scene, &cams[i], cfg, host ? nullptr : o_rgb, host ? nullptr : o_T,
-                         host ? o_rgb : nullptr, host ? o_T : nullptr, stats, nullptr, kRender);
-    }
-    for (int k = 0; k < lanes; ++k) {  // settle the views still in flight, in order
-        Lane& L = ctx->lane[(n + k) % lanes];
-        sgs_status sk = finish_frame(ctx, L);
-        if (st == SGS_OK) st = sk;
+        *d_rgb = host ? nullptr : o_rgb;
+        *d_T = host ? nullptr : o_T;
+        *h_rgb = host ? o_rgb : nullptr;
+        *h_T = host ? o_T : nullptr;
+    };
+    sgs_status st = SGS_OK;
+    int lanes = 0;
+    const int group = timing ? 1 : ctx->k1_group;
+    if (group > 1 && n > 1) {
+        // groups of `group` views share one multi-view K1; two lane sets alternate so
+        // one group's K1 overlaps the previous group's sorts and compositing
+        constexpr int kSets = 2;
+        lanes = kSets * group;
+        st = fork_lanes(ctx, lanes);
+        if (st != SGS_OK) return st;
+        int gi = 0;
+        for (int i = 0; i < n && st == SGS_OK; i += group, ++gi) {
+            const int g = std::min(group, n - i);
+            Lane* ls[kMaxK1Views];
+            float *drgb[kMaxK1Views], *dT[kMaxK1Views], *hrgb[kMaxK1Views], *hT[kMaxK1Views];
+            for (int k = 0; k < g && st == SGS_OK; ++k) {
+                ls[k] = &ctx->lane[(gi % kSets) * group + k];
+                st = finish_frame(ctx, *ls[k]);
+                outs(i + k, &drgb[k], &dT[k], &hrgb[k], &hT[k]);
+            }
+            if (st == SGS_OK) st = start_group(ctx, ls, g, scene, &cams[i], cfg, drgb, dT, hrgb, hT, stats);
+        }
+        for (int s2 = 0; s2 < kSets; ++s2)  // settle the views still in flight, in order
+            for (int k = 0; k < group; ++k) {
+                sgs_status sk = finish_frame(ctx, ctx->lane[((gi + s2) % kSets) * group + k]);
+                if (st == SGS_OK) st = sk;
+            }
+    } else {
+        // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
+        lanes = std::min<int>(timing ? 1 : ctx->lanes, n);
+        st = fork_lanes(ctx, lanes);
+        if (st != SGS_OK) return st;
+        // view i runs on lane i % lanes; a lane's previous view is settled (checked,
+        // retried if needed) before the lane is reused, so views complete in order
+        for (int i = 0; i < n && st == SGS_OK; ++i) {
+            Lane& L = ctx->lane[i % lanes];
+            st = finish_frame(ctx, L);
+            if (st != SGS_OK) break;
+            float *drgb, *dT, *hrgb, *hT;
+            outs(i, &drgb, &dT, &hrgb, &hT);
+            st = start_frame(ctx, L, scene, &cams[i], cfg, drgb, dT, hrgb, hT, stats, nullptr, kRender);
+        }
+        for (int k = 0; k < lanes; ++k) {  // settle the views still in flight, in order
+            Lane& L = ctx->lane[(n + k) % lanes];
+            sgs_status sk = finish_frame(ctx, L);
+            if (st == SGS_OK) st = sk;
+        }
     }
     sgs_status sj = join_lanes(ctx, lanes);
     if (st != SGS_OK) return st;

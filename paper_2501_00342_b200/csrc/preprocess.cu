@@ -245,17 +245,178 @@ __device__ __forceinline__ float4 eval_colour(const ScenePlanes& sp, const Plane
     return make_float4(col[0] < 0.f ? 0.f : col[0], col[1] < 0.f ? 0.f : col[1], col[2] < 0.f ? 0.f : col[2], 0.f);
 }
 
+// One view's K1 work for Gaussian i (whose geometry g is loaded): projection,
+// decisions, record, rect, colour. Returns the depth key (~0 if culled) and the
+// tile count through key / count / visible.
+template <int KIND, bool DEBUG>
+__device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& cfg, const K1Stage& stg,
+                                        const K1Out& o, const float4* buf, int tid, uint64_t i, const Geo& g,
+                                        DebugSplat& dbg, unsigned long long& key, uint32_t& count, bool& visible) {
+    ProjGeo pg;
+    const int pstat = project_staged(g, o.cam, pg);
+    if (pstat == kProjZeroQuat) raise_error(o.ctr, i, kErrZeroQuaternion);
+    do {
+        if (pstat != kProjVisible) break;
+        const double radius = pg.radius, mx = pg.mx, my = pg.my, tz = pg.tz;
+        // view direction, camera.hpp:20 and raster.cpp:66-69
+        const double ox = dsub(g.p[0], o.cam.C[0]), oy = dsub(g.p[1], o.cam.C[1]),
+                     oz = dsub(g.p[2], o.cam.C[2]);
+        const double ss = dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz));
+        // The direction only feeds the FP32 colour. For |p - C|^2 in (1e-20, 1e30)
+        // the reference's distance check (dist < 1e-12) cannot fire and its unit
+        // check (color.cpp:10-16) cannot fire either (|norm - 1| ~ 1e-16), so the
+        // direction is taken in FP32 with rsqrt; outside that range (or NaN) the
+        // exact sqrt, division and checks run.
+        const bool safe_dist = ss > 1e-20 && ss < 1e30;
+        float fdx, fdy, fdz;
+        double dist = 0.0;
+        if (safe_dist) {
+            const float inv = rsqrtf(static_cast<float>(ss));
+            fdx = static_cast<float>(ox) * inv;
+            fdy = static_cast<float>(oy) * inv;
+            fdz = static_cast<float>(oz) * inv;
+        } else {
+            dist = __dsqrt_rn(ss);
+            if (dist < 1e-12) break;  // raster.cpp:66-69 (NaN continues, as in the reference)
+            const float inv = static_cast<float>(1.0 / dist);
+            fdx = static_cast<float>(ox) * inv;
+            fdy = static_cast<float>(oy) * inv;
+            fdz = static_cast<float>(oz) * inv;
+        }
+        // degree selection and the colour-model error contract (raster.cpp:70-77,
+        // color.cpp:201-206, :182-191)
+        int deg = sp.sh_degree;
+        int deg_used = -1;
+        if constexpr (KIND == SGS_MIXED) {
+            if (cfg.has_override) {
+                deg_used = cfg.override_degree;
+            } else {
+                if (cfg.lo > cfg.hi) {
+                    raise_error(o.ctr, i, kErrThresholds);
+                    break;
+                }
+                deg_used = radius < cfg.lo ? 0 : (radius < cfg.hi ? 1 : 2);
+            }
+        } else {
+            if (cfg.has_override) {
+                raise_error(o.ctr, i, kErrOverrideNonMixed);
+                break;
+            }
+        }
+        if (!safe_dist) {
+            const double dxd = ddiv(ox, dist), dyd = ddiv(oy, dist), dzd = ddiv(oz, dist);
+            const double nrm =
+                __dsqrt_rn(dadd(dadd(dmul(dxd, dxd), dmul(dyd, dyd)), dmul(dzd, dzd)));
+            if (fabs(dsub(nrm, 1.0)) > 1e-6) {
+                raise_error(o.ctr, i, kErrDirection);
+                break;
+            }
+        }
+        if constexpr (KIND == SGS_MIXED) {
+            if (deg_used < 0 || deg_used > sp.sh_degree) {
+                raise_error(o.ctr, i, kErrDegreeTooHigh);
+                break;
+            }
+            deg = deg_used;
+        }
+        // ---- outputs ----
+        // conic and opacity only feed FP32 quantities here (the compositor's guard band
+        // re-derives the exact FP64 values): one reciprocal instead of three divisions,
+        // sigmoid in FP32. The debug dump reports the exact ones.
+        double cona, conb, conc, opacity;
+        if constexpr (DEBUG) {
+            exact_conic_opacity(g, pg);
+            cona = pg.cona, conb = pg.conb, conc = pg.conc, opacity = pg.opacity;
+        } else {
+            const double rdet = 1.0 / pg.det;
+            cona = pg.c * rdet;
+            conb = -pg.b * rdet;
+            conc = pg.a * rdet;
+            opacity = 1.0f / (1.0f + __expf(-static_cast<float>(g.opl)));
+        }
+        visible = true;
+        key = depth_key(tz);
+        // tile rectangle (raster.cpp:117-122), inclusive, clamped
+        const double ts = static_cast<double>(cfg.tile_size);
+        // x / ts == x * (1/ts) bit for bit when ts is a power of two (both round the
+        // exact quotient once); other tile sizes divide.
+        const bool pow2 = (cfg.tile_size & (cfg.tile_size - 1)) == 0;
+        const double its = 1.0 / ts;
+        const double qx0 = pow2 ? dmul(dsub(mx, radius), its) : ddiv(dsub(mx, radius), ts);
+        const double qx1 = pow2 ? dmul(dadd(mx, radius), its) : ddiv(dadd(mx, radius), ts);
+        const double qy0 = pow2 ? dmul(dsub(my, radius), its) : ddiv(dsub(my, radius), ts);
+        const double qy1 = pow2 ? dmul(dadd(my, radius), its) : ddiv(dadd(my, radius), ts);
+        int32_t x0 = to_int_x86(floor(qx0));
+        int32_t x1 = to_int_x86(floor(qx1));
+        int32_t y0 = to_int_x86(floor(qy0));
+        int32_t y1 = to_int_x86(floor(qy1));
+        x0 = max(0, x0);
+        y0 = max(0, y0);
+        x1 = min(cfg.tiles_x - 1, x1);
+        y1 = min(cfg.tiles_y - 1, y1);
+        if (x1 >= x0 && y1 >= y0)
+            count = static_cast<uint32_t>(x1 - x0 + 1) * static_cast<uint32_t>(y1 - y0 + 1);
+        o.rects[i] = make_int4(x0, x1, y0, y1);
+        // FP32 m2 error bound: 2u S (9 r^2 + 3 r ts) + 1e-6
+        const double csum = fabs(cona) + 2.0 * fabs(conb) + fabs(conc);
+        const double guard =
+            2.0 * 5.9604644775390625e-08 * csum * (9.0 * radius * radius + 3.0 * radius * ts) +
+            1e-6;
+        // combined cutoff: alpha < 1/255 <=> m2 > 2 ln(255 op) (op > 0)
+        const double acut = opacity > 0.0 ? 2.0 * log(255.0 * opacity) : -1.0;
+        const double cut = acut < kSupportMahalanobisSq ? acut : kSupportMahalanobisSq;
+        // extents of {d : d^T conic d <= cut + guard} = sqrt(K cov_xx), sqrt(K cov_yy);
+        // cov = the dilated 2D covariance (a, b, c), slightly inflated
+        const double K = fmax(cut + guard, 0.0);
+        SplatRec r;
+        r.mx = mx;
+        r.my = my;
+        r.ca = static_cast<float>(cona);
+        r.cb2 = static_cast<float>(2.0 * conb);
+        r.cc = static_cast<float>(conc);
+        r.lop = opacity > 0.0 ? __log2f(static_cast<float>(opacity)) : -1e30f;
+        r.cut = static_cast<float>(cut);
+        r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
+        r.ext_x = sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
+        r.ext_y = sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
+        // colour (FP32), direction from the FP64 offset
+        {
+            const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
+            const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
+            const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
+            o.colour[i] = col;
+            if constexpr (DEBUG) {
+                dbg.color[0] = col.x;
+                dbg.color[1] = col.y;
+                dbg.color[2] = col.z;
+            }
+        }
+        o.rec[i] = r;
+        if constexpr (DEBUG) {
+            dbg.mean2d[0] = mx;
+            dbg.mean2d[1] = my;
+            dbg.conic[0] = cona;
+            dbg.conic[1] = conb;
+            dbg.conic[2] = conc;
+            dbg.depth = tz;
+            dbg.opacity = opacity;
+            dbg.radius = radius;
+            dbg.degree = KIND == SGS_MIXED ? deg_used : -1;
+            dbg.visible = 1;
+        }
+    } while (false);
+}
+
 // K1: persistent CTAs walk the Gaussians with a two-stage cp.async pipeline (the
 // next Gaussian's geometry, covariance and colour planes land in shared memory
-// while this one is projected), so the FP64 chain overlaps the HBM latency.
+// while this one is projected), so the FP64 chain overlaps the HBM latency. With
+// NV > 1 views (a batch's cameras) every Gaussian is read once
+// and projected into each view's arenas.
 // MINB (min resident CTAs per SM) trades registers for occupancy; selected at run
 // time by SGS_K1_MINB for tuning (default kDefaultMinB, see profiles/).
-template <bool F64, int KIND, int MINB, bool DEBUG>
+template <bool F64, int KIND, int MINB, bool DEBUG, int NV>
 __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
-    const ScenePlanes sp, const CamParams cam, const CfgParams cfg, const K1Stage stg,
-    unsigned long long* __restrict__ depth_keys,
-    SplatRec* __restrict__ rec, int4* __restrict__ rects,
-    uint32_t* __restrict__ ntiles, float4* __restrict__ colour, Counters* __restrict__ ctr,
+    const ScenePlanes sp, const CfgParams cfg, const K1Stage stg, const K1Views views,
     DebugSplat* __restrict__ debug) {
     extern __shared__ float4 k1_smem[];
     const int tid = threadIdx.x;
@@ -264,8 +425,14 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
     uint64_t i = static_cast<uint64_t>(blockIdx.x) * kK1Threads + tid;
     if (i < sp.n) stage_item<F64>(sp, stg, i, k1_smem, tid);
     cp_async_commit();
-    uint32_t nvis = 0;
-    unsigned long long kmin = ~0ULL, kmax = 0ULL;
+    uint32_t nvis[NV];
+    unsigned long long kmin[NV], kmax[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        nvis[v] = 0;
+        kmin[v] = ~0ULL;
+        kmax[v] = 0ULL;
+    }
     for (int it = 0; static_cast<uint64_t>(blockIdx.x) * kK1Threads + static_cast<uint64_t>(it) * stride < sp.n;
          ++it, i += stride) {
         if (i + stride < sp.n) stage_item<F64>(sp, stg, i + stride, k1_smem + ((it + 1) & 1) * buf_stride, tid);
@@ -273,189 +440,45 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
         cp_async_wait1();
         if (i >= sp.n) continue;
         const float4* buf = k1_smem + (it & 1) * buf_stride;
-        unsigned long long key = ~0ULL;
-        uint32_t count = 0;
-        bool visible = false;
         Geo g;
-        ProjGeo pg;
-        DebugSplat dbg;
-        if constexpr (DEBUG) {
-            memset(&dbg, 0, sizeof(dbg));
-            dbg.degree = -1;
-        }
         geo_from_stage<F64>(buf, stg.geo_slots, tid, g);
-        const int pstat = project_staged(g, cam, pg);
-        if (pstat == kProjZeroQuat) raise_error(ctr, i, kErrZeroQuaternion);
-        do {
-            if (pstat != kProjVisible) break;
-            const double radius = pg.radius, mx = pg.mx, my = pg.my, tz = pg.tz;
-            // view direction, camera.hpp:20 and raster.cpp:66-69
-            const double ox = dsub(g.p[0], cam.C[0]), oy = dsub(g.p[1], cam.C[1]),
-                         oz = dsub(g.p[2], cam.C[2]);
-            const double ss = dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz));
-            // The direction only feeds the FP32 colour. For |p - C|^2 in (1e-20, 1e30)
-            // the reference's distance check (dist < 1e-12) cannot fire and its unit
-            // check (color.cpp:10-16) cannot fire either (|norm - 1| ~ 1e-16), so the
-            // direction is taken in FP32 with rsqrt; outside that range (or NaN) the
-            // exact sqrt, division and checks run.
-            const bool safe_dist = ss > 1e-20 && ss < 1e30;
-            float fdx, fdy, fdz;
-            double dist = 0.0;
-            if (safe_dist) {
-                const float inv = rsqrtf(static_cast<float>(ss));
-                fdx = static_cast<float>(ox) * inv;
-                fdy = static_cast<float>(oy) * inv;
-                fdz = static_cast<float>(oz) * inv;
-            } else {
-                dist = __dsqrt_rn(ss);
-                if (dist < 1e-12) break;  // raster.cpp:66-69 (NaN continues, as in the reference)
-                const float inv = static_cast<float>(1.0 / dist);
-                fdx = static_cast<float>(ox) * inv;
-                fdy = static_cast<float>(oy) * inv;
-                fdz = static_cast<float>(oz) * inv;
-            }
-            // degree selection and the colour-model error contract (raster.cpp:70-77,
-            // color.cpp:201-206, :182-191)
-            int deg = sp.sh_degree;
-            int deg_used = -1;
-            if constexpr (KIND == SGS_MIXED) {
-                if (cfg.has_override) {
-                    deg_used = cfg.override_degree;
-                } else {
-                    if (cfg.lo > cfg.hi) {
-                        raise_error(ctr, i, kErrThresholds);
-                        break;
-                    }
-                    deg_used = radius < cfg.lo ? 0 : (radius < cfg.hi ? 1 : 2);
-                }
-            } else {
-                if (cfg.has_override) {
-                    raise_error(ctr, i, kErrOverrideNonMixed);
-                    break;
-                }
-            }
-            if (!safe_dist) {
-                const double dxd = ddiv(ox, dist), dyd = ddiv(oy, dist), dzd = ddiv(oz, dist);
-                const double nrm =
-                    __dsqrt_rn(dadd(dadd(dmul(dxd, dxd), dmul(dyd, dyd)), dmul(dzd, dzd)));
-                if (fabs(dsub(nrm, 1.0)) > 1e-6) {
-                    raise_error(ctr, i, kErrDirection);
-                    break;
-                }
-            }
-            if constexpr (KIND == SGS_MIXED) {
-                if (deg_used < 0 || deg_used > sp.sh_degree) {
-                    raise_error(ctr, i, kErrDegreeTooHigh);
-                    break;
-                }
-                deg = deg_used;
-            }
-            // ---- outputs ----
-            // conic and opacity only feed FP32 quantities here (the compositor's guard band
-            // re-derives the exact FP64 values): one reciprocal instead of three divisions,
-            // sigmoid in FP32. The debug dump reports the exact ones.
-            double cona, conb, conc, opacity;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const K1Out& o = views.v[v];
+            unsigned long long key = ~0ULL;
+            uint32_t count = 0;
+            bool visible = false;
+            DebugSplat dbg;
             if constexpr (DEBUG) {
-                exact_conic_opacity(g, pg);
-                cona = pg.cona, conb = pg.conb, conc = pg.conc, opacity = pg.opacity;
-            } else {
-                const double rdet = 1.0 / pg.det;
-                cona = pg.c * rdet;
-                conb = -pg.b * rdet;
-                conc = pg.a * rdet;
-                opacity = 1.0f / (1.0f + __expf(-static_cast<float>(g.opl)));
+                memset(&dbg, 0, sizeof(dbg));
+                dbg.degree = -1;
             }
-            visible = true;
-            key = depth_key(tz);
-            // tile rectangle (raster.cpp:117-122), inclusive, clamped
-            const double ts = static_cast<double>(cfg.tile_size);
-            // x / ts == x * (1/ts) bit for bit when ts is a power of two (both round the
-            // exact quotient once); other tile sizes divide.
-            const bool pow2 = (cfg.tile_size & (cfg.tile_size - 1)) == 0;
-            const double its = 1.0 / ts;
-            const double qx0 = pow2 ? dmul(dsub(mx, radius), its) : ddiv(dsub(mx, radius), ts);
-            const double qx1 = pow2 ? dmul(dadd(mx, radius), its) : ddiv(dadd(mx, radius), ts);
-            const double qy0 = pow2 ? dmul(dsub(my, radius), its) : ddiv(dsub(my, radius), ts);
-            const double qy1 = pow2 ? dmul(dadd(my, radius), its) : ddiv(dadd(my, radius), ts);
-            int32_t x0 = to_int_x86(floor(qx0));
-            int32_t x1 = to_int_x86(floor(qx1));
-            int32_t y0 = to_int_x86(floor(qy0));
-            int32_t y1 = to_int_x86(floor(qy1));
-            x0 = max(0, x0);
-            y0 = max(0, y0);
-            x1 = min(cfg.tiles_x - 1, x1);
-            y1 = min(cfg.tiles_y - 1, y1);
-            if (x1 >= x0 && y1 >= y0)
-                count = static_cast<uint32_t>(x1 - x0 + 1) * static_cast<uint32_t>(y1 - y0 + 1);
-            rects[i] = make_int4(x0, x1, y0, y1);
-            // FP32 m2 error bound: 2u S (9 r^2 + 3 r ts) + 1e-6
-            const double csum = fabs(cona) + 2.0 * fabs(conb) + fabs(conc);
-            const double guard =
-                2.0 * 5.9604644775390625e-08 * csum * (9.0 * radius * radius + 3.0 * radius * ts) +
-                1e-6;
-            // combined cutoff: alpha < 1/255 <=> m2 > 2 ln(255 op) (op > 0)
-            const double acut = opacity > 0.0 ? 2.0 * log(255.0 * opacity) : -1.0;
-            const double cut = acut < kSupportMahalanobisSq ? acut : kSupportMahalanobisSq;
-            // extents of {d : d^T conic d <= cut + guard} = sqrt(K cov_xx), sqrt(K cov_yy);
-            // cov = the dilated 2D covariance (a, b, c), slightly inflated
-            const double K = fmax(cut + guard, 0.0);
-            SplatRec r;
-            r.mx = mx;
-            r.my = my;
-            r.ca = static_cast<float>(cona);
-            r.cb2 = static_cast<float>(2.0 * conb);
-            r.cc = static_cast<float>(conc);
-            r.lop = opacity > 0.0 ? __log2f(static_cast<float>(opacity)) : -1e30f;
-            r.cut = static_cast<float>(cut);
-            r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
-            r.ext_x = sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
-            r.ext_y = sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
-            // colour (FP32), direction from the FP64 offset
-            {
-                const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
-                const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
-                const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
-                colour[i] = col;
-                if constexpr (DEBUG) {
-                    dbg.color[0] = col.x;
-                    dbg.color[1] = col.y;
-                    dbg.color[2] = col.z;
-                }
+            k1_view<KIND, DEBUG>(sp, cfg, stg, o, buf, tid, i, g, dbg, key, count, visible);
+            o.keys[i] = key;
+            o.ntiles[i] = count;
+            if constexpr (DEBUG) debug[i] = dbg;
+            if (visible) {
+                ++nvis[v];
+                kmin[v] = min(kmin[v], key);
+                kmax[v] = max(kmax[v], key);
             }
-            rec[i] = r;
-            if constexpr (DEBUG) {
-                dbg.mean2d[0] = mx;
-                dbg.mean2d[1] = my;
-                dbg.conic[0] = cona;
-                dbg.conic[1] = conb;
-                dbg.conic[2] = conc;
-                dbg.depth = tz;
-                dbg.opacity = opacity;
-                dbg.radius = radius;
-                dbg.degree = KIND == SGS_MIXED ? deg_used : -1;
-                dbg.visible = 1;
-            }
-        } while (false);
-        depth_keys[i] = key;
-        ntiles[i] = count;
-        if constexpr (DEBUG) debug[i] = dbg;
-        if (visible) {
-            ++nvis;
-            kmin = min(kmin, key);
-            kmax = max(kmax, key);
         }
     }
-    // visible count and depth-key range: one atomic each per warp
+    // visible count and depth-key range per view: one atomic each per warp
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        nvis += __shfl_xor_sync(0xffffffffu, nvis, o);
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if ((tid & 31) == 0 && nvis) {
-        atomicAdd(&ctr->visible, static_cast<unsigned long long>(nvis));
-        atomicMin(&ctr->kmin, kmin);
-        atomicMax(&ctr->kmax, kmax);
+    for (int v = 0; v < NV; ++v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            nvis[v] += __shfl_xor_sync(0xffffffffu, nvis[v], o);
+            kmin[v] = min(kmin[v], __shfl_xor_sync(0xffffffffu, kmin[v], o));
+            kmax[v] = max(kmax[v], __shfl_xor_sync(0xffffffffu, kmax[v], o));
+        }
+        if ((tid & 31) == 0 && nvis[v]) {
+            Counters* ctr = views.v[v].ctr;
+            atomicAdd(&ctr->visible, static_cast<unsigned long long>(nvis[v]));
+            atomicMin(&ctr->kmin, kmin[v]);
+            atomicMax(&ctr->kmax, kmax[v]);
+        }
     }
 }
 
@@ -484,13 +507,12 @@ K1Stage make_stage(const ScenePlanes& sp, const CfgParams& cfg) {
     return st;
 }
 
-template <bool F64, int KIND, int MINB>
-void launch_k1(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
-               SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
+template <bool F64, int KIND, int MINB, bool DEBUG, int NV>
+void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
                cudaStream_t stream) {
     const K1Stage st = make_stage(sp, cfg);
     const size_t smem = static_cast<size_t>(2) * st.slots * kK1Threads * sizeof(float4);
-    auto kern = debug ? preprocess_kernel<F64, KIND, 1, true> : preprocess_kernel<F64, KIND, MINB, false>;
+    auto kern = preprocess_kernel<F64, KIND, MINB, DEBUG, NV>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -498,28 +520,7 @@ void launch_k1(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kK1Threads, smem);
     const uint64_t need = (sp.n + kK1Threads - 1) / kK1Threads;
     const uint64_t grid = std::min<uint64_t>(need, static_cast<uint64_t>(sms) * std::max(per_sm, 1));
-    kern<<<static_cast<unsigned>(grid), kK1Threads, smem, stream>>>(sp, cam, cfg, st, keys, rec, rects, ntiles,
-                                                                    colour, ctr, debug);
-}
-
-template <bool F64, int MINB>
-void launch_kind_b(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
-                   SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
-                   cudaStream_t stream) {
-    switch (sp.kind) {
-        case SGS_SH:
-            launch_k1<F64, SGS_SH, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
-            break;
-        case SGS_SG1:
-            launch_k1<F64, SGS_SG1, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
-            break;
-        case SGS_SG3:
-            launch_k1<F64, SGS_SG3, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
-            break;
-        default:
-            launch_k1<F64, SGS_MIXED, MINB>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream);
-            break;
-    }
+    kern<<<static_cast<unsigned>(grid), kK1Threads, smem, stream>>>(sp, cfg, st, views, debug);
 }
 
 constexpr int kDefaultMinB = 2;
@@ -533,15 +534,35 @@ int k1_minb() {
     return v;
 }
 
-template <bool F64>
-void launch_kind(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, unsigned long long* keys,
-                 SplatRec* rec, int4* rects, uint32_t* ntiles, float4* colour, Counters* ctr, DebugSplat* debug,
-                 cudaStream_t stream) {
+template <bool F64, int KIND>
+void launch_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
+                  cudaStream_t stream) {
+    if (debug) {
+        launch_k1<F64, KIND, 1, true, 1>(sp, cfg, views, debug, stream);
+        return;
+    }
+    switch (views.nv) {
+        case 2: launch_k1<F64, KIND, kDefaultMinB, false, 2>(sp, cfg, views, nullptr, stream); return;
+        case 3: launch_k1<F64, KIND, kDefaultMinB, false, 3>(sp, cfg, views, nullptr, stream); return;
+        case 4: launch_k1<F64, KIND, kDefaultMinB, false, 4>(sp, cfg, views, nullptr, stream); return;
+        default: break;
+    }
     switch (k1_minb()) {
-        case 1: launch_kind_b<F64, 1>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
-        case 2: launch_kind_b<F64, 2>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
-        case 4: launch_kind_b<F64, 4>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
-        default: launch_kind_b<F64, 3>(sp, cam, cfg, keys, rec, rects, ntiles, colour, ctr, debug, stream); break;
+        case 1: launch_k1<F64, KIND, 1, false, 1>(sp, cfg, views, nullptr, stream); break;
+        case 3: launch_k1<F64, KIND, 3, false, 1>(sp, cfg, views, nullptr, stream); break;
+        case 4: launch_k1<F64, KIND, 4, false, 1>(sp, cfg, views, nullptr, stream); break;
+        default: launch_k1<F64, KIND, 2, false, 1>(sp, cfg, views, nullptr, stream); break;
+    }
+}
+
+template <bool F64>
+void launch_kind(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
+                 cudaStream_t stream) {
+    switch (sp.kind) {
+        case SGS_SH: launch_views<F64, SGS_SH>(sp, cfg, views, debug, stream); break;
+        case SGS_SG1: launch_views<F64, SGS_SG1>(sp, cfg, views, debug, stream); break;
+        case SGS_SG3: launch_views<F64, SGS_SG3>(sp, cfg, views, debug, stream); break;
+        default: launch_views<F64, SGS_MIXED>(sp, cfg, views, debug, stream); break;
     }
 }
 
@@ -592,13 +613,19 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
                        uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream) {
+    K1Views views{};
+    views.nv = 1;
+    views.v[0] = K1Out{depth_keys, rec, rects, ntiles, colour, counters, cam};
+    launch_preprocess_views(sp, cfg, views, debug, stream);
+}
+
+void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
+                             cudaStream_t stream) {
     if (sp.n == 0) return;
     if (sp.geometry_f64)
-        launch_kind<true>(sp, cam, cfg, depth_keys, rec, rects, ntiles, colour, counters, debug,
-                          stream);
+        launch_kind<true>(sp, cfg, views, debug, stream);
     else
-        launch_kind<false>(sp, cam, cfg, depth_keys, rec, rects, ntiles, colour, counters, debug,
-                           stream);
+        launch_kind<false>(sp, cfg, views, debug, stream);
 }
 
 }  // namespace sgs

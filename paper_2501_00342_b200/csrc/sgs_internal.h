@@ -144,6 +144,24 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
                        uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream);
+// K1 over up to kMaxK1Views cameras of one batch: every Gaussian is read once and
+// projected into each view's arenas.
+constexpr int kMaxK1Views = 4;
+struct K1Out {
+    unsigned long long* keys;
+    SplatRec* rec;
+    int4* rects;
+    uint32_t* ntiles;
+    float4* colour;
+    Counters* ctr;
+    CamParams cam;
+};
+struct K1Views {
+    int nv;
+    K1Out v[kMaxK1Views];
+};
+void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
+                             cudaStream_t stream);
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
 // per-scene 3D covariance cache: 3 planes of n double2 (projection.cuh)
 void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream);
