@@ -15,6 +15,7 @@
  *   sgsplat::param_count       color.hpp:139-140                   sgs_color_param_count
  *   make_synthetic_scene       synth.hpp:29, synth.cpp:26-106      sgs_synth_scene
  *   make_orbit_camera(s)       camera.hpp:34-35, synth.hpp:32-33   sgs_orbit_camera(s)
+ *   sgsplat::backward          grad.hpp:32-33, grad.cpp:69-246     sgs_backward
  *   sgsplat::psnr / ssim / ssim_with_grad  metrics.hpp:7-21      sgs_psnr / sgs_ssim
  *   sgsplat::load_ply          ply.hpp:26-29, ply.cpp:295-306      sgs_ply_read (host) /
  *                                                                  sgs_scene_load_ply (device)
@@ -217,6 +218,17 @@ sgs_status sgs_orbit_camera(const double* target, double distance, double angle,
                             sgs_camera* out);
 sgs_status sgs_orbit_cameras(int32_t count, int32_t width, int32_t height, double distance,
                              double focal, double elevation, sgs_camera* out);
+
+/* --- backward (grad.hpp, grad.cpp) ------------------------------------------------ */
+/* backward (grad.cpp:69-246): d(sum_pixels upstream . rendered) / d(stored params).
+ * upstream: height x width x 3 doubles; grads: count x (11 + colour params) doubles in
+ * the flat order of Scene::param (SceneGradients::flat); both in host or device
+ * memory (memory = SGS_HOST / SGS_DEVICE). Culled Gaussians get zero gradients. A
+ * non-finite upstream value is SGS_ERR_NUMERIC ("non-finite upstream gradient"). FP64
+ * throughout and deterministic; agrees with the reference to rounding. */
+sgs_status sgs_backward(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                        const sgs_render_config* cfg, const double* upstream, int32_t memory,
+                        double* grads);
 
 /* --- image metrics (metrics.hpp, metrics.cpp) ------------------------------------ */
 /* Images are height x width x channels, row-major (the reference's Image layout),

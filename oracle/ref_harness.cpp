@@ -8,6 +8,7 @@
 // detail::build_tile_grid / testing::render_bruteforce themselves.
 #include "oracle.h"
 
+#include "sgsplat/grad.hpp"
 #include "sgsplat/metrics.hpp"
 #include "sgsplat/ply.hpp"
 #include "sgsplat/raster.hpp"
@@ -328,6 +329,20 @@ int ref_ssim(const double* a, const double* b, int w, int h, int c, double* out,
         } else {
             *out = ssim(image_of(a, w, h, c), image_of(b, w, h, c));
         }
+        return ORC_OK;
+    })
+}
+
+// sgsplat::backward (proj/src/grad.cpp:69-246): upstream H x W x 3; grads in
+// SceneGradients::flat order (count x params_per_gaussian).
+int ref_backward(void* s, const orc_camera* cam, const orc_config* cfg, const double* upstream, double* grads) {
+    REF_GUARD({
+        const Scene& sc = *static_cast<Scene*>(s);
+        Camera c = to_cam(cam);
+        Image up(c.width, c.height, 3);
+        std::memcpy(up.data.data(), upstream, up.size() * sizeof(double));
+        SceneGradients g = backward(sc, c, to_cfg(cfg), up);
+        for (std::size_t i = 0; i < sc.total_params(); ++i) grads[i] = g.flat(sc, i);
         return ORC_OK;
     })
 }

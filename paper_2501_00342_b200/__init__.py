@@ -27,7 +27,7 @@ __all__ = [
     "Camera", "Scene", "Renderer", "DeviceScene", "RenderStats", "render", "synth_scene",
     "orbit_camera", "orbit_cameras", "flops_per_gaussian", "param_count", "shared_param_count",
     "select_degree", "InvalidArgumentError", "NumericError", "FormatError", "IoError", "CudaError",
-    "load_scene", "load_ply", "ply_info", "psnr", "ssim", "ssim_with_grad",
+    "load_scene", "load_ply", "ply_info", "psnr", "ssim", "ssim_with_grad", "backward",
 ]
 
 KINDS = {"sh": C.SGS_SH, "sg1": C.SGS_SG1, "sg3": C.SGS_SG3, "mixed": C.SGS_MIXED}
@@ -375,6 +375,33 @@ class Renderer:
                                             ctypes.byref(h)))
         return DeviceScene(self, h.value)
 
+    def backward(self, dscene: DeviceScene, cam: Camera, upstream, tile_size=16, thresholds=(2.0, 8.0),
+                 degree_override=-1, early_stop=1e-4):
+        """backward (grad.cpp:69-246) on the GPU: d(sum upstream . render) / d(stored
+        params) as an (N, 11 + colour params) float64 array in Scene.params order --
+        numpy for numpy upstream, a CUDA tensor for a CUDA tensor upstream."""
+        cfg = _config(tile_size, thresholds, 0, degree_override, early_stop)
+        meta = dscene.meta
+        stride = 11 + param_count(KIND_NAMES[meta.kind], meta.sh_degree)
+        shape = (cam.height, cam.width, 3)
+        if hasattr(upstream, "is_cuda") and upstream.is_cuda:
+            import torch
+
+            up = upstream.to(torch.float64).contiguous()
+            if tuple(up.shape) != shape:
+                raise InvalidArgumentError("upstream image dimensions do not match the render output")
+            grads = torch.zeros((meta.count, stride), dtype=torch.float64, device=up.device)
+            _check(self._lib.sgs_backward(self.handle, dscene.handle, ctypes.byref(cam._c()), ctypes.byref(cfg),
+                                          up.data_ptr(), C.SGS_DEVICE, grads.data_ptr()))
+            return grads
+        up = np.ascontiguousarray(upstream, dtype=np.float64)
+        if up.shape != shape:
+            raise InvalidArgumentError("upstream image dimensions do not match the render output")
+        grads = np.zeros((meta.count, stride), dtype=np.float64)
+        _check(self._lib.sgs_backward(self.handle, dscene.handle, ctypes.byref(cam._c()), ctypes.byref(cfg),
+                                      up.ctypes.data, C.SGS_HOST, grads.ctypes.data if grads.size else None))
+        return grads
+
     @staticmethod
     def plan(scene: Scene) -> C.sgs_scene_meta:
         d, keep = scene._desc()
@@ -576,3 +603,14 @@ def ssim_with_grad(a, b):
         gptr = grad.ctypes.data
     _check(_lib().sgs_ssim(_renderer().handle, pa, pb, w, h, c, dt, mem, ctypes.byref(out), gptr))
     return out.value, grad
+
+
+def backward(scene: Scene, camera: Camera, upstream, tile_size: int = 16, thresholds=(2.0, 8.0),
+             degree_override: int = -1, early_stop: float = 1e-4) -> np.ndarray:
+    """backward (grad.hpp:32-33) for a host Scene: (N, 11 + colour params) float64."""
+    r = _renderer()
+    ds = r.upload(scene)
+    try:
+        return r.backward(ds, camera, upstream, tile_size, thresholds, degree_override, early_stop)
+    finally:
+        ds.free()

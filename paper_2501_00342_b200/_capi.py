@@ -170,6 +170,8 @@ SIGNATURES = {
                               ctypes.POINTER(sgs_camera)]),
     "sgs_orbit_cameras": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, ctypes.POINTER(sgs_camera)]),
+    "sgs_backward": (_S, [_P, _P, ctypes.POINTER(sgs_camera), ctypes.POINTER(sgs_render_config), _P,
+                          ctypes.c_int32, _P]),
     "sgs_psnr": (_S, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                       ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "sgs_ssim": (_S, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,

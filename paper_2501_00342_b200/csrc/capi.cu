@@ -148,6 +148,7 @@ struct sgs_context {
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
     DevBuf metrics;  // PSNR / SSIM scratch (inputs staged from host, maps, partial sums)
+    DevBuf bwd;      // backward scratch (FP64 splats, ranks, per-entry partials, staging)
     uint64_t own_launches = 0, lib_launches = 0;
 };
 
@@ -785,7 +786,8 @@ void fill_blob(const sgs_scene_desc* d, const sgs_scene_meta& m, std::vector<cha
                 break;
             }
             case SGS_SG1: {
-                // plane 0 (diffuse rgb, log_lambda), plane 1 (alpha rgb, 0), plane 2 (mu/|mu|, 0);
+                // plane 0 (diffuse rgb, log_lambda), plane 1 (alpha rgb, 0), plane 2 (mu/|mu|, 0),
+                // plane 3 (raw mu, 0);
                 // mu normalised in FP64 exactly as DiffuseSGModel::lobe (color.cpp:49-56)
                 for (int k = 0; k < 3; ++k) c[k] = static_cast<float>(param_at(d, co + k));
                 c[3] = static_cast<float>(param_at(d, co + 6));
@@ -794,6 +796,7 @@ void fill_blob(const sgs_scene_desc* d, const sgs_scene_meta& m, std::vector<cha
                 const double nn = std::sqrt((mu[0] * mu[0] + mu[1] * mu[1]) + mu[2] * mu[2]);
                 for (int k = 0; k < 3; ++k)
                     c[8 + k] = static_cast<float>(nn > 1e-12 ? mu[k] / nn : (k == 0 ? 1.0 : 0.0));
+                for (int k = 0; k < 3; ++k) c[12 + k] = static_cast<float>(mu[k]);  // raw axis (backward)
                 break;
             }
             case SGS_SG3:
@@ -922,6 +925,7 @@ std::vector<int32_t> ply_slot_table(const PlyTable& t, int color_planes, int* mu
             c[3] = flat(co + 6);
             for (int k = 0; k < 3; ++k) c[4 + k] = flat(co + 3 + k);
             for (int k = 0; k < 3; ++k) c[8 + k] = -2 - k;
+            for (int k = 0; k < 3; ++k) c[12 + k] = flat(co + 7 + k);  // raw axis (backward)
             *mu_col = flat(co + 7);
             break;
         case SGS_SG3:
@@ -1009,6 +1013,7 @@ void sgs_destroy(sgs_context* ctx) {
         if (L.stream) cudaStreamDestroy(L.stream);
     }
     ctx->metrics.release();
+    ctx->bwd.release();
     if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     cudaStreamDestroy(ctx->own_stream);
@@ -1482,6 +1487,71 @@ sgs_status sgs_psnr(sgs_context* ctx, const void* a, const void* b, int32_t widt
 sgs_status sgs_ssim(sgs_context* ctx, const void* a, const void* b, int32_t width, int32_t height,
                     int32_t channels, int32_t dtype, int32_t memory, double* value, double* grad_a) {
     return run_metric(ctx, a, b, width, height, channels, dtype, memory, true, value, grad_a);
+}
+
+sgs_status sgs_backward(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                        const sgs_render_config* cfg, const double* upstream, int32_t memory, double* grads) {
+    if (!ctx || !scene || !cam || !cfg || !upstream || (!grads && scene->meta.count))
+        return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
+    sgs_status st = validate_camera(cam);
+    if (st != SGS_OK) return st;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const bool host = memory != SGS_DEVICE;
+    const uint64_t n = scene->meta.count;
+    const int stride = 11 + color_param_count_impl(scene->meta.kind, scene->meta.sh_degree);
+    const size_t npx = static_cast<size_t>(cam->width) * static_cast<size_t>(cam->height);
+    // grad.cpp:72-75: finite upstream (before any projection error)
+    if (host) {
+        for (size_t k = 0; k < npx * 3; ++k)
+            if (!std::isfinite(upstream[k])) return fail(SGS_ERR_NUMERIC, "non-finite upstream gradient");
+    } else {
+        SGS_CUDA(ctx->bwd.ensure(256));
+        int* d_bad = ctx->bwd.as<int>();
+        SGS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        launch_finite_check(upstream, npx * 3, d_bad, s);
+        int bad = 0;
+        SGS_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGS_CUDA(cudaStreamSynchronize(s));
+        if (bad) return fail(SGS_ERR_NUMERIC, "non-finite upstream gradient");
+    }
+    if (n == 0) return SGS_OK;
+    // the forward's depth order and full tile lists (one chunk), as sgs_debug_tile_grid
+    st = run_frame(ctx, scene, cam, cfg, nullptr, kTileGrid);
+    if (st != SGS_OK) return st;
+    Lane& L = ctx->lane[0];
+    const uint64_t V = L.last_v, P = L.last_p;
+    const CfgParams kp = make_cfg(cfg, cam);
+    const size_t ntile = static_cast<size_t>(kp.tiles_x) * static_cast<size_t>(kp.tiles_y);
+    // scratch: FP64 splats | rank_of | used | partials | (host) upstream | (host) grads
+    const size_t o_rank = align_up(n * bwd_splat_bytes(), 256);
+    const size_t o_used = o_rank + align_up(n * 4, 256);
+    const size_t o_part = o_used + align_up(ntile * 4, 256);
+    const size_t o_up = o_part + align_up(std::max<uint64_t>(P, 1) * bwd_partial_bytes(), 256);
+    const size_t o_gr = o_up + (host ? align_up(npx * 3 * 8, 256) : 0);
+    const size_t total = o_gr + (host ? n * stride * 8 : 0) + 256;
+    SGS_CUDA(ctx->bwd.ensure(total));
+    char* base = static_cast<char*>(ctx->bwd.ptr);
+    const double* d_up = upstream;
+    double* d_gr = grads;
+    if (host) {
+        SGS_CUDA(cudaMemcpyAsync(base + o_up, upstream, npx * 3 * 8, cudaMemcpyHostToDevice, s));
+        d_up = reinterpret_cast<const double*>(base + o_up);
+        d_gr = reinterpret_cast<double*>(base + o_gr);
+    }
+    SGS_CUDA(cudaMemsetAsync(d_gr, 0, n * stride * 8, s));
+    launch_backward(scene->planes, make_cam(cam), kp, scene->meta.shared_axes, scene->meta.background,
+                    cfg->has_override ? cfg->override_degree : -1, V, composite_pixel_chunks(cfg->tile_size),
+                    L.last_order, L.brect.as<int4>(), L.ranges.as<uint2>(), L.last_tile_keys, base,
+                    reinterpret_cast<uint32_t*>(base + o_rank), reinterpret_cast<uint32_t*>(base + o_used),
+                    reinterpret_cast<double*>(base + o_part), d_up, d_gr, stride, s);
+    SGS_CUDA(cudaGetLastError());
+    ctx->own_launches += 3;
+    if (host) SGS_CUDA(cudaMemcpyAsync(grads, d_gr, n * stride * 8, cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaStreamSynchronize(s));
+    return SGS_OK;
 }
 
 }  // extern "C"

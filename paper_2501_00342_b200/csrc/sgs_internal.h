@@ -132,7 +132,7 @@ inline int color_plane_count(int kind, int degree) {
     int ncoef = (degree + 1) * (degree + 1);
     switch (kind) {
         case SGS_SH: return (3 * ncoef + 3) / 4;
-        case SGS_SG1: return 3;
+        case SGS_SG1: return 4;  // + raw lobe axis (plane 3) for the backward
         case SGS_SG3: return 4;
         case SGS_MIXED: return (3 * ncoef + 3) / 4 + 3;
     }
@@ -187,6 +187,15 @@ size_t bin_emit_status_bytes(uint64_t ranks);
 void launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
                      int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
                      unsigned long long* status, Counters* ctr, cudaStream_t stream);
+// backward (backward.cu)
+size_t bwd_splat_bytes();
+size_t bwd_partial_bytes();
+void launch_finite_check(const double* v, size_t n, int* bad, cudaStream_t s);
+void launch_backward(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
+                     const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
+                     const int4* brect, const uint2* ranges, const unsigned long long* keys, void* bs,
+                     uint32_t* rank_of, uint32_t* used, double* partial, const double* upstream, double* grads,
+                     int stride, cudaStream_t s);
 // image metrics (metrics.cu)
 size_t metrics_scratch_doubles(size_t n, bool grad);
 void launch_psnr_sum(const void* a, const void* b, bool f64, size_t n, double* scratch, double* d_sum,

@@ -206,6 +206,8 @@ class RefLib(_Lib):
                                         ctypes.POINTER(ctypes.c_int)]
         L.ref_color_param_count.argtypes = [ctypes.c_int, ctypes.c_int]
         L.ref_load_ply.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.ref_backward.argtypes = [ctypes.c_void_p, ctypes.POINTER(OrcCamera), ctypes.POINTER(OrcConfig),
+                                   ctypes.c_void_p, ctypes.c_void_p]
         L.ref_psnr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                ctypes.POINTER(ctypes.c_double)]
         L.ref_ssim.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -234,6 +236,18 @@ class RefLib(_Lib):
             self.lib.ref_scene_free(h)
         name = KIND_NAMES.get(kind.value, "empty")
         return 0, FlatScene(name, deg.value, params, axes.reshape(3, 3), bg)
+
+    def backward(self, s: FlatScene, cam, cfg, upstream):
+        """backward (grad.cpp): (N, stride) flat gradients."""
+        h = self._handle(s)
+        try:
+            up = np.ascontiguousarray(upstream, dtype=np.float64)
+            out = np.zeros_like(np.ascontiguousarray(s.params, dtype=np.float64))
+            rc = self.lib.ref_backward(h, ctypes.byref(cam), ctypes.byref(cfg), _ptr(up), _ptr(out))
+            assert rc == 0, self.err()
+            return out
+        finally:
+            self.lib.ref_scene_free(h)
 
     # -- image metrics (metrics.cpp) -----------------------------------------
     def psnr(self, a, b):
