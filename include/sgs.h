@@ -108,7 +108,8 @@ typedef struct {
     int32_t kind;
     int32_t sh_degree;
     int32_t geometry_f64; /* 0: float32 planes (inputs were f32-exact), 1: float64 planes */
-    int32_t reserved;
+    int32_t color_f64;    /* 1: colour parameters not f32-exact: FP64 copies are kept too
+                             (read by the exact mode and the backward) */
     uint64_t blob_bytes; /* bytes of the single device allocation holding every plane */
     double shared_axes[9];
     double background[3];
@@ -218,6 +219,15 @@ sgs_status sgs_orbit_camera(const double* target, double distance, double angle,
                             sgs_camera* out);
 sgs_status sgs_orbit_cameras(int32_t count, int32_t width, int32_t height, double distance,
                              double focal, double elevation, sgs_camera* out);
+
+/* --- exact mode ------------------------------------------------------------------ */
+/* render in the reference's precision: the same culling, depth order and tile lists,
+ * then the per-pixel loop (raster.cpp:155-186) in FP64 with the reference's operation
+ * order (no FMA contraction). rgb: height x width x 3 doubles, T: height x width
+ * (either may be NULL), in host or device memory. Slower than sgs_render; images
+ * match the reference to FP64 rounding (CUDA vs glibc exp, <= 1 ulp). */
+sgs_status sgs_render_f64(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                          const sgs_render_config* cfg, double* rgb, double* T, int32_t memory);
 
 /* --- backward (grad.hpp, grad.cpp) ------------------------------------------------ */
 /* backward (grad.cpp:69-246): d(sum_pixels upstream . rendered) / d(stored params).

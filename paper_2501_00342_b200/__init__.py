@@ -375,6 +375,17 @@ class Renderer:
                                             ctypes.byref(h)))
         return DeviceScene(self, h.value)
 
+    def render_f64(self, dscene: DeviceScene, cam: Camera, tile_size=16, thresholds=(2.0, 8.0),
+                   degree_override=-1, early_stop=1e-4):
+        """The reference's FP64 compositing (sgs_render_f64): float64 (H, W, 3) and
+        (H, W, 1) arrays."""
+        cfg = _config(tile_size, thresholds, 0, degree_override, early_stop)
+        rgb = np.empty((cam.height, cam.width, 3), dtype=np.float64)
+        T = np.empty((cam.height, cam.width, 1), dtype=np.float64)
+        _check(self._lib.sgs_render_f64(self.handle, dscene.handle, ctypes.byref(cam._c()), ctypes.byref(cfg),
+                                        rgb.ctypes.data, T.ctypes.data, C.SGS_HOST))
+        return rgb, T
+
     def backward(self, dscene: DeviceScene, cam: Camera, upstream, tile_size=16, thresholds=(2.0, 8.0),
                  degree_override=-1, early_stop=1e-4):
         """backward (grad.cpp:69-246) on the GPU: d(sum upstream . render) / d(stored
@@ -523,17 +534,25 @@ def _renderer() -> Renderer:
 
 
 def render(scene: Scene, camera: Camera, tile_size: int = 16, thresholds=(2.0, 8.0),
-           threads: int = 0, degree_override: int = -1, return_transmittance: bool = False):
+           threads: int = 0, degree_override: int = -1, return_transmittance: bool = False,
+           exact: Optional[bool] = None):
     """sgsplat.render (bindings.cpp:109-121): float64 (H, W, 3) image, optionally with
     the (H, W, 1) transmittance. Uploads the scene on every call, as the reference
-    re-reads its Scene on every call (no caching by identity: train mutates scenes)."""
+    re-reads its Scene on every call (no caching by identity: train mutates scenes).
+    exact=True (or SGS_EXACT=1) composites in FP64 like the reference (sgs_render_f64);
+    the default is the FP32 throughput path."""
     r = _renderer()
     cfg_args = dict(tile_size=tile_size, thresholds=thresholds, degree_override=degree_override)
     if tile_size < 1:
         raise InvalidArgumentError("tile_size must be >= 1")
+    if exact is None:
+        exact = os.environ.get("SGS_EXACT", "0") not in ("", "0")
     ds = r.upload(scene)
     try:
-        rgb, T = r.render(ds, camera, **cfg_args)
+        if exact:
+            rgb, T = r.render_f64(ds, camera, **cfg_args)
+        else:
+            rgb, T = r.render(ds, camera, **cfg_args)
     finally:
         ds.free()
     img = rgb.astype(np.float64)

@@ -74,7 +74,7 @@ class sgs_scene_meta(ctypes.Structure):
         ("kind", ctypes.c_int32),
         ("sh_degree", ctypes.c_int32),
         ("geometry_f64", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("color_f64", ctypes.c_int32),
         ("blob_bytes", ctypes.c_uint64),
         ("shared_axes", ctypes.c_double * 9),
         ("background", ctypes.c_double * 3),
@@ -170,6 +170,8 @@ SIGNATURES = {
                               ctypes.POINTER(sgs_camera)]),
     "sgs_orbit_cameras": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, ctypes.POINTER(sgs_camera)]),
+    "sgs_render_f64": (_S, [_P, _P, ctypes.POINTER(sgs_camera), ctypes.POINTER(sgs_render_config), _P, _P,
+                            ctypes.c_int32]),
     "sgs_backward": (_S, [_P, _P, ctypes.POINTER(sgs_camera), ctypes.POINTER(sgs_render_config), _P,
                           ctypes.c_int32, _P]),
     "sgs_psnr": (_S, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,

@@ -20,9 +20,11 @@
 //                  in depth order), then chains through projection, covariance, the
 //                  activations and the colour model (grad.cpp:155-244, grad_color
 //                  color.cpp:291-358).
-// The arithmetic is FP64 throughout; sums run in different orders than the
-// reference's worker-merged buffers, so gradients agree to rounding (tests state the
-// tolerance), not bit for bit.
+// The arithmetic is FP64 throughout, and this file is compiled without FMA
+// contraction (Makefile: -fmad=false), as the reference's x86-64 build rounds; the
+// per-splat sums run in different orders than the reference's worker-merged buffers,
+// so gradients agree to rounding (tests state the tolerance), not bit for bit.
+// The same splats feed render_f64_kernel, the reference's render loop in FP64.
 #include "projection.cuh"
 
 namespace sgs {
@@ -115,6 +117,7 @@ __device__ void sh_dbasis(double x, double y, double z, int deg, double (*g)[3])
 // (fill_blob's layout: SG1 keeps the raw lobe axis in plane 3).
 template <int KIND>
 __device__ __forceinline__ double cparam(const ScenePlanes& sp, uint64_t i, int k) {
+    if (sp.color64) return sp.color64[static_cast<uint64_t>(k) * sp.n + i];  // not f32-exact: FP64 copies
     int slot = k;
     if constexpr (KIND == SGS_MIXED) {
         const int nsh = 3 * (sp.sh_degree + 1) * (sp.sh_degree + 1);
@@ -361,6 +364,51 @@ __global__ void __launch_bounds__(kBThreads) bwd_pixels_kernel(
     if (threadIdx.x == 0) used[tile] = static_cast<uint32_t>(tile_used);
 }
 
+// The reference's per-pixel render loop (raster.cpp:155-186) in FP64 over the full
+// tile lists, in its exact operation order (this file is compiled without FMA
+// contraction): the exact mode behind sgs_render_f64.
+__global__ void __launch_bounds__(kBThreads) render_f64_kernel(const BwdParams p, int nchunks,
+                                                               const uint2* __restrict__ ranges,
+                                                               const unsigned long long* __restrict__ keys,
+                                                               const BwdSplat* __restrict__ bs, double* __restrict__ rgb,
+                                                               double* __restrict__ Tout) {
+    const int tile = blockIdx.x;
+    const uint2 range = ranges[tile];
+    const int ts = p.cfg.tile_size;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int W = p.cam.width, H = p.cam.height;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int pp = ch * kBThreads + threadIdx.x;
+        const int lx = pp % ts, ly = pp / ts;
+        const int px = tx * ts + lx, py = ty * ts + ly;
+        if (!(pp < ts * ts && px < W && py < H)) continue;
+        const double cx = px + 0.5, cy = py + 0.5;
+        double acc[3] = {0.0, 0.0, 0.0};
+        double T = 1.0;
+        for (uint32_t j = range.x; j < range.y; ++j) {
+            const BwdSplat s = bs[static_cast<uint32_t>(keys[j])];
+            const double dx = cx - s.mx, dy = cy - s.my;
+            const double m2 = s.c0 * dx * dx + 2.0 * s.c1 * dx * dy + s.c2 * dy * dy;
+            if (m2 > kSupportMahalanobisSq) continue;
+            const double a0 = s.op * exp(-0.5 * m2);
+            const double alpha = a0 < kAlphaClamp ? a0 : kAlphaClamp;  // std::min(a, 0.999)
+            if (alpha < kAlphaMin) continue;
+            const double w = alpha * T;
+            acc[0] += s.cr * w;
+            acc[1] += s.cg * w;
+            acc[2] += s.cb * w;
+            T *= 1.0 - alpha;
+            if (T < p.cfg.early_stop) break;
+        }
+        const size_t pix = static_cast<size_t>(py) * W + px;
+        for (int c = 0; c < 3; ++c) {
+            acc[c] += T * p.bg[c];
+            if (rgb) rgb[pix * 3 + c] = acc[c];
+        }
+        if (Tout) Tout[pix] = T;
+    }
+}
+
 // rotation_quat_jacobians (grad.cpp:31-42), (w, x, y, z)
 __device__ void quat_jacobians(const double* q, double (*J)[9]) {
     const double w = q[0], x = q[1], y = q[2], z = q[3];
@@ -601,7 +649,40 @@ void launch_kind_bwd(const BwdParams& p, uint64_t V, int nchunks, int ntile, con
                                                        grads, stride);
 }
 
+template <bool F64, int KIND>
+void launch_kind_render64(const BwdParams& p, uint64_t V, int nchunks, int ntile, const uint32_t* order,
+                          const uint2* ranges, const unsigned long long* keys, BwdSplat* bs, uint32_t* rank_of,
+                          double* rgb, double* T, cudaStream_t s) {
+    if (V) bwd_prep_kernel<F64, KIND><<<static_cast<unsigned>((V + 127) / 128), 128, 0, s>>>(p, V, order, bs, rank_of);
+    if (ntile) render_f64_kernel<<<ntile, kBThreads, 0, s>>>(p, nchunks, ranges, keys, bs, rgb, T);
+}
+
 }  // namespace
+
+void launch_render_f64(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
+                       const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
+                       const uint2* ranges, const unsigned long long* keys, void* bs, uint32_t* rank_of, double* rgb,
+                       double* T, cudaStream_t s) {
+    BwdParams p{};
+    p.sp = sp;
+    p.cam = cam;
+    p.cfg = cfg;
+    for (int k = 0; k < 9; ++k) p.axes[k] = axes[k];
+    for (int k = 0; k < 3; ++k) p.bg[k] = bg[k];
+    p.override_degree = override_degree;
+    p.tiles_x = cfg.tiles_x;
+    const int ntile = cfg.tiles_x * cfg.tiles_y;
+    BwdSplat* b = static_cast<BwdSplat*>(bs);
+#define SGS_R64(F, K) launch_kind_render64<F, K>(p, V, nchunks, ntile, order, ranges, keys, b, rank_of, rgb, T, s)
+    const bool f64 = sp.geometry_f64 != 0;
+    switch (sp.kind) {
+        case SGS_SH: f64 ? SGS_R64(true, SGS_SH) : SGS_R64(false, SGS_SH); break;
+        case SGS_SG1: f64 ? SGS_R64(true, SGS_SG1) : SGS_R64(false, SGS_SG1); break;
+        case SGS_SG3: f64 ? SGS_R64(true, SGS_SG3) : SGS_R64(false, SGS_SG3); break;
+        default: f64 ? SGS_R64(true, SGS_MIXED) : SGS_R64(false, SGS_MIXED); break;
+    }
+#undef SGS_R64
+}
 
 size_t bwd_splat_bytes() { return sizeof(BwdSplat); }
 size_t bwd_partial_bytes() { return kNP * sizeof(double); }

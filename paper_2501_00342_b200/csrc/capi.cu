@@ -686,6 +686,7 @@ sgs_status run_frame(sgs_context* ctx, const sgs_scene* scene, const sgs_camera*
 struct Layout {
     size_t geo_off[11];
     size_t color_off;
+    size_t color64_off;  // FP64 colour copies (meta.color_f64)
     size_t bytes;
     int color_planes;
 };
@@ -708,6 +709,8 @@ Layout make_layout(const sgs_scene_meta& m) {
     L.color_planes = color_plane_count(m.kind, m.sh_degree);
     L.color_off = off;
     off = align_up(off + static_cast<size_t>(L.color_planes) * n * 16, 256);
+    L.color64_off = off;
+    if (m.color_f64) off = align_up(off + static_cast<size_t>(color_param_count_impl(m.kind, m.sh_degree)) * n * 8, 256);
     L.bytes = std::max<size_t>(off, 256);
     return L;
 }
@@ -729,6 +732,7 @@ void bind_planes(sgs_scene* sc) {
         for (int k = 0; k < 3; ++k) p.g4[k] = reinterpret_cast<const float4*>(base + L.geo_off[k]);
     }
     p.color = reinterpret_cast<const float4*>(base + L.color_off);
+    p.color64 = m.color_f64 ? reinterpret_cast<const double*>(base + L.color64_off) : nullptr;
     for (int k = 0; k < 3; ++k) p.cov[k] = sc->cov.ptr ? sc->cov.as<double2>() + k * m.count : nullptr;
     for (int k = 0; k < 9; ++k) p.axes[k] = static_cast<float>(m.shared_axes[k]);
     for (int k = 0; k < 3; ++k) p.bg[k] = static_cast<float>(m.background[k]);
@@ -807,6 +811,10 @@ void fill_blob(const sgs_scene_desc* d, const sgs_scene_meta& m, std::vector<cha
         float4* cp = reinterpret_cast<float4*>(base + L.color_off);
         for (int pl = 0; pl < L.color_planes; ++pl)
             cp[static_cast<size_t>(pl) * n + i] = make_float4(c[4 * pl], c[4 * pl + 1], c[4 * pl + 2], c[4 * pl + 3]);
+        if (m.color_f64) {
+            double* c64 = reinterpret_cast<double*>(base + L.color64_off);
+            for (int k = 0; k < cpc; ++k) c64[static_cast<size_t>(k) * n + i] = param_at(d, co + k);
+        }
     }
 }
 
@@ -1074,6 +1082,23 @@ sgs_status sgs_scene_plan(const sgs_scene_desc* d, sgs_scene_meta* m) {
             }
     }
     m->geometry_f64 = f64;
+    // colour: the float planes feed the FP32 compositor; FP64 copies are added when
+    // some colour parameter is not f32-exact (the exact mode and the backward read them)
+    int cf64 = 0;
+    if (d->dtype == SGS_F64) {
+        const int cpc = color_param_count_impl(d->kind, deg);
+        const size_t stride = 11 + static_cast<size_t>(cpc);
+        const double* p = static_cast<const double*>(d->params);
+        for (size_t i = 0; i < d->count && !cf64; ++i)
+            for (int k = 0; k < cpc; ++k) {
+                const double v = p[i * stride + 11 + k];
+                if (static_cast<double>(static_cast<float>(v)) != v) {
+                    cf64 = 1;
+                    break;
+                }
+            }
+    }
+    m->color_f64 = cf64;
     for (int k = 0; k < 9; ++k) m->shared_axes[k] = d->shared_axes[k];
     for (int k = 0; k < 3; ++k) m->background[k] = d->background[k];
     m->blob_bytes = make_layout(*m).bytes;
@@ -1550,6 +1575,42 @@ sgs_status sgs_backward(sgs_context* ctx, const sgs_scene* scene, const sgs_came
     SGS_CUDA(cudaGetLastError());
     ctx->own_launches += 3;
     if (host) SGS_CUDA(cudaMemcpyAsync(grads, d_gr, n * stride * 8, cudaMemcpyDeviceToHost, s));
+    SGS_CUDA(cudaStreamSynchronize(s));
+    return SGS_OK;
+}
+
+sgs_status sgs_render_f64(sgs_context* ctx, const sgs_scene* scene, const sgs_camera* cam,
+                          const sgs_render_config* cfg, double* rgb, double* T, int32_t memory) {
+    if (!ctx || !scene || !cam || !cfg) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
+    sgs_status st = validate_camera(cam);
+    if (st != SGS_OK) return st;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const bool host = memory != SGS_DEVICE;
+    const uint64_t n = scene->meta.count;
+    const size_t npx = static_cast<size_t>(cam->width) * static_cast<size_t>(cam->height);
+    st = run_frame(ctx, scene, cam, cfg, nullptr, kTileGrid);
+    if (st != SGS_OK) return st;
+    Lane& L = ctx->lane[0];
+    const CfgParams kp = make_cfg(cfg, cam);
+    const size_t o_rank = align_up(std::max<uint64_t>(n, 1) * bwd_splat_bytes(), 256);
+    const size_t o_img = o_rank + align_up(std::max<uint64_t>(n, 1) * 4, 256);
+    const size_t o_T = o_img + (host ? align_up(npx * 3 * 8, 256) : 0);
+    const size_t total = o_T + (host ? npx * 8 : 0) + 256;
+    SGS_CUDA(ctx->bwd.ensure(total));
+    char* base = static_cast<char*>(ctx->bwd.ptr);
+    double* d_rgb = host ? (rgb ? reinterpret_cast<double*>(base + o_img) : nullptr) : rgb;
+    double* d_T = host ? (T ? reinterpret_cast<double*>(base + o_T) : nullptr) : T;
+    launch_render_f64(scene->planes, make_cam(cam), kp, scene->meta.shared_axes, scene->meta.background,
+                      cfg->has_override ? cfg->override_degree : -1, L.last_v, composite_pixel_chunks(cfg->tile_size),
+                      L.last_order, L.ranges.as<uint2>(), L.last_tile_keys, base,
+                      reinterpret_cast<uint32_t*>(base + o_rank), d_rgb, d_T, s);
+    SGS_CUDA(cudaGetLastError());
+    ctx->own_launches += 2;
+    if (host && rgb) SGS_CUDA(cudaMemcpyAsync(rgb, d_rgb, npx * 3 * 8, cudaMemcpyDeviceToHost, s));
+    if (host && T) SGS_CUDA(cudaMemcpyAsync(T, d_T, npx * 8, cudaMemcpyDeviceToHost, s));
     SGS_CUDA(cudaStreamSynchronize(s));
     return SGS_OK;
 }

@@ -65,6 +65,7 @@ struct ScenePlanes {
     const float4* g4[3];
     const double* g8[11];
     const double2* cov[3];  // cached 3D covariance (projection.cuh covariance3d)
+    const double* color64;  // FP64 colour parameters [k * n + i] when not f32-exact, else null
     const float4* color;  // color_planes consecutive planes of n float4
     float axes[9];        // row-major lobe axes
     float bg[3];
@@ -196,6 +197,10 @@ void launch_backward(const ScenePlanes& sp, const CamParams& cam, const CfgParam
                      const int4* brect, const uint2* ranges, const unsigned long long* keys, void* bs,
                      uint32_t* rank_of, uint32_t* used, double* partial, const double* upstream, double* grads,
                      int stride, cudaStream_t s);
+void launch_render_f64(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
+                       const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
+                       const uint2* ranges, const unsigned long long* keys, void* bs, uint32_t* rank_of, double* rgb,
+                       double* T, cudaStream_t s);
 // image metrics (metrics.cu)
 size_t metrics_scratch_doubles(size_t n, bool grad);
 void launch_psnr_sum(const void* a, const void* b, bool f64, size_t n, double* scratch, double* d_sum,

@@ -9,6 +9,8 @@
 // scene / camera helpers are host code with the reference's semantics; they are
 // utilities, not a render fallback -- render() has no CPU path.
 #include "sgs.h"
+#include "sgsplat/grad.hpp"
+#include "sgsplat/metrics.hpp"
 #include "sgsplat/ply.hpp"
 #include "sgsplat/raster.hpp"
 #include "sgsplat/synth.hpp"
@@ -155,11 +157,21 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
     const sgs_camera c = to_c(cam);
     const sgs_render_config k = to_c(cfg);
     const std::size_t npx = static_cast<std::size_t>(cam.width) * static_cast<std::size_t>(cam.height);
-    std::vector<float> rgb(npx * 3), T(npx);
-    check(sgs_render(context(), ds.s, &c, &k, rgb.data(), T.data(), SGS_HOST, nullptr));
     RenderResult out;
     out.image = Image(cam.width, cam.height, 3);
     out.transmittance = Image(cam.width, cam.height, 1);
+    // SGS_EXACT=1: the reference's FP64 compositing (sgs_render_f64); default: the
+    // FP32 throughput path (exact decisions, image within 1e-5)
+    static const bool exact = [] {
+        const char* e = std::getenv("SGS_EXACT");
+        return e && std::atoi(e) != 0;
+    }();
+    if (exact) {
+        check(sgs_render_f64(context(), ds.s, &c, &k, out.image.data.data(), out.transmittance.data.data(), SGS_HOST));
+        return out;
+    }
+    std::vector<float> rgb(npx * 3), T(npx);
+    check(sgs_render(context(), ds.s, &c, &k, rgb.data(), T.data(), SGS_HOST, nullptr));
     for (std::size_t i = 0; i < npx * 3; ++i) out.image.data[i] = rgb[i];
     for (std::size_t i = 0; i < npx; ++i) out.transmittance.data[i] = T[i];
     return out;
@@ -607,6 +619,132 @@ Scene load_ply(const std::string& path) {
         for (int c = 0; c < 3; ++c) scene.shared_axes(r, c) = info.shared_axes[3 * r + c];
     scene.background = Vec3(info.background[0], info.background[1], info.background[2]);
     return scene;
+}
+
+// ---------------------------------------------------------------------------
+// backward (grad.hpp) and metrics (metrics.hpp) through the C-ABI.
+namespace {
+std::vector<double> flat_params(const Scene& scene) {
+    std::vector<double> flat(scene.total_params());
+    for (std::size_t i = 0; i < flat.size(); ++i) flat[i] = scene.param(i);
+    return flat;
+}
+
+sgs_scene* upload_scene(const Scene& scene, std::vector<double>& flat) {
+    scene.check_homogeneous();
+    flat = flat_params(scene);
+    sgs_scene_desc d{};
+    d.count = scene.gaussians.size();
+    if (d.count) {
+        d.kind = static_cast<int32_t>(kind_of(scene.gaussians.front().color));
+        d.sh_degree = stored_degree(scene.gaussians.front().color);
+    }
+    d.dtype = SGS_F64;
+    d.params = flat.empty() ? nullptr : flat.data();
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) d.shared_axes[3 * r + c] = scene.shared_axes(r, c);
+    for (int k = 0; k < 3; ++k) d.background[k] = scene.background[k];
+    sgs_scene* s = nullptr;
+    check(sgs_scene_upload(context(), &d, &s));
+    return s;
+}
+
+void check_image_shapes(const Image& a, const Image& b) {
+    if (!a.same_shape(b)) throw InvalidArgument("image dimensions do not match");
+}
+}  // namespace
+
+double SceneGradients::flat(const Scene& scene, std::size_t flat_index) const {
+    const std::size_t stride = scene.params_per_gaussian();
+    if (stride == 0 || flat_index >= scene.total_params()) throw InvalidArgument("gradient index out of range");
+    const GaussianGrad& g = gaussians[flat_index / stride];
+    const int slot = static_cast<int>(flat_index % stride);
+    if (slot < 3) return g.position[slot];
+    if (slot < 7) return g.rotation[slot - 3];
+    if (slot < 10) return g.log_scale[slot - 7];
+    if (slot == 10) return g.opacity_logit;
+    return g.color[static_cast<std::size_t>(slot - 11)];
+}
+
+void SceneGradients::add_scaled(const SceneGradients& other, double scale) {
+    for (std::size_t i = 0; i < gaussians.size(); ++i) {
+        gaussians[i].position += scale * other.gaussians[i].position;
+        gaussians[i].rotation += scale * other.gaussians[i].rotation;
+        gaussians[i].log_scale += scale * other.gaussians[i].log_scale;
+        gaussians[i].opacity_logit += scale * other.gaussians[i].opacity_logit;
+        for (std::size_t k = 0; k < gaussians[i].color.size(); ++k)
+            gaussians[i].color[k] += scale * other.gaussians[i].color[k];
+    }
+}
+
+SceneGradients backward(const Scene& scene, const Camera& cam, const RenderConfig& cfg, const Image& upstream) {
+    if (upstream.width != cam.width || upstream.height != cam.height || upstream.channels != 3)
+        throw InvalidArgument("upstream image dimensions do not match the render output");
+    SceneGradients grads;
+    grads.gaussians.resize(scene.gaussians.size());
+    for (std::size_t i = 0; i < scene.gaussians.size(); ++i)
+        grads.gaussians[i].color.assign(static_cast<std::size_t>(param_count(scene.gaussians[i].color)), 0.0);
+    std::vector<double> flat;
+    sgs_scene* s = upload_scene(scene, flat);
+    std::vector<double> g(flat.size());
+    const sgs_camera c = to_c(cam);
+    const sgs_render_config k = to_c(cfg);
+    const int st = sgs_backward(context(), s, &c, &k, upstream.data.data(), SGS_HOST, g.empty() ? nullptr : g.data());
+    sgs_scene_free(s);
+    check(st);
+    const std::size_t stride = scene.params_per_gaussian();
+    for (std::size_t i = 0; i < scene.gaussians.size(); ++i) {
+        GaussianGrad& o = grads.gaussians[i];
+        const double* p = g.data() + i * stride;
+        o.position = Vec3(p[0], p[1], p[2]);
+        o.rotation = Vec4(p[3], p[4], p[5], p[6]);
+        o.log_scale = Vec3(p[7], p[8], p[9]);
+        o.opacity_logit = p[10];
+        for (std::size_t k2 = 0; k2 < o.color.size(); ++k2) o.color[k2] = p[11 + k2];
+    }
+    return grads;
+}
+
+double fd_gradient(const Scene& scene, const Camera& cam, const RenderConfig& cfg, const Image& upstream,
+                   std::size_t param_index, double h) {
+    if (h <= 0.0) throw InvalidArgument("finite-difference step must be positive");
+    auto objective = [&](const Scene& s) {
+        RenderResult r = render(s, cam, cfg);
+        double total = 0.0;
+        for (std::size_t i = 0; i < r.image.size(); ++i) total += r.image.data[i] * upstream.data[i];
+        return total;
+    };
+    Scene probe = scene;
+    const double original = probe.param(param_index);
+    probe.set_param(param_index, original + h);
+    const double hi = objective(probe);
+    probe.set_param(param_index, original - h);
+    const double lo = objective(probe);
+    return (hi - lo) / (2.0 * h);
+}
+
+double psnr(const Image& a, const Image& b) {
+    check_image_shapes(a, b);
+    double out = 0.0;
+    check(sgs_psnr(context(), a.data.data(), b.data.data(), a.width, a.height, a.channels, SGS_F64, SGS_HOST, &out));
+    return out;
+}
+
+double ssim(const Image& a, const Image& b) {
+    check_image_shapes(a, b);
+    double out = 0.0;
+    check(sgs_ssim(context(), a.data.data(), b.data.data(), a.width, a.height, a.channels, SGS_F64, SGS_HOST, &out,
+                   nullptr));
+    return out;
+}
+
+SsimResult ssim_with_grad(const Image& a, const Image& b) {
+    check_image_shapes(a, b);
+    SsimResult r;
+    r.grad_a = Image(a.width, a.height, a.channels);
+    check(sgs_ssim(context(), a.data.data(), b.data.data(), a.width, a.height, a.channels, SGS_F64, SGS_HOST,
+                   &r.value, r.grad_a.data.data()));
+    return r;
 }
 
 }  // namespace sgsplat

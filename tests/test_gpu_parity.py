@@ -295,3 +295,28 @@ def test_pipeline_variants_are_bitwise_equal(env):
     finally:
         a_ds.free()
         b_ds.free()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["configB_small_override1", "configB_small_adaptive", "models_mixed",
+                                  "models_sg1", "models_sg3", "models_sh", "tile13_stop1e-2", "tile8"])
+def test_exact_mode_matches_reference_to_fp64_rounding(case):
+    """sgs_render_f64: the reference's FP64 compositing over the same lists; images
+    match the committed reference goldens to FP64 rounding (1e-12), far inside the
+    1e-3 bar of the FP32 path."""
+    if case not in GOLDEN_CASES:
+        pytest.skip(case)
+    scene_f, cam_o, cfg_o, golden = load_golden(case)
+    scene = sg.Scene(scene_f.kind, scene_f.degree, scene_f.params, scene_f.axes, scene_f.background)
+    cam = sg.Camera._from_c(sg._capi.sgs_camera.from_buffer_copy(bytes(cam_o)))
+    r = sg.Renderer(0)
+    ds = r.upload(scene)
+    try:
+        rgb, T = r.render_f64(ds, cam, tile_size=cfg_o.tile_size,
+                              thresholds=(cfg_o.degree_threshold_lo, cfg_o.degree_threshold_hi),
+                              degree_override=cfg_o.override_degree if cfg_o.has_override else -1,
+                              early_stop=cfg_o.early_stop_transmittance)
+    finally:
+        ds.free()
+    assert np.abs(rgb - golden["image"]).max() <= 1e-12
+    assert np.abs(T - golden["T"].reshape(T.shape)).max() <= 1e-12
