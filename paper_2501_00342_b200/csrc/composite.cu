@@ -37,7 +37,6 @@ namespace sgs {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBatch = 256;
 
 // The reference's FP64 decision for one (pixel, splat) pair (raster.cpp:165-176).
 __device__ __noinline__ bool exact_alpha(const FrameConsts* __restrict__ fc, uint32_t g, int px, int py,
@@ -114,7 +113,7 @@ __device__ __forceinline__ float fast_alpha(float m2, float lop) {
 
 // GROUP records per ILP group; MINB min resident CTAs per SM (register cap).
 // Selected at run time by SGS_K7_GROUP / SGS_K7_MINB for tuning.
-template <int kGroup, int MINB>
+template <int kGroup, int MINB, int kBatchT>
 __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
@@ -129,9 +128,12 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
     // Slot kBatch of the current buffer is a null record (never contributes) that pads
     // the compacted lists to whole groups.
-    __shared__ float4 sRaw[2][kBatch + 1][4];
-    __shared__ float4 sF[kBatch];  // (lmx, lmy, ext_x, ext_y)
-    __shared__ uint16_t sIdx[kThreads / 32][kBatch + 8];
+    constexpr int kBatch = kBatchT;
+    constexpr int kPer = kBatch / kThreads;  // records staged per thread per batch
+    extern __shared__ float4 k7_smem[];
+    float4(*sRaw)[kBatch + 1][4] = reinterpret_cast<float4(*)[kBatch + 1][4]>(k7_smem);
+    float4* sF = k7_smem + 2 * (kBatch + 1) * 4;  // (lmx, lmy, ext_x, ext_y)
+    uint16_t(*sIdx)[kBatch + 8] = reinterpret_cast<uint16_t(*)[kBatch + 8]>(sF + kBatch);
     __shared__ unsigned long long s_red[2][kThreads / 32];
     __shared__ uint32_t s_item;
 
@@ -207,23 +209,31 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     // batch ahead in shared memory via cp.async, so the dependent key -> record
     // gather of batch b+1 overlaps the walk of batch b.
     const int t = threadIdx.x;
-    uint32_t g_next = 0;  // gaussian index of this thread's record in the next batch
-    if (start + t < end) g_next = static_cast<uint32_t>(__ldg(&keys[start + t]));
-    if (start + t < end) {
-        stage_record(rec, colour, g_next, sRaw[0][t]);
+    uint32_t g_next[kPer], g_cur[kPer];  // gaussian indices of this thread's records (next / current batch)
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+        const uint32_t k = start + t + h * kThreads;
+        g_next[h] = k < end ? static_cast<uint32_t>(__ldg(&keys[k])) : 0u;
+        if (k < end) stage_record(rec, colour, g_next[h], sRaw[0][t + h * kThreads]);
     }
     asm volatile("cp.async.commit_group;\n" ::);
-    uint32_t g_cur = g_next;
-    if (start + kBatch + t < end) g_next = static_cast<uint32_t>(__ldg(&keys[start + kBatch + t]));
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+        g_cur[h] = g_next[h];
+        const uint32_t k = start + kBatch + t + h * kThreads;
+        g_next[h] = k < end ? static_cast<uint32_t>(__ldg(&keys[k])) : 0u;
+    }
     int buf = 0;
 
     for (uint32_t base = start; base < end; base += kBatch) {
         asm volatile("cp.async.wait_group 0;\n" ::);
         if (__syncthreads_count(!P.done) == 0) break;
-        {
-            // convert this thread's record of the current batch
-            if (base + t < end) {
-                float4* r = sRaw[buf][t];
+#pragma unroll
+        for (int h = 0; h < kPer; ++h) {
+            // convert this thread's records of the current batch
+            const int rt = t + h * kThreads;
+            if (base + rt < end) {
+                float4* r = sRaw[buf][rt];
                 const double2 m = *reinterpret_cast<const double2*>(&r[0]);
                 const float4 q1 = r[1];  // ca, cb2, cc, lop
                 const float4 q2 = r[2];  // cut, guard, ext_x, ext_y
@@ -231,19 +241,17 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
                 const float lmx = static_cast<float>(m.x - px0), lmy = static_cast<float>(m.y - py0);
                 r[0] = make_float4(lmx, lmy, q1.x, q1.y);
                 r[1] = make_float4(q1.z, q2.x + q2.y, q2.x - q2.y, q1.w);
-                r[2] = make_float4(q3.x, q3.y, q3.z, __uint_as_float(g_cur));
-                sF[t] = make_float4(lmx, lmy, q2.z, q2.w);
+                r[2] = make_float4(q3.x, q3.y, q3.z, __uint_as_float(g_cur[h]));
+                sF[rt] = make_float4(lmx, lmy, q2.z, q2.w);
             }
             // prefetch the next batch's record, then the key after it
-            const uint32_t kn = base + kBatch + t;
-            if (kn < end) {
-                stage_record(rec, colour, g_next, sRaw[buf ^ 1][t]);
-            }
-            asm volatile("cp.async.commit_group;\n" ::);
-            g_cur = g_next;
-            if (kn + kBatch < end) g_next = static_cast<uint32_t>(__ldg(&keys[kn + kBatch]));
-            buf ^= 1;
+            const uint32_t kn = base + kBatch + rt;
+            if (kn < end) stage_record(rec, colour, g_next[h], sRaw[buf ^ 1][rt]);
+            g_cur[h] = g_next[h];
+            g_next[h] = kn + kBatch < end ? static_cast<uint32_t>(__ldg(&keys[kn + kBatch])) : 0u;
         }
+        asm volatile("cp.async.commit_group;\n" ::);
+        buf ^= 1;
         __syncthreads();
         const uint32_t nb = min(static_cast<uint32_t>(kBatch), end - base);
         const float4(*R)[4] = sRaw[buf ^ 1];  // the batch converted above (+ null record)
@@ -403,20 +411,38 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
     }();
     // persistent grid: resident CTAs only
     const unsigned grid = 148u * static_cast<unsigned>(minb);
-#define SGS_K7(G, M)                                                                                         \
-    composite_kernel<G, M><<<grid, kThreads, 0, stream>>>(                                                   \
-        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, rgb, T, state, processed, tile_done, \
-        tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap)
-    if (group == 8 && minb == 2)
-        SGS_K7(8, 2);
+    static const int batch = [] {
+        const char* e = std::getenv("SGS_K7_BATCH");
+        return e && std::atoi(e) == 512 ? 512 : 256;
+    }();
+    auto smem_for = [](int bt) {
+        return static_cast<size_t>(2 * (bt + 1) * 4 + bt) * sizeof(float4) +
+               static_cast<size_t>(kThreads / 32) * (bt + 8) * sizeof(uint16_t);
+    };
+#define SGS_K7(G, M, B)                                                                                       \
+    do {                                                                                                      \
+        static const bool attr_ = [] {                                                                        \
+            cudaFuncSetAttribute(composite_kernel<G, M, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                 static_cast<int>(2 * (B + 1) * 4 * 16 + B * 16 + (kThreads / 32) * (B + 8) * 2)); \
+            return true;                                                                                      \
+        }();                                                                                                  \
+        (void)attr_;                                                                                          \
+        composite_kernel<G, M, B><<<grid, kThreads, smem_for(B), stream>>>(                                   \
+            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, rgb, T, state, processed, tile_done, \
+            tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap); \
+    } while (0)
+    if (batch == 512)
+        SGS_K7(4, 2, 512);
+    else if (group == 8 && minb == 2)
+        SGS_K7(8, 2, 256);
     else if (group == 2 && minb == 2)
-        SGS_K7(2, 2);
+        SGS_K7(2, 2, 256);
     else if (group == 4 && minb == 3)
-        SGS_K7(4, 3);
+        SGS_K7(4, 3, 256);
     else if (group == 2 && minb == 3)
-        SGS_K7(2, 3);
+        SGS_K7(2, 3, 256);
     else
-        SGS_K7(4, 2);
+        SGS_K7(4, 2, 256);
 #undef SGS_K7
 }
 
