@@ -320,3 +320,52 @@ def test_exact_mode_matches_reference_to_fp64_rounding(case):
         ds.free()
     assert np.abs(rgb - golden["image"]).max() <= 1e-12
     assert np.abs(T - golden["T"].reshape(T.shape)).max() <= 1e-12
+
+
+def _adversarial(orc, name):
+    """Scenes that drive the rare paths of the frame pipeline."""
+    rng = np.random.default_rng(4242)
+    if name == "ties":  # 600 splats at one depth: a fine bucket > 64 -> 64-bit CUB depth sort
+        f = orc.synth(3000, 11, "mixed", 2, ls=(-4.0, -3.0))
+        f.params[:600, 0:3] = f.params[600, 0:3]  # identical positions: identical depth keys
+        cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
+        return f, cam, make_config(16, degree_override=1)
+    if name == "spike":  # 60k of 70k splats in a thin depth slab: a coarse bucket > 4096 -> retry
+        f = orc.synth(70_000, 12, "sg3", 0, ls=(-5.5, -4.5))
+        f.params[:60_000, 0:3] = f.params[0, 0:3] + rng.uniform(-1e-9, 1e-9, size=(60_000, 3))
+        cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 200, 150, 180.0)
+        return f, cam, make_config(16)
+    if name == "huge":  # splats covering every tile: cooperative emission, arena regrowth
+        f = orc.synth(5000, 13, "sh", 1, ls=(-1.0, 0.2))
+        cam = orc.orbit_camera([0, 0, 0], 3.0, 0.3, 0.2, 256, 256, 240.0)
+        return f, cam, make_config(8)
+    if name == "culled":  # the camera looks away: V = 0, background only
+        f = orc.synth(2000, 14, "sg1", 0, ls=(-4.0, -3.0))
+        f.background = np.array([0.3, 0.6, 0.9])
+        cam = orc.orbit_camera([0, 0, 40.0], 3.0, 0.0, 0.0, 64, 48, 60.0)
+        return f, cam, make_config(16)
+    if name == "tile32":  # 32x32 tiles: four pixel chunks per tile in K7
+        f = orc.synth(8000, 15, "mixed", 2, ls=(-4.0, -2.8))
+        cam = orc.orbit_camera([0, 0, 0], 3.0, 1.0, 0.1, 150, 110, 130.0)
+        return f, cam, make_config(32)
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["ties", "spike", "huge", "culled", "tile32"])
+def test_adversarial_scenes_vs_restatement(renderer, orc, name):
+    f, ocam, cfg = _adversarial(orc, name)
+    ref_rgb, ref_T = orc.render(f, ocam, cfg)
+    scene, cam = to_scene(f), to_cam(ocam)
+    ds = renderer.upload(scene)
+    try:
+        kw = cfg_kwargs(cfg)
+        got = renderer.tile_grid(ds, cam, **kw)
+        want = orc.tile_grid(f, ocam, cfg)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)  # depth order and every tile list
+        rgb, T = renderer.render(ds, cam, early_stop=cfg.early_stop_transmittance, **kw)
+        check_image(rgb, T, ref_rgb, ref_T)
+        rgb64, T64 = renderer.render_f64(ds, cam, early_stop=cfg.early_stop_transmittance, **kw)
+        assert np.abs(rgb64 - ref_rgb).max() <= 1e-12 and np.abs(T64 - ref_T).max() <= 1e-12
+    finally:
+        ds.free()
