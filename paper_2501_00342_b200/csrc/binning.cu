@@ -300,6 +300,21 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     }
 }
 
+// Per-frame counters without the copy engines: the init is a kernel, and the final
+// block is written straight into mapped pinned host memory, so the readback never
+// queues behind the host frame copies on the D2H engine.
+__global__ void counters_init_kernel(Counters* __restrict__ c) {
+    const int t = threadIdx.x;
+    if (t < 16) reinterpret_cast<unsigned long long*>(c)[t] = (t == 0 || t == 5) ? ~0ULL : 0ULL;  // err, kmin
+}
+
+__global__ void counters_publish_kernel(const Counters* __restrict__ d, Counters* __restrict__ h_mapped) {
+    const int t = threadIdx.x;
+    if (t < 16)
+        reinterpret_cast<volatile unsigned long long*>(h_mapped)[t] = reinterpret_cast<const unsigned long long*>(d)[t];
+    __threadfence_system();
+}
+
 __global__ void tile_ranges_kernel(const unsigned long long* __restrict__ count,
                                    const unsigned long long* __restrict__ keys, uint2* __restrict__ ranges) {
     const uint64_t p = *count;
@@ -375,6 +390,12 @@ void launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* b
     cudaMemsetAsync(status, 0, (grid + 1) * sizeof(unsigned long long), stream);
     bin_emit_kernel<<<grid, kBinThreads, bitmap_smem(done, ntile), stream>>>(rb, re, bmeta, brect, done, tiles_x,
                                                                              ntile, keys, capacity, status, ctr);
+}
+
+void launch_counters_init(Counters* c, cudaStream_t stream) { counters_init_kernel<<<1, 32, 0, stream>>>(c); }
+
+void launch_counters_publish(const Counters* d, Counters* h_mapped, cudaStream_t stream) {
+    counters_publish_kernel<<<1, 32, 0, stream>>>(d, h_mapped);
 }
 
 }  // namespace sgs

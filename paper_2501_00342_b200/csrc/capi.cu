@@ -99,11 +99,20 @@ struct Lane {
     DevBuf keys_a, keys_b, iota, order, rec, colour, rects, ntiles, brect, bmeta, counts, offsets;
     DevBuf buckets;  // K2 bucket histogram / offsets / cursors
     DevBuf work;     // K7 work list (+ 3 control words)
-    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist, out_rgb, out_T;
+    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist;
+    // host-output frames: kOutSlots device buffers per lane drained by the lane's copy
+    // stream, so the lane renders its next views while earlier ones cross PCIe
+    static constexpr int kOutSlots = 3;
+    DevBuf out_rgb[kOutSlots], out_T[kOutSlots];
+    cudaEvent_t rendered[kOutSlots] = {};
+    cudaEvent_t copied[kOutSlots] = {};
+    cudaStream_t copy_stream = nullptr;
+    int out_slot = 0;
     uint64_t iota_n = 0;
     uint64_t tkey_cap = 0;  // tile keys per buffer (grow-only, sized from observed P)
     Counters* d_ctr = nullptr;
-    Counters* h_ctr = nullptr;
+    Counters* h_ctr = nullptr;      // mapped pinned host block the frame's counters land in
+    Counters* h_ctr_dev = nullptr;  // its device-side address
     FrameConsts* d_consts = nullptr;  // per-frame scene planes + camera for K7's FP64 path
     FrameConsts* h_consts = nullptr;  // pinned staging copy
     cudaEvent_t ev[8] = {};
@@ -147,6 +156,12 @@ struct sgs_context {
     bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
+    bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
+    struct TraceRec {
+        int lane;
+        cudaEvent_t ev[3];  // frame start, compositing done, host copies done
+    };
+    std::vector<TraceRec> trace_recs;
     DevBuf metrics;  // PSNR / SSIM scratch (inputs staged from host, maps, partial sums)
     DevBuf bwd;      // backward scratch (FP64 splats, ranks, per-entry partials, staging)
     uint64_t own_launches = 0, lib_launches = 0;
@@ -354,17 +369,18 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     SGS_CUDA(L.tkeys_b.ensure(L.tkey_cap * 8));
     float* d_rgb = j.d_rgb;
     float* d_T = j.d_T;
+    const int slot = L.out_slot;
     if (j.h_rgb) {
-        SGS_CUDA(L.out_rgb.ensure(npx * 3 * sizeof(float)));
-        d_rgb = L.out_rgb.as<float>();
+        SGS_CUDA(L.out_rgb[slot].ensure(npx * 3 * sizeof(float)));
+        d_rgb = L.out_rgb[slot].as<float>();
     }
     if (j.h_T) {
-        SGS_CUDA(L.out_T.ensure(npx * sizeof(float)));
-        d_T = L.out_T.as<float>();
+        SGS_CUDA(L.out_T[slot].ensure(npx * sizeof(float)));
+        d_T = L.out_T[slot].as<float>();
     }
 
     if (part != kPost) {
-        SGS_CUDA(cudaMemcpyAsync(L.d_ctr, ctx->h_ctr_init, sizeof(Counters), cudaMemcpyHostToDevice, s));
+        launch_counters_init(L.d_ctr, s);
         if (mode == kRender) {
             // the pinned staging block is per lane; the lane's previous frame has
             // completed (finish_frame waits for it before the lane is reused)
@@ -378,6 +394,19 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         }
     }
     if (part == kPre) return SGS_OK;
+    const bool host_out = mode == kRender && (j.h_rgb || j.h_T);
+    if (host_out) {
+        // the slot's previous frame must have left the device before K7 rewrites it
+        SGS_CUDA(cudaStreamWaitEvent(s, L.copied[slot], 0));
+        L.out_slot = (slot + 1) % Lane::kOutSlots;
+    }
+    sgs_context::TraceRec* tr = nullptr;
+    if (ctx->trace && mode == kRender) {
+        ctx->trace_recs.push_back(sgs_context::TraceRec{static_cast<int>(&L - ctx->lane), {}});
+        tr = &ctx->trace_recs.back();
+        for (auto& e : tr->ev) SGS_CUDA(cudaEventCreate(&e));
+        SGS_CUDA(cudaEventRecord(tr->ev[0], s));
+    }
 
     // K1
     if (part == kAll) {
@@ -390,7 +419,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[1], s));
     }
     if (mode == kProjectOnly) {
-        SGS_CUDA(cudaMemcpyAsync(L.h_ctr, L.d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+        launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
         SGS_CUDA(cudaEventRecord(L.done, s));
         return SGS_OK;
     }
@@ -467,6 +496,15 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[5], s));
         L.last_order = order;
         L.last_tile_keys = tkeys;
+        // Every decision the host acts on (device errors, depth-tie and tile-key
+        // overflows) is final once the last chunk is binned: without stats the
+        // counters are published here, so the host settles this frame and queues the
+        // lane's next one while K7 still runs (K7 itself raises nothing).
+        const bool early_done = mode == kRender && !j.stats && c == nchunks - 1;
+        if (early_done) {
+            launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
+            SGS_CUDA(cudaEventRecord(L.done, s));
+        }
         // K7
         if (mode == kRender) {
             launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), tkeys, L.rec.as<SplatRec>(),
@@ -490,13 +528,22 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         }
     }
     if (timing) SGS_CUDA(cudaEventRecord(L.ev[7], s));
-    if (mode == kRender) {
-        if (j.h_rgb)
-            SGS_CUDA(cudaMemcpyAsync(j.h_rgb, d_rgb, npx * 3 * sizeof(float), cudaMemcpyDeviceToHost, s));
-        if (j.h_T) SGS_CUDA(cudaMemcpyAsync(j.h_T, d_T, npx * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (tr) SGS_CUDA(cudaEventRecord(tr->ev[1], s));
+    if (host_out) {
+        cudaStream_t cs = L.copy_stream;
+        SGS_CUDA(cudaEventRecord(L.rendered[slot], s));
+        SGS_CUDA(cudaStreamWaitEvent(cs, L.rendered[slot], 0));
+        if (j.h_rgb) SGS_CUDA(cudaMemcpyAsync(j.h_rgb, d_rgb, npx * 3 * sizeof(float), cudaMemcpyDeviceToHost, cs));
+        if (j.h_T) SGS_CUDA(cudaMemcpyAsync(j.h_T, d_T, npx * sizeof(float), cudaMemcpyDeviceToHost, cs));
+        SGS_CUDA(cudaEventRecord(L.copied[slot], cs));
+        if (tr) SGS_CUDA(cudaEventRecord(tr->ev[2], cs));
+    } else if (tr) {
+        SGS_CUDA(cudaEventRecord(tr->ev[2], s));
     }
-    SGS_CUDA(cudaMemcpyAsync(L.h_ctr, L.d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-    SGS_CUDA(cudaEventRecord(L.done, s));
+    if (mode != kRender || j.stats) {  // (otherwise published before K7)
+        launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
+        SGS_CUDA(cudaEventRecord(L.done, s));
+    }
     return SGS_OK;
 }
 
@@ -973,13 +1020,20 @@ sgs_status sgs_create(int device, sgs_context** out) {
     for (Lane& L : ctx->lane) {
         SGS_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
         SGS_CUDA(cudaMalloc(&L.d_ctr, sizeof(Counters)));
-        SGS_CUDA(cudaMallocHost(&L.h_ctr, sizeof(Counters)));
+        SGS_CUDA(cudaHostAlloc(&L.h_ctr, sizeof(Counters), cudaHostAllocMapped));
+        SGS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&L.h_ctr_dev), L.h_ctr, 0));
         SGS_CUDA(cudaMalloc(&L.d_consts, sizeof(FrameConsts)));
         SGS_CUDA(cudaMallocHost(&L.h_consts, sizeof(FrameConsts)));
         for (auto& ev : L.ev) SGS_CUDA(cudaEventCreate(&ev));
         SGS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
         SGS_CUDA(cudaEventCreateWithFlags(&L.k1ev, cudaEventDisableTiming));
+        SGS_CUDA(cudaStreamCreateWithFlags(&L.copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < Lane::kOutSlots; ++k) {
+            SGS_CUDA(cudaEventCreateWithFlags(&L.rendered[k], cudaEventDisableTiming));
+            SGS_CUDA(cudaEventCreateWithFlags(&L.copied[k], cudaEventDisableTiming));
+        }
     }
+    if (const char* e = std::getenv("SGS_TRACE")) ctx->trace = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
     if (const char* e = std::getenv("SGS_K1_GROUP"))
         ctx->k1_group = std::min(std::max(std::atoi(e), 1), std::min(kMaxK1Views, kLanes / 2));
@@ -1008,7 +1062,7 @@ void sgs_destroy(sgs_context* ctx) {
         if (L.stream) cudaStreamSynchronize(L.stream);
         for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.iota, &L.order, &L.rec, &L.colour, &L.rects, &L.ntiles, &L.brect,
                           &L.bmeta, &L.counts, &L.offsets, &L.buckets, &L.work, &L.tkeys_a, &L.tkeys_b, &L.ranges,
-                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist, &L.out_rgb, &L.out_T})
+                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist})
             b->release();
         if (L.d_ctr) cudaFree(L.d_ctr);
         if (L.h_ctr) cudaFreeHost(L.h_ctr);
@@ -1018,6 +1072,16 @@ void sgs_destroy(sgs_context* ctx) {
             if (ev) cudaEventDestroy(ev);
         if (L.done) cudaEventDestroy(L.done);
         if (L.k1ev) cudaEventDestroy(L.k1ev);
+        if (L.copy_stream) {
+            cudaStreamSynchronize(L.copy_stream);
+            cudaStreamDestroy(L.copy_stream);
+        }
+        for (int k = 0; k < Lane::kOutSlots; ++k) {
+            L.out_rgb[k].release();
+            L.out_T[k].release();
+            if (L.rendered[k]) cudaEventDestroy(L.rendered[k]);
+            if (L.copied[k]) cudaEventDestroy(L.copied[k]);
+        }
         if (L.stream) cudaStreamDestroy(L.stream);
     }
     ctx->metrics.release();
@@ -1038,7 +1102,10 @@ sgs_status sgs_set_stream(sgs_context* ctx, void* stream) {
 sgs_status sgs_synchronize(sgs_context* ctx) {
     if (!ctx) return fail(SGS_ERR_INVALID_ARGUMENT, "null context");
     SGS_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (Lane& L : ctx->lane) SGS_CUDA(cudaStreamSynchronize(L.stream));
+    for (Lane& L : ctx->lane) {
+        SGS_CUDA(cudaStreamSynchronize(L.stream));
+        SGS_CUDA(cudaStreamSynchronize(L.copy_stream));
+    }
     return SGS_OK;
 }
 
@@ -1255,9 +1322,29 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
         }
     }
     sgs_status sj = join_lanes(ctx, lanes);
+    // host frames are complete (or abandoned, on an error) once the copies drained
+    if (host)
+        for (int k = 0; k < lanes; ++k) cudaStreamSynchronize(ctx->lane[k].copy_stream);
+    if (ctx->trace && !ctx->trace_recs.empty()) {
+        cudaDeviceSynchronize();
+        const cudaEvent_t t0 = ctx->trace_recs.front().ev[0];
+        std::fprintf(stderr, "sgs trace: frame lane start_ms composite_done_ms copies_done_ms\n");
+        int f = 0;
+        for (auto& r : ctx->trace_recs) {
+            float a = 0, b = 0, c = 0;
+            cudaEventElapsedTime(&a, t0, r.ev[0]);
+            cudaEventElapsedTime(&b, t0, r.ev[1]);
+            cudaEventElapsedTime(&c, t0, r.ev[2]);
+            std::fprintf(stderr, "sgs trace: %d %d %.3f %.3f %.3f\n", f++, r.lane, a, b, c);
+        }
+        for (auto& r : ctx->trace_recs)
+            for (auto& e : r.ev) cudaEventDestroy(e);
+        ctx->trace_recs.clear();
+    }
     if (st != SGS_OK) return st;
     if (sj != SGS_OK) return sj;
-    if (host) SGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    // frames are settled once binned; the call returns with every frame composited
+    SGS_CUDA(cudaStreamSynchronize(ctx->stream));
     return SGS_OK;
 }
 

@@ -207,6 +207,8 @@ void launch_psnr_sum(const void* a, const void* b, bool f64, size_t n, double* s
                      cudaStream_t s);
 void launch_ssim(const void* a, const void* b, bool f64, int W, int H, int C, double* scratch, double* d_sum,
                  double* grad, cudaStream_t s);
+void launch_counters_init(Counters* c, cudaStream_t stream);
+void launch_counters_publish(const Counters* d, Counters* h_mapped, cudaStream_t stream);
 void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
                         int4* brect, uint2* bmeta, cudaStream_t stream);
 void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
