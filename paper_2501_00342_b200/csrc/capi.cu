@@ -100,6 +100,7 @@ struct Lane {
     DevBuf buckets;  // K2 bucket histogram / offsets / cursors
     DevBuf work;     // K7 work list (+ 3 control words)
     DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist;
+    DevBuf tb_cnt, tb_cur, tb_items, tb_ctl;  // tile-major binning (tile_bins.cu)
     // host-output frames: kOutSlots device buffers per lane drained by the lane's copy
     // stream, so the lane renders its next views while earlier ones cross PCIe
     static constexpr int kOutSlots = 3;
@@ -131,6 +132,7 @@ struct Lane {
         DebugSplat* d_debug = nullptr;
         int mode = 0;
         bool wide = false;
+        bool rank_major = false;  // rank-major binning + tile sort (a tile list overflowed tile_bins)
         float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
     } job;
     bool busy = false;
@@ -153,9 +155,11 @@ struct sgs_context {
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
     bool two_level = true;   // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
+    bool tile_major = false;  // tile-major binning (tile_bins.cu, SGS_BIN=tile; measured slower)
     bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
+    int skip = 0;  // SGS_SKIP (timing probe only; renders garbage): 1 = no K7, 2 = no K1, 4 = no K2
     bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
     struct TraceRec {
         int lane;
@@ -246,6 +250,7 @@ enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
 // run_frame_once results besides sgs_status
 constexpr int kRetryWide = 100;  // a run of equal 32-bit depth keys: redo with 64-bit keys
 constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, redo
+constexpr int kRetryRankMajor = 102;  // a tile list exceeded tile_bins' sort capacity: redo rank-major
 
 // Depth chunking: the first chunk holds the
 // nearest ceil(N / kFirstChunkDiv) ranks; tiles whose pixels all terminate inside it
@@ -347,6 +352,10 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     const uint64_t npx = static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height);
     const bool timing = j.stats && j.stats->want_timing;
     const uint64_t n1 = std::max<uint64_t>(n, 1);
+    {
+        const char* e = std::getenv("SGS_SKIP");  // read per frame: set it after warm-up
+        ctx->skip = e ? std::atoi(e) : 0;
+    }
     j.ms_bin = j.ms_tsort = j.ms_comp = 0;
 
     SGS_CUDA(L.keys_a.ensure(n1 * 8));
@@ -409,7 +418,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     }
 
     // K1
-    if (part == kAll) {
+    if (part == kAll && !(ctx->skip & 2)) {
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
         launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
                           L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
@@ -427,7 +436,9 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     // K2
     const uint32_t* order = L.iota.as<uint32_t>();
     bool gathered = false;
-    if (n > 1) {
+    if (n > 1 && (ctx->skip & 4)) {
+        gathered = true;
+    } else if (n > 1) {
         sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order, &gathered);
         if (st != SGS_OK) return st;
     }
@@ -451,7 +462,8 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         SGS_CUDA(L.tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
         SGS_CUDA(L.pix_state.ensure(npx * sizeof(PixelState)));
         SGS_CUDA(L.pix_walked.ensure(npx * sizeof(uint32_t)));
-        SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
+        if (!(ctx->skip & 1))  // (probe: with K7 skipped the last frame's finished tiles stand in)
+            SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
     }
     bounds.push_back(n);
     const int nchunks = static_cast<int>(bounds.size()) - 1;
@@ -462,37 +474,67 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
     SGS_CUDA(L.work.ensure((work_cap + 4) * sizeof(uint32_t)));
     const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
+    // the tile-major binning serves the compositor; the parity dumps, the backward and
+    // a frame whose tile list overflowed its sort use the rank-major keys
+    const bool tile_major = mode == kRender && ctx->tile_major && !j.rank_major;
+    const int pchunks = composite_pixel_chunks(cfg->tile_size);
+    if (tile_major) {
+        SGS_CUDA(L.tb_cnt.ensure(std::max<uint64_t>(ntile, 1) * 4));
+        SGS_CUDA(L.tb_cur.ensure(std::max<uint64_t>(ntile, 1) * 4));
+        SGS_CUDA(L.tb_items.ensure(std::max<uint64_t>(ntile, 1) * 4 * 4));  // 4 size classes
+        SGS_CUDA(L.tb_ctl.ensure(64));
+        SGS_CUDA(cudaMemsetAsync(L.tb_cnt.ptr, 0, ntile * 4, s));  // tb_scan re-zeroes it per chunk
+    }
     for (int c = 0; c < nchunks; ++c) {
         const uint64_t rb = bounds[c], re = bounds[c + 1];
         const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
-        // K3 + K4
-        if (ctx->fused_bin) {
-            SGS_CUDA(L.counts.ensure(bin_emit_status_bytes(n)));
-            launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
-                            static_cast<int>(ntile), L.tkeys_a.as<unsigned long long>(), L.tkey_cap,
-                            L.counts.as<unsigned long long>(), L.d_ctr, s);
+        const uint32_t* list = nullptr;  // the compositor's per-tile lists of Gaussian indices
+        int kstride = 1;
+        const unsigned long long* tkeys = nullptr;
+        if (tile_major) {
+            // B1-B4 (tile_bins.cu); also builds K7's work list
+            launch_tile_bins(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+                             static_cast<int>(ntile), pchunks, c == 0, c == nchunks - 1, order,
+                             L.tb_cnt.as<uint32_t>(), L.tb_cur.as<uint32_t>(), L.ranges.as<uint2>(),
+                             L.tkeys_a.as<uint32_t>(), L.tkey_cap, L.work.as<uint32_t>(),
+                             static_cast<uint32_t>(work_cap), L.work.as<uint32_t>() + work_cap,
+                             L.tb_items.as<uint32_t>(), L.tb_ctl.as<uint32_t>(), L.d_ctr, s);
+            SGS_CUDA(cudaGetLastError());
+            ctx->own_launches += 4;
+            list = L.tkeys_a.as<uint32_t>();
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
+        } else {
+            // K3 + K4
+            if (ctx->fused_bin) {
+                SGS_CUDA(L.counts.ensure(bin_emit_status_bytes(n)));
+                launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+                                static_cast<int>(ntile), L.tkeys_a.as<unsigned long long>(), L.tkey_cap,
+                                L.counts.as<unsigned long long>(), L.d_ctr, s);
+                SGS_CUDA(cudaGetLastError());
+                ctx->own_launches += 1;
+            } else {
+                sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
+                if (st != SGS_OK) return st;
+                launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
+                                      L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
+                                      L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
+                SGS_CUDA(cudaGetLastError());
+                if (re > rb) ctx->own_launches += 1;
+            }
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
+            // K5 (device-sized stable radix sort on the tile bits)
+            tkeys =
+                tile_sort(L.tkeys_a.as<unsigned long long>(), L.tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
+                          L.sort_hist.as<uint32_t>(), s, &ctx->own_launches);
+            // K6
+            SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
+            launch_tile_ranges(d_pc, tkeys, L.ranges.as<uint2>(), s);
             SGS_CUDA(cudaGetLastError());
             ctx->own_launches += 1;
-        } else {
-            sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
-            if (st != SGS_OK) return st;
-            launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
-                                  L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
-                                  L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
-            SGS_CUDA(cudaGetLastError());
-            if (re > rb) ctx->own_launches += 1;
+            list = reinterpret_cast<const uint32_t*>(tkeys);  // low words of (tile << 32 | index)
+            kstride = 2;
         }
-        if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
-        // K5 (device-sized stable radix sort on the tile bits)
-        const unsigned long long* tkeys =
-            tile_sort(L.tkeys_a.as<unsigned long long>(), L.tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
-                      L.sort_hist.as<uint32_t>(), s, &ctx->own_launches);
-        // K6
-        SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
-        launch_tile_ranges(d_pc, tkeys, L.ranges.as<uint2>(), s);
-        SGS_CUDA(cudaGetLastError());
-        ctx->own_launches += 1;
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[5], s));
         L.last_order = order;
         L.last_tile_keys = tkeys;
@@ -506,14 +548,15 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             SGS_CUDA(cudaEventRecord(L.done, s));
         }
         // K7
-        if (mode == kRender) {
-            launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), tkeys, L.rec.as<SplatRec>(),
+        if (mode == kRender && !(ctx->skip & 1)) {
+            launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, kstride, L.rec.as<SplatRec>(),
                              L.colour.as<float4>(), bg, d_rgb, d_T, L.pix_state.as<PixelState>(),
                              L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
                              L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1, L.d_ctr,
-                             j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + work_cap, s);
+                             j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + work_cap,
+                             tile_major, s);
             SGS_CUDA(cudaGetLastError());
-            ctx->own_launches += 2;  // work list + persistent compositor
+            ctx->own_launches += tile_major ? 1 : 2;  // (+ the work list kernel)
         }
         if (timing) {
             SGS_CUDA(cudaEventRecord(L.ev[6], s));
@@ -556,6 +599,7 @@ int check_frame(Lane& L) {
     if (hc.err != ~0ULL) return device_error(hc.err, j.scene, &j.cfg);
     if (j.mode == kProjectOnly) return SGS_OK;
     if (hc.tie_overflow && !j.wide) return kRetryWide;
+    if (hc.list_overflow && !j.rank_major) return kRetryRankMajor;
     if (hc.key_overflow) {
         L.tkey_cap = hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024;
         return kRetryGrow;
@@ -588,8 +632,9 @@ sgs_status finish_frame(sgs_context* ctx, Lane& L) {
     if (!L.busy) return SGS_OK;
     for (int attempt = 0; attempt < 4; ++attempt) {
         const int rc = check_frame(L);
-        if (rc == kRetryWide || rc == kRetryGrow) {
+        if (rc == kRetryWide || rc == kRetryGrow || rc == kRetryRankMajor) {
             if (rc == kRetryWide) L.job.wide = true;
+            if (rc == kRetryRankMajor) L.job.rank_major = true;
             sgs_status st = enqueue_frame(ctx, L);
             if (st != SGS_OK) {
                 L.busy = false;
@@ -1038,6 +1083,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
     if (const char* e = std::getenv("SGS_K1_GROUP"))
         ctx->k1_group = std::min(std::max(std::atoi(e), 1), std::min(kMaxK1Views, kLanes / 2));
     if (const char* e = std::getenv("SGS_BIN_FUSED")) ctx->fused_bin = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SGS_BIN")) ctx->tile_major = std::strcmp(e, "tile") == 0;
     if (const char* e = std::getenv("SGS_DEPTH_SORT")) ctx->two_level = std::strcmp(e, "bucket") != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
@@ -1062,7 +1108,8 @@ void sgs_destroy(sgs_context* ctx) {
         if (L.stream) cudaStreamSynchronize(L.stream);
         for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.iota, &L.order, &L.rec, &L.colour, &L.rects, &L.ntiles, &L.brect,
                           &L.bmeta, &L.counts, &L.offsets, &L.buckets, &L.work, &L.tkeys_a, &L.tkeys_b, &L.ranges,
-                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist})
+                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist, &L.tb_cnt, &L.tb_cur,
+                          &L.tb_items, &L.tb_ctl})
             b->release();
         if (L.d_ctr) cudaFree(L.d_ctr);
         if (L.h_ctr) cudaFreeHost(L.h_ctr);

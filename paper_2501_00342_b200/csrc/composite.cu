@@ -116,7 +116,7 @@ __device__ __forceinline__ float fast_alpha(float m2, float lop) {
 template <int kGroup, int MINB, int kBatchT>
 __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
-    const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
     const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
     float* __restrict__ out_rgb, float* __restrict__ out_T,
     PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
 #pragma unroll
     for (int h = 0; h < kPer; ++h) {
         const uint32_t k = start + t + h * kThreads;
-        g_next[h] = k < end ? static_cast<uint32_t>(__ldg(&keys[k])) : 0u;
+        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
         if (k < end) stage_record(rec, colour, g_next[h], sRaw[0][t + h * kThreads]);
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     for (int h = 0; h < kPer; ++h) {
         g_cur[h] = g_next[h];
         const uint32_t k = start + kBatch + t + h * kThreads;
-        g_next[h] = k < end ? static_cast<uint32_t>(__ldg(&keys[k])) : 0u;
+        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
     }
     int buf = 0;
 
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
             const uint32_t kn = base + kBatch + rt;
             if (kn < end) stage_record(rec, colour, g_next[h], sRaw[buf ^ 1][rt]);
             g_cur[h] = g_next[h];
-            g_next[h] = kn + kBatch < end ? static_cast<uint32_t>(__ldg(&keys[kn + kBatch])) : 0u;
+            g_next[h] = kn + kBatch < end ? __ldg(&keys[static_cast<size_t>(kn + kBatch) * kstride]) : 0u;
         }
         asm volatile("cp.async.commit_group;\n" ::);
         buf ^= 1;
@@ -363,6 +363,360 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     }  // persistent loop
 }
 
+// ---------------------------------------------------------------------------
+// K7, two pixels per thread (the default). One CTA of 128 threads per (tile,
+// 256-pixel chunk); on 16x16 tiles warp w owns rows 4w..4w+3 and a thread the two
+// horizontally adjacent pixels (2c, 2c+1) of one row, so a record's dy terms
+// (dy, 2b dy, c dy^2) and its shared-memory reads serve both pixels. m2 is formed
+// per pixel exactly as in composite_kernel (same operations, same rounding), and
+// the blend chain drops the per-step termination bookkeeping: transmittance only
+// decreases, so "the pixel stopped before this splat" is T < stop, tested in the
+// chain; the splat that stopped it is found afterwards by replaying the group's T
+// products (bit-identical), which happens once per pixel.
+constexpr int kThreads2 = 128;
+
+struct Pix {
+    float T, r, g, b;
+};
+
+// One blend step (raster.cpp:177-180) unless the pixel already stopped.
+__device__ __forceinline__ void step2(Pix& P, float alpha, const float4& C, float stop) {
+    const float a = P.T < stop ? 0.0f : alpha;
+    const float w = a * P.T;
+    P.r = fmaf(C.x, w, P.r);
+    P.g = fmaf(C.y, w, P.g);
+    P.b = fmaf(C.z, w, P.b);
+    P.T = P.T * (1.0f - a);
+}
+
+// m2 of both pixels; same formula as mahal2 (dy terms shared when on one row).
+template <bool kSameRow>
+__device__ __forceinline__ void mahal2x2(const float4& A, float Bx, float fcx0, float fcy0, float fcx1, float fcy1,
+                                         float& m0, float& m1) {
+    const float dy0 = fcy0 - A.y;
+    const float b0 = A.w * dy0, c0 = Bx * dy0 * dy0;
+    const float dx0 = fcx0 - A.x, dx1 = fcx1 - A.x;
+    m0 = fmaf(fmaf(A.z, dx0, b0), dx0, c0);
+    if constexpr (kSameRow) {
+        m1 = fmaf(fmaf(A.z, dx1, b0), dx1, c0);
+    } else {
+        const float dy1 = fcy1 - A.y;
+        m1 = fmaf(fmaf(A.z, dx1, A.w * dy1), dx1, Bx * dy1 * dy1);
+    }
+}
+
+template <int kGroup, int MINB, bool kSameRow>
+__global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
+    const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
+    const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
+    float* __restrict__ out_rgb, float* __restrict__ out_T,
+    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
+    uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
+    const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
+    uint32_t work_cap) {
+    // shared layout as composite_kernel (batch 256, null record at slot kBatch)
+    constexpr int kBatch = 256;
+    constexpr int kPer = kBatch / kThreads2;
+    constexpr int kWarps = kThreads2 / 32;
+    extern __shared__ float4 k7_smem[];
+    float4(*sRaw)[kBatch + 1][4] = reinterpret_cast<float4(*)[kBatch + 1][4]>(k7_smem);
+    float4* sF = k7_smem + 2 * (kBatch + 1) * 4;
+    uint16_t(*sIdx)[kBatch + 8] = reinterpret_cast<uint16_t(*)[kBatch + 8]>(sF + kBatch);
+    __shared__ unsigned long long s_red[2][kWarps];
+    __shared__ uint32_t s_item;
+
+    if (threadIdx.x < 8) {
+        const int b = threadIdx.x >> 2, c = threadIdx.x & 3;
+        sRaw[b][kBatch][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const uint32_t n_long = work_count[0], n_items = work_count[0] + work_count[1];
+    // T < stop is the stop test; a threshold above 1 stops every pixel right after
+    // its first blended splat, exactly as 1.0 does (T starts at 1 and every blended
+    // splat has alpha >= 1/255), and keeps T < stop false for a pixel that has not
+    // blended anything yet.
+    const float stop = cfg.early_stop > 1.0f ? 1.0f : cfg.early_stop;
+    for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(work_next, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    __syncthreads();
+    if (item >= n_items) break;
+    const uint32_t witem = item < n_long ? work[item] : work[work_cap - 1 - (item - n_long)];
+    const int ts = cfg.tile_size;
+    const int tile = static_cast<int>(witem / nchunks);
+    const int chunk = static_cast<int>(witem - static_cast<uint32_t>(tile) * nchunks);
+    const uint2 range = ranges[tile];
+    const uint32_t start = range.x, end = range.y;
+    const bool touched = !first && ((tile_touched[tile >> 5] >> (tile & 31)) & 1u);
+    const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
+    const int px0 = tx * ts, py0 = ty * ts;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int lx0, ly0, lx1, ly1;
+    bool in0, in1;
+    if (ts == 16) {
+        lx0 = (lane & 7) * 2;
+        lx1 = lx0 + 1;
+        ly0 = ly1 = warp * 4 + (lane >> 3);
+        in0 = in1 = true;
+    } else {
+        const int p = chunk * 256 + 2 * static_cast<int>(threadIdx.x);
+        lx0 = p % ts;
+        ly0 = p / ts;
+        lx1 = (p + 1) % ts;
+        ly1 = (p + 1) / ts;
+        in0 = p < ts * ts;
+        in1 = p + 1 < ts * ts;
+    }
+    const int pxa = px0 + lx0, pya = py0 + ly0, pxb = px0 + lx1, pyb = py0 + ly1;
+    const bool v0 = in0 && pxa < W && pya < H, v1 = in1 && pxb < W && pyb < H;
+    const size_t pix0 = v0 ? static_cast<size_t>(pya) * W + pxa : 0;
+    const size_t pix1 = v1 ? static_cast<size_t>(pyb) * W + pxb : 0;
+    const float fcx0 = static_cast<float>(lx0) + 0.5f, fcy0 = static_cast<float>(ly0) + 0.5f;
+    const float fcx1 = static_cast<float>(lx1) + 0.5f, fcy1 = static_cast<float>(ly1) + 0.5f;
+    Pix P0{1.f, 0.f, 0.f, 0.f}, P1{1.f, 0.f, 0.f, 0.f};
+    uint32_t walked0 = 0, walked1 = 0;
+    if (touched) {
+        if (v0) {
+            const PixelState st = state[pix0];
+            P0 = Pix{st.T, st.r, st.g, st.b};
+            walked0 = processed_io[pix0];
+        }
+        if (v1) {
+            const PixelState st = state[pix1];
+            P1 = Pix{st.T, st.r, st.g, st.b};
+            walked1 = processed_io[pix1];
+        }
+    }
+    bool live0 = v0 && !(P0.T < stop), live1 = v1 && !(P1.T < stop);
+    uint32_t processed0 = live0 ? end - start : 0u, processed1 = live1 ? end - start : 0u;
+    int term0 = -1, term1 = -1;  // compacted-walk position of the stopping splat in this batch
+
+    float wx0 = 1e30f, wx1 = -1e30f, wy0 = 1e30f, wy1 = -1e30f;
+    if (live0) wx0 = fminf(wx0, fcx0), wx1 = fmaxf(wx1, fcx0), wy0 = fminf(wy0, fcy0), wy1 = fmaxf(wy1, fcy0);
+    if (live1) wx0 = fminf(wx0, fcx1), wx1 = fmaxf(wx1, fcx1), wy0 = fminf(wy0, fcy1), wy1 = fmaxf(wy1, fcy1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        wx0 = fminf(wx0, __shfl_xor_sync(0xffffffffu, wx0, o));
+        wx1 = fmaxf(wx1, __shfl_xor_sync(0xffffffffu, wx1, o));
+        wy0 = fminf(wy0, __shfl_xor_sync(0xffffffffu, wy0, o));
+        wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
+    }
+    uint32_t guard_hits = 0;
+    uint16_t* idx = sIdx[warp];
+
+    const int t = threadIdx.x;
+    uint32_t g_next[kPer], g_cur[kPer];
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+        const uint32_t k = start + t + h * kThreads2;
+        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
+        if (k < end) stage_record(rec, colour, g_next[h], sRaw[0][t + h * kThreads2]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+        g_cur[h] = g_next[h];
+        const uint32_t k = start + kBatch + t + h * kThreads2;
+        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
+    }
+    int buf = 0;
+
+    for (uint32_t base = start; base < end; base += kBatch) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        if (__syncthreads_count(live0 || live1) == 0) break;
+#pragma unroll
+        for (int h = 0; h < kPer; ++h) {
+            const int rt = t + h * kThreads2;
+            if (base + rt < end) {
+                float4* r = sRaw[buf][rt];
+                const double2 m = *reinterpret_cast<const double2*>(&r[0]);
+                const float4 q1 = r[1];
+                const float4 q2 = r[2];
+                const float4 q3 = r[3];
+                const float lmx = static_cast<float>(m.x - px0), lmy = static_cast<float>(m.y - py0);
+                r[0] = make_float4(lmx, lmy, q1.x, q1.y);
+                r[1] = make_float4(q1.z, q2.x + q2.y, q2.x - q2.y, q1.w);
+                r[2] = make_float4(q3.x, q3.y, q3.z, __uint_as_float(g_cur[h]));
+                sF[rt] = make_float4(lmx, lmy, q2.z, q2.w);
+            }
+            const uint32_t kn = base + kBatch + rt;
+            if (kn < end) stage_record(rec, colour, g_next[h], sRaw[buf ^ 1][rt]);
+            g_cur[h] = g_next[h];
+            g_next[h] = kn + kBatch < end ? __ldg(&keys[static_cast<size_t>(kn + kBatch) * kstride]) : 0u;
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        buf ^= 1;
+        __syncthreads();
+        const uint32_t nb = min(static_cast<uint32_t>(kBatch), end - base);
+        const float4(*R)[4] = sRaw[buf ^ 1];
+        int cnt = 0;
+        if (__any_sync(0xffffffffu, live0 || live1)) {
+            for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                bool hit = false;
+                if (j < nb) {
+                    const float4 F = sF[j];
+                    hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit) idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
+                cnt += __popc(m);
+            }
+        }
+        if (lane < kGroup) idx[cnt + lane] = kBatch;
+        __syncwarp();
+        for (int q = 0; q < cnt && (live0 || live1); q += kGroup) {
+            float a0[kGroup], a1[kGroup];
+            bool guard = false;
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+                const int j = idx[q + k];
+                const float4 A = R[j][0];
+                const float4 B = R[j][1];
+                float m0, m1;
+                mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
+                guard |= (m0 <= B.y && m0 >= B.z) || (m1 <= B.y && m1 >= B.z);
+                a0[k] = m0 < B.z ? fast_alpha(m0, B.w) : 0.0f;
+                a1[k] = m1 < B.z ? fast_alpha(m1, B.w) : 0.0f;
+            }
+            if (!guard) {
+                const float T0s = P0.T, T1s = P1.T;
+#pragma unroll
+                for (int k = 0; k < kGroup; ++k) {
+                    const float4 C = R[idx[q + k]][2];
+                    step2(P0, a0[k], C, stop);
+                    step2(P1, a1[k], C, stop);
+                }
+                if (live0 && P0.T < stop) {  // stopped inside this group: find the splat
+                    float tt = T0s;
+#pragma unroll
+                    for (int k = 0; k < kGroup; ++k) {
+                        tt = tt * (1.0f - a0[k]);
+                        if (tt < stop) {
+                            term0 = q + k;
+                            break;
+                        }
+                    }
+                    live0 = false;
+                }
+                if (live1 && P1.T < stop) {
+                    float tt = T1s;
+#pragma unroll
+                    for (int k = 0; k < kGroup; ++k) {
+                        tt = tt * (1.0f - a1[k]);
+                        if (tt < stop) {
+                            term1 = q + k;
+                            break;
+                        }
+                    }
+                    live1 = false;
+                }
+            } else {
+                // a pair inside the guard band: one record at a time, banded pairs in FP64
+                for (int k = 0; k < kGroup && q + k < cnt && (live0 || live1); ++k) {
+                    const int j = idx[q + k];
+                    const float4 A = R[j][0];
+                    const float4 B = R[j][1];
+                    const float4 C = R[j][2];
+                    float m0, m1;
+                    mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
+                    if (live0 && m0 <= B.y) {
+                        float a = a0[k];
+                        bool use = true;
+                        if (m0 >= B.z) {
+                            ++guard_hits;
+                            use = exact_alpha(fc, __float_as_uint(C.w), pxa, pya, &a);
+                        }
+                        if (use) {
+                            step2(P0, a, C, stop);
+                            if (P0.T < stop) {
+                                term0 = q + k;
+                                live0 = false;
+                            }
+                        }
+                    }
+                    if (live1 && m1 <= B.y) {
+                        float a = a1[k];
+                        bool use = true;
+                        if (m1 >= B.z) {
+                            ++guard_hits;
+                            use = exact_alpha(fc, __float_as_uint(C.w), pxb, pyb, &a);
+                        }
+                        if (use) {
+                            step2(P1, a, C, stop);
+                            if (P1.T < stop) {
+                                term1 = q + k;
+                                live1 = false;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (term0 >= 0) {
+            processed0 = base + idx[term0] + 1 - start;
+            term0 = -2;
+        }
+        if (term1 >= 0) {
+            processed1 = base + idx[term1] + 1 - start;
+            term1 = -2;
+        }
+        __syncthreads();
+    }
+
+    asm volatile("cp.async.wait_all;\n" ::);
+    const bool all_done = __syncthreads_and(!live0 && !live1) != 0;
+    const bool finalize = last || all_done;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const bool v = e ? v1 : v0;
+        if (!v) continue;
+        const Pix& P = e ? P1 : P0;
+        const size_t pix = e ? pix1 : pix0;
+        if (finalize) {
+            if (out_rgb) {
+                out_rgb[pix * 3 + 0] = P.r + P.T * bg.x;
+                out_rgb[pix * 3 + 1] = P.g + P.T * bg.y;
+                out_rgb[pix * 3 + 2] = P.b + P.T * bg.z;
+            }
+            if (out_T) out_T[pix] = P.T;
+        } else {
+            state[pix] = PixelState{P.r, P.g, P.b, P.T};
+            processed_io[pix] = (e ? walked1 : walked0) + (e ? processed1 : processed0);
+        }
+    }
+    if (!last && all_done && threadIdx.x == 0) atomicOr(&tile_done[tile >> 5], 1u << (tile & 31));
+    if (!finalize && !touched && threadIdx.x == 0) atomicOr(&tile_touched[tile >> 5], 1u << (tile & 31));
+    if (want_stats) {
+        unsigned long long e = 0;
+        if (finalize && v0) e = max(e, static_cast<unsigned long long>(walked0 + processed0));
+        if (finalize && v1) e = max(e, static_cast<unsigned long long>(walked1 + processed1));
+        unsigned long long h = guard_hits;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+            h += __shfl_xor_sync(0xffffffffu, h, o);
+        }
+        if (lane == 0) {
+            s_red[0][warp] = e;
+            s_red[1][warp] = h;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long em = 0, hs = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                em = max(em, s_red[0][w]);
+                hs += s_red[1][w];
+            }
+            if (em) atomicAdd(&ctr->block_entries, em);
+            if (hs) atomicAdd(&ctr->guard_hits, hs);
+        }
+    }
+    __syncthreads();
+    }  // persistent loop
+}
+
 // Work list of a depth chunk: (tile, pixel chunk) items that still need K7 -- every
 // unfinished tile in the last chunk (it writes the final pixels), otherwise only
 // tiles with entries in this chunk. Tiles with long lists are queued from the front
@@ -391,16 +745,18 @@ int composite_pixel_chunks(int ts) {
 }
 
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
-                      const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
+                      const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
                       const float4* colour, float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
                       uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
-                      bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream) {
+                      bool want_stats, uint32_t* work, uint32_t* wctl, bool work_ready, cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
     const uint32_t ntile = static_cast<uint32_t>(cfg.tiles_x) * static_cast<uint32_t>(cfg.tiles_y);
     const uint32_t cap = ntile * static_cast<uint32_t>(nchunks);
-    cudaMemsetAsync(wctl, 0, 3 * sizeof(uint32_t), stream);
-    build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, first ? 1 : 0, last ? 1 : 0,
-                                                             ntile, nchunks, cap, work, wctl);
+    if (!work_ready) {  // (the tile-major binning's scan builds the list itself)
+        cudaMemsetAsync(wctl, 0, 3 * sizeof(uint32_t), stream);
+        build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, first ? 1 : 0, last ? 1 : 0,
+                                                                 ntile, nchunks, cap, work, wctl);
+    }
     static const int group = [] {
         const char* e = std::getenv("SGS_K7_GROUP");
         return e ? std::atoi(e) : 4;
@@ -428,9 +784,30 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
         }();                                                                                                  \
         (void)attr_;                                                                                          \
         composite_kernel<G, M, B><<<grid, kThreads, smem_for(B), stream>>>(                                   \
-            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, rgb, T, state, processed, tile_done, \
+            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, rgb, T, state, processed, tile_done, \
             tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap); \
     } while (0)
+    static const int px = [] {
+        const char* e = std::getenv("SGS_K7_PX");
+        return e && std::atoi(e) == 1 ? 1 : 2;
+    }();
+    if (px == 2) {
+        const unsigned grid2 = 148u * 4u;
+        const size_t smem2 = smem_for(256) - static_cast<size_t>(kThreads / 32 - kThreads2 / 32) * (256 + 8) * 2;
+        static const bool attr2 = [smem2] {
+            cudaFuncSetAttribute(composite2_kernel<4, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem2));
+            cudaFuncSetAttribute(composite2_kernel<4, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem2));
+            return true;
+        }();
+        (void)attr2;
+        auto k = cfg.tile_size == 16 ? composite2_kernel<4, 4, true> : composite2_kernel<4, 4, false>;
+        k<<<grid2, kThreads2, smem2, stream>>>(fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg,
+                                               rgb, T, state, processed, tile_done, tile_touched, first ? 1 : 0,
+                                               last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap);
+        return;
+    }
     if (batch == 512)
         SGS_K7(4, 2, 512);
     else if (group == 8 && minb == 2)

@@ -119,7 +119,8 @@ struct Counters {
     unsigned long long chunk_entries;  // P of the chunk in flight (clamped to capacity)
     unsigned long long culled_cursor;  // K2 scatter slot for culled splats
     unsigned long long big_buckets;    // K2 buckets queued for the warp sort
-    unsigned long long pad[2];
+    unsigned long long list_overflow;  // a tile list exceeded the tile-major sort's capacity
+    unsigned long long pad;
 };
 static_assert(sizeof(Counters) == 128, "counters block");
 
@@ -231,12 +232,20 @@ unsigned long long* tile_sort(unsigned long long* a, unsigned long long* b, cons
 // K7 over one depth chunk. first/last select state init / final output; tile_done and
 // state may be null when the frame is a single chunk.
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
-                      const uint2* ranges, const unsigned long long* keys, const SplatRec* rec,
+                      const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
                       const float4* colour, float3 bg, float* rgb, float* T,
                       PixelState* state, uint32_t* processed, uint32_t* tile_done, uint32_t* tile_touched,
                       bool first,
                       bool last, Counters* counters, bool want_stats, uint32_t* work, uint32_t* wctl,
-                      cudaStream_t stream);
+                      bool work_ready, cudaStream_t stream);
+// Tile-major binning of one depth chunk (tile_bins.cu): counts, scan (+ the K7 work
+// list), scatter, per-tile sort; list[ranges[t]] holds Gaussian indices.
+size_t tb_sort_smem_bytes();
+void launch_tile_bins(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
+                      int tiles_x, int ntile, int pchunks, bool first, bool last, const uint32_t* order,
+                      uint32_t* cnt, uint32_t* cur, uint2* ranges, uint32_t* list, uint64_t capacity,
+                      uint32_t* work, uint32_t work_cap, uint32_t* wctl, uint32_t* sitems, uint32_t* sctl,
+                      Counters* ctr, cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
 
 }  // namespace sgs

@@ -265,11 +265,11 @@ def test_depth_chunking_is_bitwise_neutral():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"SGS_BIN_FUSED": "1"}, {"SGS_DEPTH_SORT": "bucket"}, {"SGS_LANES": "1"},
+@pytest.mark.parametrize("env", [{"SGS_BIN": "tile"}, {"SGS_K7_PX": "1"}, {"SGS_K7_PX": "1", "SGS_K7_GROUP": "2"}, {"SGS_DEPTH_SORT": "bucket"}, {"SGS_LANES": "1"},
                                  {"SGS_K1_GROUP": "1"}, {"SGS_K1_GROUP": "2"}, {"SGS_K1_GROUP": "3"},
-                                 {"SGS_K1_MINB": "1"}, {"SGS_K7_GROUP": "2"}, {"SGS_K7_BATCH": "512"}])
+                                 {"SGS_K1_MINB": "1"}, {"SGS_K7_PX": "1", "SGS_K7_BATCH": "512"}])
 def test_pipeline_variants_are_bitwise_equal(env):
-    """Every alternative pipeline path (fused look-back binning, one-level bucket
+    """Every alternative pipeline path (tile-major binning with per-tile sorts, fused look-back binning, one-level bucket
     depth sort, a single lane, other K1 / K7 instantiations) renders the same bits,
     image, transmittance and E_t, as the default path, over a batch of views."""
     scene = sg.synth_scene(150_000, "mixed", 91, log_scale_range=(-5.0, -3.5))
@@ -339,6 +339,17 @@ def _adversarial(orc, name):
         f = orc.synth(5000, 13, "sh", 1, ls=(-1.0, 0.2))
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.3, 0.2, 256, 256, 240.0)
         return f, cam, make_config(8)
+    if name == "longlist":  # 20k splats in a few tiles: a list above tile_bins' sort cap -> rank-major retry
+        f = orc.synth(20_000, 16, "mixed", 2, ls=(-6.0, -5.0))
+        f.params[:, 0:3] = (f.params[0, 0:3] + rng.uniform(-2e-3, 2e-3, size=(20_000, 3))).astype(np.float32)
+        cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
+        return f, cam, make_config(16, degree_override=1)
+    if name == "midlist":  # 9k splats over 4 tiles: lists of thousands through the block radix sort
+        f = orc.synth(9000, 17, "mixed", 2, ls=(-5.5, -4.5))
+        f.params[:, 0:3] = (f.params[0, 0:3] + rng.uniform(-0.02, 0.02, size=(9000, 3))).astype(np.float32)
+        f.params[:, 10] = -4.0  # low opacity: pixels do not terminate, whole lists are walked
+        cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
+        return f, cam, make_config(16, degree_override=1)
     if name == "culled":  # the camera looks away: V = 0, background only
         f = orc.synth(2000, 14, "sg1", 0, ls=(-4.0, -3.0))
         f.background = np.array([0.3, 0.6, 0.9])
@@ -351,7 +362,7 @@ def _adversarial(orc, name):
     raise KeyError(name)
 
 
-@pytest.mark.parametrize("name", ["ties", "spike", "huge", "culled", "tile32"])
+@pytest.mark.parametrize("name", ["ties", "spike", "huge", "longlist", "midlist", "culled", "tile32"])
 def test_adversarial_scenes_vs_restatement(renderer, orc, name):
     f, ocam, cfg = _adversarial(orc, name)
     ref_rgb, ref_T = orc.render(f, ocam, cfg)
@@ -369,3 +380,29 @@ def test_adversarial_scenes_vs_restatement(renderer, orc, name):
         assert np.abs(rgb64 - ref_rgb).max() <= 1e-12 and np.abs(T64 - ref_T).max() <= 1e-12
     finally:
         ds.free()
+
+
+@pytest.mark.parametrize("name", ["longlist", "midlist", "huge"])
+def test_tile_major_binning_on_long_lists(orc, name):
+    """The optional tile-major binning (SGS_BIN=tile) sorts every tile list in shared
+    memory: lists of thousands go through its block radix sort, and a list above its
+    capacity (longlist: 20k entries in one tile) makes the host redo the frame
+    rank-major. Both must render the default path's bits."""
+    f, ocam, cfg = _adversarial(orc, name)
+    scene, cam = to_scene(f), to_cam(ocam)
+    os.environ["SGS_BIN"] = "tile"
+    try:
+        tile = sg.Renderer(0)
+    finally:
+        os.environ.pop("SGS_BIN")
+    base = sg.Renderer(0)
+    a_ds, b_ds = base.upload(scene), tile.upload(scene)
+    try:
+        kw = cfg_kwargs(cfg)
+        a = base.render(a_ds, cam, early_stop=cfg.early_stop_transmittance, stats=True, **kw)
+        b = tile.render(b_ds, cam, early_stop=cfg.early_stop_transmittance, stats=True, **kw)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert a[2].block_entries == b[2].block_entries and a[2].tile_entries == b[2].tile_entries
+    finally:
+        a_ds.free()
+        b_ds.free()
