@@ -70,7 +70,10 @@ __global__ void count_tiles_kernel(uint64_t rb, uint64_t re, const uint2* __rest
     const uint64_t r = rb + k;
     if (r < re) {
         uint32_t c = bmeta[r].y;
-        if (c && done_bytes) c = live_tiles(brect[r], done, tiles_x);
+        if (done_bytes) {
+            const int4 rc = brect[r];  // issued with the bmeta load (stale when c == 0, unused)
+            if (c) c = live_tiles(rc, done, tiles_x);
+        }
         counts[k] = c;
     } else if (r == re) {
         counts[k] = 0;
@@ -100,12 +103,14 @@ __global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint2* __restri
     int4 rc = make_int4(0, -1, 0, -1);
     unsigned long long off = 0;
     if (r < re) {
-        const uint2 m = bmeta[r];
-        g = m.x;
-        area = m.y;
-        if (area) {
+        // the scanned counts tell which ranks emit anything: in late chunks most
+        // ranks only cover finished tiles and are skipped before their rect is read
+        off = offsets[k];
+        if (offsets[k + 1] != off) {
+            const uint2 m = bmeta[r];
+            g = m.x;
+            area = m.y;
             rc = brect[r];
-            off = offsets[k];
         }
     }
     const uint32_t w = static_cast<uint32_t>(rc.y - rc.x + 1);

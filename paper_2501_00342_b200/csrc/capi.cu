@@ -472,7 +472,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
                                   static_cast<float>(scene->meta.background[2]));
     const int tile_bits = std::max(1, ceil_log2(ntile));
     const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
-    SGS_CUDA(L.work.ensure((work_cap + 4) * sizeof(uint32_t)));
+    SGS_CUDA(L.work.ensure((2 * work_cap + 8) * sizeof(uint32_t)));  // lists, 8 control words, background items
     const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
     // the tile-major binning serves the compositor; the parity dumps, the backward and
     // a frame whose tile list overflowed its sort use the rank-major keys
@@ -494,7 +494,8 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         const unsigned long long* tkeys = nullptr;
         if (tile_major) {
             // B1-B4 (tile_bins.cu); also builds K7's work list
-            launch_tile_bins(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+            launch_tile_bins(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
+                             L.tile_done.as<uint32_t>() + (ntile + 31) / 32, kp.tiles_x,
                              static_cast<int>(ntile), pchunks, c == 0, c == nchunks - 1, order,
                              L.tb_cnt.as<uint32_t>(), L.tb_cur.as<uint32_t>(), L.ranges.as<uint2>(),
                              L.tkeys_a.as<uint32_t>(), L.tkey_cap, L.work.as<uint32_t>(),

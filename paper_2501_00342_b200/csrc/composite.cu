@@ -111,6 +111,36 @@ __device__ __forceinline__ float fast_alpha(float m2, float lop) {
     return fminf(ex2_approx(fmaf(m2, -0.72134752044448170f, lop)), 0.999f);
 }
 
+constexpr int kWorkCtl = 8;
+
+// Background-only (tile, pixel-chunk) items of the last chunk, flat over all CTAs:
+// the pixels of a tile that never received an entry are bg (acc 0 + T 1 * bg).
+template <int NT>
+__device__ __forceinline__ void write_background(int W, int H, const CfgParams& cfg, int nchunks,
+                                                 const uint32_t* __restrict__ work_count, float* __restrict__ out_rgb,
+                                                 float* __restrict__ out_T, float3 bg) {
+    const uint32_t n_bg = work_count[3];
+    const uint32_t* bgl = work_count + kWorkCtl;
+    const int ts = cfg.tile_size;
+    const uint64_t total = static_cast<uint64_t>(n_bg) * 256;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * NT + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * NT) {
+        const uint32_t it = bgl[i >> 8];
+        const int tile = static_cast<int>(it / nchunks), chunk = static_cast<int>(it % nchunks);
+        const int p = chunk * 256 + static_cast<int>(i & 255);
+        if (p >= ts * ts) continue;
+        const int px = (tile % cfg.tiles_x) * ts + p % ts, py = (tile / cfg.tiles_x) * ts + p / ts;
+        if (px >= W || py >= H) continue;
+        const size_t pix = static_cast<size_t>(py) * W + px;
+        if (out_rgb) {
+            out_rgb[pix * 3 + 0] = 0.0f + 1.0f * bg.x;
+            out_rgb[pix * 3 + 1] = 0.0f + 1.0f * bg.y;
+            out_rgb[pix * 3 + 2] = 0.0f + 1.0f * bg.z;
+        }
+        if (out_T) out_T[pix] = 1.0f;
+    }
+}
+
 // GROUP records per ILP group; MINB min resident CTAs per SM (register cap).
 // Selected at run time by SGS_K7_GROUP / SGS_K7_MINB for tuning.
 template <int kGroup, int MINB, int kBatchT>
@@ -361,6 +391,8 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     }
     __syncthreads();
     }  // persistent loop
+    // background-only items (tiles that never received an entry): T = 1, rgb = bg
+    write_background<kThreads>(W, H, cfg, nchunks, work_count, out_rgb, out_T, bg);
 }
 
 // ---------------------------------------------------------------------------
@@ -470,8 +502,8 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     }
     const int pxa = px0 + lx0, pya = py0 + ly0, pxb = px0 + lx1, pyb = py0 + ly1;
     const bool v0 = in0 && pxa < W && pya < H, v1 = in1 && pxb < W && pyb < H;
-    const size_t pix0 = v0 ? static_cast<size_t>(pya) * W + pxa : 0;
-    const size_t pix1 = v1 ? static_cast<size_t>(pyb) * W + pxb : 0;
+    const uint32_t pix0 = v0 ? static_cast<uint32_t>(pya) * W + pxa : 0;  // (W H < 2^32)
+    const uint32_t pix1 = v1 ? static_cast<uint32_t>(pyb) * W + pxb : 0;
     const float fcx0 = static_cast<float>(lx0) + 0.5f, fcy0 = static_cast<float>(ly0) + 0.5f;
     const float fcx1 = static_cast<float>(lx1) + 0.5f, fcy1 = static_cast<float>(ly1) + 0.5f;
     Pix P0{1.f, 0.f, 0.f, 0.f}, P1{1.f, 0.f, 0.f, 0.f};
@@ -566,21 +598,26 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
         }
         if (lane < kGroup) idx[cnt + lane] = kBatch;
         __syncwarp();
-        for (int q = 0; q < cnt && (live0 || live1); q += kGroup) {
-            float a0[kGroup], a1[kGroup];
-            bool guard = false;
+        // Fast groups until one holds a pair inside the guard band; that group is
+        // walked by the cold path below (outside the fast loop, so the FP64 call does
+        // not weigh on the fast loop's registers), then the fast loop resumes.
+        int q = 0;
+        while (q < cnt && (live0 || live1)) {
+            for (; q < cnt && (live0 || live1); q += kGroup) {
+                float a0[kGroup], a1[kGroup];
+                bool guard = false;
 #pragma unroll
-            for (int k = 0; k < kGroup; ++k) {
-                const int j = idx[q + k];
-                const float4 A = R[j][0];
-                const float4 B = R[j][1];
-                float m0, m1;
-                mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
-                guard |= (m0 <= B.y && m0 >= B.z) || (m1 <= B.y && m1 >= B.z);
-                a0[k] = m0 < B.z ? fast_alpha(m0, B.w) : 0.0f;
-                a1[k] = m1 < B.z ? fast_alpha(m1, B.w) : 0.0f;
-            }
-            if (!guard) {
+                for (int k = 0; k < kGroup; ++k) {
+                    const int j = idx[q + k];
+                    const float4 A = R[j][0];
+                    const float4 B = R[j][1];
+                    float m0, m1;
+                    mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
+                    guard |= (m0 <= B.y && m0 >= B.z) || (m1 <= B.y && m1 >= B.z);
+                    a0[k] = m0 < B.z ? fast_alpha(m0, B.w) : 0.0f;
+                    a1[k] = m1 < B.z ? fast_alpha(m1, B.w) : 0.0f;
+                }
+                if (guard) break;
                 const float T0s = P0.T, T1s = P1.T;
 #pragma unroll
                 for (int k = 0; k < kGroup; ++k) {
@@ -612,47 +649,34 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
                     }
                     live1 = false;
                 }
-            } else {
-                // a pair inside the guard band: one record at a time, banded pairs in FP64
-                for (int k = 0; k < kGroup && q + k < cnt && (live0 || live1); ++k) {
-                    const int j = idx[q + k];
-                    const float4 A = R[j][0];
-                    const float4 B = R[j][1];
-                    const float4 C = R[j][2];
-                    float m0, m1;
-                    mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
-                    if (live0 && m0 <= B.y) {
-                        float a = a0[k];
-                        bool use = true;
-                        if (m0 >= B.z) {
-                            ++guard_hits;
-                            use = exact_alpha(fc, __float_as_uint(C.w), pxa, pya, &a);
-                        }
-                        if (use) {
-                            step2(P0, a, C, stop);
-                            if (P0.T < stop) {
-                                term0 = q + k;
-                                live0 = false;
-                            }
-                        }
+            }
+            if (!(q < cnt && (live0 || live1))) break;
+            // the group at q holds a banded pair: one record at a time, banded pairs in FP64
+            for (int k = 0; k < kGroup && q + k < cnt && (live0 || live1); ++k) {
+                const int j = idx[q + k];
+                const float4 A = R[j][0];
+                const float4 B = R[j][1];
+                const float4 C = R[j][2];
+                float m[2];
+                mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m[0], m[1]);
+#pragma unroll 1
+                for (int e = 0; e < 2; ++e) {
+                    Pix& P = e ? P1 : P0;
+                    bool& live = e ? live1 : live0;
+                    if (!live || m[e] > B.y) continue;
+                    float a = m[e] < B.z ? fast_alpha(m[e], B.w) : 0.0f;
+                    if (m[e] >= B.z) {
+                        ++guard_hits;
+                        if (!exact_alpha(fc, __float_as_uint(C.w), e ? pxb : pxa, e ? pyb : pya, &a)) continue;
                     }
-                    if (live1 && m1 <= B.y) {
-                        float a = a1[k];
-                        bool use = true;
-                        if (m1 >= B.z) {
-                            ++guard_hits;
-                            use = exact_alpha(fc, __float_as_uint(C.w), pxb, pyb, &a);
-                        }
-                        if (use) {
-                            step2(P1, a, C, stop);
-                            if (P1.T < stop) {
-                                term1 = q + k;
-                                live1 = false;
-                            }
-                        }
+                    step2(P, a, C, stop);
+                    if (P.T < stop) {
+                        (e ? term1 : term0) = q + k;
+                        live = false;
                     }
                 }
             }
+            q += kGroup;
         }
         if (term0 >= 0) {
             processed0 = base + idx[term0] + 1 - start;
@@ -715,15 +739,21 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     }
     __syncthreads();
     }  // persistent loop
+    // background-only items (tiles that never received an entry): T = 1, rgb = bg
+    write_background<kThreads2>(W, H, cfg, nchunks, work_count, out_rgb, out_T, bg);
 }
 
+// Work buffer: [0, cap) long items from the front, short items from the back;
+// [cap, cap + kWorkCtl) control words (long count, short count, cursor, background
+// count); [cap + kWorkCtl, 2 cap + kWorkCtl) background-only items.
 // Work list of a depth chunk: (tile, pixel chunk) items that still need K7 -- every
 // unfinished tile in the last chunk (it writes the final pixels), otherwise only
 // tiles with entries in this chunk. Tiles with long lists are queued from the front
 // of `work`, the rest from the back, so the persistent CTAs start on the longest.
 __global__ void build_work_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ tile_done,
-                                  int first, int last, uint32_t ntile, int nchunks, uint32_t cap,
-                                  uint32_t* __restrict__ work, uint32_t* __restrict__ wctl) {
+                                  const uint32_t* __restrict__ tile_touched, int first, int last, uint32_t ntile,
+                                  int nchunks, uint32_t cap, uint32_t* __restrict__ work,
+                                  uint32_t* __restrict__ wctl) {
     const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
     if (it >= ntile * static_cast<uint32_t>(nchunks)) return;
     const uint32_t tile = it / nchunks;
@@ -731,6 +761,11 @@ __global__ void build_work_kernel(const uint2* __restrict__ ranges, const uint32
     const uint2 r = ranges[tile];
     const uint32_t len = r.y - r.x;
     if (!last && len == 0) return;
+    if (len == 0 && (first || !((tile_touched[tile >> 5] >> (tile & 31)) & 1u))) {
+        // never received an entry: background pixels, written by the tail loop
+        work[cap + kWorkCtl + atomicAdd(&wctl[3], 1u)] = it;
+        return;
+    }
     if (len >= 1024)
         work[atomicAdd(&wctl[0], 1u)] = it;
     else
@@ -753,9 +788,9 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
     const uint32_t ntile = static_cast<uint32_t>(cfg.tiles_x) * static_cast<uint32_t>(cfg.tiles_y);
     const uint32_t cap = ntile * static_cast<uint32_t>(nchunks);
     if (!work_ready) {  // (the tile-major binning's scan builds the list itself)
-        cudaMemsetAsync(wctl, 0, 3 * sizeof(uint32_t), stream);
-        build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, first ? 1 : 0, last ? 1 : 0,
-                                                                 ntile, nchunks, cap, work, wctl);
+        cudaMemsetAsync(wctl, 0, 4 * sizeof(uint32_t), stream);
+        build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
+                                                                 last ? 1 : 0, ntile, nchunks, cap, work, wctl);
     }
     static const int group = [] {
         const char* e = std::getenv("SGS_K7_GROUP");
@@ -794,18 +829,26 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
     if (px == 2) {
         const unsigned grid2 = 148u * 4u;
         const size_t smem2 = smem_for(256) - static_cast<size_t>(kThreads / 32 - kThreads2 / 32) * (256 + 8) * 2;
-        static const bool attr2 = [smem2] {
-            cudaFuncSetAttribute(composite2_kernel<4, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem2));
-            cudaFuncSetAttribute(composite2_kernel<4, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem2));
-            return true;
-        }();
-        (void)attr2;
-        auto k = cfg.tile_size == 16 ? composite2_kernel<4, 4, true> : composite2_kernel<4, 4, false>;
-        k<<<grid2, kThreads2, smem2, stream>>>(fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg,
-                                               rgb, T, state, processed, tile_done, tile_touched, first ? 1 : 0,
-                                               last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap);
+#define SGS_K7X2(G, ROW)                                                                                      \
+    do {                                                                                                      \
+        static const bool attr_ = [smem2] {                                                                   \
+            cudaFuncSetAttribute(composite2_kernel<G, 4, ROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                 static_cast<int>(smem2));                                                    \
+            return true;                                                                                      \
+        }();                                                                                                  \
+        (void)attr_;                                                                                          \
+        composite2_kernel<G, 4, ROW><<<grid2, kThreads2, smem2, stream>>>(                                     \
+            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, rgb, T, state, processed,  \
+            tile_done, tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl,    \
+            wctl + 2, cap);                                                                                   \
+    } while (0)
+        const bool row = cfg.tile_size == 16;
+        if (group == 2) {
+            if (row) SGS_K7X2(2, true); else SGS_K7X2(2, false);
+        } else {
+            if (row) SGS_K7X2(4, true); else SGS_K7X2(4, false);
+        }
+#undef SGS_K7X2
         return;
     }
     if (batch == 512)

@@ -242,7 +242,7 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
 // list), scatter, per-tile sort; list[ranges[t]] holds Gaussian indices.
 size_t tb_sort_smem_bytes();
 void launch_tile_bins(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                      int tiles_x, int ntile, int pchunks, bool first, bool last, const uint32_t* order,
+                      const uint32_t* touched, int tiles_x, int ntile, int pchunks, bool first, bool last, const uint32_t* order,
                       uint32_t* cnt, uint32_t* cur, uint2* ranges, uint32_t* list, uint64_t capacity,
                       uint32_t* work, uint32_t work_cap, uint32_t* wctl, uint32_t* sitems, uint32_t* sctl,
                       Counters* ctr, cudaStream_t stream);

@@ -41,6 +41,7 @@ constexpr int kGroupThreads = 256;                  // mid lists: 4 groups of 8 
 constexpr int kBitonicCap = 64;
 constexpr int kMaxBitmapTiles = 1 << 18;
 constexpr uint32_t kLongList = 1024;  // compositor: lists this long are scheduled first
+constexpr uint32_t kWorkCtlWords = 8;  // composite.cu kWorkCtl: background items follow the control words
 // sort classes: 0 warp bitonic (<= 64), 1 warp radix (<= 512), 2 group radix
 // (<= 4096), 3 CTA radix (<= kSortCap)
 constexpr uint32_t kClassCap[4] = {kBitonicCap, 32 * kSortPer, kGroupThreads * kSortPer, kSortCap};
@@ -202,13 +203,13 @@ __device__ __forceinline__ uint32_t warp_append(bool take, uint32_t* s_count) {
 // sctl: [k] sort items of class k, [4 + k] their cursor.
 __global__ void __launch_bounds__(kScanThreads) tb_scan_kernel(
     int ntile, int pchunks, uint32_t* __restrict__ cnt, uint32_t* __restrict__ cur, uint2* __restrict__ ranges,
-    const uint32_t* __restrict__ done_g, int first, int last, uint64_t capacity, Counters* __restrict__ ctr,
-    uint32_t* __restrict__ work, uint32_t work_cap, uint32_t* __restrict__ wctl, uint32_t* __restrict__ sitems,
-    uint32_t* __restrict__ sctl) {
+    const uint32_t* __restrict__ done_g, const uint32_t* __restrict__ touched_g, int first, int last,
+    uint64_t capacity, Counters* __restrict__ ctr, uint32_t* __restrict__ work, uint32_t work_cap,
+    uint32_t* __restrict__ wctl, uint32_t* __restrict__ sitems, uint32_t* __restrict__ sctl) {
     __shared__ uint32_t s_warp[33];
-    __shared__ uint32_t s_n[6];  // long, short work items; sort items per class
+    __shared__ uint32_t s_n[7];  // long, short work items; sort items per class; background items
     __shared__ uint32_t s_over;
-    if (threadIdx.x < 6) s_n[threadIdx.x] = 0;
+    if (threadIdx.x < 7) s_n[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_over = 0;
     __syncthreads();
     uint64_t carry = 0;
@@ -239,12 +240,17 @@ __global__ void __launch_bounds__(kScanThreads) tb_scan_kernel(
         }
         // compositor work items (build_work_kernel's rules)
         const bool live = t < ntile && (first || !done(static_cast<uint32_t>(t))) && (last || len > 0);
+        // a tile that never received an entry only writes background (K7's tail loop)
+        const bool bgt = live && len == 0 &&
+                         (first || !((touched_g[static_cast<uint32_t>(t) >> 5] >> (t & 31)) & 1u));
         for (int c = 0; c < pchunks; ++c) {
             const uint32_t item = static_cast<uint32_t>(t) * pchunks + c;
-            const bool lng = live && len >= kLongList;
+            const bool lng = live && !bgt && len >= kLongList;
             const uint32_t pl = warp_append(lng, &s_n[0]);
-            const uint32_t ps = warp_append(live && !lng, &s_n[1]);
+            const uint32_t ps = warp_append(live && !bgt && !lng, &s_n[1]);
+            const uint32_t pb = warp_append(bgt, &s_n[6]);
             if (lng) work[pl] = item;
+            else if (bgt) wctl[kWorkCtlWords + pb] = item;
             else if (live) work[work_cap - 1 - ps] = item;
         }
     }
@@ -253,6 +259,7 @@ __global__ void __launch_bounds__(kScanThreads) tb_scan_kernel(
         wctl[0] = s_n[0];
         wctl[1] = s_n[1];
         wctl[2] = 0;
+        wctl[3] = s_n[6];
         for (int k = 0; k < 4; ++k) {
             sctl[k] = s_n[2 + k];
             sctl[4 + k] = 0;
@@ -514,7 +521,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) tb_sort_kernel(
 size_t tb_sort_smem_bytes() { return static_cast<size_t>(pad(kSortCap) + pad(16 * kSortThreads)) * 4; }
 
 void launch_tile_bins(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                      int tiles_x, int ntile, int pchunks, bool first, bool last, const uint32_t* order,
+                      const uint32_t* touched, int tiles_x, int ntile, int pchunks, bool first, bool last, const uint32_t* order,
                       uint32_t* cnt, uint32_t* cur, uint2* ranges, uint32_t* list, uint64_t capacity,
                       uint32_t* work, uint32_t work_cap, uint32_t* wctl, uint32_t* sitems, uint32_t* sctl,
                       Counters* ctr, cudaStream_t stream) {
@@ -539,8 +546,8 @@ void launch_tile_bins(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* 
     (void)attr;
     tb_pairs_kernel<false><<<grid, kPairThreads, bm + agg, stream>>>(rb, re, static_cast<uint32_t>(per), bmeta,
                                                                       brect, done, tiles_x, ntile, cnt, list, capacity);
-    tb_scan_kernel<<<1, kScanThreads, 0, stream>>>(ntile, pchunks, cnt, cur, ranges, done, first ? 1 : 0,
-                                                   last ? 1 : 0, capacity, ctr, work, work_cap, wctl, sitems, sctl);
+    tb_scan_kernel<<<1, kScanThreads, 0, stream>>>(ntile, pchunks, cnt, cur, ranges, done, touched,
+                                                   first ? 1 : 0, last ? 1 : 0, capacity, ctr, work, work_cap, wctl, sitems, sctl);
     tb_pairs_kernel<true><<<grid, kPairThreads, bm + 2 * agg, stream>>>(rb, re, static_cast<uint32_t>(per), bmeta,
                                                                          brect, done, tiles_x, ntile, cur, list,
                                                                          capacity);

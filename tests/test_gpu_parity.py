@@ -265,7 +265,7 @@ def test_depth_chunking_is_bitwise_neutral():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"SGS_BIN": "tile"}, {"SGS_K7_PX": "1"}, {"SGS_K7_PX": "1", "SGS_K7_GROUP": "2"}, {"SGS_DEPTH_SORT": "bucket"}, {"SGS_LANES": "1"},
+@pytest.mark.parametrize("env", [{"SGS_BIN": "tile"}, {"SGS_K7_PX": "1"}, {"SGS_K7_PX": "1", "SGS_K7_GROUP": "2"}, {"SGS_K7_GROUP": "2"}, {"SGS_DEPTH_SORT": "bucket"}, {"SGS_LANES": "1"},
                                  {"SGS_K1_GROUP": "1"}, {"SGS_K1_GROUP": "2"}, {"SGS_K1_GROUP": "3"},
                                  {"SGS_K1_MINB": "1"}, {"SGS_K7_PX": "1", "SGS_K7_BATCH": "512"}])
 def test_pipeline_variants_are_bitwise_equal(env):
