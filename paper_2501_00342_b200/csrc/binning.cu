@@ -45,16 +45,18 @@ __device__ __forceinline__ uint32_t live_tiles(const int4 rc, const DoneView& do
 
 // Rank-ordered copy of the binning inputs, gathered once per frame so that every
 // chunk's K3/K4 reads them coalesced: brect[r] = rects[order[r]],
-// bmeta[r] = (order[r], ntiles[order[r]]).
+// bmeta[r] = (order[r], tiles of its rectangle).
 __global__ void gather_bins_kernel(uint64_t n, const uint32_t* __restrict__ order,
-                                   const int4* __restrict__ rects, const uint32_t* __restrict__ ntiles,
+                                   const int4* __restrict__ rects, const Counters* __restrict__ ctr,
                                    int4* __restrict__ brect, uint2* __restrict__ bmeta) {
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint32_t g = order[r];
-    const uint32_t c = ntiles[g];
+    // visible splats (ranks below V) carry their rectangle from K1; culled ones none
+    const int4 rc = r < ctr->visible ? rects[g] : make_int4(0, -1, 0, -1);
+    const uint32_t c = rect_area(rc);
     bmeta[r] = make_uint2(g, c);
-    if (c) brect[r] = rects[g];
+    if (c) brect[r] = rc;
 }
 
 __global__ void count_tiles_kernel(uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta,
@@ -347,10 +349,10 @@ static size_t bitmap_smem(const uint32_t* done, int ntile) {
     return done && ntile <= kMaxBitmapTiles ? static_cast<size_t>((ntile + 31) / 32) * 4 : 0;
 }
 
-void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
+void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const Counters* ctr,
                         int4* brect, uint2* bmeta, cudaStream_t stream) {
     if (n == 0) return;
-    gather_bins_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, order, rects, ntiles,
+    gather_bins_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, order, rects, ctr,
                                                                                  brect, bmeta);
 }
 

@@ -96,7 +96,7 @@ struct sgs_scene {
 // view i+1 while view i runs.
 struct Lane {
     cudaStream_t stream = nullptr;
-    DevBuf keys_a, keys_b, iota, order, rec, colour, rects, ntiles, brect, bmeta, counts, offsets;
+    DevBuf keys_a, keys_b, iota, order, rec, colour, rects, brect, bmeta, counts, offsets;
     DevBuf buckets;  // K2 bucket histogram / offsets / cursors
     DevBuf work;     // K7 work list (+ 3 control words)
     DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist;
@@ -272,7 +272,7 @@ sgs_status sort_depth(sgs_context* ctx, Lane& L, uint64_t n, bool wide, cudaStre
         const size_t cub_bytes = depth_two_level_cub_bytes(n, log2c);
         SGS_CUDA(L.cub_temp.ensure(cub_bytes));
         launch_depth_two_level(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2c, mat, off,
-                               L.keys_b.as<unsigned long long>(), order, L.rects.as<int4>(), L.ntiles.as<uint32_t>(),
+                               L.keys_b.as<unsigned long long>(), order, L.rects.as<int4>(),
                                L.brect.as<int4>(), L.bmeta.as<uint2>(), L.cub_temp.ptr, cub_bytes, s);
         ctx->own_launches += 3;
         ctx->lib_launches += 2;
@@ -366,7 +366,6 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     SGS_CUDA(L.rec.ensure(n1 * sizeof(SplatRec)));
     SGS_CUDA(L.rects.ensure(n1 * sizeof(int4)));
     SGS_CUDA(L.colour.ensure(n1 * sizeof(float4)));
-    SGS_CUDA(L.ntiles.ensure(n1 * 4));
     SGS_CUDA(L.brect.ensure(n1 * sizeof(int4)));
     SGS_CUDA(L.bmeta.ensure(n1 * sizeof(uint2)));
     SGS_CUDA(L.counts.ensure((n + 1) * 8));
@@ -421,7 +420,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     if (part == kAll && !(ctx->skip & 2)) {
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
         launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
-                          L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
+                          L.rects.as<int4>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
                           s);
         SGS_CUDA(cudaGetLastError());
         if (n) ctx->own_launches += 1;
@@ -443,7 +442,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         if (st != SGS_OK) return st;
     }
     if (!gathered) {  // rank-ordered binning inputs, gathered once for every chunk
-        launch_gather_bins(n, order, L.rects.as<int4>(), L.ntiles.as<uint32_t>(), L.brect.as<int4>(),
+        launch_gather_bins(n, order, L.rects.as<int4>(), L.d_ctr, L.brect.as<int4>(),
                            L.bmeta.as<uint2>(), s);
         if (n) ctx->own_launches += 1;
     }
@@ -724,7 +723,7 @@ sgs_status start_group(sgs_context* ctx, Lane* const* lanes, int g, const sgs_sc
         for (int k = 0; k < g; ++k) {
             Lane& L = *lanes[k];
             views.v[k] = K1Out{L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(), L.rects.as<int4>(),
-                               L.ntiles.as<uint32_t>(), L.colour.as<float4>(), L.d_ctr, make_cam(&cams[k])};
+                               L.colour.as<float4>(), L.d_ctr, make_cam(&cams[k])};
         }
         launch_preprocess_views(scene->planes, make_cfg(cfg, &cams[0]), views, nullptr, lead.stream);
         cudaError_t e = cudaGetLastError();
@@ -1107,7 +1106,7 @@ void sgs_destroy(sgs_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (Lane& L : ctx->lane) {
         if (L.stream) cudaStreamSynchronize(L.stream);
-        for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.iota, &L.order, &L.rec, &L.colour, &L.rects, &L.ntiles, &L.brect,
+        for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.iota, &L.order, &L.rec, &L.colour, &L.rects, &L.brect,
                           &L.bmeta, &L.counts, &L.offsets, &L.buckets, &L.work, &L.tkeys_a, &L.tkeys_b, &L.ranges,
                           &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist, &L.tb_cnt, &L.tb_cur,
                           &L.tb_items, &L.tb_ctl})

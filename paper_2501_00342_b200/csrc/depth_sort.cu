@@ -296,10 +296,10 @@ __device__ void block_exclusive_scan(uint32_t* v, int m, uint32_t* warp_tot) {
 
 // visible splats always have their rect written by K1: both gathers issue together
 __device__ __forceinline__ void put_rank(uint32_t r, uint32_t g, const int4* __restrict__ rects,
-                                         const uint32_t* __restrict__ ntiles, uint32_t* __restrict__ order,
-                                         int4* __restrict__ brect, uint2* __restrict__ bmeta) {
-    const uint32_t c = ntiles[g];
+                                         uint32_t* __restrict__ order, int4* __restrict__ brect,
+                                         uint2* __restrict__ bmeta) {
     const int4 rc = rects[g];
+    const uint32_t c = rect_area(rc);
     order[r] = g;
     bmeta[r] = make_uint2(g, c);
     brect[r] = rc;
@@ -307,7 +307,7 @@ __device__ __forceinline__ void put_rank(uint32_t r, uint32_t g, const int4* __r
 
 __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
-    Counters* __restrict__ ctr, int log2c, const int4* __restrict__ rects, const uint32_t* __restrict__ ntiles,
+    Counters* __restrict__ ctr, int log2c, const int4* __restrict__ rects,
     int4* __restrict__ brect, uint2* __restrict__ bmeta) {
     extern __shared__ unsigned long long sKey[];  // kL2Cap keys, then kL2Cap indices
     uint32_t* sIdx = reinterpret_cast<uint32_t*>(sKey + kL2Cap);
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
         }
     }
     __syncthreads();
-    for (uint32_t e = tid; e < m; e += kL2Threads) put_rank(s + e, sIdx[e], rects, ntiles, order, brect, bmeta);
+    for (uint32_t e = tid; e < m; e += kL2Threads) put_rank(s + e, sIdx[e], rects, order, brect, bmeta);
 }
 
 }  // namespace
@@ -476,7 +476,7 @@ size_t depth_two_level_scratch(uint64_t n, int log2c) {
 
 void launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters* ctr, int log2c, uint32_t* ghist,
                             uint32_t* cur, unsigned long long* part_key, uint32_t* order, const int4* rects,
-                            const uint32_t* ntiles, int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
+                            int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
                             cudaStream_t stream) {
     const uint32_t C = 1u << log2c;
     const uint32_t G = l1_grid(n);
@@ -490,7 +490,7 @@ void launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters*
         return true;
     }();
     (void)attr;
-    local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, ctr, log2c, rects, ntiles, brect,
+    local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, ctr, log2c, rects, brect,
                                                           bmeta);
 }
 

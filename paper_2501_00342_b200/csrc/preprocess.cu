@@ -455,7 +455,6 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
             }
             k1_view<KIND, DEBUG>(sp, cfg, stg, o, buf, tid, i, g, dbg, key, count, visible);
             o.keys[i] = key;
-            o.ntiles[i] = count;
             if constexpr (DEBUG) debug[i] = dbg;
             if (visible) {
                 ++nvis[v];
@@ -611,11 +610,11 @@ void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream) {
 
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
-                       uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
+                       float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream) {
     K1Views views{};
     views.nv = 1;
-    views.v[0] = K1Out{depth_keys, rec, rects, ntiles, colour, counters, cam};
+    views.v[0] = K1Out{depth_keys, rec, rects, colour, counters, cam};
     launch_preprocess_views(sp, cfg, views, debug, stream);
 }
 

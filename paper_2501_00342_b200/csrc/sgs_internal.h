@@ -124,6 +124,12 @@ struct Counters {
 };
 static_assert(sizeof(Counters) == 128, "counters block");
 
+// Tiles of an inclusive tile rectangle (x0, x1, y0, y1); empty when x1 < x0 or y1 < y0.
+__host__ __device__ inline uint32_t rect_area(int4 rc) {
+    return rc.y >= rc.x && rc.w >= rc.z ? static_cast<uint32_t>(rc.y - rc.x + 1) * static_cast<uint32_t>(rc.w - rc.z + 1)
+                                        : 0u;
+}
+
 // Per-pixel compositing state carried between depth chunks (K7).
 struct __align__(16) PixelState {
     float r, g, b, T;
@@ -144,7 +150,7 @@ inline int color_plane_count(int kind, int degree) {
 // Launchers (defined in the .cu files).
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
-                       uint32_t* ntiles, float4* colour, Counters* counters, DebugSplat* debug,
+                       float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream);
 // K1 over up to kMaxK1Views cameras of one batch: every Gaussian is read once and
 // projected into each view's arenas.
@@ -153,7 +159,6 @@ struct K1Out {
     unsigned long long* keys;
     SplatRec* rec;
     int4* rects;
-    uint32_t* ntiles;
     float4* colour;
     Counters* ctr;
     CamParams cam;
@@ -182,7 +187,7 @@ size_t depth_two_level_scratch(uint64_t n, int log2c);
 size_t depth_two_level_cub_bytes(uint64_t n, int log2c);
 void launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters* ctr, int log2c, uint32_t* mat,
                             uint32_t* off, unsigned long long* part_key, uint32_t* order, const int4* rects,
-                            const uint32_t* ntiles, int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
+                            int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
                             cudaStream_t stream);
 // K3+K4 fused: count, decoupled look-back scan and key emission in one pass
 size_t bin_emit_status_bytes(uint64_t ranks);
@@ -210,7 +215,7 @@ void launch_ssim(const void* a, const void* b, bool f64, int W, int H, int C, do
                  double* grad, cudaStream_t s);
 void launch_counters_init(Counters* c, cudaStream_t stream);
 void launch_counters_publish(const Counters* d, Counters* h_mapped, cudaStream_t stream);
-void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const uint32_t* ntiles,
+void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const Counters* ctr,
                         int4* brect, uint2* bmeta, cudaStream_t stream);
 void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
                         const uint32_t* done, int tiles_x, int ntile, unsigned long long* counts,
