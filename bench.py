@@ -63,8 +63,8 @@ def k1_algorithmic_bytes(v, n=N_GAUSS, n_c=24):
     """K1 (preprocess) per launch: the scene read of SURVEY.md §8(d), 4N(11 + n_c)
     (11 geometry floats + the n_c colour floats the evaluated degree needs), plus its
     per-visible-splat writes: 48-B compositing record + 8-B depth key + 16-B tile
-    rect + 4-B tile count + 16-B colour = 92 B."""
-    return 4 * n * (11 + n_c) + 92 * v
+    rect + 16-B colour = 88 B."""
+    return 4 * n * (11 + n_c) + 88 * v
 
 
 class ClockSampler:

@@ -55,7 +55,7 @@ def main():
         json.dump({"report": rep, "kernels": kernels}, f, indent=1)
     if traffic_out:
         k1 = [k for k in kernels if "preprocess" in k["kernel"]]
-        k7 = [k for k in kernels if "composite_kernel" in k["kernel"]]
+        k7 = [k for k in kernels if "composite" in k["kernel"] and "kernel" in k["kernel"]]
         t = {"source": out}
         if k1:
             t["k1_dram_bytes_per_launch"] = k1[0]["dram__bytes_read.sum"] + k1[0]["dram__bytes_write.sum"]
