@@ -150,7 +150,7 @@ struct sgs_context {
     cudaStream_t stream = nullptr;  // the caller's stream: lanes fork from and join back to it
     std::mutex mu;
     Lane lane[kLanes];
-    int lanes = 4;                     // lanes of the one-view-per-K1 schedule (SGS_LANES, 1..kLanes)
+    int lanes = 8;                     // lanes of the one-view-per-K1 schedule (SGS_LANES, 1..kLanes; 8 measured best)
     int k1_group = 1;                  // views per multi-view K1 (SGS_K1_GROUP, 2..4; measured: no gain)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
