@@ -474,7 +474,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
                                   static_cast<float>(scene->meta.background[2]));
     const int tile_bits = std::max(1, ceil_log2(ntile));
     const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
-    SGS_CUDA(L.work.ensure((2 * work_cap + 8) * sizeof(uint32_t)));  // lists, 8 control words, background items
+    SGS_CUDA(L.work.ensure((7 * work_cap + 8) * sizeof(uint32_t)));  // 6 length classes, 8 control words, background items
     const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
     // the tile-major binning serves the compositor; the parity dumps, the backward and
     // a frame whose tile list overflowed its sort use the rank-major keys
@@ -501,7 +501,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
                              static_cast<int>(ntile), pchunks, c == 0, c == nchunks - 1, order,
                              L.tb_cnt.as<uint32_t>(), L.tb_cur.as<uint32_t>(), L.ranges.as<uint2>(),
                              L.tkeys_a.as<uint32_t>(), L.tkey_cap, L.work.as<uint32_t>(),
-                             static_cast<uint32_t>(work_cap), L.work.as<uint32_t>() + work_cap,
+                             static_cast<uint32_t>(work_cap), L.work.as<uint32_t>() + 6 * work_cap,
                              L.tb_items.as<uint32_t>(), L.tb_ctl.as<uint32_t>(), L.d_ctr, s);
             SGS_CUDA(cudaGetLastError());
             ctx->own_launches += 4;
@@ -556,7 +556,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
                              L.colour.as<float4>(), bg, d_rgb, d_T, L.pix_state.as<PixelState>(),
                              L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
                              L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1, L.d_ctr,
-                             j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + work_cap,
+                             j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + 6 * work_cap,
                              tile_major, s);
             SGS_CUDA(cudaGetLastError());
             ctx->own_launches += tile_major ? 1 : 2;  // (+ the work list kernel)

@@ -112,6 +112,22 @@ __device__ __forceinline__ float fast_alpha(float m2, float lop) {
 }
 
 constexpr int kWorkCtl = 8;
+constexpr int kWorkClasses = 6;  // list-length classes, longest first (LPT order for the persistent CTAs)
+
+__device__ __forceinline__ int work_class(uint32_t len) {
+    return len >= 4096 ? 0 : len >= 2048 ? 1 : len >= 1024 ? 2 : len >= 512 ? 3 : len >= 128 ? 4 : 5;
+}
+
+// item-th entry of the class-ordered work list (class c's items at work[c * cap ...]).
+__device__ __forceinline__ uint32_t work_item(const uint32_t* __restrict__ work, const uint32_t* n_class,
+                                              uint32_t cap, uint32_t item) {
+#pragma unroll
+    for (int c = 0; c < kWorkClasses - 1; ++c) {
+        if (item < n_class[c]) return work[static_cast<size_t>(c) * cap + item];
+        item -= n_class[c];
+    }
+    return work[static_cast<size_t>(kWorkClasses - 1) * cap + item];
+}
 
 // Background-only (tile, pixel-chunk) items of the last chunk, flat over all CTAs:
 // the pixels of a tile that never received an entry are bg (acc 0 + T 1 * bg).
@@ -119,7 +135,7 @@ template <int NT>
 __device__ __forceinline__ void write_background(int W, int H, const CfgParams& cfg, int nchunks,
                                                  const uint32_t* __restrict__ work_count, float* __restrict__ out_rgb,
                                                  float* __restrict__ out_T, float3 bg) {
-    const uint32_t n_bg = work_count[3];
+    const uint32_t n_bg = work_count[7];
     const uint32_t* bgl = work_count + kWorkCtl;
     const int ts = cfg.tile_size;
     const uint64_t total = static_cast<uint64_t>(n_bg) * 256;
@@ -172,7 +188,9 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
         const int b = threadIdx.x >> 2, c = threadIdx.x & 3;
         sRaw[b][kBatch][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const uint32_t n_long = work_count[0], n_items = work_count[0] + work_count[1];
+    uint32_t n_class[kWorkClasses], n_items = 0;
+#pragma unroll
+    for (int c = 0; c < kWorkClasses; ++c) n_items += (n_class[c] = work_count[c]);
     // Persistent CTAs: each pulls (tile, pixel-chunk) items from the chunk's work list
     // (long tile lists first, built by build_work_kernel).
     for (;;) {
@@ -181,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const uint32_t item = s_item;
     __syncthreads();
     if (item >= n_items) break;
-    const uint32_t witem = item < n_long ? work[item] : work[work_cap - 1 - (item - n_long)];
+    const uint32_t witem = work_item(work, n_class, work_cap, item);
     const int ts = cfg.tile_size;
     const int tile = static_cast<int>(witem / nchunks);
     const int chunk = static_cast<int>(witem - static_cast<uint32_t>(tile) * nchunks);
@@ -462,7 +480,9 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
         const int b = threadIdx.x >> 2, c = threadIdx.x & 3;
         sRaw[b][kBatch][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const uint32_t n_long = work_count[0], n_items = work_count[0] + work_count[1];
+    uint32_t n_class[kWorkClasses], n_items = 0;
+#pragma unroll
+    for (int c = 0; c < kWorkClasses; ++c) n_items += (n_class[c] = work_count[c]);
     // T < stop is the stop test; a threshold above 1 stops every pixel right after
     // its first blended splat, exactly as 1.0 does (T starts at 1 and every blended
     // splat has alpha >= 1/255), and keeps T < stop false for a pixel that has not
@@ -474,7 +494,7 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     const uint32_t item = s_item;
     __syncthreads();
     if (item >= n_items) break;
-    const uint32_t witem = item < n_long ? work[item] : work[work_cap - 1 - (item - n_long)];
+    const uint32_t witem = work_item(work, n_class, work_cap, item);
     const int ts = cfg.tile_size;
     const int tile = static_cast<int>(witem / nchunks);
     const int chunk = static_cast<int>(witem - static_cast<uint32_t>(tile) * nchunks);
@@ -743,9 +763,10 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     write_background<kThreads2>(W, H, cfg, nchunks, work_count, out_rgb, out_T, bg);
 }
 
-// Work buffer: [0, cap) long items from the front, short items from the back;
-// [cap, cap + kWorkCtl) control words (long count, short count, cursor, background
-// count); [cap + kWorkCtl, 2 cap + kWorkCtl) background-only items.
+// Work buffer: kWorkClasses regions of cap items, one per list-length class (the
+// persistent CTAs take the longest lists first); then kWorkCtl control words (the
+// class counts, the compositor's cursor [6], the background count [7]); then the
+// background-only items.
 // Work list of a depth chunk: (tile, pixel chunk) items that still need K7 -- every
 // unfinished tile in the last chunk (it writes the final pixels), otherwise only
 // tiles with entries in this chunk. Tiles with long lists are queued from the front
@@ -763,13 +784,11 @@ __global__ void build_work_kernel(const uint2* __restrict__ ranges, const uint32
     if (!last && len == 0) return;
     if (len == 0 && (first || !((tile_touched[tile >> 5] >> (tile & 31)) & 1u))) {
         // never received an entry: background pixels, written by the tail loop
-        work[cap + kWorkCtl + atomicAdd(&wctl[3], 1u)] = it;
+        wctl[kWorkCtl + atomicAdd(&wctl[7], 1u)] = it;
         return;
     }
-    if (len >= 1024)
-        work[atomicAdd(&wctl[0], 1u)] = it;
-    else
-        work[cap - 1 - atomicAdd(&wctl[1], 1u)] = it;
+    const int c = work_class(len);
+    work[static_cast<size_t>(c) * cap + atomicAdd(&wctl[c], 1u)] = it;
 }
 
 }  // namespace
@@ -788,7 +807,7 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
     const uint32_t ntile = static_cast<uint32_t>(cfg.tiles_x) * static_cast<uint32_t>(cfg.tiles_y);
     const uint32_t cap = ntile * static_cast<uint32_t>(nchunks);
     if (!work_ready) {  // (the tile-major binning's scan builds the list itself)
-        cudaMemsetAsync(wctl, 0, 4 * sizeof(uint32_t), stream);
+        cudaMemsetAsync(wctl, 0, kWorkCtl * sizeof(uint32_t), stream);
         build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
                                                                  last ? 1 : 0, ntile, nchunks, cap, work, wctl);
     }
@@ -820,7 +839,7 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
         (void)attr_;                                                                                          \
         composite_kernel<G, M, B><<<grid, kThreads, smem_for(B), stream>>>(                                   \
             fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, rgb, T, state, processed, tile_done, \
-            tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 2, cap); \
+            tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 6, cap); \
     } while (0)
     static const int px = [] {
         const char* e = std::getenv("SGS_K7_PX");
@@ -840,7 +859,7 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
         composite2_kernel<G, 4, ROW><<<grid2, kThreads2, smem2, stream>>>(                                     \
             fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, rgb, T, state, processed,  \
             tile_done, tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl,    \
-            wctl + 2, cap);                                                                                   \
+            wctl + 6, cap);                                                                                   \
     } while (0)
         const bool row = cfg.tile_size == 16;
         if (group == 2) {

@@ -199,7 +199,8 @@ __device__ __forceinline__ uint32_t warp_append(bool take, uint32_t* s_count) {
 }
 
 // B2. cnt holds the chunk's per-tile counts (zeroed here for the next chunk).
-// wctl: [0] long work items, [1] short work items, [2] the compositor's cursor.
+// wctl (composite.cu's work layout): [2] long items (class 2), [5] short items (class 5),
+// [6] the compositor's cursor, [7] background items.
 // sctl: [k] sort items of class k, [4 + k] their cursor.
 __global__ void __launch_bounds__(kScanThreads) tb_scan_kernel(
     int ntile, int pchunks, uint32_t* __restrict__ cnt, uint32_t* __restrict__ cur, uint2* __restrict__ ranges,
@@ -249,17 +250,18 @@ __global__ void __launch_bounds__(kScanThreads) tb_scan_kernel(
             const uint32_t pl = warp_append(lng, &s_n[0]);
             const uint32_t ps = warp_append(live && !bgt && !lng, &s_n[1]);
             const uint32_t pb = warp_append(bgt, &s_n[6]);
-            if (lng) work[pl] = item;
+            if (lng) work[2 * work_cap + pl] = item;  // composite.cu work classes: 2 (>= 1024) and 5
             else if (bgt) wctl[kWorkCtlWords + pb] = item;
-            else if (live) work[work_cap - 1 - ps] = item;
+            else if (live) work[5 * work_cap + ps] = item;
         }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        wctl[0] = s_n[0];
-        wctl[1] = s_n[1];
-        wctl[2] = 0;
-        wctl[3] = s_n[6];
+        for (int c = 0; c < 6; ++c) wctl[c] = 0;
+        wctl[2] = s_n[0];
+        wctl[5] = s_n[1];
+        wctl[6] = 0;
+        wctl[7] = s_n[6];
         for (int k = 0; k < 4; ++k) {
             sctl[k] = s_n[2 + k];
             sctl[4 + k] = 0;
