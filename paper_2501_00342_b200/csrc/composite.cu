@@ -706,7 +706,8 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
             processed1 = base + idx[term1] + 1 - start;
             term1 = -2;
         }
-        __syncthreads();
+        // (no barrier here: the next iteration's first barrier is reached by every
+        // warp only after this walk, before anything overwrites the buffer it read)
     }
 
     asm volatile("cp.async.wait_all;\n" ::);
