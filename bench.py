@@ -366,6 +366,20 @@ def main():
     h2d = vpr * 144  # sgs_camera structs (kernel parameters) per rank per step
     d2h = vpr * H * W * 16  # RGB + T float32 per frame
 
+    # the same call returning the image only, as the reference's Python render does by
+    # default (return_transmittance=False, bindings.cpp:113-121): RGB float32 per frame
+    def step_e2e_rgb():
+        renderer.render_batch(dscene, my_cams, degree_override=1, rgb=rgb_np, T=False)
+
+    step_e2e_rgb()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e_rgb()
+    torch.cuda.synchronize()
+    e2e_rgb_value = total_frames / max_over_ranks(time.perf_counter() - t0)
+
     gather_ms = None
     if args.gather and world > 1:
         torch.cuda.synchronize()
@@ -418,6 +432,9 @@ def main():
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
+            "e2e_rgb_only": {"value": e2e_rgb_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                             "d2h_bytes_per_step": vpr * H * W * 12,
+                             "note": "image only, the reference Python render's default output"},
             "gpu_launches": int(launches1[0] - launches0[0]),
             "library_launches": int(launches1[1] - launches0[1]),
             "clocks": clocks,

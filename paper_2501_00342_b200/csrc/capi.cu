@@ -161,7 +161,6 @@ struct sgs_context {
     bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
     std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
     cudaEvent_t fork = nullptr;
-    int skip = 0;  // SGS_SKIP (timing probe only; renders garbage): 1 = no K7, 2 = no K1, 4 = no K2
     bool rank_host = true;  // ranked lane streams for host-frame batches (SGS_RANK_HOST=0 disables)
     bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
     struct TraceRec {
@@ -355,10 +354,6 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     const uint64_t npx = static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height);
     const bool timing = j.stats && j.stats->want_timing;
     const uint64_t n1 = std::max<uint64_t>(n, 1);
-    {
-        const char* e = std::getenv("SGS_SKIP");  // read per frame: set it after warm-up
-        ctx->skip = e ? std::atoi(e) : 0;
-    }
     j.ms_bin = j.ms_tsort = j.ms_comp = 0;
 
     SGS_CUDA(L.keys_a.ensure(n1 * 8));
@@ -420,7 +415,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     }
 
     // K1
-    if (part == kAll && !(ctx->skip & 2)) {
+    if (part == kAll) {
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
         launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
                           L.rects.as<int4>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
@@ -438,9 +433,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     // K2
     const uint32_t* order = L.iota.as<uint32_t>();
     bool gathered = false;
-    if (n > 1 && (ctx->skip & 4)) {
-        gathered = true;
-    } else if (n > 1) {
+    if (n > 1) {
         sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order, &gathered);
         if (st != SGS_OK) return st;
     }
@@ -464,8 +457,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         SGS_CUDA(L.tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
         SGS_CUDA(L.pix_state.ensure(npx * sizeof(PixelState)));
         SGS_CUDA(L.pix_walked.ensure(npx * sizeof(uint32_t)));
-        if (!(ctx->skip & 1))  // (probe: with K7 skipped the last frame's finished tiles stand in)
-            SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
+        SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
     }
     bounds.push_back(n);
     const int nchunks = static_cast<int>(bounds.size()) - 1;
@@ -551,7 +543,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             SGS_CUDA(cudaEventRecord(L.done, s));
         }
         // K7
-        if (mode == kRender && !(ctx->skip & 1)) {
+        if (mode == kRender) {
             launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, kstride, L.rec.as<SplatRec>(),
                              L.colour.as<float4>(), bg, d_rgb, d_T, L.pix_state.as<PixelState>(),
                              L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
