@@ -159,7 +159,8 @@ struct sgs_context {
     bool two_level = true;   // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
     bool tile_major = false;  // tile-major binning (tile_bins.cu, SGS_BIN=tile; measured slower)
     bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
-    std::vector<uint64_t> chunk_divs{16, 4};  // depth-chunk boundaries at N/16, N/4
+    std::vector<uint64_t> chunk_divs;  // depth-chunk boundaries N/div (SGS_DEPTH_CHUNKS; else by N)
+    bool chunk_divs_set = false;
     cudaEvent_t fork = nullptr;
     bool rank_host = true;  // ranked lane streams for host-frame batches (SGS_RANK_HOST=0 disables)
     bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
@@ -255,9 +256,18 @@ constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, red
 constexpr int kRetryRankMajor = 102;  // a tile list exceeded tile_bins' sort capacity: redo rank-major
 
 // Depth chunking: the first chunk holds the
-// nearest ceil(N / kFirstChunkDiv) ranks; tiles whose pixels all terminate inside it
-// are finished and receive no keys from the second chunk.
-constexpr uint64_t kMinChunkedN = 1 << 16;
+// nearest ceil(N / div0) ranks; tiles whose pixels all terminate inside it are
+// finished and receive no keys from the next chunk. Each chunk costs a fixed chain of
+// launches, so the boundaries follow N unless SGS_DEPTH_CHUNKS sets them (measured on
+// the B200, 32-view batches: 100K at 800x800 0.164 ms/frame unchunked against 0.19
+// with one boundary and 0.25 with two; 1M at 1080p 0.300 with one at N/8, 0.311 with
+// N/16 and N/4, 0.372 unchunked; 3M at 1080p 0.624 with N/16 and N/4, 0.659 with N/8).
+constexpr uint64_t kMinChunkedN = 1 << 16;  // floor for explicitly requested boundaries
+std::vector<uint64_t> default_chunk_divs(uint64_t n) {
+    if (n < (1u << 18)) return {};
+    if (n < (2u << 20)) return {8};
+    return {16, 4};
+}
 
 sgs_status sort_depth(sgs_context* ctx, Lane& L, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out,
                       bool* gathered) {
@@ -446,11 +456,12 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
 
     // depth chunks over ranks (bounds known on the host: culled splats sort last and
     // contribute no tiles, so rank bounds can be taken over N)
-    const bool multi = mode == kRender && ctx->chunking && n >= kMinChunkedN &&
+    const std::vector<uint64_t> divs = ctx->chunk_divs_set ? ctx->chunk_divs : default_chunk_divs(n);
+    const bool multi = mode == kRender && ctx->chunking && !divs.empty() && n >= kMinChunkedN &&
                        composite_pixel_chunks(cfg->tile_size) == 1;
     std::vector<uint64_t> bounds{0};
     if (multi) {
-        for (uint64_t div : ctx->chunk_divs) {
+        for (uint64_t div : divs) {
             const uint64_t b = (n + div - 1) / div;
             if (b > bounds.back() && b < n) bounds.push_back(b);
         }
@@ -1108,6 +1119,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
         ctx->chunk_divs.clear();
+        ctx->chunk_divs_set = true;
         for (const char* q = e; *q;) {
             char* endp = nullptr;
             const long v = std::strtol(q, &endp, 10);
