@@ -8,6 +8,7 @@
 // retries, stats). Batches alternate views over two lanes. CUB (CCCL 2.8) supplies
 // the scans and the rare 64-bit fallback sort.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -43,11 +44,15 @@ sgs_status fail(sgs_status code, const std::string& msg) {
         }                                                                                    \
     } while (0)
 
+// bumped by every (re)allocation: a captured frame graph holds buffer addresses
+std::atomic<uint64_t> g_alloc_generation{0};
+
 struct DevBuf {
     void* ptr = nullptr;
     size_t bytes = 0;
     cudaError_t ensure(size_t need) {
         if (need <= bytes) return cudaSuccess;
+        g_alloc_generation.fetch_add(1);
         if (ptr) cudaFree(ptr);
         ptr = nullptr;
         bytes = 0;
@@ -138,6 +143,14 @@ struct Lane {
         float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
     } job;
     bool busy = false;
+    // the frame graph (launch_frame_graph): captured on the second frame with the same
+    // key, replayed while the key holds
+    cudaGraph_t graph = nullptr;  // kept alive: gk1 is one of its nodes
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraphNode_t gk1 = nullptr;  // the K1 node, whose camera is patched per frame
+    K1Record* grec = nullptr;
+    std::vector<uint64_t> gkey, gpending;
+    uint64_t g_launches = 0, g_lib_launches = 0;
     // results of the last frame (device pointers into the buffers above)
     const uint32_t* last_order = nullptr;
     const unsigned long long* last_tile_keys = nullptr;
@@ -162,6 +175,7 @@ struct sgs_context {
     std::vector<uint64_t> chunk_divs;  // depth-chunk boundaries N/div (SGS_DEPTH_CHUNKS; else by N)
     bool chunk_divs_set = false;
     cudaEvent_t fork = nullptr;
+    bool graphs = true;     // frame graphs (SGS_GRAPHS=0 enqueues every frame directly)
     bool rank_host = true;  // ranked lane streams for host-frame batches (SGS_RANK_HOST=0 disables)
     bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
     struct TraceRec {
@@ -350,6 +364,97 @@ sgs_status count_and_scan(sgs_context* ctx, Lane& L, uint64_t rb, uint64_t re, c
 // kPost = everything after K1 (a multi-view K1 ran in between, start_group).
 enum EnqueuePart { kAll = 0, kPre = 1, kPost = 2 };
 
+// Everything the captured frame depends on besides the per-frame constants (camera,
+// outputs) and the K1 camera: a frame whose key differs is enqueued directly; the
+// second consecutive frame with one key is captured; later ones replay the graph.
+std::vector<uint64_t> frame_graph_key(const sgs_context* ctx, const Lane& L) {
+    const Lane::Job& j = L.job;
+    auto bits = [](double v) {
+        uint64_t u;
+        std::memcpy(&u, &v, 8);
+        return u;
+    };
+    std::vector<uint64_t> k{reinterpret_cast<uint64_t>(j.scene), j.scene->meta.count,
+                            static_cast<uint64_t>(j.cam.width), static_cast<uint64_t>(j.cam.height),
+                            static_cast<uint64_t>(j.cfg.tile_size), static_cast<uint64_t>(j.cfg.has_override),
+                            static_cast<uint64_t>(j.cfg.override_degree), bits(j.cfg.degree_threshold_lo),
+                            bits(j.cfg.degree_threshold_hi), bits(j.cfg.early_stop_transmittance),
+                            j.stats ? 1u : 0u, j.wide ? 1u : 0u, j.rank_major ? 1u : 0u,
+                            static_cast<uint64_t>(j.mode), L.tkey_cap, g_alloc_generation.load(),
+                            ctx->chunking ? 1u : 0u, ctx->tile_major ? 1u : 0u, ctx->fused_bin ? 1u : 0u,
+                            ctx->two_level ? 1u : 0u, ctx->chunk_divs_set ? 1u : 0u};
+    for (uint64_t d : ctx->chunk_divs) k.push_back(d);
+    return k;
+}
+
+template <typename Body>
+sgs_status launch_frame_graph(sgs_context* ctx, Lane& L, const CamParams& cp, Body&& body, bool& capturing) {
+    cudaStream_t s = L.stream;
+    const std::vector<uint64_t> key = frame_graph_key(ctx, L);
+    if (!(L.gexec && key == L.gkey)) {
+        if (key != L.gpending) {  // first frame with this key: direct (it sizes the arenas)
+            L.gpending = key;
+            return body();
+        }
+        if (L.gexec) {
+            cudaGraphExecDestroy(L.gexec);
+            L.gexec = nullptr;
+        }
+        if (L.graph) {
+            cudaGraphDestroy(L.graph);
+            L.graph = nullptr;
+        }
+        if (L.grec) {
+            k1_record_free(L.grec);
+            L.grec = nullptr;
+        }
+        const uint64_t own0 = ctx->own_launches, lib0 = ctx->lib_launches;
+        cudaGraph_t g = nullptr;
+        SGS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        capturing = true;
+        const sgs_status st = body();
+        capturing = false;
+        const cudaError_t ec = cudaStreamEndCapture(s, &g);
+        if (st != SGS_OK) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        SGS_CUDA(ec);
+        L.g_launches = ctx->own_launches - own0;
+        L.g_lib_launches = ctx->lib_launches - lib0;
+        ctx->own_launches = own0;
+        ctx->lib_launches = lib0;
+        // the K1 node: the kernel node running the recorded K1 function
+        L.grec = k1_last_launch_clone();
+        size_t nn = 0;
+        SGS_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        SGS_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        L.gk1 = nullptr;
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            SGS_CUDA(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            SGS_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+            if (kp.func == k1_record_func(L.grec)) L.gk1 = nd;
+        }
+        const cudaError_t ei = L.gk1 ? cudaGraphInstantiate(&L.gexec, g, 0) : cudaErrorInvalidValue;
+        if (ei != cudaSuccess) {
+            cudaGraphDestroy(g);
+            L.gexec = nullptr;
+            return fail(SGS_ERR_CUDA, std::string("frame graph: ") + cudaGetErrorString(ei));
+        }
+        L.graph = g;
+        L.gkey = key;
+    }
+    SGS_CUDA(k1_record_patch(L.gexec, L.gk1, L.grec, cp));
+    SGS_CUDA(cudaGraphLaunch(L.gexec, s));
+    ctx->own_launches += L.g_launches;
+    ctx->lib_launches += L.g_lib_launches;
+    return SGS_OK;
+}
+
 sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     Lane::Job& j = L.job;
     cudaStream_t s = L.stream;
@@ -395,186 +500,214 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         d_T = L.out_T[slot].as<float>();
     }
 
+    const bool host_out = mode == kRender && (j.h_rgb || j.h_T);
     if (part != kPost) {
-        launch_counters_init(L.d_ctr, s);
         if (mode == kRender) {
             // the pinned staging block is per lane; the lane's previous frame has
             // completed (finish_frame waits for it before the lane is reused)
             L.h_consts->sp = scene->planes;
             L.h_consts->cam = cp;
-            SGS_CUDA(cudaMemcpyAsync(L.d_consts, L.h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
+            L.h_consts->out_rgb = d_rgb;
+            L.h_consts->out_T = d_T;
         }
         if (L.iota_n < n) {  // identity values for the depth sort (kept across frames)
             launch_iota(n, L.iota.as<uint32_t>(), s);
             L.iota_n = n;
         }
     }
-    if (part == kPre) return SGS_OK;
-    const bool host_out = mode == kRender && (j.h_rgb || j.h_T);
-    if (host_out) {
+    if (host_out && part != kPre) {
         // the slot's previous frame must have left the device before K7 rewrites it
         SGS_CUDA(cudaStreamWaitEvent(s, L.copied[slot], 0));
         L.out_slot = (slot + 1) % Lane::kOutSlots;
     }
     sgs_context::TraceRec* tr = nullptr;
-    if (ctx->trace && mode == kRender) {
+    if (ctx->trace && mode == kRender && part != kPre) {
         ctx->trace_recs.push_back(sgs_context::TraceRec{static_cast<int>(&L - ctx->lane), {}});
         tr = &ctx->trace_recs.back();
         for (auto& e : tr->ev) SGS_CUDA(cudaEventCreate(&e));
         SGS_CUDA(cudaEventRecord(tr->ev[0], s));
     }
 
-    // K1
-    if (part == kAll) {
-        if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
-        launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
-                          L.rects.as<int4>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
-                          s);
-        SGS_CUDA(cudaGetLastError());
-        if (n) ctx->own_launches += 1;
-        if (timing) SGS_CUDA(cudaEventRecord(L.ev[1], s));
-    }
-    if (mode == kProjectOnly) {
-        launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
-        SGS_CUDA(cudaEventRecord(L.done, s));
-        return SGS_OK;
-    }
-
-    // K2
-    const uint32_t* order = L.iota.as<uint32_t>();
-    bool gathered = false;
-    if (n > 1) {
-        sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order, &gathered);
-        if (st != SGS_OK) return st;
-    }
-    if (!gathered) {  // rank-ordered binning inputs, gathered once for every chunk
-        launch_gather_bins(n, order, L.rects.as<int4>(), L.d_ctr, L.brect.as<int4>(),
-                           L.bmeta.as<uint2>(), s);
-        if (n) ctx->own_launches += 1;
-    }
-    if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
-
-    // depth chunks over ranks (bounds known on the host: culled splats sort last and
-    // contribute no tiles, so rank bounds can be taken over N)
-    const std::vector<uint64_t> divs = ctx->chunk_divs_set ? ctx->chunk_divs : default_chunk_divs(n);
-    const bool multi = mode == kRender && ctx->chunking && !divs.empty() && n >= kMinChunkedN &&
-                       composite_pixel_chunks(cfg->tile_size) == 1;
-    std::vector<uint64_t> bounds{0};
-    if (multi) {
-        for (uint64_t div : divs) {
-            const uint64_t b = (n + div - 1) / div;
-            if (b > bounds.back() && b < n) bounds.push_back(b);
+    // The frame's device work (counters, constants, K1 ... K7, counters published):
+    // enqueued directly, or captured once per lane and configuration into a CUDA
+    // graph and replayed (one launch per frame instead of ~40 commands, the camera
+    // patched into the K1 node; outputs come from the per-frame constants).
+    bool capturing = false;
+    auto rec_done = [&]() -> cudaError_t {
+        return capturing ? cudaEventRecordWithFlags(L.done, s, cudaEventRecordExternal) : cudaEventRecord(L.done, s);
+    };
+    auto body = [&]() -> sgs_status {
+        if (part != kPost) {
+            launch_counters_init(L.d_ctr, s);
+            if (mode == kRender)
+                SGS_CUDA(cudaMemcpyAsync(L.d_consts, L.h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
         }
-        SGS_CUDA(L.tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
-        SGS_CUDA(L.pix_state.ensure(npx * sizeof(PixelState)));
-        SGS_CUDA(L.pix_walked.ensure(npx * sizeof(uint32_t)));
-        SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
-    }
-    bounds.push_back(n);
-    const int nchunks = static_cast<int>(bounds.size()) - 1;
-    const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
-                                  static_cast<float>(scene->meta.background[1]),
-                                  static_cast<float>(scene->meta.background[2]));
-    const int tile_bits = std::max(1, ceil_log2(ntile));
-    const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
-    SGS_CUDA(L.work.ensure((7 * work_cap + 8) * sizeof(uint32_t)));  // 6 length classes, 8 control words, background items
-    const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
-    // the tile-major binning serves the compositor; the parity dumps, the backward and
-    // a frame whose tile list overflowed its sort use the rank-major keys
-    const bool tile_major = mode == kRender && ctx->tile_major && !j.rank_major;
-    const int pchunks = composite_pixel_chunks(cfg->tile_size);
-    if (tile_major) {
-        SGS_CUDA(L.tb_cnt.ensure(std::max<uint64_t>(ntile, 1) * 4));
-        SGS_CUDA(L.tb_cur.ensure(std::max<uint64_t>(ntile, 1) * 4));
-        SGS_CUDA(L.tb_items.ensure(std::max<uint64_t>(ntile, 1) * 4 * 4));  // 4 size classes
-        SGS_CUDA(L.tb_ctl.ensure(64));
-        SGS_CUDA(cudaMemsetAsync(L.tb_cnt.ptr, 0, ntile * 4, s));  // tb_scan re-zeroes it per chunk
-    }
-    for (int c = 0; c < nchunks; ++c) {
-        const uint64_t rb = bounds[c], re = bounds[c + 1];
-        const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
-        if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
-        const uint32_t* list = nullptr;  // the compositor's per-tile lists of Gaussian indices
-        int kstride = 1;
-        const unsigned long long* tkeys = nullptr;
-        if (tile_major) {
-            // B1-B4 (tile_bins.cu); also builds K7's work list
-            launch_tile_bins(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
-                             L.tile_done.as<uint32_t>() + (ntile + 31) / 32, kp.tiles_x,
-                             static_cast<int>(ntile), pchunks, c == 0, c == nchunks - 1, order,
-                             L.tb_cnt.as<uint32_t>(), L.tb_cur.as<uint32_t>(), L.ranges.as<uint2>(),
-                             L.tkeys_a.as<uint32_t>(), L.tkey_cap, L.work.as<uint32_t>(),
-                             static_cast<uint32_t>(work_cap), L.work.as<uint32_t>() + 6 * work_cap,
-                             L.tb_items.as<uint32_t>(), L.tb_ctl.as<uint32_t>(), L.d_ctr, s);
+        if (part == kPre) return SGS_OK;
+        // K1
+        if (part == kAll) {
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
+            launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
+                              L.rects.as<int4>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
+                              s);
             SGS_CUDA(cudaGetLastError());
-            ctx->own_launches += 4;
-            list = L.tkeys_a.as<uint32_t>();
-            if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
-        } else {
-            // K3 + K4
-            if (ctx->fused_bin) {
-                SGS_CUDA(L.counts.ensure(bin_emit_status_bytes(n)));
-                launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
-                                static_cast<int>(ntile), L.tkeys_a.as<unsigned long long>(), L.tkey_cap,
-                                L.counts.as<unsigned long long>(), L.d_ctr, s);
+            if (n) ctx->own_launches += 1;
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[1], s));
+        }
+        if (mode == kProjectOnly) {
+            launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
+            SGS_CUDA(rec_done());
+            return SGS_OK;
+        }
+
+        // K2
+        const uint32_t* order = L.iota.as<uint32_t>();
+        bool gathered = false;
+        if (n > 1) {
+            sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order, &gathered);
+            if (st != SGS_OK) return st;
+        }
+        if (!gathered) {  // rank-ordered binning inputs, gathered once for every chunk
+            launch_gather_bins(n, order, L.rects.as<int4>(), L.d_ctr, L.brect.as<int4>(),
+                               L.bmeta.as<uint2>(), s);
+            if (n) ctx->own_launches += 1;
+        }
+        if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
+
+        // depth chunks over ranks (bounds known on the host: culled splats sort last and
+        // contribute no tiles, so rank bounds can be taken over N)
+        const std::vector<uint64_t> divs = ctx->chunk_divs_set ? ctx->chunk_divs : default_chunk_divs(n);
+        const bool multi = mode == kRender && ctx->chunking && !divs.empty() && n >= kMinChunkedN &&
+                           composite_pixel_chunks(cfg->tile_size) == 1;
+        std::vector<uint64_t> bounds{0};
+        if (multi) {
+            for (uint64_t div : divs) {
+                const uint64_t b = (n + div - 1) / div;
+                if (b > bounds.back() && b < n) bounds.push_back(b);
+            }
+            SGS_CUDA(L.tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
+            SGS_CUDA(L.pix_state.ensure(npx * sizeof(PixelState)));
+            SGS_CUDA(L.pix_walked.ensure(npx * sizeof(uint32_t)));
+            SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
+        }
+        bounds.push_back(n);
+        const int nchunks = static_cast<int>(bounds.size()) - 1;
+        const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
+                                      static_cast<float>(scene->meta.background[1]),
+                                      static_cast<float>(scene->meta.background[2]));
+        const int tile_bits = std::max(1, ceil_log2(ntile));
+        const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
+        SGS_CUDA(L.work.ensure((7 * work_cap + 8) * sizeof(uint32_t)));  // 6 length classes, 8 control words, background items
+        const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
+        // the tile-major binning serves the compositor; the parity dumps, the backward and
+        // a frame whose tile list overflowed its sort use the rank-major keys
+        const bool tile_major = mode == kRender && ctx->tile_major && !j.rank_major;
+        const int pchunks = composite_pixel_chunks(cfg->tile_size);
+        if (tile_major) {
+            SGS_CUDA(L.tb_cnt.ensure(std::max<uint64_t>(ntile, 1) * 4));
+            SGS_CUDA(L.tb_cur.ensure(std::max<uint64_t>(ntile, 1) * 4));
+            SGS_CUDA(L.tb_items.ensure(std::max<uint64_t>(ntile, 1) * 4 * 4));  // 4 size classes
+            SGS_CUDA(L.tb_ctl.ensure(64));
+            SGS_CUDA(cudaMemsetAsync(L.tb_cnt.ptr, 0, ntile * 4, s));  // tb_scan re-zeroes it per chunk
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            const uint64_t rb = bounds[c], re = bounds[c + 1];
+            const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
+            const uint32_t* list = nullptr;  // the compositor's per-tile lists of Gaussian indices
+            int kstride = 1;
+            const unsigned long long* tkeys = nullptr;
+            if (tile_major) {
+                // B1-B4 (tile_bins.cu); also builds K7's work list
+                launch_tile_bins(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
+                                 L.tile_done.as<uint32_t>() + (ntile + 31) / 32, kp.tiles_x,
+                                 static_cast<int>(ntile), pchunks, c == 0, c == nchunks - 1, order,
+                                 L.tb_cnt.as<uint32_t>(), L.tb_cur.as<uint32_t>(), L.ranges.as<uint2>(),
+                                 L.tkeys_a.as<uint32_t>(), L.tkey_cap, L.work.as<uint32_t>(),
+                                 static_cast<uint32_t>(work_cap), L.work.as<uint32_t>() + 6 * work_cap,
+                                 L.tb_items.as<uint32_t>(), L.tb_ctl.as<uint32_t>(), L.d_ctr, s);
+                SGS_CUDA(cudaGetLastError());
+                ctx->own_launches += 4;
+                list = L.tkeys_a.as<uint32_t>();
+                if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
+            } else {
+                // K3 + K4
+                if (ctx->fused_bin) {
+                    SGS_CUDA(L.counts.ensure(bin_emit_status_bytes(n)));
+                    launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+                                    static_cast<int>(ntile), L.tkeys_a.as<unsigned long long>(), L.tkey_cap,
+                                    L.counts.as<unsigned long long>(), L.d_ctr, s);
+                    SGS_CUDA(cudaGetLastError());
+                    ctx->own_launches += 1;
+                } else {
+                    sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
+                    if (st != SGS_OK) return st;
+                    launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
+                                          L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
+                                          L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
+                    SGS_CUDA(cudaGetLastError());
+                    if (re > rb) ctx->own_launches += 1;
+                }
+                if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
+                // K5 (device-sized stable radix sort on the tile bits)
+                tkeys =
+                    tile_sort(L.tkeys_a.as<unsigned long long>(), L.tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
+                              L.sort_hist.as<uint32_t>(), s, &ctx->own_launches);
+                // K6
+                SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
+                launch_tile_ranges(d_pc, tkeys, L.ranges.as<uint2>(), s);
                 SGS_CUDA(cudaGetLastError());
                 ctx->own_launches += 1;
-            } else {
-                sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
-                if (st != SGS_OK) return st;
-                launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
-                                      L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
-                                      L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
-                SGS_CUDA(cudaGetLastError());
-                if (re > rb) ctx->own_launches += 1;
+                list = reinterpret_cast<const uint32_t*>(tkeys);  // low words of (tile << 32 | index)
+                kstride = 2;
             }
-            if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
-            // K5 (device-sized stable radix sort on the tile bits)
-            tkeys =
-                tile_sort(L.tkeys_a.as<unsigned long long>(), L.tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
-                          L.sort_hist.as<uint32_t>(), s, &ctx->own_launches);
-            // K6
-            SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
-            launch_tile_ranges(d_pc, tkeys, L.ranges.as<uint2>(), s);
-            SGS_CUDA(cudaGetLastError());
-            ctx->own_launches += 1;
-            list = reinterpret_cast<const uint32_t*>(tkeys);  // low words of (tile << 32 | index)
-            kstride = 2;
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[5], s));
+            L.last_order = order;
+            L.last_tile_keys = tkeys;
+            // Every decision the host acts on (device errors, depth-tie and tile-key
+            // overflows) is final once the last chunk is binned: without stats the
+            // counters are published here, so the host settles this frame and queues the
+            // lane's next one while K7 still runs (K7 itself raises nothing).
+            const bool early_done = mode == kRender && !j.stats && c == nchunks - 1;
+            if (early_done) {
+                launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
+                SGS_CUDA(rec_done());
+            }
+            // K7
+            if (mode == kRender) {
+                launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, kstride, L.rec.as<SplatRec>(),
+                                 L.colour.as<float4>(), bg, L.pix_state.as<PixelState>(),
+                                 L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
+                                 L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1, L.d_ctr,
+                                 j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + 6 * work_cap,
+                                 tile_major, s);
+                SGS_CUDA(cudaGetLastError());
+                ctx->own_launches += tile_major ? 1 : 2;  // (+ the work list kernel)
+            }
+            if (timing) {
+                SGS_CUDA(cudaEventRecord(L.ev[6], s));
+                SGS_CUDA(cudaEventSynchronize(L.ev[6]));
+                float a = 0, b = 0, d = 0;
+                SGS_CUDA(cudaEventElapsedTime(&a, L.ev[3], L.ev[4]));
+                SGS_CUDA(cudaEventElapsedTime(&b, L.ev[4], L.ev[5]));
+                SGS_CUDA(cudaEventElapsedTime(&d, L.ev[5], L.ev[6]));
+                j.ms_bin += a;
+                j.ms_tsort += b;
+                j.ms_comp += d;
+            }
         }
-        if (timing) SGS_CUDA(cudaEventRecord(L.ev[5], s));
-        L.last_order = order;
-        L.last_tile_keys = tkeys;
-        // Every decision the host acts on (device errors, depth-tie and tile-key
-        // overflows) is final once the last chunk is binned: without stats the
-        // counters are published here, so the host settles this frame and queues the
-        // lane's next one while K7 still runs (K7 itself raises nothing).
-        const bool early_done = mode == kRender && !j.stats && c == nchunks - 1;
-        if (early_done) {
+        if (mode != kRender || j.stats) {  // (otherwise published before K7)
             launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
-            SGS_CUDA(cudaEventRecord(L.done, s));
+            SGS_CUDA(rec_done());
         }
-        // K7
-        if (mode == kRender) {
-            launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, kstride, L.rec.as<SplatRec>(),
-                             L.colour.as<float4>(), bg, d_rgb, d_T, L.pix_state.as<PixelState>(),
-                             L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
-                             L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1, L.d_ctr,
-                             j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + 6 * work_cap,
-                             tile_major, s);
-            SGS_CUDA(cudaGetLastError());
-            ctx->own_launches += tile_major ? 1 : 2;  // (+ the work list kernel)
-        }
-        if (timing) {
-            SGS_CUDA(cudaEventRecord(L.ev[6], s));
-            SGS_CUDA(cudaEventSynchronize(L.ev[6]));
-            float a = 0, b = 0, d = 0;
-            SGS_CUDA(cudaEventElapsedTime(&a, L.ev[3], L.ev[4]));
-            SGS_CUDA(cudaEventElapsedTime(&b, L.ev[4], L.ev[5]));
-            SGS_CUDA(cudaEventElapsedTime(&d, L.ev[5], L.ev[6]));
-            j.ms_bin += a;
-            j.ms_tsort += b;
-            j.ms_comp += d;
-        }
+        return SGS_OK;
+    };
+    const bool graph = ctx->graphs && mode == kRender && part == kAll && !timing && !tr && !j.d_debug;
+    if (!graph) {
+        sgs_status st = body();
+        if (st != SGS_OK) return st;
+    } else {
+        sgs_status st = launch_frame_graph(ctx, L, cp, body, capturing);
+        if (st != SGS_OK) return st;
     }
     if (timing) SGS_CUDA(cudaEventRecord(L.ev[7], s));
     if (tr) SGS_CUDA(cudaEventRecord(tr->ev[1], s));
@@ -588,10 +721,6 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         if (tr) SGS_CUDA(cudaEventRecord(tr->ev[2], cs));
     } else if (tr) {
         SGS_CUDA(cudaEventRecord(tr->ev[2], s));
-    }
-    if (mode != kRender || j.stats) {  // (otherwise published before K7)
-        launch_counters_publish(L.d_ctr, L.h_ctr_dev, s);
-        SGS_CUDA(cudaEventRecord(L.done, s));
     }
     return SGS_OK;
 }
@@ -1108,6 +1237,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
             SGS_CUDA(cudaEventCreateWithFlags(&L.copied[k], cudaEventDisableTiming));
         }
     }
+    if (const char* e = std::getenv("SGS_GRAPHS")) ctx->graphs = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_RANK_HOST")) ctx->rank_host = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_TRACE")) ctx->trace = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
@@ -1161,6 +1291,9 @@ void sgs_destroy(sgs_context* ctx) {
             if (L.rendered[k]) cudaEventDestroy(L.rendered[k]);
             if (L.copied[k]) cudaEventDestroy(L.copied[k]);
         }
+        if (L.gexec) cudaGraphExecDestroy(L.gexec);
+        if (L.graph) cudaGraphDestroy(L.graph);
+        if (L.grec) k1_record_free(L.grec);
         if (L.plain) cudaStreamDestroy(L.plain);
         if (L.ranked) cudaStreamDestroy(L.ranked);
         if (L.swap) cudaEventDestroy(L.swap);

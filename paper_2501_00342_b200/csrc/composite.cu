@@ -164,7 +164,6 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
     const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
-    float* __restrict__ out_rgb, float* __restrict__ out_T,
     PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
     uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
     const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
@@ -177,6 +176,8 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     constexpr int kBatch = kBatchT;
     constexpr int kPer = kBatch / kThreads;  // records staged per thread per batch
     extern __shared__ float4 k7_smem[];
+    float* const out_rgb = fc->out_rgb;  // the frame's outputs (FrameConsts)
+    float* const out_T = fc->out_T;
     float4(*sRaw)[kBatch + 1][4] = reinterpret_cast<float4(*)[kBatch + 1][4]>(k7_smem);
     float4* sF = k7_smem + 2 * (kBatch + 1) * 4;  // (lmx, lmy, ext_x, ext_y)
     uint16_t(*sIdx)[kBatch + 8] = reinterpret_cast<uint16_t(*)[kBatch + 8]>(sF + kBatch);
@@ -460,7 +461,6 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
     const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
-    float* __restrict__ out_rgb, float* __restrict__ out_T,
     PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
     uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
     const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
@@ -470,6 +470,8 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     constexpr int kPer = kBatch / kThreads2;
     constexpr int kWarps = kThreads2 / 32;
     extern __shared__ float4 k7_smem[];
+    float* const out_rgb = fc->out_rgb;  // the frame's outputs (FrameConsts)
+    float* const out_T = fc->out_T;
     float4(*sRaw)[kBatch + 1][4] = reinterpret_cast<float4(*)[kBatch + 1][4]>(k7_smem);
     float4* sF = k7_smem + 2 * (kBatch + 1) * 4;
     uint16_t(*sIdx)[kBatch + 8] = reinterpret_cast<uint16_t(*)[kBatch + 8]>(sF + kBatch);
@@ -801,7 +803,7 @@ int composite_pixel_chunks(int ts) {
 
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
-                      const float4* colour, float3 bg, float* rgb, float* T, PixelState* state, uint32_t* processed,
+                      const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
                       uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
                       bool want_stats, uint32_t* work, uint32_t* wctl, bool work_ready, cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
@@ -839,7 +841,7 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
         }();                                                                                                  \
         (void)attr_;                                                                                          \
         composite_kernel<G, M, B><<<grid, kThreads, smem_for(B), stream>>>(                                   \
-            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, rgb, T, state, processed, tile_done, \
+            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed, tile_done, \
             tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 6, cap); \
     } while (0)
     static const int px = [] {
@@ -858,7 +860,7 @@ void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgPara
         }();                                                                                                  \
         (void)attr_;                                                                                          \
         composite2_kernel<G, 4, ROW><<<grid2, kThreads2, smem2, stream>>>(                                     \
-            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, rgb, T, state, processed,  \
+            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,  \
             tile_done, tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl,    \
             wctl + 6, cap);                                                                                   \
     } while (0)

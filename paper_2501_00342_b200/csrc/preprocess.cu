@@ -506,6 +506,23 @@ K1Stage make_stage(const ScenePlanes& sp, const CfgParams& cfg) {
     return st;
 }
 
+}  // namespace
+
+struct K1Record {
+    const void* func = nullptr;
+    dim3 grid, block;
+    size_t smem = 0;
+    ScenePlanes sp;
+    CfgParams cfg;
+    K1Stage st;
+    K1Views views;
+    DebugSplat* debug = nullptr;
+};
+
+namespace {
+
+thread_local K1Record t_last_k1;
+
 template <bool F64, int KIND, int MINB, bool DEBUG, int NV>
 void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
                cudaStream_t stream) {
@@ -519,6 +536,8 @@ void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kK1Threads, smem);
     const uint64_t need = (sp.n + kK1Threads - 1) / kK1Threads;
     const uint64_t grid = std::min<uint64_t>(need, static_cast<uint64_t>(sms) * std::max(per_sm, 1));
+    t_last_k1 = K1Record{reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(grid)), dim3(kK1Threads),
+                         smem, sp, cfg, st, views, debug};
     kern<<<static_cast<unsigned>(grid), kK1Threads, smem, stream>>>(sp, cfg, st, views, debug);
 }
 
@@ -625,6 +644,25 @@ void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const 
         launch_kind<true>(sp, cfg, views, debug, stream);
     else
         launch_kind<false>(sp, cfg, views, debug, stream);
+}
+
+K1Record* k1_last_launch_clone() { return new K1Record(t_last_k1); }
+
+void k1_record_free(K1Record* r) { delete r; }
+
+const void* k1_record_func(const K1Record* r) { return r->func; }
+
+cudaError_t k1_record_patch(cudaGraphExec_t exec, cudaGraphNode_t node, K1Record* r, const CamParams& cam) {
+    r->views.v[0].cam = cam;
+    void* args[] = {&r->sp, &r->cfg, &r->st, &r->views, &r->debug};
+    cudaKernelNodeParams p{};
+    p.func = const_cast<void*>(r->func);
+    p.gridDim = r->grid;
+    p.blockDim = r->block;
+    p.sharedMemBytes = static_cast<unsigned>(r->smem);
+    p.kernelParams = args;
+    p.extra = nullptr;
+    return cudaGraphExecKernelNodeSetParams(exec, node, &p);
 }
 
 }  // namespace sgs

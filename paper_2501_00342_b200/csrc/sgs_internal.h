@@ -76,6 +76,8 @@ struct ScenePlanes {
 struct FrameConsts {
     ScenePlanes sp;
     CamParams cam;
+    float* out_rgb;  // the frame's outputs (K7 reads them here, so a captured frame graph
+    float* out_T;    // replays with new output buffers); either may be null
 };
 
 // Compositing record written by K1 for visible splats (48 B, 16-B aligned); the
@@ -170,6 +172,13 @@ struct K1Views {
 void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
                              cudaStream_t stream);
 void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
+// The last K1 launch of this thread (function, configuration, arguments), so a frame
+// graph can patch the camera of its captured K1 node (capi.cu launch_frame_graph).
+struct K1Record;
+K1Record* k1_last_launch_clone();
+void k1_record_free(K1Record* r);
+const void* k1_record_func(const K1Record* r);
+cudaError_t k1_record_patch(cudaGraphExec_t exec, cudaGraphNode_t node, K1Record* r, const CamParams& cam);
 // per-scene 3D covariance cache: 3 planes of n double2 (projection.cuh)
 void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream);
 int depth_bucket_log2(uint64_t n);
@@ -238,7 +247,7 @@ unsigned long long* tile_sort(unsigned long long* a, unsigned long long* b, cons
 // state may be null when the frame is a single chunk.
 void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                       const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
-                      const float4* colour, float3 bg, float* rgb, float* T,
+                      const float4* colour, float3 bg,
                       PixelState* state, uint32_t* processed, uint32_t* tile_done, uint32_t* tile_touched,
                       bool first,
                       bool last, Counters* counters, bool want_stats, uint32_t* work, uint32_t* wctl,
