@@ -166,6 +166,8 @@ struct sgs_context {
     std::mutex mu;
     Lane lane[kLanes];
     int lanes = 8;                     // lanes of the one-view-per-K1 schedule (SGS_LANES, 1..kLanes; 8 measured best)
+    int host_lanes = 6;                // lanes for host-frame batches (SGS_HOST_LANES; fewer frames in flight
+                                       // hand the copy engines their first frames sooner)
     int k1_group = 1;                  // views per multi-view K1 (SGS_K1_GROUP, 2..4; measured: no gain)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
@@ -1241,6 +1243,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
     if (const char* e = std::getenv("SGS_RANK_HOST")) ctx->rank_host = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_TRACE")) ctx->trace = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
+    if (const char* e = std::getenv("SGS_HOST_LANES")) ctx->host_lanes = std::min(std::max(std::atoi(e), 1), kLanes);
     if (const char* e = std::getenv("SGS_K1_GROUP"))
         ctx->k1_group = std::min(std::max(std::atoi(e), 1), std::min(kMaxK1Views, kLanes / 2));
     if (const char* e = std::getenv("SGS_BIN_FUSED")) ctx->fused_bin = std::atoi(e) != 0;
@@ -1517,7 +1520,7 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
             }
     } else {
         // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
-        lanes = std::min<int>(timing ? 1 : ctx->lanes, n);
+        lanes = std::min<int>(timing ? 1 : (host ? ctx->host_lanes : ctx->lanes), n);
         st = fork_lanes(ctx, lanes);
         if (st != SGS_OK) return st;
         // view i runs on lane i % lanes; a lane's previous view is settled (checked,
