@@ -9,6 +9,7 @@
 // the scans and the rare 64-bit fallback sort.
 #include <algorithm>
 #include <atomic>
+#include <iterator>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -386,6 +387,13 @@ std::vector<uint64_t> frame_graph_key(const sgs_context* ctx, const Lane& L) {
                             ctx->chunking ? 1u : 0u, ctx->tile_major ? 1u : 0u, ctx->fused_bin ? 1u : 0u,
                             ctx->two_level ? 1u : 0u, ctx->chunk_divs_set ? 1u : 0u};
     for (uint64_t d : ctx->chunk_divs) k.push_back(d);
+    // the scene as the captured kernels see it (plane addresses, layout, axes) and
+    // its background (a K7 argument): a freed and re-uploaded scene can reuse the host
+    // struct's address, so the key holds the contents, not the pointer alone
+    uint64_t w[(sizeof(ScenePlanes) + 7) / 8] = {};
+    std::memcpy(w, &j.scene->planes, sizeof(ScenePlanes));
+    k.insert(k.end(), std::begin(w), std::end(w));
+    for (int c = 0; c < 3; ++c) k.push_back(bits(j.scene->meta.background[c]));
     return k;
 }
 

@@ -452,3 +452,39 @@ def test_frame_graph_replay_is_bitwise_equal():
     finally:
         a_ds.free()
         b_ds.free()
+
+
+def test_frame_graph_follows_scene_changes():
+    """A captured frame graph must not outlive what it baked in: a new background
+    (a compositor argument) and a freed-and-reuploaded scene of the same size (whose
+    host struct may reuse the old address) both re-capture."""
+    cams = sg.orbit_cameras(16, 256, 160, 4.0, 190.0)
+    os.environ["SGS_GRAPHS"] = "0"
+    try:
+        plain = sg.Renderer(0)
+    finally:
+        os.environ.pop("SGS_GRAPHS")
+    graphed = sg.Renderer(0)
+    s1 = sg.synth_scene(90_000, "mixed", 96, log_scale_range=(-5.0, -3.5))
+    s2 = sg.synth_scene(90_000, "mixed", 97, log_scale_range=(-5.0, -3.5))
+    b1 = graphed.upload(s1)
+    for _ in range(3):  # direct, captured, replayed
+        graphed.render_batch(b1, cams, degree_override=1)
+    b1.set_background([0.25, 0.5, 0.75])
+    a1 = plain.upload(s1)
+    a1.set_background([0.25, 0.5, 0.75])
+    for _ in range(3):
+        g = graphed.render_batch(b1, cams, degree_override=1)
+        p = plain.render_batch(a1, cams, degree_override=1)
+        assert np.array_equal(g[0], p[0]) and np.array_equal(g[1], p[1])
+    b1.free()
+    a1.free()
+    b2, a2 = graphed.upload(s2), plain.upload(s2)
+    try:
+        for _ in range(3):
+            g = graphed.render_batch(b2, cams, degree_override=1)
+            p = plain.render_batch(a2, cams, degree_override=1)
+            assert np.array_equal(g[0], p[0]) and np.array_equal(g[1], p[1])
+    finally:
+        b2.free()
+        a2.free()
