@@ -429,7 +429,14 @@ sgs_status launch_frame_graph(sgs_context* ctx, Lane& L, const CamParams& cp, Bo
             if (g) cudaGraphDestroy(g);
             return st;
         }
-        SGS_CUDA(ec);
+        if (ec != cudaSuccess || !g) {
+            // a capture the driver refused: this context enqueues frames directly from now on
+            cudaGetLastError();
+            ctx->graphs = false;
+            ctx->own_launches = own0;
+            ctx->lib_launches = lib0;
+            return body();
+        }
         L.g_launches = ctx->own_launches - own0;
         L.g_lib_launches = ctx->lib_launches - lib0;
         ctx->own_launches = own0;
