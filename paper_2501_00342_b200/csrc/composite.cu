@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     }
     const int px = px0 + lx, py = py0 + ly;
     const bool valid = inside && px < W && py < H;
-    const float stop = cfg.early_stop;
+    const float stop = cfg.early_stop > 1.0f ? 1.0f : cfg.early_stop;  // (see composite2_kernel)
     const size_t pix = valid ? static_cast<size_t>(py) * W + px : 0;
     const float fcx = static_cast<float>(lx) + 0.5f, fcy = static_cast<float>(ly) + 0.5f;
     Pixel P{1.f, 0.f, 0.f, 0.f, -1, !valid};

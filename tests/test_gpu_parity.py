@@ -488,3 +488,33 @@ def test_frame_graph_follows_scene_changes():
     finally:
         b2.free()
         a2.free()
+
+
+@pytest.mark.parametrize("stop", [0.0, 0.3, 1.0, 2.0])
+@pytest.mark.parametrize("chunked", [False, True])
+def test_early_stop_thresholds_vs_restatement(orc, stop, chunked):
+    """The stop test at thresholds the defaults never use: 0 (never stop), one that
+    stops after a few splats, 1 and above 1 (the reference accumulates a pixel's first
+    blended splat and then stops; K7 clamps the threshold to 1, which is the same),
+    on the single-chunk and the depth-chunked paths (per-pixel state across chunks)."""
+    f = orc.synth(120_000 if chunked else 3000, 31, "mixed", 2, ls=(-4.5, -3.0))
+    f.background = np.array([0.2, 0.4, 0.6])
+    ocam = orc.orbit_camera([0, 0, 0], 3.5, 0.7, 0.2, 160, 120, 150.0)
+    cfg = make_config(16, degree_override=1, early_stop=stop)
+    ref_rgb, ref_T = orc.render(f, ocam, cfg)
+    env = {"SGS_DEPTH_CHUNKS": "16,4"} if chunked else {"SGS_DEPTH_CHUNKING": "0"}
+    os.environ.update(env)
+    try:
+        r = sg.Renderer(0)
+    finally:
+        for k in env:
+            os.environ.pop(k)
+    ds = r.upload(to_scene(f))
+    try:
+        rgb, T = r.render(ds, to_cam(ocam), early_stop=stop, **cfg_kwargs(cfg))
+        check_image(rgb, T, ref_rgb, ref_T)
+        if not chunked:  # the exact FP64 mode runs the reference's own loop
+            rgb64, T64 = r.render_f64(ds, to_cam(ocam), early_stop=stop, **cfg_kwargs(cfg))
+            assert np.abs(rgb64 - ref_rgb).max() <= 1e-12 and np.abs(T64 - ref_T).max() <= 1e-12
+    finally:
+        ds.free()
