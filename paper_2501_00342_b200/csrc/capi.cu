@@ -456,7 +456,13 @@ sgs_status launch_frame_graph(sgs_context* ctx, Lane& L, const CamParams& cp, Bo
             SGS_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
             if (kp.func == k1_record_func(L.grec)) L.gk1 = nd;
         }
-        const cudaError_t ei = L.gk1 ? cudaGraphInstantiate(&L.gexec, g, 0) : cudaErrorInvalidValue;
+        // (an empty scene launches no K1: nothing to patch)
+        if (!L.gk1 && L.job.scene->meta.count > 0) {  // the K1 node was not found: no graphs
+            cudaGraphDestroy(g);
+            ctx->graphs = false;
+            return body();
+        }
+        const cudaError_t ei = cudaGraphInstantiate(&L.gexec, g, 0);
         if (ei != cudaSuccess) {
             cudaGraphDestroy(g);
             L.gexec = nullptr;
@@ -465,7 +471,7 @@ sgs_status launch_frame_graph(sgs_context* ctx, Lane& L, const CamParams& cp, Bo
         L.graph = g;
         L.gkey = key;
     }
-    SGS_CUDA(k1_record_patch(L.gexec, L.gk1, L.grec, cp));
+    if (L.gk1) SGS_CUDA(k1_record_patch(L.gexec, L.gk1, L.grec, cp));
     SGS_CUDA(cudaGraphLaunch(L.gexec, s));
     ctx->own_launches += L.g_launches;
     ctx->lib_launches += L.g_lib_launches;

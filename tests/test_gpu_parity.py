@@ -518,3 +518,24 @@ def test_early_stop_thresholds_vs_restatement(orc, stop, chunked):
             assert np.abs(rgb64 - ref_rgb).max() <= 1e-12 and np.abs(T64 - ref_T).max() <= 1e-12
     finally:
         ds.free()
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (3, 17), (17, 3), (16, 16), (33, 1)])
+@pytest.mark.parametrize("n", [0, 1, 2000])
+def test_tiny_images_and_scenes_vs_restatement(orc, renderer, wh, n):
+    """Degenerate shapes: one-pixel and one-row images, images narrower than a tile,
+    and scenes of 0 or 1 Gaussians, rendered three times (direct, captured, replayed
+    frame) against the restatement."""
+    f = orc.synth(n, 41, "mixed", 2, ls=(-3.0, -1.5))
+    f.background = np.array([0.1, 0.2, 0.3])
+    W, H = wh
+    ocam = orc.orbit_camera([0, 0, 0], 3.0, 0.4, 0.1, W, H, 2.0 * max(W, H))
+    cfg = make_config(16, degree_override=1)
+    ref_rgb, ref_T = orc.render(f, ocam, cfg)
+    ds = renderer.upload(to_scene(f))
+    try:
+        for _ in range(3):
+            rgb, T = renderer.render(ds, to_cam(ocam), **cfg_kwargs(cfg))
+            check_image(rgb, T, ref_rgb, ref_T)
+    finally:
+        ds.free()
