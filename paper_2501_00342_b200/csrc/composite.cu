@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
 
 // ---------------------------------------------------------------------------
 // K7, two pixels per thread (the default). One CTA of 128 threads per (tile,
-// 256-pixel chunk); on 16x16 tiles warp w owns rows 4w..4w+3 and a thread the two
+// 256-pixel chunk); on 16x16 tiles warp w owns one 8x8 quadrant and a thread the two
 // horizontally adjacent pixels (2c, 2c+1) of one row, so a record's dy terms
 // (dy, 2b dy, c dy^2) and its shared-memory reads serve both pixels. m2 is formed
 // per pixel exactly as in composite_kernel (same operations, same rounding), and
@@ -509,9 +509,11 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     int lx0, ly0, lx1, ly1;
     bool in0, in1;
     if (ts == 16) {
-        lx0 = (lane & 7) * 2;
+        // warp w owns the 8x8 quadrant (w & 1, w >> 1): a square strip meets fewer
+        // splat boxes per pixel than a 16x4 one
+        lx0 = (warp & 1) * 8 + (lane & 3) * 2;
         lx1 = lx0 + 1;
-        ly0 = ly1 = warp * 4 + (lane >> 3);
+        ly0 = ly1 = (warp >> 1) * 8 + (lane >> 2);
         in0 = in1 = true;
     } else {
         const int p = chunk * 256 + 2 * static_cast<int>(threadIdx.x);
