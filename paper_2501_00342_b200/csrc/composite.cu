@@ -548,16 +548,6 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     uint32_t processed0 = live0 ? end - start : 0u, processed1 = live1 ? end - start : 0u;
     int term0 = -1, term1 = -1;  // compacted-walk position of the stopping splat in this batch
 
-    float wx0 = 1e30f, wx1 = -1e30f, wy0 = 1e30f, wy1 = -1e30f;
-    if (live0) wx0 = fminf(wx0, fcx0), wx1 = fmaxf(wx1, fcx0), wy0 = fminf(wy0, fcy0), wy1 = fmaxf(wy1, fcy0);
-    if (live1) wx0 = fminf(wx0, fcx1), wx1 = fmaxf(wx1, fcx1), wy0 = fminf(wy0, fcy1), wy1 = fmaxf(wy1, fcy1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        wx0 = fminf(wx0, __shfl_xor_sync(0xffffffffu, wx0, o));
-        wx1 = fmaxf(wx1, __shfl_xor_sync(0xffffffffu, wx1, o));
-        wy0 = fminf(wy0, __shfl_xor_sync(0xffffffffu, wy0, o));
-        wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
-    }
     uint32_t guard_hits = 0;
     uint16_t* idx = sIdx[warp];
 
@@ -608,6 +598,17 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
         const float4(*R)[4] = sRaw[buf ^ 1];
         int cnt = 0;
         if (__any_sync(0xffffffffu, live0 || live1)) {
+            // the warp's live-pixel box, shrinking as its pixels stop
+            float wx0 = 1e30f, wx1 = -1e30f, wy0 = 1e30f, wy1 = -1e30f;
+            if (live0) wx0 = fminf(wx0, fcx0), wx1 = fmaxf(wx1, fcx0), wy0 = fminf(wy0, fcy0), wy1 = fmaxf(wy1, fcy0);
+            if (live1) wx0 = fminf(wx0, fcx1), wx1 = fmaxf(wx1, fcx1), wy0 = fminf(wy0, fcy1), wy1 = fmaxf(wy1, fcy1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wx0 = fminf(wx0, __shfl_xor_sync(0xffffffffu, wx0, o));
+                wx1 = fmaxf(wx1, __shfl_xor_sync(0xffffffffu, wx1, o));
+                wy0 = fminf(wy0, __shfl_xor_sync(0xffffffffu, wy0, o));
+                wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
+            }
             for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
                 const uint32_t j = j0 + lane;
                 bool hit = false;
