@@ -179,6 +179,7 @@ struct sgs_context {
     bool chunk_divs_set = false;
     cudaEvent_t fork = nullptr;
     bool graphs = true;     // frame graphs (SGS_GRAPHS=0 enqueues every frame directly)
+    bool tight_rect = true; // render frames bin into the cut ellipse's tiles (SGS_TIGHT_RECT=0: 3-sigma rects)
     bool rank_host = true;  // ranked lane streams for host-frame batches (SGS_RANK_HOST=0 disables)
     bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
     struct TraceRec {
@@ -487,7 +488,10 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     const FrameMode mode = static_cast<FrameMode>(j.mode);
     const uint64_t n = scene->meta.count;
     const CamParams cp = make_cam(cam);
-    const CfgParams kp = make_cfg(cfg, cam);
+    CfgParams kp = make_cfg(cfg, cam);
+    // render frames without stats bin each splat into the tiles its cut ellipse reaches
+    // (E_t, a stat, is defined over the reference's lists, so stats frames keep them)
+    kp.tight_rect = ctx->tight_rect && mode == kRender && !j.stats ? 1 : 0;
     const uint64_t ntile = static_cast<uint64_t>(kp.tiles_x) * static_cast<uint64_t>(kp.tiles_y);
     const uint64_t npx = static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height);
     const bool timing = j.stats && j.stats->want_timing;
@@ -1261,6 +1265,7 @@ sgs_status sgs_create(int device, sgs_context** out) {
         }
     }
     if (const char* e = std::getenv("SGS_GRAPHS")) ctx->graphs = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SGS_TIGHT_RECT")) ctx->tight_rect = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_RANK_HOST")) ctx->rank_host = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_TRACE")) ctx->trace = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);

@@ -356,7 +356,6 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
         y1 = min(cfg.tiles_y - 1, y1);
         if (x1 >= x0 && y1 >= y0)
             count = static_cast<uint32_t>(x1 - x0 + 1) * static_cast<uint32_t>(y1 - y0 + 1);
-        o.rects[i] = make_int4(x0, x1, y0, y1);
         // FP32 m2 error bound: 2u S (9 r^2 + 3 r ts) + 1e-6
         const double csum = fabs(cona) + 2.0 * fabs(conb) + fabs(conc);
         const double guard =
@@ -379,6 +378,22 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
         r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
         r.ext_x = sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
         r.ext_y = sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
+        if (cfg.tight_rect && x1 >= x0 && y1 >= y0) {
+            // Render frames list a splat only in the tiles its cut ellipse's box reaches:
+            // every pixel outside it has m2 > cut and is skipped by the reference, so the
+            // image is unchanged (the parity dumps and stats frames keep the reference's
+            // 3-sigma rectangle, which bounds this one).
+            const double ex = r.ext_x, ey = r.ext_y;
+            const double ex0 = pow2 ? dmul(dsub(mx, ex), its) : ddiv(dsub(mx, ex), ts);
+            const double ex1 = pow2 ? dmul(dadd(mx, ex), its) : ddiv(dadd(mx, ex), ts);
+            const double ey0 = pow2 ? dmul(dsub(my, ey), its) : ddiv(dsub(my, ey), ts);
+            const double ey1 = pow2 ? dmul(dadd(my, ey), its) : ddiv(dadd(my, ey), ts);
+            x0 = max(x0, to_int_x86(floor(ex0)));
+            x1 = min(x1, to_int_x86(floor(ex1)));
+            y0 = max(y0, to_int_x86(floor(ey0)));
+            y1 = min(y1, to_int_x86(floor(ey1)));
+        }
+        o.rects[i] = make_int4(x0, x1, y0, y1);
         // colour (FP32), direction from the FP64 offset
         {
             const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;

@@ -52,6 +52,7 @@ struct CfgParams {
     int32_t has_override, override_degree;
     double lo, hi;
     float early_stop;
+    int32_t tight_rect;  // K1: tile rectangles of the cut ellipse's box, not the 3-sigma circle's
 };
 
 // Scene planes inside one device blob.

@@ -540,3 +540,35 @@ def test_tiny_images_and_scenes_vs_restatement(orc, renderer, wh, n):
             check_image(rgb, T, ref_rgb, ref_T)
     finally:
         ds.free()
+
+
+@pytest.mark.parametrize("ts", [16, 8, 13, 32])
+@pytest.mark.parametrize("chunks", ["16,4", "0"])
+def test_tight_tile_rectangles_are_bitwise_neutral(ts, chunks):
+    """Render frames without stats bin each splat only into the tiles its cut ellipse's
+    box reaches (the reference's 3-sigma rectangle bounds it); every dropped pair is one
+    the reference skips, so the frames must equal the 3-sigma binning bit for bit."""
+    scene = sg.synth_scene(150_000, "mixed", 98, log_scale_range=(-5.5, -3.0))
+    cams = sg.orbit_cameras(6, 400, 240, 4.0, 300.0)
+    env = {"SGS_DEPTH_CHUNKS": chunks} if chunks != "0" else {"SGS_DEPTH_CHUNKING": "0"}
+    saved = {k: os.environ.get(k) for k in list(env) + ["SGS_TIGHT_RECT"]}
+    try:
+        os.environ.update(env)
+        tight = sg.Renderer(0)
+        os.environ["SGS_TIGHT_RECT"] = "0"
+        wide = sg.Renderer(0)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    a_ds, b_ds = tight.upload(scene), wide.upload(scene)
+    try:
+        for _ in range(2):  # direct and captured frames
+            a = tight.render_batch(a_ds, cams, tile_size=ts, degree_override=1)
+            b = wide.render_batch(b_ds, cams, tile_size=ts, degree_override=1)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    finally:
+        a_ds.free()
+        b_ds.free()
