@@ -6,11 +6,14 @@
 // skip alpha < 1/255, accumulate c * alpha * T, T *= 1 - alpha, stop after the
 // splat that pushed T below the threshold, then add T * background.
 //
-// Layout. One CTA of 256 threads per (tile, 256-pixel chunk) -- one CTA per 16x16
-// tile, one pixel per thread, warp w owning the 16x2 strip of rows 2w, 2w+1. The
-// tile's list streams through shared memory in batches of 256 64-B records (one
-// coalesced gather per thread). Each warp compacts the batch to the records whose
-// support box reaches its live pixels (ballot + popc).
+// Two kernels share the scheme below: composite2_kernel (the default: 128 threads
+// per (tile, 256-pixel chunk), two horizontally adjacent pixels per thread, warp w
+// owning one 8x8 quadrant of a 16x16 tile) and composite_kernel (SGS_K7_PX=1: 256
+// threads, one pixel per thread, warp w owning the 16x2 strip of rows 2w, 2w+1).
+//
+// Layout. The tile's list streams through shared memory in batches of 256 64-B
+// records (cp.async gathers, double-buffered). Each warp compacts the batch to the
+// records whose support box reaches its live pixels (ballot + popc).
 //
 // Latency. A pixel's walk is inherently sequential, so long lists (tiles on the
 // silhouette whose pixels never saturate) sit on the critical path. The walk goes
