@@ -392,6 +392,8 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
             x1 = min(x1, to_int_x86(floor(ex1)));
             y0 = max(y0, to_int_x86(floor(ey0)));
             y1 = min(y1, to_int_x86(floor(ey1)));
+            // opacity below 1/255 (cut < 0): alpha < 1/255 at every pixel, no tile at all
+            if (cut + guard < 0.0) x1 = x0 - 1;
         }
         o.rects[i] = make_int4(x0, x1, y0, y1);
         // colour (FP32), direction from the FP64 offset

@@ -549,6 +549,7 @@ def test_tight_tile_rectangles_are_bitwise_neutral(ts, chunks):
     box reaches (the reference's 3-sigma rectangle bounds it); every dropped pair is one
     the reference skips, so the frames must equal the 3-sigma binning bit for bit."""
     scene = sg.synth_scene(150_000, "mixed", 98, log_scale_range=(-5.5, -3.0))
+    scene.params[::7, 10] = -7.0  # opacity ~ 9e-4 < 1/255: splats that never blend, no tiles
     cams = sg.orbit_cameras(6, 400, 240, 4.0, 300.0)
     env = {"SGS_DEPTH_CHUNKS": chunks} if chunks != "0" else {"SGS_DEPTH_CHUNKING": "0"}
     saved = {k: os.environ.get(k) for k in list(env) + ["SGS_TIGHT_RECT"]}
