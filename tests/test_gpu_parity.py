@@ -573,3 +573,21 @@ def test_tight_tile_rectangles_are_bitwise_neutral(ts, chunks):
     finally:
         a_ds.free()
         b_ds.free()
+
+
+@pytest.mark.parametrize("ts", [1, 2, 3, 64])
+def test_unusual_tile_sizes_vs_restatement(orc, renderer, ts):
+    """Tile sizes far from 16: one-pixel and two-pixel tiles (thousands of tiles, the
+    compositor's general pixel mapping) and 64-pixel tiles (sixteen 256-pixel chunks
+    per tile), direct and replayed frames, against the restatement."""
+    f = orc.synth(4000, 51, "mixed", 2, ls=(-3.8, -2.5))
+    ocam = orc.orbit_camera([0, 0, 0], 3.0, 0.9, 0.2, 72, 56, 70.0)
+    cfg = make_config(ts, degree_override=1)
+    ref_rgb, ref_T = orc.render(f, ocam, cfg)
+    ds = renderer.upload(to_scene(f))
+    try:
+        for _ in range(3):
+            rgb, T = renderer.render(ds, to_cam(ocam), **cfg_kwargs(cfg))
+            check_image(rgb, T, ref_rgb, ref_T)
+    finally:
+        ds.free()
