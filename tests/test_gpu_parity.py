@@ -591,3 +591,21 @@ def test_unusual_tile_sizes_vs_restatement(orc, renderer, ts):
             check_image(rgb, T, ref_rgb, ref_T)
     finally:
         ds.free()
+
+
+@pytest.mark.parametrize("kind,deg", [("mixed", 2), ("sh", 3), ("sg3", 0)])
+def test_camera_inside_the_scene_vs_restatement(orc, renderer, kind, deg):
+    """The camera inside the Gaussian cloud: near-plane culls, splats just past the
+    near plane covering most of the image (cooperative emission, long lists, the
+    Jacobian's lateral clamp), adaptive degrees; direct and replayed frames."""
+    f = orc.synth(20_000, 61, kind, deg, ls=(-4.0, -2.5))
+    ocam = orc.orbit_camera([0, 0, 0], 0.4, 0.3, 0.1, 120, 90, 100.0)
+    cfg = make_config(16)
+    ref_rgb, ref_T = orc.render(f, ocam, cfg)
+    ds = renderer.upload(to_scene(f))
+    try:
+        for _ in range(3):
+            rgb, T = renderer.render(ds, to_cam(ocam), **cfg_kwargs(cfg))
+            check_image(rgb, T, ref_rgb, ref_T)
+    finally:
+        ds.free()
