@@ -254,7 +254,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __global__ void __launch_bounds__(kBThreads) bwd_pixels_kernel(
-    const BwdParams p, int nchunks, const uint2* __restrict__ ranges, const unsigned long long* __restrict__ keys,
+    const BwdParams p, int nchunks, const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys,
     const BwdSplat* __restrict__ bs, const double* __restrict__ upstream, double* __restrict__ partial,
     uint32_t* __restrict__ used) {
     __shared__ double sAcc[kBWarps][kBE][kNP];
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kBThreads) bwd_pixels_kernel(
         int last = start - 1;
         if (valid) {
             for (int j = start; j < end; ++j) {
-                const BwdSplat s = bs[static_cast<uint32_t>(keys[j])];
+                const BwdSplat s = bs[keys[j]];
                 const Hit h = pixel_hit(s, cx, cy);
                 if (!h.hit) continue;
                 T *= 1.0 - h.alpha;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kBThreads) bwd_pixels_kernel(
 #pragma unroll
                 for (int q = 0; q < kNP; ++q) c[q] = 0.0;
                 if (j >= start && j <= last) {
-                    const BwdSplat s = bs[static_cast<uint32_t>(keys[j])];
+                    const BwdSplat s = bs[keys[j]];
                     const Hit h = pixel_hit(s, cx, cy);
                     if (h.hit) {
                         const double Tb = T / (1.0 - h.alpha);  // transmittance before this splat
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kBThreads) bwd_pixels_kernel(
 // contraction): the exact mode behind sgs_render_f64.
 __global__ void __launch_bounds__(kBThreads) render_f64_kernel(const BwdParams p, int nchunks,
                                                                const uint2* __restrict__ ranges,
-                                                               const unsigned long long* __restrict__ keys,
+                                                               const uint32_t* __restrict__ keys,
                                                                const BwdSplat* __restrict__ bs, double* __restrict__ rgb,
                                                                double* __restrict__ Tout) {
     const int tile = blockIdx.x;
@@ -386,12 +386,12 @@ __global__ void __launch_bounds__(kBThreads) render_f64_kernel(const BwdParams p
         double acc[3] = {0.0, 0.0, 0.0};
         double T = 1.0;
         for (uint32_t j = range.x; j < range.y; ++j) {
-            const BwdSplat s = bs[static_cast<uint32_t>(keys[j])];
+            const BwdSplat s = bs[keys[j]];
             const double dx = cx - s.mx, dy = cy - s.my;
             const double m2 = s.c0 * dx * dx + 2.0 * s.c1 * dx * dy + s.c2 * dy * dy;
             if (m2 > kSupportMahalanobisSq) continue;
             const double a0 = s.op * exp(-0.5 * m2);
-            const double alpha = a0 < kAlphaClamp ? a0 : kAlphaClamp;  // std::min(a, 0.999)
+            const double alpha = kAlphaClamp < a0 ? kAlphaClamp : a0;  // std::min(a, 0.999): NaN stays NaN
             if (alpha < kAlphaMin) continue;
             const double w = alpha * T;
             acc[0] += s.cr * w;
@@ -453,7 +453,7 @@ __device__ void lobe_grad(const double* alpha, double lambda, const double* mu, 
 template <bool F64, int KIND>
 __global__ void bwd_splat_kernel(const BwdParams p, uint64_t V, const uint32_t* __restrict__ order,
                                  const int4* __restrict__ brect, const uint2* __restrict__ ranges,
-                                 const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ rank_of,
+                                 const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank_of,
                                  const uint32_t* __restrict__ used, const double* __restrict__ partial,
                                  double* __restrict__ grads, int stride) {
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -469,12 +469,12 @@ __global__ void bwd_splat_kernel(const BwdParams p, uint64_t V, const uint32_t* 
             const int lim = lo + static_cast<int>(used[tile]);
             while (lo < hi) {  // first entry with rank >= r (lists are in depth order)
                 const int mid = (lo + hi) >> 1;
-                if (rank_of[static_cast<uint32_t>(keys[mid])] < r)
+                if (rank_of[keys[mid]] < r)
                     lo = mid + 1;
                 else
                     hi = mid;
             }
-            if (lo < lim && static_cast<uint32_t>(keys[lo]) == g)
+            if (lo < lim && keys[lo] == g)
                 for (int q = 0; q < kNP; ++q) acc[q] += partial[static_cast<size_t>(lo) * kNP + q];
         }
     // ---- pass 2 (grad.cpp:155-244) ----
@@ -638,7 +638,7 @@ __global__ void finite_check_kernel(const double* __restrict__ v, size_t n, int*
 
 template <bool F64, int KIND>
 void launch_kind_bwd(const BwdParams& p, uint64_t V, int nchunks, int ntile, const uint32_t* order,
-                     const int4* brect, const uint2* ranges, const unsigned long long* keys, BwdSplat* bs,
+                     const int4* brect, const uint2* ranges, const uint32_t* keys, BwdSplat* bs,
                      uint32_t* rank_of, uint32_t* used, double* partial, const double* upstream, double* grads,
                      int stride, cudaStream_t s) {
     const unsigned vb = static_cast<unsigned>((V + 127) / 128);
@@ -651,7 +651,7 @@ void launch_kind_bwd(const BwdParams& p, uint64_t V, int nchunks, int ntile, con
 
 template <bool F64, int KIND>
 void launch_kind_render64(const BwdParams& p, uint64_t V, int nchunks, int ntile, const uint32_t* order,
-                          const uint2* ranges, const unsigned long long* keys, BwdSplat* bs, uint32_t* rank_of,
+                          const uint2* ranges, const uint32_t* keys, BwdSplat* bs, uint32_t* rank_of,
                           double* rgb, double* T, cudaStream_t s) {
     if (V) bwd_prep_kernel<F64, KIND><<<static_cast<unsigned>((V + 127) / 128), 128, 0, s>>>(p, V, order, bs, rank_of);
     if (ntile) render_f64_kernel<<<ntile, kBThreads, 0, s>>>(p, nchunks, ranges, keys, bs, rgb, T);
@@ -661,7 +661,7 @@ void launch_kind_render64(const BwdParams& p, uint64_t V, int nchunks, int ntile
 
 void launch_render_f64(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
                        const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
-                       const uint2* ranges, const unsigned long long* keys, void* bs, uint32_t* rank_of, double* rgb,
+                       const uint2* ranges, const uint32_t* keys, void* bs, uint32_t* rank_of, double* rgb,
                        double* T, cudaStream_t s) {
     BwdParams p{};
     p.sp = sp;
@@ -693,7 +693,7 @@ void launch_finite_check(const double* v, size_t n, int* bad, cudaStream_t s) {
 
 void launch_backward(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
                      const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
-                     const int4* brect, const uint2* ranges, const unsigned long long* keys, void* bs,
+                     const int4* brect, const uint2* ranges, const uint32_t* keys, void* bs,
                      uint32_t* rank_of, uint32_t* used, double* partial, const double* upstream, double* grads,
                      int stride, cudaStream_t s) {
     BwdParams p{};

@@ -1,19 +1,20 @@
-// binning.cu -- K3 (per-rank tile counts), K4 (tile-key emission), K6 (tile ranges).
+// binning.cu -- K3+K4 (tile binning in one pass) and K6 (tile ranges).
 //
 // Replaces build_tile_grid (proj/src/raster.cpp:108-130). The reference walks the
 // splats in blending order and push_backs the rank into every tile of the
-// inclusive rectangle. Here, for a depth chunk of ranks [rb, re):
-//   K3  counts[r-rb] = tiles of rect(order[r]) not yet terminated; a device-wide
-//       exclusive scan gives each rank its first output slot (so a warp of 32
-//       consecutive ranks owns one contiguous output range)
-//   K4  keys[off + j] = (tile << 32) | gaussian_index, tiles row-major as the
-//       reference's (ty, tx) double loop visits them; keys leave K4 in rank order
-//   K5  stable radix sort on the tile bits only (capi.cu) keeps rank order inside a
-//       tile, so each tile's run equals the reference's TileGrid list exactly
-//   K6  ranges[tile] = [first, last + 1) of the tile's run.
+// inclusive rectangle. Here, for a depth chunk of ranks [rb, re), ONE kernel
+// (bin_emit_kernel) counts each rank's live tiles, turns the counts into output
+// offsets with a warp-level decoupled look-back scan across the grid (so a warp of 32
+// consecutive ranks owns one contiguous output range), and emits the (tile id,
+// Gaussian index) pairs, tiles row-major as the reference's (ty, tx) double loop
+// visits them. The pairs leave in rank order; K5 (radix.cu, stable on the tile id)
+// then yields every tile's run in rank order -- the reference's TileGrid list -- and
+// K6 finds each tile's [first, last + 1).
 // A tile whose every pixel has terminated (transmittance below the threshold) in
-// an earlier chunk receives no further keys: the reference never reads past that
+// an earlier chunk receives no further pairs: the reference never reads past that
 // point of its list (raster.cpp:177-179), so the image is unchanged.
+#include <cstddef>
+
 #include "sgs_internal.h"
 
 namespace sgs {
@@ -43,127 +44,21 @@ __device__ __forceinline__ uint32_t live_tiles(const int4 rc, const DoneView& do
     return c;
 }
 
-// Rank-ordered copy of the binning inputs, gathered once per frame so that every
-// chunk's K3/K4 reads them coalesced: brect[r] = rects[order[r]],
-// bmeta[r] = (order[r], tiles of its rectangle).
-__global__ void gather_bins_kernel(uint64_t n, const uint32_t* __restrict__ order,
-                                   const int4* __restrict__ rects, const Counters* __restrict__ ctr,
-                                   int4* __restrict__ brect, uint2* __restrict__ bmeta) {
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const uint32_t g = order[r];
-    // visible splats (ranks below V) carry their rectangle from K1; culled ones none
-    const int4 rc = r < ctr->visible ? rects[g] : make_int4(0, -1, 0, -1);
-    const uint32_t c = rect_area(rc);
-    bmeta[r] = make_uint2(g, c);
-    if (c) brect[r] = rc;
-}
-
-__global__ void count_tiles_kernel(uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta,
-                                   const int4* __restrict__ brect, const uint32_t* __restrict__ done_bytes,
-                                   int tiles_x, int ntile, unsigned long long* __restrict__ counts) {
-    extern __shared__ uint32_t done_bits[];
-    DoneView done{done_bytes};
-    if (done_bytes && ntile <= kMaxBitmapTiles) {
-        load_done_bitmap(done_bytes, ntile, done_bits);
-        done.bits = done_bits;
-    }
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t r = rb + k;
-    if (r < re) {
-        uint32_t c = bmeta[r].y;
-        if (done_bytes) {
-            const int4 rc = brect[r];  // issued with the bmeta load (stale when c == 0, unused)
-            if (c) c = live_tiles(rc, done, tiles_x);
-        }
-        counts[k] = c;
-    } else if (r == re) {
-        counts[k] = 0;
-    }
-}
-
-// One thread per rank writes its splat's keys into its own slot range. Splats
-// covering more than kCoop tiles are emitted cooperatively by the whole warp
-// (ballot-compacted over the live tiles) so one large splat does not serialise a
-// lane while 31 idle.
-constexpr uint32_t kCoop = 32;
-
-__global__ void emit_keys_kernel(uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta,
-                                 const int4* __restrict__ brect, const uint32_t* __restrict__ done_bytes,
-                                 const unsigned long long* __restrict__ offsets, int tiles_x, int ntile,
-                                 unsigned long long* __restrict__ keys, uint64_t capacity) {
-    extern __shared__ uint32_t done_bits[];
-    DoneView done{done_bytes};
-    if (done_bytes && ntile <= kMaxBitmapTiles) {
-        load_done_bitmap(done_bytes, ntile, done_bits);
-        done.bits = done_bits;
-    }
-    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t r = rb + k;
-    const unsigned lane = threadIdx.x & 31;
-    uint32_t g = 0, area = 0;
-    int4 rc = make_int4(0, -1, 0, -1);
-    unsigned long long off = 0;
-    if (r < re) {
-        // the scanned counts tell which ranks emit anything: in late chunks most
-        // ranks only cover finished tiles and are skipped before their rect is read
-        off = offsets[k];
-        if (offsets[k + 1] != off) {
-            const uint2 m = bmeta[r];
-            g = m.x;
-            area = m.y;
-            rc = brect[r];
-        }
-    }
-    const uint32_t w = static_cast<uint32_t>(rc.y - rc.x + 1);
-    if (area && area <= kCoop) {
-        uint32_t o = 0;
-        for (uint32_t j = 0; j < area; ++j) {
-            const uint32_t tile = static_cast<uint32_t>(rc.z + static_cast<int>(j / w)) * tiles_x +
-                                  static_cast<uint32_t>(rc.x + static_cast<int>(j % w));
-            if (done(tile)) continue;
-            if (off + o < capacity) keys[off + o] = (static_cast<unsigned long long>(tile) << 32) | g;
-            ++o;
-        }
-    }
-    unsigned big = __ballot_sync(0xffffffffu, area > kCoop);
-    while (big) {
-        const int src = __ffs(big) - 1;
-        big &= big - 1;
-        const uint32_t a = __shfl_sync(0xffffffffu, area, src);
-        const uint32_t gg = __shfl_sync(0xffffffffu, g, src);
-        const int x0 = __shfl_sync(0xffffffffu, rc.x, src);
-        const int x1 = __shfl_sync(0xffffffffu, rc.y, src);
-        const int y0 = __shfl_sync(0xffffffffu, rc.z, src);
-        unsigned long long o = __shfl_sync(0xffffffffu, off, src);
-        const uint32_t ww = static_cast<uint32_t>(x1 - x0 + 1);
-        for (uint32_t base = 0; base < a; base += 32) {
-            const uint32_t j = base + lane;
-            uint32_t tile = 0;
-            bool live = false;
-            if (j < a) {
-                tile = static_cast<uint32_t>(y0 + static_cast<int>(j / ww)) * tiles_x +
-                       static_cast<uint32_t>(x0 + static_cast<int>(j % ww));
-                live = !done(tile);
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, live);
-            const unsigned long long pos = o + __popc(m & ((1u << lane) - 1u));
-            if (live && pos < capacity) keys[pos] = (static_cast<unsigned long long>(tile) << 32) | gg;
-            o += __popc(m);
-        }
-    }
-}
-
-// K3+K4 fused (the default): one pass per chunk counts each rank's live tiles,
-// scans the counts across the grid with a decoupled look-back (CTAs take logical
-// block numbers from a ticket, so every predecessor a CTA waits on is already
-// resident), and emits the keys at the scanned offsets. The last block finishes
-// the scan as finish_scan_kernel does (total, overflow flag, chunk count).
+// K3+K4: one pass per chunk counts each rank's live tiles, scans the counts across
+// the grid with a decoupled look-back (CTAs take logical block numbers from a
+// ticket, so every predecessor a CTA waits on is already resident), and emits the
+// pairs at the scanned offsets, adding each tile id's K5 digits to block histograms.
+// The last block records the chunk's P (total, overflow flag) and opens the sort's
+// epoch.
 // status[b] = flag << 62 | value: flag 1 = block aggregate, 2 = inclusive prefix.
 constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagPre = 2ULL << 62;
 constexpr unsigned long long kValMask = (1ULL << 62) - 1;
 constexpr int kBinThreads = 1024;
+// Splats covering more than kCoop tiles are emitted cooperatively by the whole warp
+// (ballot-compacted over the live tiles) so one large splat does not serialise a
+// lane while 31 idle.
+constexpr uint32_t kCoop = 32;
 
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -176,10 +71,13 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta, const int4* __restrict__ brect,
-    const uint32_t* __restrict__ done_bytes, int tiles_x, int ntile, unsigned long long* __restrict__ keys,
-    uint64_t capacity, unsigned long long* __restrict__ status, Counters* __restrict__ ctr) {
+    const uint32_t* __restrict__ done_bytes, int tiles_x, int ntile, uint32_t* __restrict__ tk,
+    uint32_t* __restrict__ tv, uint64_t capacity, unsigned long long* __restrict__ status, const TileDigits td,
+    SortCtl* __restrict__ ctl, Counters* __restrict__ ctr) {
     extern __shared__ uint32_t done_bits[];
     __shared__ uint32_t s_blk;
+    __shared__ uint32_t s_hist[4 * 256];
+    for (int k = threadIdx.x; k < td.passes * 256; k += kBinThreads) s_hist[k] = 0;
     __shared__ unsigned long long s_warp[kBinThreads / 32];
     __shared__ unsigned long long s_base;
     const unsigned nblk = gridDim.x;
@@ -257,16 +155,26 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
         if (lane == 0) {
             s_base = excl;
             if (blk == nblk - 1) {
-                // finish the chunk's scan (finish_scan_kernel)
+                // the chunk's P: total, overflow flag, clamped count for K5-K7
                 const unsigned long long p = excl + total;
                 ctr->tile_entries += p;
                 if (p > ctr->max_chunk_entries) ctr->max_chunk_entries = p;
                 if (p > capacity) ctr->key_overflow = 1;
                 ctr->chunk_entries = p < capacity ? p : capacity;
+                ctl->epoch += 1;  // (the K5 passes of this chunk run after this kernel)
             }
         }
     }
     __syncthreads();
+    // emit one (tile, index) pair at slot pos (dropped past the capacity: the frame is redone)
+    auto put = [&](unsigned long long pos, uint32_t tile, uint32_t gi) {
+        if (pos < capacity) {
+            tk[pos] = tile;
+            tv[pos] = gi;
+            for (int p = 0; p < td.passes; ++p)
+                atomicAdd(&s_hist[p * 256 + ((tile >> td.shift[p]) & ((1u << td.bits[p]) - 1u))], 1u);
+        }
+    };
     const unsigned long long off = s_base + s_warp[warp] + inc - c;
     const uint32_t w = static_cast<uint32_t>(rc.y - rc.x + 1);
     if (area && area <= kCoop) {
@@ -275,7 +183,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
             const uint32_t tile = static_cast<uint32_t>(rc.z + static_cast<int>(j / w)) * tiles_x +
                                   static_cast<uint32_t>(rc.x + static_cast<int>(j % w));
             if (done(tile)) continue;
-            if (off + o < capacity) keys[off + o] = (static_cast<unsigned long long>(tile) << 32) | g;
+            put(off + o, tile, g);
             ++o;
         }
     }
@@ -301,10 +209,13 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
             }
             const unsigned m = __ballot_sync(0xffffffffu, live);
             const unsigned long long pos = o + __popc(m & ((1u << lane) - 1u));
-            if (live && pos < capacity) keys[pos] = (static_cast<unsigned long long>(tile) << 32) | gg;
+            if (live) put(pos, tile, gg);
             o += __popc(m);
         }
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < td.passes * 256; k += kBinThreads)
+        if (s_hist[k]) atomicAdd(&ctl->hist[k >> 8][k & 255], s_hist[k]);
 }
 
 // Per-frame counters without the copy engines: the init is a kernel, and the final
@@ -323,24 +234,14 @@ __global__ void counters_publish_kernel(const Counters* __restrict__ d, Counters
 }
 
 __global__ void tile_ranges_kernel(const unsigned long long* __restrict__ count,
-                                   const unsigned long long* __restrict__ keys, uint2* __restrict__ ranges) {
+                                   const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges) {
     const uint64_t p = *count;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < p;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
-        if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t) ranges[t].x = static_cast<uint32_t>(i);
-        if (i == p - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t)
-            ranges[t].y = static_cast<uint32_t>(i + 1);
+        const uint32_t t = tiles[i];
+        if (i == 0 || tiles[i - 1] != t) ranges[t].x = static_cast<uint32_t>(i);
+        if (i == p - 1 || tiles[i + 1] != t) ranges[t].y = static_cast<uint32_t>(i + 1);
     }
-}
-
-__global__ void finish_scan_kernel(const unsigned long long* __restrict__ total, uint64_t capacity,
-                                   Counters* __restrict__ ctr) {
-    const unsigned long long p = *total;
-    ctr->tile_entries += p;
-    if (p > ctr->max_chunk_entries) ctr->max_chunk_entries = p;
-    if (p > capacity) ctr->key_overflow = 1;
-    ctr->chunk_entries = p < capacity ? p : capacity;
 }
 
 }  // namespace
@@ -349,54 +250,42 @@ static size_t bitmap_smem(const uint32_t* done, int ntile) {
     return done && ntile <= kMaxBitmapTiles ? static_cast<size_t>((ntile + 31) / 32) * 4 : 0;
 }
 
-void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const Counters* ctr,
-                        int4* brect, uint2* bmeta, cudaStream_t stream) {
-    if (n == 0) return;
-    gather_bins_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, order, rects, ctr,
-                                                                                 brect, bmeta);
-}
-
-void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
-                        const uint32_t* done, int tiles_x, int ntile, unsigned long long* counts,
+void launch_tile_ranges(const unsigned long long* d_count, const uint32_t* tiles, uint2* ranges,
                         cudaStream_t stream) {
-    const uint64_t n = re - rb + 1;
-    // large CTAs amortise the bitmap load
-    count_tiles_kernel<<<static_cast<unsigned>((n + 1023) / 1024), 1024, bitmap_smem(done, ntile), stream>>>(
-        rb, re, bmeta, brect, done, tiles_x, ntile, counts);
+    tile_ranges_kernel<<<148 * 8, 256, 0, stream>>>(d_count, tiles, ranges);
 }
 
-void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
-                           const uint32_t* done, const unsigned long long* offsets,
-                           int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
-                           cudaStream_t stream) {
-    if (re <= rb) return;
-    const uint64_t n = re - rb;
-    emit_keys_kernel<<<static_cast<unsigned>((n + 1023) / 1024), 1024, bitmap_smem(done, ntile), stream>>>(
-        rb, re, bmeta, brect, done, offsets, tiles_x, ntile, keys, capacity);
-}
-
-void launch_tile_ranges(const unsigned long long* d_count, const unsigned long long* keys, uint2* ranges,
-                        cudaStream_t stream) {
-    tile_ranges_kernel<<<148 * 8, 256, 0, stream>>>(d_count, keys, ranges);
-}
-
-void launch_finish_scan(const unsigned long long* total, uint64_t capacity, Counters* ctr,
-                        cudaStream_t stream) {
-    finish_scan_kernel<<<1, 1, 0, stream>>>(total, capacity, ctr);
+TileDigits tile_digits(int tile_bits) {
+    // digit widths split evenly (13 tile bits at 1080p -> 7 + 6)
+    TileDigits td{};
+    td.passes = (tile_bits + 7) / 8;
+    int shift = 0;
+    for (int i = 0; i < td.passes; ++i) {
+        td.bits[i] = tile_bits / td.passes + (i < tile_bits % td.passes ? 1 : 0);
+        td.shift[i] = shift;
+        shift += td.bits[i];
+    }
+    return td;
 }
 
 size_t bin_emit_status_bytes(uint64_t ranks) {
     return ((ranks + kBinThreads - 1) / kBinThreads + 1) * sizeof(unsigned long long);
 }
 
-void launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                     int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
-                     unsigned long long* status, Counters* ctr, cudaStream_t stream) {
+cudaError_t launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
+                            int tiles_x, int ntile, uint32_t* tk, uint32_t* tv, uint64_t capacity,
+                            unsigned long long* status, const TileDigits& td, SortCtl* ctl, Counters* ctr,
+                            cudaStream_t stream) {
     const uint64_t n = re > rb ? re - rb : 0;
     const unsigned grid = static_cast<unsigned>(n ? (n + kBinThreads - 1) / kBinThreads : 1);
-    cudaMemsetAsync(status, 0, (grid + 1) * sizeof(unsigned long long), stream);
+    cudaError_t e = cudaMemsetAsync(status, 0, (grid + 1) * sizeof(unsigned long long), stream);
+    if (e == cudaSuccess)  // the K5 tickets and histograms this chunk's pairs fill
+        e = cudaMemsetAsync(&ctl->ticket[0], 0, sizeof(SortCtl) - offsetof(SortCtl, ticket), stream);
+    if (e != cudaSuccess) return e;
     bin_emit_kernel<<<grid, kBinThreads, bitmap_smem(done, ntile), stream>>>(rb, re, bmeta, brect, done, tiles_x,
-                                                                             ntile, keys, capacity, status, ctr);
+                                                                             ntile, tk, tv, capacity, status, td,
+                                                                             ctl, ctr);
+    return cudaGetLastError();
 }
 
 void launch_counters_init(Counters* c, cudaStream_t stream) { counters_init_kernel<<<1, 32, 0, stream>>>(c); }

@@ -1,12 +1,12 @@
 // capi.cu -- the C-ABI (include/sgs.h): contexts, device scenes, frame orchestration.
 //
 // Frame pipeline, enqueued on a lane stream with no host
-// round trip: K1 preprocess -> K2 exact bucket sort of the FP64 depth keys ->
-// rank-ordered bin gather -> per depth chunk { K3 tile counts + scan -> K4 emit
-// (tile, index) keys -> K5 radix sort on the tile bits -> K6 tile ranges -> K7
-// persistent compositor } -> one 128-B D2H of the counters (errors, overflow
-// retries, stats). Batches alternate views over two lanes. CUB (CCCL 2.8) supplies
-// the scans and the rare 64-bit fallback sort.
+// round trip: K1 preprocess -> K2 exact depth order (radix.cu: 32-bit keys, 4 onesweep
+// passes, run fix-up, rank-ordered binning inputs) -> per depth chunk { K3+K4 count,
+// look-back scan and emission of (tile, index) pairs -> K5 onesweep passes on the
+// tile id -> K6 tile ranges -> K7 persistent compositor } -> the counters (errors,
+// overflow retries, stats) written to mapped host memory. Views are dealt over
+// lanes (streams with their own arenas). Every kernel is the library's own.
 #include <algorithm>
 #include <atomic>
 #include <iterator>
@@ -17,9 +17,6 @@
 #include <mutex>
 #include <string>
 #include <vector>
-
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "ply_internal.h"
 #include "projection.cuh"
@@ -104,11 +101,13 @@ struct Lane {
     cudaStream_t stream = nullptr;  // the lane's current stream: plain or ranked
     cudaStream_t plain = nullptr, ranked = nullptr;
     cudaEvent_t swap = nullptr;
-    DevBuf keys_a, keys_b, iota, order, rec, colour, rects, brect, bmeta, counts, offsets;
-    DevBuf buckets;  // K2 bucket histogram / offsets / cursors
-    DevBuf work;     // K7 work list (+ 3 control words)
-    DevBuf tkeys_a, tkeys_b, ranges, tile_done, pix_state, pix_walked, cub_temp, sort_hist;
-    DevBuf tb_cnt, tb_cur, tb_items, tb_ctl;  // tile-major binning (tile_bins.cu)
+    DevBuf keys_a, order, rec, colour, rects, brect, bmeta;
+    DevBuf bin_status;  // K3+K4 look-back status
+    DevBuf work;        // K7 work list (+ control words)
+    // (tile id, Gaussian index) pairs, ping-pong for K5; also K2's sort scratch
+    DevBuf tk_a, tv_a, tk_b, tv_b;
+    DevBuf sort_ctl, sort_status;  // radix sort control block and per-tile status
+    DevBuf ranges, tile_done, pix_state, pix_walked;
     // host-output frames: kOutSlots device buffers per lane drained by the lane's copy
     // stream, so the lane renders its next views while earlier ones cross PCIe
     static constexpr int kOutSlots = 3;
@@ -117,8 +116,7 @@ struct Lane {
     cudaEvent_t copied[kOutSlots] = {};
     cudaStream_t copy_stream = nullptr;
     int out_slot = 0;
-    uint64_t iota_n = 0;
-    uint64_t tkey_cap = 0;  // tile keys per buffer (grow-only, sized from observed P)
+    uint64_t tkey_cap = 0;  // tile pairs per buffer (grow-only, sized from observed P)
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;      // mapped pinned host block the frame's counters land in
     Counters* h_ctr_dev = nullptr;  // its device-side address
@@ -139,8 +137,7 @@ struct Lane {
         sgs_render_stats* stats = nullptr;
         DebugSplat* d_debug = nullptr;
         int mode = 0;
-        bool wide = false;
-        bool rank_major = false;  // rank-major binning + tile sort (a tile list overflowed tile_bins)
+        bool wide = false;  // K2 on the full 64-bit keys (a long run of equal 32-bit keys)
         float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
     } job;
     bool busy = false;
@@ -154,7 +151,8 @@ struct Lane {
     uint64_t g_launches = 0, g_lib_launches = 0;
     // results of the last frame (device pointers into the buffers above)
     const uint32_t* last_order = nullptr;
-    const unsigned long long* last_tile_keys = nullptr;
+    const uint32_t* last_tiles = nullptr;  // sorted tile ids of the last chunk
+    const uint32_t* last_list = nullptr;   // their Gaussian indices (the tile lists)
     uint64_t last_v = 0, last_p = 0;
 };
 
@@ -172,9 +170,6 @@ struct sgs_context {
     int k1_group = 1;                  // views per multi-view K1 (SGS_K1_GROUP, 2..4; measured: no gain)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
-    bool two_level = true;   // K2 variant (SGS_DEPTH_SORT=bucket selects the one-level bucket sort)
-    bool tile_major = false;  // tile-major binning (tile_bins.cu, SGS_BIN=tile; measured slower)
-    bool fused_bin = false;  // K3+K4 in one look-back pass (SGS_BIN_FUSED=1); default: count, CUB scan, emit
     std::vector<uint64_t> chunk_divs;  // depth-chunk boundaries N/div (SGS_DEPTH_CHUNKS; else by N)
     bool chunk_divs_set = false;
     cudaEvent_t fork = nullptr;
@@ -182,6 +177,7 @@ struct sgs_context {
     bool tight_rect = true; // render frames bin into the cut ellipse's tiles (SGS_TIGHT_RECT=0: 3-sigma rects)
     bool rank_host = true;  // ranked lane streams for host-frame batches (SGS_RANK_HOST=0 disables)
     bool trace = false;  // SGS_TRACE=1: per-frame lane timeline of each batch on stderr
+    bool debug_capture_fail = false;  // SGS_DEBUG_CAPTURE_FAIL=1: a call the capture refuses (tests the fallback)
     struct TraceRec {
         int lane;
         cudaEvent_t ev[3];  // frame start, compositing done, host copies done
@@ -202,6 +198,9 @@ sgs_status validate_camera(const sgs_camera* cam) {
     // Camera::validate, camera.cpp:10-13
     if (cam->fx <= 0 || cam->fy <= 0) return fail(SGS_ERR_INVALID_ARGUMENT, "camera focal lengths must be positive");
     if (cam->width < 1 || cam->height < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "camera image size must be >= 1");
+    // the compositor indexes pixels with 32 bits (the reference would need W H x 32 B)
+    if (static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height) >= (1ULL << 32))
+        return fail(SGS_ERR_INVALID_ARGUMENT, "camera image too large: width * height must be < 2^32");
     return SGS_OK;
 }
 
@@ -271,7 +270,8 @@ enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
 // run_frame_once results besides sgs_status
 constexpr int kRetryWide = 100;  // a run of equal 32-bit depth keys: redo with 64-bit keys
 constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, redo
-constexpr int kRetryRankMajor = 102;  // a tile list exceeded tile_bins' sort capacity: redo rank-major
+// the radix sort's status words hold prefix counts in 30 bits
+constexpr uint64_t kMaxSortKeys = (1ULL << 30) - 1;
 
 // Depth chunking: the first chunk holds the
 // nearest ceil(N / div0) ranks; tiles whose pixels all terminate inside it are
@@ -285,79 +285,6 @@ std::vector<uint64_t> default_chunk_divs(uint64_t n) {
     if (n < (1u << 18)) return {};
     if (n < (2u << 20)) return {8};
     return {16, 4};
-}
-
-sgs_status sort_depth(sgs_context* ctx, Lane& L, uint64_t n, bool wide, cudaStream_t s, const uint32_t** order_out,
-                      bool* gathered) {
-    *gathered = false;
-    uint32_t* order = L.order.as<uint32_t>();
-    size_t temp = 0;
-    if (!wide && ctx->two_level) {
-        // K2: two-level exact sort; also writes brect/bmeta (depth_sort.cu)
-        const int log2c = depth_coarse_log2(n);
-        const size_t half = align_up(depth_two_level_scratch(n, log2c), 256);
-        SGS_CUDA(L.buckets.ensure(2 * half));
-        uint32_t* mat = L.buckets.as<uint32_t>();
-        uint32_t* off = mat + half / 4;
-        const size_t cub_bytes = depth_two_level_cub_bytes(n, log2c);
-        SGS_CUDA(L.cub_temp.ensure(cub_bytes));
-        launch_depth_two_level(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2c, mat, off,
-                               L.keys_b.as<unsigned long long>(), order, L.rects.as<int4>(),
-                               L.brect.as<int4>(), L.bmeta.as<uint2>(), L.cub_temp.ptr, cub_bytes, s);
-        ctx->own_launches += 3;
-        ctx->lib_launches += 2;
-        *gathered = true;
-    } else if (!wide) {
-        // K2: exact bucket sort (depth_sort.cu)
-        const int log2b = depth_bucket_log2(n);
-        const uint32_t nb = 1u << log2b;
-        SGS_CUDA(L.buckets.ensure(static_cast<size_t>(nb + 1) * 4 * 4));
-        uint32_t* hist = L.buckets.as<uint32_t>();
-        uint32_t* off = hist + (nb + 1);
-        uint32_t* cursor = off + (nb + 1);
-        SGS_CUDA(cudaMemsetAsync(hist, 0, static_cast<size_t>(nb + 1) * 4, s));
-        SGS_CUDA(cudaMemsetAsync(cursor, 0, static_cast<size_t>(nb + 1) * 4, s));
-        launch_bucket_hist(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2b, hist, s);
-        SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, hist, off, static_cast<int>(nb + 1), s));
-        SGS_CUDA(L.cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_temp.ptr, temp, hist, off, static_cast<int>(nb + 1), s));
-        launch_bucket_scatter(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2b, off, cursor, order,
-                              L.keys_b.as<unsigned long long>(), s);
-        launch_bucket_sort(nb, off, L.keys_b.as<unsigned long long>(), order, L.d_ctr, cursor + (nb + 1), s);
-        ctx->own_launches += 4;
-        ctx->lib_launches += 2;
-    } else {
-        // fallback: full 64-bit keys (8 passes); stable, so ties keep index order
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, L.keys_a.as<unsigned long long>(),
-                                                 L.keys_b.as<unsigned long long>(), L.iota.as<uint32_t>(), order,
-                                                 static_cast<int>(n), 0, 64, s));
-        SGS_CUDA(L.cub_temp.ensure(temp));
-        SGS_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_temp.ptr, temp, L.keys_a.as<unsigned long long>(),
-                                                 L.keys_b.as<unsigned long long>(), L.iota.as<uint32_t>(), order,
-                                                 static_cast<int>(n), 0, 64, s));
-        ctx->lib_launches += 1 + 8;
-    }
-    SGS_CUDA(cudaGetLastError());
-    *order_out = order;
-    return SGS_OK;
-}
-
-// K3 for ranks [rb, re): counts -> exclusive scan; the total P stays on the device.
-sgs_status count_and_scan(sgs_context* ctx, Lane& L, uint64_t rb, uint64_t re, const uint32_t* done, int tiles_x,
-                          int ntile, cudaStream_t s) {
-    const uint64_t m = re - rb;
-    launch_count_tiles(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, tiles_x, ntile,
-                       L.counts.as<unsigned long long>(), s);
-    size_t temp = 0;
-    SGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, L.counts.as<unsigned long long>(),
-                                           L.offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
-    SGS_CUDA(L.cub_temp.ensure(temp));
-    SGS_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_temp.ptr, temp, L.counts.as<unsigned long long>(),
-                                           L.offsets.as<unsigned long long>(), static_cast<int>(m + 1), s));
-    launch_finish_scan(L.offsets.as<unsigned long long>() + m, L.tkey_cap, L.d_ctr, s);
-    ctx->own_launches += 2;
-    ctx->lib_launches += 2;
-    return SGS_OK;
 }
 
 // Enqueue lane L's job on L.stream without a host round trip (every data-dependent
@@ -383,10 +310,9 @@ std::vector<uint64_t> frame_graph_key(const sgs_context* ctx, const Lane& L) {
                             static_cast<uint64_t>(j.cfg.tile_size), static_cast<uint64_t>(j.cfg.has_override),
                             static_cast<uint64_t>(j.cfg.override_degree), bits(j.cfg.degree_threshold_lo),
                             bits(j.cfg.degree_threshold_hi), bits(j.cfg.early_stop_transmittance),
-                            j.stats ? 1u : 0u, j.wide ? 1u : 0u, j.rank_major ? 1u : 0u,
+                            j.stats ? 1u : 0u, j.wide ? 1u : 0u,
                             static_cast<uint64_t>(j.mode), L.tkey_cap, g_alloc_generation.load(),
-                            ctx->chunking ? 1u : 0u, ctx->tile_major ? 1u : 0u, ctx->fused_bin ? 1u : 0u,
-                            ctx->two_level ? 1u : 0u, ctx->chunk_divs_set ? 1u : 0u};
+                            ctx->chunking ? 1u : 0u, ctx->chunk_divs_set ? 1u : 0u};
     for (uint64_t d : ctx->chunk_divs) k.push_back(d);
     // the scene as the captured kernels see it (plane addresses, layout, axes) and
     // its background (a K7 argument): a freed and re-uploaded scene can reuse the host
@@ -426,12 +352,11 @@ sgs_status launch_frame_graph(sgs_context* ctx, Lane& L, const CamParams& cp, Bo
         const sgs_status st = body();
         capturing = false;
         const cudaError_t ec = cudaStreamEndCapture(s, &g);
-        if (st != SGS_OK) {
+        if (st != SGS_OK || ec != cudaSuccess || !g) {
+            // A capture the driver refused -- at the end, or as a failing call inside the
+            // body (StreamCaptureUnsupported / Invalidated): this context enqueues frames
+            // directly from now on, starting with this one.
             if (g) cudaGraphDestroy(g);
-            return st;
-        }
-        if (ec != cudaSuccess || !g) {
-            // a capture the driver refused: this context enqueues frames directly from now on
             cudaGetLastError();
             ctx->graphs = false;
             ctx->own_launches = own0;
@@ -499,22 +424,34 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     j.ms_bin = j.ms_tsort = j.ms_comp = 0;
 
     SGS_CUDA(L.keys_a.ensure(n1 * 8));
-    SGS_CUDA(L.keys_b.ensure(n1 * 8));
-    if (L.iota.bytes < n1 * 4) L.iota_n = 0;
-    SGS_CUDA(L.iota.ensure(n1 * 4));
     SGS_CUDA(L.order.ensure(n1 * 4));
     SGS_CUDA(L.rec.ensure(n1 * sizeof(SplatRec)));
     SGS_CUDA(L.rects.ensure(n1 * sizeof(int4)));
     SGS_CUDA(L.colour.ensure(n1 * sizeof(float4)));
     SGS_CUDA(L.brect.ensure(n1 * sizeof(int4)));
     SGS_CUDA(L.bmeta.ensure(n1 * sizeof(uint2)));
-    SGS_CUDA(L.counts.ensure((n + 1) * 8));
-    SGS_CUDA(L.offsets.ensure((n + 1) * 8));
+    SGS_CUDA(L.bin_status.ensure(bin_emit_status_bytes(n1)));
     SGS_CUDA(L.ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
-    SGS_CUDA(L.sort_hist.ensure(tile_sort_hist_bytes()));
+    // tile pairs (grow-only; P above the capacity makes the frame regrow and redo);
+    // at least n1, as K2 sorts in these arrays too
     if (L.tkey_cap == 0) L.tkey_cap = std::max<uint64_t>(16 * n, 1 << 20);
-    SGS_CUDA(L.tkeys_a.ensure(L.tkey_cap * 8));
-    SGS_CUDA(L.tkeys_b.ensure(L.tkey_cap * 8));
+    L.tkey_cap = std::min<uint64_t>(std::max<uint64_t>(L.tkey_cap, n1), kMaxSortKeys);
+    if (n1 > kMaxSortKeys) return fail(SGS_ERR_INVALID_ARGUMENT, "more than 2^30 Gaussians in one frame");
+    SGS_CUDA(L.tk_a.ensure(L.tkey_cap * 4));
+    SGS_CUDA(L.tv_a.ensure(L.tkey_cap * 4));
+    SGS_CUDA(L.tk_b.ensure(L.tkey_cap * 4));
+    SGS_CUDA(L.tv_b.ensure(L.tkey_cap * 4));
+    if (L.sort_ctl.bytes < sizeof(SortCtl)) {
+        SGS_CUDA(L.sort_ctl.ensure(sizeof(SortCtl)));
+        SGS_CUDA(cudaMemsetAsync(L.sort_ctl.ptr, 0, L.sort_ctl.bytes, s));
+    }
+    const size_t status_bytes = sort_status_words(L.tkey_cap) * 4;
+    if (L.sort_status.bytes < status_bytes) {  // (tagged per sort: zeroed once, never cleared)
+        SGS_CUDA(L.sort_status.ensure(status_bytes));
+        SGS_CUDA(cudaMemsetAsync(L.sort_status.ptr, 0, L.sort_status.bytes, s));
+    }
+    SortCtl* const sctl = L.sort_ctl.as<SortCtl>();
+    uint32_t* const sstatus = L.sort_status.as<uint32_t>();
     float* d_rgb = j.d_rgb;
     float* d_T = j.d_T;
     const int slot = L.out_slot;
@@ -536,10 +473,6 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             L.h_consts->cam = cp;
             L.h_consts->out_rgb = d_rgb;
             L.h_consts->out_T = d_T;
-        }
-        if (L.iota_n < n) {  // identity values for the depth sort (kept across frames)
-            launch_iota(n, L.iota.as<uint32_t>(), s);
-            L.iota_n = n;
         }
     }
     if (host_out && part != kPre) {
@@ -564,6 +497,9 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         return capturing ? cudaEventRecordWithFlags(L.done, s, cudaEventRecordExternal) : cudaEventRecord(L.done, s);
     };
     auto body = [&]() -> sgs_status {
+        // (test hook: a stream synchronize is illegal inside a capture, as the driver
+        // refusing it mid-body would be)
+        if (capturing && ctx->debug_capture_fail) SGS_CUDA(cudaStreamSynchronize(s));
         if (part != kPost) {
             launch_counters_init(L.d_ctr, s);
             if (mode == kRender)
@@ -586,18 +522,12 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             return SGS_OK;
         }
 
-        // K2
-        const uint32_t* order = L.iota.as<uint32_t>();
-        bool gathered = false;
-        if (n > 1) {
-            sgs_status st = sort_depth(ctx, L, n, j.wide, s, &order, &gathered);
-            if (st != SGS_OK) return st;
-        }
-        if (!gathered) {  // rank-ordered binning inputs, gathered once for every chunk
-            launch_gather_bins(n, order, L.rects.as<int4>(), L.d_ctr, L.brect.as<int4>(),
-                               L.bmeta.as<uint2>(), s);
-            if (n) ctx->own_launches += 1;
-        }
+        // K2: ranks and the rank-ordered binning inputs (radix.cu)
+        const uint32_t* order = L.order.as<uint32_t>();
+        SGS_CUDA(launch_depth_sort(n, L.keys_a.as<unsigned long long>(), L.d_ctr, j.wide, L.tk_a.as<uint32_t>(),
+                                   L.tv_a.as<uint32_t>(), L.tk_b.as<uint32_t>(), L.tv_b.as<uint32_t>(), sctl,
+                                   sstatus, L.rects.as<int4>(), L.order.as<uint32_t>(), L.brect.as<int4>(),
+                                   L.bmeta.as<uint2>(), s, &ctx->own_launches));
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 
         // depth chunks over ranks (bounds known on the host: culled splats sort last and
@@ -621,75 +551,42 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         const float3 bg = make_float3(static_cast<float>(scene->meta.background[0]),
                                       static_cast<float>(scene->meta.background[1]),
                                       static_cast<float>(scene->meta.background[2]));
-        const int tile_bits = std::max(1, ceil_log2(ntile));
+        const TileDigits td = tile_digits(std::max(1, ceil_log2(ntile)));
         const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
         SGS_CUDA(L.work.ensure((7 * work_cap + 8) * sizeof(uint32_t)));  // 6 length classes, 8 control words, background items
         const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
-        // the tile-major binning serves the compositor; the parity dumps, the backward and
-        // a frame whose tile list overflowed its sort use the rank-major keys
-        const bool tile_major = mode == kRender && ctx->tile_major && !j.rank_major;
-        const int pchunks = composite_pixel_chunks(cfg->tile_size);
-        if (tile_major) {
-            SGS_CUDA(L.tb_cnt.ensure(std::max<uint64_t>(ntile, 1) * 4));
-            SGS_CUDA(L.tb_cur.ensure(std::max<uint64_t>(ntile, 1) * 4));
-            SGS_CUDA(L.tb_items.ensure(std::max<uint64_t>(ntile, 1) * 4 * 4));  // 4 size classes
-            SGS_CUDA(L.tb_ctl.ensure(64));
-            SGS_CUDA(cudaMemsetAsync(L.tb_cnt.ptr, 0, ntile * 4, s));  // tb_scan re-zeroes it per chunk
-        }
         for (int c = 0; c < nchunks; ++c) {
             const uint64_t rb = bounds[c], re = bounds[c + 1];
             const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
             if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
-            const uint32_t* list = nullptr;  // the compositor's per-tile lists of Gaussian indices
-            int kstride = 1;
-            const unsigned long long* tkeys = nullptr;
-            if (tile_major) {
-                // B1-B4 (tile_bins.cu); also builds K7's work list
-                launch_tile_bins(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
-                                 L.tile_done.as<uint32_t>() + (ntile + 31) / 32, kp.tiles_x,
-                                 static_cast<int>(ntile), pchunks, c == 0, c == nchunks - 1, order,
-                                 L.tb_cnt.as<uint32_t>(), L.tb_cur.as<uint32_t>(), L.ranges.as<uint2>(),
-                                 L.tkeys_a.as<uint32_t>(), L.tkey_cap, L.work.as<uint32_t>(),
-                                 static_cast<uint32_t>(work_cap), L.work.as<uint32_t>() + 6 * work_cap,
-                                 L.tb_items.as<uint32_t>(), L.tb_ctl.as<uint32_t>(), L.d_ctr, s);
-                SGS_CUDA(cudaGetLastError());
-                ctx->own_launches += 4;
-                list = L.tkeys_a.as<uint32_t>();
-                if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
-            } else {
-                // K3 + K4
-                if (ctx->fused_bin) {
-                    SGS_CUDA(L.counts.ensure(bin_emit_status_bytes(n)));
-                    launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
-                                    static_cast<int>(ntile), L.tkeys_a.as<unsigned long long>(), L.tkey_cap,
-                                    L.counts.as<unsigned long long>(), L.d_ctr, s);
-                    SGS_CUDA(cudaGetLastError());
-                    ctx->own_launches += 1;
-                } else {
-                    sgs_status st = count_and_scan(ctx, L, rb, re, done, kp.tiles_x, static_cast<int>(ntile), s);
-                    if (st != SGS_OK) return st;
-                    launch_emit_tile_keys(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done,
-                                          L.offsets.as<unsigned long long>(), kp.tiles_x, static_cast<int>(ntile),
-                                          L.tkeys_a.as<unsigned long long>(), L.tkey_cap, s);
-                    SGS_CUDA(cudaGetLastError());
-                    if (re > rb) ctx->own_launches += 1;
-                }
-                if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
-                // K5 (device-sized stable radix sort on the tile bits)
-                tkeys =
-                    tile_sort(L.tkeys_a.as<unsigned long long>(), L.tkeys_b.as<unsigned long long>(), d_pc, tile_bits,
-                              L.sort_hist.as<uint32_t>(), s, &ctx->own_launches);
-                // K6
-                SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
-                launch_tile_ranges(d_pc, tkeys, L.ranges.as<uint2>(), s);
-                SGS_CUDA(cudaGetLastError());
-                ctx->own_launches += 1;
-                list = reinterpret_cast<const uint32_t*>(tkeys);  // low words of (tile << 32 | index)
-                kstride = 2;
+            // K3 + K4: (tile, index) pairs of the chunk's ranks, in rank order
+            SGS_CUDA(launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+                                     static_cast<int>(ntile), L.tk_a.as<uint32_t>(), L.tv_a.as<uint32_t>(),
+                                     L.tkey_cap, L.bin_status.as<unsigned long long>(), td, sctl, L.d_ctr, s));
+            ctx->own_launches += 1;
+            if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
+            // K5: stable onesweep passes on the tile id (device-sized)
+            uint32_t* tk = L.tk_a.as<uint32_t>();
+            uint32_t* tv = L.tv_a.as<uint32_t>();
+            uint32_t* tk2 = L.tk_b.as<uint32_t>();
+            uint32_t* tv2 = L.tv_b.as<uint32_t>();
+            for (int p = 0; p < td.passes; ++p) {
+                SGS_CUDA(launch_onesweep_pass(tk, tv, tk2, tv2, d_pc, 0, td.shift[p], td.bits[p], sctl, p, sstatus,
+                                              s));
+                std::swap(tk, tk2);
+                std::swap(tv, tv2);
             }
+            ctx->own_launches += td.passes;
+            // K6
+            SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
+            launch_tile_ranges(d_pc, tk, L.ranges.as<uint2>(), s);
+            SGS_CUDA(cudaGetLastError());
+            ctx->own_launches += 1;
+            const uint32_t* list = tv;  // the compositor's per-tile lists of Gaussian indices
             if (timing) SGS_CUDA(cudaEventRecord(L.ev[5], s));
             L.last_order = order;
-            L.last_tile_keys = tkeys;
+            L.last_tiles = tk;
+            L.last_list = tv;
             // Every decision the host acts on (device errors, depth-tie and tile-key
             // overflows) is final once the last chunk is binned: without stats the
             // counters are published here, so the host settles this frame and queues the
@@ -701,14 +598,13 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             }
             // K7
             if (mode == kRender) {
-                launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, kstride, L.rec.as<SplatRec>(),
-                                 L.colour.as<float4>(), bg, L.pix_state.as<PixelState>(),
-                                 L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
-                                 L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1, L.d_ctr,
-                                 j.stats != nullptr, L.work.as<uint32_t>(), L.work.as<uint32_t>() + 6 * work_cap,
-                                 tile_major, s);
-                SGS_CUDA(cudaGetLastError());
-                ctx->own_launches += tile_major ? 1 : 2;  // (+ the work list kernel)
+                SGS_CUDA(launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, 1, L.rec.as<SplatRec>(),
+                                          L.colour.as<float4>(), bg, L.pix_state.as<PixelState>(),
+                                          L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
+                                          L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1,
+                                          L.d_ctr, j.stats != nullptr, L.work.as<uint32_t>(),
+                                          L.work.as<uint32_t>() + 6 * work_cap, s));
+                ctx->own_launches += 2;  // (+ the work list kernel)
             }
             if (timing) {
                 SGS_CUDA(cudaEventRecord(L.ev[6], s));
@@ -761,9 +657,9 @@ int check_frame(Lane& L) {
     if (hc.err != ~0ULL) return device_error(hc.err, j.scene, &j.cfg);
     if (j.mode == kProjectOnly) return SGS_OK;
     if (hc.tie_overflow && !j.wide) return kRetryWide;
-    if (hc.list_overflow && !j.rank_major) return kRetryRankMajor;
     if (hc.key_overflow) {
-        L.tkey_cap = hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024;
+        if (L.tkey_cap >= kMaxSortKeys) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^30 tile entries in one chunk");
+        L.tkey_cap = std::min<uint64_t>(hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024, kMaxSortKeys);
         return kRetryGrow;
     }
     L.last_v = hc.visible;
@@ -794,9 +690,8 @@ sgs_status finish_frame(sgs_context* ctx, Lane& L) {
     if (!L.busy) return SGS_OK;
     for (int attempt = 0; attempt < 4; ++attempt) {
         const int rc = check_frame(L);
-        if (rc == kRetryWide || rc == kRetryGrow || rc == kRetryRankMajor) {
+        if (rc == kRetryWide || rc == kRetryGrow) {
             if (rc == kRetryWide) L.job.wide = true;
-            if (rc == kRetryRankMajor) L.job.rank_major = true;
             sgs_status st = enqueue_frame(ctx, L);
             if (st != SGS_OK) {
                 L.busy = false;
@@ -1268,13 +1163,11 @@ sgs_status sgs_create(int device, sgs_context** out) {
     if (const char* e = std::getenv("SGS_TIGHT_RECT")) ctx->tight_rect = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_RANK_HOST")) ctx->rank_host = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_TRACE")) ctx->trace = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SGS_DEBUG_CAPTURE_FAIL")) ctx->debug_capture_fail = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
     if (const char* e = std::getenv("SGS_HOST_LANES")) ctx->host_lanes = std::min(std::max(std::atoi(e), 1), kLanes);
     if (const char* e = std::getenv("SGS_K1_GROUP"))
         ctx->k1_group = std::min(std::max(std::atoi(e), 1), std::min(kMaxK1Views, kLanes / 2));
-    if (const char* e = std::getenv("SGS_BIN_FUSED")) ctx->fused_bin = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SGS_BIN")) ctx->tile_major = std::strcmp(e, "tile") == 0;
-    if (const char* e = std::getenv("SGS_DEPTH_SORT")) ctx->two_level = std::strcmp(e, "bucket") != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
         ctx->chunk_divs.clear();
@@ -1297,10 +1190,9 @@ void sgs_destroy(sgs_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (Lane& L : ctx->lane) {
         if (L.stream) cudaStreamSynchronize(L.stream);
-        for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.iota, &L.order, &L.rec, &L.colour, &L.rects, &L.brect,
-                          &L.bmeta, &L.counts, &L.offsets, &L.buckets, &L.work, &L.tkeys_a, &L.tkeys_b, &L.ranges,
-                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.cub_temp, &L.sort_hist, &L.tb_cnt, &L.tb_cur,
-                          &L.tb_items, &L.tb_ctl})
+        for (DevBuf* b : {&L.keys_a, &L.order, &L.rec, &L.colour, &L.rects, &L.brect, &L.bmeta, &L.bin_status,
+                          &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_ctl, &L.sort_status, &L.ranges,
+                          &L.tile_done, &L.pix_state, &L.pix_walked})
             b->release();
         if (L.d_ctr) cudaFree(L.d_ctr);
         if (L.h_ctr) cudaFreeHost(L.h_ctr);
@@ -1629,13 +1521,14 @@ sgs_status sgs_debug_tile_grid(sgs_context* ctx, const sgs_scene* scene, const s
     if (v) SGS_CUDA(cudaMemcpy(ord.data(), L.last_order, v * 4, cudaMemcpyDeviceToHost));
     if (order && v) std::memcpy(order, ord.data(), v * 4);
     if (!offsets && !entries) return SGS_OK;
-    std::vector<unsigned long long> keys(p);
-    if (p) SGS_CUDA(cudaMemcpy(keys.data(), L.last_tile_keys, p * 8, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> tiles(p), list(p);
+    if (p) SGS_CUDA(cudaMemcpy(tiles.data(), L.last_tiles, p * 4, cudaMemcpyDeviceToHost));
+    if (p) SGS_CUDA(cudaMemcpy(list.data(), L.last_list, p * 4, cudaMemcpyDeviceToHost));
     const uint64_t ntile = static_cast<uint64_t>((cam->width + cfg->tile_size - 1) / cfg->tile_size) *
                            static_cast<uint64_t>((cam->height + cfg->tile_size - 1) / cfg->tile_size);
     if (offsets) {
         std::vector<uint64_t> cnt(ntile + 1, 0);
-        for (uint64_t i = 0; i < p; ++i) cnt[keys[i] >> 32]++;
+        for (uint64_t i = 0; i < p; ++i) cnt[tiles[i]]++;
         uint64_t acc = 0;
         for (uint64_t t = 0; t < ntile; ++t) {
             offsets[t] = acc;
@@ -1646,7 +1539,7 @@ sgs_status sgs_debug_tile_grid(sgs_context* ctx, const sgs_scene* scene, const s
     if (entries) {
         std::vector<uint32_t> rank_of(scene->meta.count, 0xFFFFFFFFu);
         for (uint64_t r = 0; r < v; ++r) rank_of[ord[r]] = static_cast<uint32_t>(r);
-        for (uint64_t i = 0; i < p && i < capacity; ++i) entries[i] = rank_of[static_cast<uint32_t>(keys[i])];
+        for (uint64_t i = 0; i < p && i < capacity; ++i) entries[i] = rank_of[list[i]];
     }
     return SGS_OK;
 }
@@ -1900,7 +1793,7 @@ sgs_status sgs_backward(sgs_context* ctx, const sgs_scene* scene, const sgs_came
     SGS_CUDA(cudaMemsetAsync(d_gr, 0, n * stride * 8, s));
     launch_backward(scene->planes, make_cam(cam), kp, scene->meta.shared_axes, scene->meta.background,
                     cfg->has_override ? cfg->override_degree : -1, V, composite_pixel_chunks(cfg->tile_size),
-                    L.last_order, L.brect.as<int4>(), L.ranges.as<uint2>(), L.last_tile_keys, base,
+                    L.last_order, L.brect.as<int4>(), L.ranges.as<uint2>(), L.last_list, base,
                     reinterpret_cast<uint32_t*>(base + o_rank), reinterpret_cast<uint32_t*>(base + o_used),
                     reinterpret_cast<double*>(base + o_part), d_up, d_gr, stride, s);
     SGS_CUDA(cudaGetLastError());
@@ -1936,7 +1829,7 @@ sgs_status sgs_render_f64(sgs_context* ctx, const sgs_scene* scene, const sgs_ca
     double* d_T = host ? (T ? reinterpret_cast<double*>(base + o_T) : nullptr) : T;
     launch_render_f64(scene->planes, make_cam(cam), kp, scene->meta.shared_axes, scene->meta.background,
                       cfg->has_override ? cfg->override_degree : -1, L.last_v, composite_pixel_chunks(cfg->tile_size),
-                      L.last_order, L.ranges.as<uint2>(), L.last_tile_keys, base,
+                      L.last_order, L.ranges.as<uint2>(), L.last_list, base,
                       reinterpret_cast<uint32_t*>(base + o_rank), d_rgb, d_T, s);
     SGS_CUDA(cudaGetLastError());
     ctx->own_launches += 2;

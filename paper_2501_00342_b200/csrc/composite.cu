@@ -6,10 +6,8 @@
 // skip alpha < 1/255, accumulate c * alpha * T, T *= 1 - alpha, stop after the
 // splat that pushed T below the threshold, then add T * background.
 //
-// Two kernels share the scheme below: composite2_kernel (the default: 128 threads
-// per (tile, 256-pixel chunk), two horizontally adjacent pixels per thread, warp w
-// owning one 8x8 quadrant of a 16x16 tile) and composite_kernel (SGS_K7_PX=1: 256
-// threads, one pixel per thread, warp w owning the 16x2 strip of rows 2w, 2w+1).
+// composite2_kernel: 128 threads per (tile, 256-pixel chunk), two horizontally
+// adjacent pixels per thread, warp w owning one 8x8 quadrant of a 16x16 tile.
 //
 // Layout. The tile's list streams through shared memory in batches of 256 64-B
 // records (cp.async gathers, double-buffered). Each warp compacts the batch to the
@@ -39,7 +37,7 @@
 namespace sgs {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kChunkPx = 256;  // pixels per K7 work item (one 16x16 tile)
 
 // The reference's FP64 decision for one (pixel, splat) pair (raster.cpp:165-176).
 __device__ __noinline__ bool exact_alpha(const FrameConsts* __restrict__ fc, uint32_t g, int px, int py,
@@ -57,7 +55,7 @@ __device__ __noinline__ bool exact_alpha(const FrameConsts* __restrict__ fc, uin
                            dmul(dmul(pg.conc, dy), dy));
     if (m2 > kSupportMahalanobisSq) return false;
     double alpha = dmul(pg.opacity, exp(dmul(-0.5, m2)));
-    alpha = alpha < kAlphaClamp ? alpha : kAlphaClamp;  // std::min(a, 0.999)
+    alpha = kAlphaClamp < alpha ? kAlphaClamp : alpha;  // std::min(a, 0.999): NaN stays NaN
     if (alpha < kAlphaMin) return false;
     *alpha_out = static_cast<float>(alpha);
     return true;
@@ -75,31 +73,6 @@ __device__ __forceinline__ void stage_record(const SplatRec* __restrict__ rec, c
     }
     const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&slot[3]));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(colour + g));
-}
-
-struct Pixel {
-    float T, r, g, b;
-    int term;  // position in the batch's compacted walk where T fell below stop
-    bool done;
-};
-
-// One blend step (raster.cpp:177-180). alpha == 0 is an exact no-op.
-__device__ __forceinline__ void step(Pixel& P, float alpha, const float4& C, float stop, int pos) {
-    const float w = alpha * P.T;
-    P.r = fmaf(C.x, w, P.r);
-    P.g = fmaf(C.y, w, P.g);
-    P.b = fmaf(C.z, w, P.b);
-    P.T = P.T * (1.0f - alpha);
-    if (!P.done && P.T < stop) {
-        P.done = true;
-        P.term = pos;
-    }
-}
-
-// FP32 m2 of a record at the pixel centre (fcx, fcy).
-__device__ __forceinline__ float mahal2(const float4& A, float Bx, float fcx, float fcy) {
-    const float dx = fcx - A.x, dy = fcy - A.y;
-    return fmaf(fmaf(A.z, dx, A.w * dy), dx, Bx * dy * dy);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -160,269 +133,12 @@ __device__ __forceinline__ void write_background(int W, int H, const CfgParams& 
     }
 }
 
-// GROUP records per ILP group; MINB min resident CTAs per SM (register cap).
-// Selected at run time by SGS_K7_GROUP / SGS_K7_MINB for tuning.
-template <int kGroup, int MINB, int kBatchT>
-__global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
-    const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
-    const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
-    const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
-    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
-    uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
-    const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
-    uint32_t work_cap) {
-    // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
-    // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
-    // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
-    // Slot kBatch of the current buffer is a null record (never contributes) that pads
-    // the compacted lists to whole groups.
-    constexpr int kBatch = kBatchT;
-    constexpr int kPer = kBatch / kThreads;  // records staged per thread per batch
-    extern __shared__ float4 k7_smem[];
-    float* const out_rgb = fc->out_rgb;  // the frame's outputs (FrameConsts)
-    float* const out_T = fc->out_T;
-    float4(*sRaw)[kBatch + 1][4] = reinterpret_cast<float4(*)[kBatch + 1][4]>(k7_smem);
-    float4* sF = k7_smem + 2 * (kBatch + 1) * 4;  // (lmx, lmy, ext_x, ext_y)
-    uint16_t(*sIdx)[kBatch + 8] = reinterpret_cast<uint16_t(*)[kBatch + 8]>(sF + kBatch);
-    __shared__ unsigned long long s_red[2][kThreads / 32];
-    __shared__ uint32_t s_item;
-
-    if (threadIdx.x < 8) {
-        // null records: m2 = 0 > cut + guard = -1 -> skipped, alpha 0
-        const int b = threadIdx.x >> 2, c = threadIdx.x & 3;
-        sRaw[b][kBatch][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    uint32_t n_class[kWorkClasses], n_items = 0;
-#pragma unroll
-    for (int c = 0; c < kWorkClasses; ++c) n_items += (n_class[c] = work_count[c]);
-    // Persistent CTAs: each pulls (tile, pixel-chunk) items from the chunk's work list
-    // (long tile lists first, built by build_work_kernel).
-    for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(work_next, 1u);
-    __syncthreads();
-    const uint32_t item = s_item;
-    __syncthreads();
-    if (item >= n_items) break;
-    const uint32_t witem = work_item(work, n_class, work_cap, item);
-    const int ts = cfg.tile_size;
-    const int tile = static_cast<int>(witem / nchunks);
-    const int chunk = static_cast<int>(witem - static_cast<uint32_t>(tile) * nchunks);
-    const uint2 range = ranges[tile];
-    const uint32_t start = range.x, end = range.y;
-    // A tile that has never received an entry keeps no per-pixel state at all
-    // (tile_touched), so empty tiles cost neither state writes nor reads.
-    const bool touched = !first && ((tile_touched[tile >> 5] >> (tile & 31)) & 1u);
-
-    const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
-    const int px0 = tx * ts, py0 = ty * ts;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // 16x16: warp strips of 16x2; other tile sizes: 256 consecutive pixels per CTA.
-    int lx, ly;
-    bool inside;
-    if (ts == 16) {
-        lx = lane & 15;
-        ly = warp * 2 + (lane >> 4);
-        inside = true;
-    } else {
-        const int p = chunk * kThreads + threadIdx.x;
-        lx = p % ts;
-        ly = p / ts;
-        inside = p < ts * ts;
-    }
-    const int px = px0 + lx, py = py0 + ly;
-    const bool valid = inside && px < W && py < H;
-    const float stop = cfg.early_stop > 1.0f ? 1.0f : cfg.early_stop;  // (see composite2_kernel)
-    const size_t pix = valid ? static_cast<size_t>(py) * W + px : 0;
-    const float fcx = static_cast<float>(lx) + 0.5f, fcy = static_cast<float>(ly) + 0.5f;
-    Pixel P{1.f, 0.f, 0.f, 0.f, -1, !valid};
-    uint32_t walked = 0;  // entries of the full list walked in earlier chunks
-    if (touched && valid) {
-        const PixelState s = state[pix];
-        P.r = s.r, P.g = s.g, P.b = s.b, P.T = s.T;
-        walked = processed_io[pix];
-        P.done = P.T < stop;
-    }
-    uint32_t processed = P.done ? 0u : end - start;  // entries walked in this chunk
-
-    // The warp's live-pixel-centre bounding box (tile-local) for the batch filter.
-    float wx0 = P.done ? 1e30f : fcx, wx1 = P.done ? -1e30f : fcx;
-    float wy0 = P.done ? 1e30f : fcy, wy1 = P.done ? -1e30f : fcy;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        wx0 = fminf(wx0, __shfl_xor_sync(0xffffffffu, wx0, o));
-        wx1 = fmaxf(wx1, __shfl_xor_sync(0xffffffffu, wx1, o));
-        wy0 = fminf(wy0, __shfl_xor_sync(0xffffffffu, wy0, o));
-        wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
-    }
-    uint32_t guard_hits = 0;
-    uint16_t* idx = sIdx[warp];
-
-    // Software pipeline over batches: keys one batch ahead in registers, records one
-    // batch ahead in shared memory via cp.async, so the dependent key -> record
-    // gather of batch b+1 overlaps the walk of batch b.
-    const int t = threadIdx.x;
-    uint32_t g_next[kPer], g_cur[kPer];  // gaussian indices of this thread's records (next / current batch)
-#pragma unroll
-    for (int h = 0; h < kPer; ++h) {
-        const uint32_t k = start + t + h * kThreads;
-        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
-        if (k < end) stage_record(rec, colour, g_next[h], sRaw[0][t + h * kThreads]);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-#pragma unroll
-    for (int h = 0; h < kPer; ++h) {
-        g_cur[h] = g_next[h];
-        const uint32_t k = start + kBatch + t + h * kThreads;
-        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
-    }
-    int buf = 0;
-
-    for (uint32_t base = start; base < end; base += kBatch) {
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        if (__syncthreads_count(!P.done) == 0) break;
-#pragma unroll
-        for (int h = 0; h < kPer; ++h) {
-            // convert this thread's records of the current batch
-            const int rt = t + h * kThreads;
-            if (base + rt < end) {
-                float4* r = sRaw[buf][rt];
-                const double2 m = *reinterpret_cast<const double2*>(&r[0]);
-                const float4 q1 = r[1];  // ca, cb2, cc, lop
-                const float4 q2 = r[2];  // cut, guard, ext_x, ext_y
-                const float4 q3 = r[3];  // r, g, b, -
-                const float lmx = static_cast<float>(m.x - px0), lmy = static_cast<float>(m.y - py0);
-                r[0] = make_float4(lmx, lmy, q1.x, q1.y);
-                r[1] = make_float4(q1.z, q2.x + q2.y, q2.x - q2.y, q1.w);
-                r[2] = make_float4(q3.x, q3.y, q3.z, __uint_as_float(g_cur[h]));
-                sF[rt] = make_float4(lmx, lmy, q2.z, q2.w);
-            }
-            // prefetch the next batch's record, then the key after it
-            const uint32_t kn = base + kBatch + rt;
-            if (kn < end) stage_record(rec, colour, g_next[h], sRaw[buf ^ 1][rt]);
-            g_cur[h] = g_next[h];
-            g_next[h] = kn + kBatch < end ? __ldg(&keys[static_cast<size_t>(kn + kBatch) * kstride]) : 0u;
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-        buf ^= 1;
-        __syncthreads();
-        const uint32_t nb = min(static_cast<uint32_t>(kBatch), end - base);
-        const float4(*R)[4] = sRaw[buf ^ 1];  // the batch converted above (+ null record)
-        int cnt = 0;
-        if (__any_sync(0xffffffffu, !P.done)) {
-            for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
-                const uint32_t j = j0 + lane;
-                bool hit = false;
-                if (j < nb) {
-                    const float4 F = sF[j];
-                    hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit) idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
-                cnt += __popc(m);
-            }
-        }
-        if (lane < kGroup) idx[cnt + lane] = kBatch;  // pad with the null record
-        __syncwarp();
-        for (int q = 0; q < cnt && !P.done; q += kGroup) {
-            // m2 / alpha of the whole group first (independent), then the blend chain;
-            // slots past cnt re-read record idx[q] and are forced to alpha = 0
-            float alpha[kGroup];
-            bool guard = false;
-            int jj[kGroup];
-#pragma unroll
-            for (int k = 0; k < kGroup; ++k) {
-                const int j = idx[q + k];
-                jj[k] = j;
-                const float4 A = R[j][0];
-                const float4 B = R[j][1];
-                const float m2 = mahal2(A, B.x, fcx, fcy);
-                guard |= m2 <= B.y && m2 >= B.z;
-                alpha[k] = m2 < B.z ? fast_alpha(m2, B.w) : 0.0f;
-            }
-            if (!guard) {
-#pragma unroll
-                for (int k = 0; k < kGroup; ++k) step(P, P.done ? 0.0f : alpha[k], R[jj[k]][2], stop, q + k);
-            } else {
-                // a pair inside the guard band: walk the group one record at a time
-                for (int k = 0; k < kGroup && q + k < cnt && !P.done; ++k) {
-                    const int j = idx[q + k];
-                    const float4 A = R[j][0];
-                    const float4 B = R[j][1];
-                    const float m2 = mahal2(A, B.x, fcx, fcy);
-                    if (m2 > B.y) continue;
-                    float a = alpha[k];
-                    if (m2 >= B.z) {
-                        ++guard_hits;
-                        if (!exact_alpha(fc, __float_as_uint(R[j][2].w), px, py, &a)) continue;
-                    }
-                    step(P, a, R[j][2], stop, q + k);
-                }
-            }
-        }
-        if (P.term >= 0) {
-            processed = base + idx[P.term] + 1 - start;
-            P.term = -2;  // recorded
-        }
-        __syncthreads();
-    }
-
-    // never leave with copies in flight into shared memory
-    asm volatile("cp.async.wait_all;\n" ::);
-    const bool all_done = __syncthreads_and(P.done) != 0;
-    const bool finalize = last || all_done;
-    if (valid) {
-        if (finalize) {
-            if (out_rgb) {
-                out_rgb[pix * 3 + 0] = P.r + P.T * bg.x;
-                out_rgb[pix * 3 + 1] = P.g + P.T * bg.y;
-                out_rgb[pix * 3 + 2] = P.b + P.T * bg.z;
-            }
-            if (out_T) out_T[pix] = P.T;
-        } else {
-            state[pix] = PixelState{P.r, P.g, P.b, P.T};
-            processed_io[pix] = walked + processed;
-        }
-    }
-    if (!last && all_done && threadIdx.x == 0) atomicOr(&tile_done[tile >> 5], 1u << (tile & 31));
-    if (!finalize && !touched && threadIdx.x == 0) atomicOr(&tile_touched[tile >> 5], 1u << (tile & 31));
-    if (want_stats) {
-        // E_t = max over the tile's pixels of the entries of its full list each pixel
-        // walked (counted when the tile finalises); guard hits summed over chunks.
-        unsigned long long e = (finalize && valid) ? walked + processed : 0ULL;
-        unsigned long long h = guard_hits;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
-            h += __shfl_xor_sync(0xffffffffu, h, o);
-        }
-        if (lane == 0) {
-            s_red[0][warp] = e;
-            s_red[1][warp] = h;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long em = 0, hs = 0;
-            for (int w = 0; w < kThreads / 32; ++w) {
-                em = max(em, s_red[0][w]);
-                hs += s_red[1][w];
-            }
-            // pixel chunks of one tile (tile_size > 16) each report their own max
-            if (em) atomicAdd(&ctr->block_entries, em);
-            if (hs) atomicAdd(&ctr->guard_hits, hs);
-        }
-    }
-    __syncthreads();
-    }  // persistent loop
-    // background-only items (tiles that never received an entry): T = 1, rgb = bg
-    write_background<kThreads>(W, H, cfg, nchunks, work_count, out_rgb, out_T, bg);
-}
-
 // ---------------------------------------------------------------------------
 // K7, two pixels per thread (the default). One CTA of 128 threads per (tile,
 // 256-pixel chunk); on 16x16 tiles warp w owns one 8x8 quadrant and a thread the two
 // horizontally adjacent pixels (2c, 2c+1) of one row, so a record's dy terms
 // (dy, 2b dy, c dy^2) and its shared-memory reads serve both pixels. m2 is formed
-// per pixel exactly as in composite_kernel (same operations, same rounding), and
+// per pixel with the same operations and rounding for both pixels, and
 // the blend chain drops the per-step termination bookkeeping: transmittance only
 // decreases, so "the pixel stopped before this splat" is T < stop, tested in the
 // chain; the splat that stopped it is found afterwards by replaying the group's T
@@ -468,7 +184,11 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
     const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
     uint32_t work_cap) {
-    // shared layout as composite_kernel (batch 256, null record at slot kBatch)
+    // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
+    // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
+    // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
+    // Slot kBatch of each buffer is a null record (never contributes) that pads the
+    // compacted lists to whole groups.
     constexpr int kBatch = 256;
     constexpr int kPer = kBatch / kThreads2;
     constexpr int kWarps = kThreads2 / 32;
@@ -641,7 +361,8 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
                     const float4 B = R[j][1];
                     float m0, m1;
                     mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
-                    guard |= (m0 <= B.y && m0 >= B.z) || (m1 <= B.y && m1 >= B.z);
+                    // (NaN-aware: a NaN m2 is decided by the FP64 path, as the reference blends it)
+                    guard |= !(m0 > B.y || m0 < B.z) || !(m1 > B.y || m1 < B.z);
                     a0[k] = m0 < B.z ? fast_alpha(m0, B.w) : 0.0f;
                     a1[k] = m1 < B.z ? fast_alpha(m1, B.w) : 0.0f;
                 }
@@ -692,8 +413,10 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
                     Pix& P = e ? P1 : P0;
                     bool& live = e ? live1 : live0;
                     if (!live || m[e] > B.y) continue;
-                    float a = m[e] < B.z ? fast_alpha(m[e], B.w) : 0.0f;
-                    if (m[e] >= B.z) {
+                    float a;
+                    if (m[e] < B.z) {
+                        a = fast_alpha(m[e], B.w);
+                    } else {  // inside the band (or NaN): the reference's FP64 decision
                         ++guard_hits;
                         if (!exact_alpha(fc, __float_as_uint(C.w), e ? pxb : pxa, e ? pyb : pya, &a)) continue;
                     }
@@ -804,94 +527,56 @@ __global__ void build_work_kernel(const uint2* __restrict__ ranges, const uint32
 
 int composite_pixel_chunks(int ts) {
     const long long tile_px = static_cast<long long>(ts) * ts;
-    return static_cast<int>((tile_px + kThreads - 1) / kThreads);
+    return static_cast<int>((tile_px + kChunkPx - 1) / kChunkPx);
 }
 
-void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
-                      const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
-                      const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
-                      uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
-                      bool want_stats, uint32_t* work, uint32_t* wctl, bool work_ready, cudaStream_t stream) {
+namespace {
+template <int G, bool ROW>
+cudaError_t k7_attr(size_t smem) {
+    static const cudaError_t e = cudaFuncSetAttribute(composite2_kernel<G, 4, ROW>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      static_cast<int>(smem));
+    return e;
+}
+}  // namespace
+
+cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
+                             const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
+                             const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
+                             uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
+                             bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
     const uint32_t ntile = static_cast<uint32_t>(cfg.tiles_x) * static_cast<uint32_t>(cfg.tiles_y);
     const uint32_t cap = ntile * static_cast<uint32_t>(nchunks);
-    if (!work_ready) {  // (the tile-major binning's scan builds the list itself)
-        cudaMemsetAsync(wctl, 0, kWorkCtl * sizeof(uint32_t), stream);
-        build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
-                                                                 last ? 1 : 0, ntile, nchunks, cap, work, wctl);
-    }
+    cudaError_t e = cudaMemsetAsync(wctl, 0, kWorkCtl * sizeof(uint32_t), stream);
+    if (e != cudaSuccess) return e;
+    build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
+                                                             last ? 1 : 0, ntile, nchunks, cap, work, wctl);
     static const int group = [] {
         const char* e = std::getenv("SGS_K7_GROUP");
-        return e ? std::atoi(e) : 4;
+        return e && std::atoi(e) == 2 ? 2 : 4;
     }();
-    static const int minb = [] {
-        const char* e = std::getenv("SGS_K7_MINB");
-        return e ? std::atoi(e) : 2;
-    }();
-    // persistent grid: resident CTAs only
-    const unsigned grid = 148u * static_cast<unsigned>(minb);
-    static const int batch = [] {
-        const char* e = std::getenv("SGS_K7_BATCH");
-        return e && std::atoi(e) == 512 ? 512 : 256;
-    }();
-    auto smem_for = [](int bt) {
-        return static_cast<size_t>(2 * (bt + 1) * 4 + bt) * sizeof(float4) +
-               static_cast<size_t>(kThreads / 32) * (bt + 8) * sizeof(uint16_t);
-    };
-#define SGS_K7(G, M, B)                                                                                       \
-    do {                                                                                                      \
-        static const bool attr_ = [] {                                                                        \
-            cudaFuncSetAttribute(composite_kernel<G, M, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                 static_cast<int>(2 * (B + 1) * 4 * 16 + B * 16 + (kThreads / 32) * (B + 8) * 2)); \
-            return true;                                                                                      \
-        }();                                                                                                  \
-        (void)attr_;                                                                                          \
-        composite_kernel<G, M, B><<<grid, kThreads, smem_for(B), stream>>>(                                   \
-            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed, tile_done, \
-            tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 6, cap); \
+    // persistent grid: 4 resident CTAs of 128 threads per SM
+    const unsigned grid = 148u * 4u;
+    constexpr int kB = 256;
+    const size_t smem = static_cast<size_t>(2 * (kB + 1) * 4 + kB) * sizeof(float4) +
+                        static_cast<size_t>(kThreads2 / 32) * (kB + 8) * sizeof(uint16_t);
+#define SGS_K7X2(G, ROW)                                                                                     \
+    do {                                                                                                     \
+        if ((e = k7_attr<G, ROW>(smem)) != cudaSuccess) return e;                                            \
+        composite2_kernel<G, 4, ROW><<<grid, kThreads2, smem, stream>>>(                                     \
+            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,        \
+            tile_done, tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl,  \
+            wctl + 6, cap);                                                                                  \
     } while (0)
-    static const int px = [] {
-        const char* e = std::getenv("SGS_K7_PX");
-        return e && std::atoi(e) == 1 ? 1 : 2;
-    }();
-    if (px == 2) {
-        const unsigned grid2 = 148u * 4u;
-        const size_t smem2 = smem_for(256) - static_cast<size_t>(kThreads / 32 - kThreads2 / 32) * (256 + 8) * 2;
-#define SGS_K7X2(G, ROW)                                                                                      \
-    do {                                                                                                      \
-        static const bool attr_ = [smem2] {                                                                   \
-            cudaFuncSetAttribute(composite2_kernel<G, 4, ROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                 static_cast<int>(smem2));                                                    \
-            return true;                                                                                      \
-        }();                                                                                                  \
-        (void)attr_;                                                                                          \
-        composite2_kernel<G, 4, ROW><<<grid2, kThreads2, smem2, stream>>>(                                     \
-            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,  \
-            tile_done, tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl,    \
-            wctl + 6, cap);                                                                                   \
-    } while (0)
-        const bool row = cfg.tile_size == 16;
-        if (group == 2) {
-            if (row) SGS_K7X2(2, true); else SGS_K7X2(2, false);
-        } else {
-            if (row) SGS_K7X2(4, true); else SGS_K7X2(4, false);
-        }
-#undef SGS_K7X2
-        return;
+    const bool row = cfg.tile_size == 16;
+    if (group == 2) {
+        if (row) SGS_K7X2(2, true); else SGS_K7X2(2, false);
+    } else {
+        if (row) SGS_K7X2(4, true); else SGS_K7X2(4, false);
     }
-    if (batch == 512)
-        SGS_K7(4, 2, 512);
-    else if (group == 8 && minb == 2)
-        SGS_K7(8, 2, 256);
-    else if (group == 2 && minb == 2)
-        SGS_K7(2, 2, 256);
-    else if (group == 4 && minb == 3)
-        SGS_K7(4, 3, 256);
-    else if (group == 2 && minb == 3)
-        SGS_K7(2, 3, 256);
-    else
-        SGS_K7(4, 2, 256);
-#undef SGS_K7
+#undef SGS_K7X2
+    return cudaGetLastError();
 }
 
 }  // namespace sgs

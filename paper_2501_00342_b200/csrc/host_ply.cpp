@@ -209,6 +209,23 @@ int ply_parse_header(const char* path, PlyTable& t, std::string& err) {
     t.payload_offset = static_cast<long>(in.tellg());
     t.info.count = t.count;
     t.info.binary = t.binary ? 1 : 0;
+    // The vertex count is untrusted: before anything is sized from it, the payload it
+    // implies (count * properties floats; checked multiplication) must fit in what the
+    // file still holds -- 4 bytes per value in binary, at least 2 ("0 ") in ASCII. The
+    // reference fails here too: resize(vertex_count) throws or the read comes up short.
+    const uint64_t np = t.props.size();
+    const uint64_t per_value = t.binary ? 4 : 2;
+    in.seekg(0, std::ios::end);
+    const long long end = static_cast<long long>(in.tellg());
+    const uint64_t avail = end > t.payload_offset ? static_cast<uint64_t>(end - t.payload_offset) : 0;
+    if (np && t.count > (avail + 1) / per_value / np) {
+        err = std::string(t.binary ? "truncated PLY payload: " : "truncated ASCII PLY payload: ") + path;
+        return SGS_ERR_IO;
+    }
+    if (t.count > 0xFFFFFFFFULL) {
+        err = "more than 2^32 Gaussians";
+        return SGS_ERR_INVALID_ARGUMENT;
+    }
     return SGS_OK;
 }
 

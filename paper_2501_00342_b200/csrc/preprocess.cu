@@ -361,9 +361,20 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
         const double guard =
             2.0 * 5.9604644775390625e-08 * csum * (9.0 * radius * radius + 3.0 * radius * ts) +
             1e-6;
+        // colour (FP32), direction from the FP64 offset
+        const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
+        const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
+        const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
+        // A non-finite colour or a NaN opacity must reach exactly the pixels the
+        // reference blends it into (it skips the others before touching acc; a NaN
+        // opacity passes std::min and the alpha test): such a splat gets an infinite
+        // guard band, so every one of its pairs is decided and blended one at a time
+        // by the compositor's FP64 path, and it keeps its 3-sigma tile rectangle.
+        const bool special = !(isfinite(col.x) && isfinite(col.y) && isfinite(col.z)) || isnan(opacity);
         // combined cutoff: alpha < 1/255 <=> m2 > 2 ln(255 op) (op > 0)
         const double acut = opacity > 0.0 ? 2.0 * log(255.0 * opacity) : -1.0;
-        const double cut = acut < kSupportMahalanobisSq ? acut : kSupportMahalanobisSq;
+        const double cut = isnan(opacity) ? kSupportMahalanobisSq
+                                          : (acut < kSupportMahalanobisSq ? acut : kSupportMahalanobisSq);
         // extents of {d : d^T conic d <= cut + guard} = sqrt(K cov_xx), sqrt(K cov_yy);
         // cov = the dilated 2D covariance (a, b, c), slightly inflated
         const double K = fmax(cut + guard, 0.0);
@@ -375,10 +386,10 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
         r.cc = static_cast<float>(conc);
         r.lop = opacity > 0.0 ? __log2f(static_cast<float>(opacity)) : -1e30f;
         r.cut = static_cast<float>(cut);
-        r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
-        r.ext_x = sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
-        r.ext_y = sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
-        if (cfg.tight_rect && x1 >= x0 && y1 >= y0) {
+        r.guard = special ? INFINITY : (guard < 1e30 ? static_cast<float>(guard) : FLT_MAX);
+        r.ext_x = special ? INFINITY : sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
+        r.ext_y = special ? INFINITY : sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
+        if (cfg.tight_rect && !special && x1 >= x0 && y1 >= y0) {
             // Render frames list a splat only in the tiles its cut ellipse's box reaches:
             // every pixel outside it has m2 > cut and is skipped by the reference, so the
             // image is unchanged (the parity dumps and stats frames keep the reference's
@@ -396,17 +407,11 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
             if (cut + guard < 0.0) x1 = x0 - 1;
         }
         o.rects[i] = make_int4(x0, x1, y0, y1);
-        // colour (FP32), direction from the FP64 offset
-        {
-            const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
-            const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
-            const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
-            o.colour[i] = col;
-            if constexpr (DEBUG) {
-                dbg.color[0] = col.x;
-                dbg.color[1] = col.y;
-                dbg.color[2] = col.z;
-            }
+        o.colour[i] = col;
+        if constexpr (DEBUG) {
+            dbg.color[0] = col.x;
+            dbg.color[1] = col.y;
+            dbg.color[2] = col.z;
         }
         o.rec[i] = r;
         if constexpr (DEBUG) {
@@ -624,10 +629,6 @@ __global__ void cov3d_kernel(const ScenePlanes sp, double2* __restrict__ cov) {
     cov[2 * sp.n + i] = make_double2(S6[4], S6[5]);
 }
 
-__global__ void iota_kernel(uint64_t n, uint32_t* __restrict__ out) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = static_cast<uint32_t>(i);
-}
 
 }  // namespace
 
@@ -640,9 +641,6 @@ void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream) {
         cov3d_kernel<false><<<blocks, 256, 0, stream>>>(sp, cov);
 }
 
-void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream) {
-    if (n) iota_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, out);
-}
 
 void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg,
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,

@@ -172,7 +172,6 @@ struct K1Views {
 };
 void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
                              cudaStream_t stream);
-void launch_iota(uint64_t n, uint32_t* out, cudaStream_t stream);
 // The last K1 launch of this thread (function, configuration, arguments), so a frame
 // graph can patch the camera of its captured K1 node (capi.cu launch_frame_graph).
 struct K1Record;
@@ -182,40 +181,54 @@ const void* k1_record_func(const K1Record* r);
 cudaError_t k1_record_patch(cudaGraphExec_t exec, cudaGraphNode_t node, K1Record* r, const CamParams& cam);
 // per-scene 3D covariance cache: 3 planes of n double2 (projection.cuh)
 void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream);
-int depth_bucket_log2(uint64_t n);
-void launch_bucket_hist(uint64_t n, const unsigned long long* key, const Counters* ctr, int log2b, uint32_t* hist,
-                        cudaStream_t stream);
-void launch_bucket_scatter(uint64_t n, const unsigned long long* key, Counters* ctr, int log2b, const uint32_t* off,
-                           uint32_t* cursor, uint32_t* out, unsigned long long* out_key, cudaStream_t stream);
-void launch_bucket_sort(uint32_t nbuckets, const uint32_t* off, const unsigned long long* key, uint32_t* order,
-                        Counters* ctr, uint32_t* big, cudaStream_t stream);
-// Tile counts for ranks [rb, re) skipping tiles already terminated (done may be null);
-// counts has re-rb+1 entries (the last is 0 so an exclusive scan yields the total).
-// two-level exact depth sort (depth_sort.cu): ranks + rank-ordered binning inputs
-int depth_coarse_log2(uint64_t n);
-size_t depth_two_level_scratch(uint64_t n, int log2c);
-size_t depth_two_level_cub_bytes(uint64_t n, int log2c);
-void launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters* ctr, int log2c, uint32_t* mat,
-                            uint32_t* off, unsigned long long* part_key, uint32_t* order, const int4* rects,
-                            int4* brect, uint2* bmeta, void* cub_temp, size_t cub_bytes,
-                            cudaStream_t stream);
-// K3+K4 fused: count, decoupled look-back scan and key emission in one pass
+// Device control block of one radix sort (radix.cu), one per lane. The epoch tags the
+// per-tile status words (never cleared); tickets and histograms are zeroed by a memset
+// from `ticket` on before the producer of the keys accumulates the histograms.
+struct SortCtl {
+    uint32_t epoch;
+    uint32_t ticket[8];      // per pass: tile tickets
+    uint32_t hist[8][256];   // per pass: global digit histogram (filled by the key producer)
+};
+// The digit split of a tile-id sort: passes of <= 8 bits, LSD first.
+struct TileDigits {
+    int passes;
+    int shift[4];
+    int bits[4];
+};
+size_t sort_status_words(uint64_t capacity);
+cudaError_t launch_onesweep_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                                 const unsigned long long* dcount, uint64_t hcount, int shift, int bits,
+                                 SortCtl* ctl, int pass, uint32_t* status, cudaStream_t stream);
+// K2: the depth order of n splats: order[r], and the rank-ordered binning inputs
+// brect[r] / bmeta[r] = (index, tiles of its rectangle). ka/va/kb/vb: 4 scratch arrays
+// of n u32. Narrow (32-bit keys + exact run fix-up) unless `wide` (full 64-bit keys).
+cudaError_t launch_depth_sort(uint64_t n, const unsigned long long* key, Counters* ctr, bool wide, uint32_t* ka,
+                              uint32_t* va, uint32_t* kb, uint32_t* vb, SortCtl* ctl, uint32_t* status,
+                              const int4* rects, uint32_t* order, int4* brect, uint2* bmeta, cudaStream_t stream,
+                              uint64_t* launches);
+// K3+K4 fused (binning.cu): for the ranks [rb, re) of a depth chunk, count each
+// rank's live tiles, scan the counts by decoupled look-back, and emit the (tile id,
+// Gaussian index) pairs into tk / tv in rank order; the tile ids' digit histograms of
+// the K5 passes go to ctl->hist, the chunk's P to ctr (chunk_entries), and the sort
+// epoch is opened. status: bin_emit_status_bytes zeroed bytes.
 size_t bin_emit_status_bytes(uint64_t ranks);
-void launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                     int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
-                     unsigned long long* status, Counters* ctr, cudaStream_t stream);
+cudaError_t launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
+                            int tiles_x, int ntile, uint32_t* tk, uint32_t* tv, uint64_t capacity,
+                            unsigned long long* status, const TileDigits& td, SortCtl* ctl, Counters* ctr,
+                            cudaStream_t stream);
+TileDigits tile_digits(int tile_bits);
 // backward (backward.cu)
 size_t bwd_splat_bytes();
 size_t bwd_partial_bytes();
 void launch_finite_check(const double* v, size_t n, int* bad, cudaStream_t s);
 void launch_backward(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
                      const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
-                     const int4* brect, const uint2* ranges, const unsigned long long* keys, void* bs,
+                     const int4* brect, const uint2* ranges, const uint32_t* keys, void* bs,
                      uint32_t* rank_of, uint32_t* used, double* partial, const double* upstream, double* grads,
                      int stride, cudaStream_t s);
 void launch_render_f64(const ScenePlanes& sp, const CamParams& cam, const CfgParams& cfg, const double* axes,
                        const double* bg, int override_degree, uint64_t V, int nchunks, const uint32_t* order,
-                       const uint2* ranges, const unsigned long long* keys, void* bs, uint32_t* rank_of, double* rgb,
+                       const uint2* ranges, const uint32_t* keys, void* bs, uint32_t* rank_of, double* rgb,
                        double* T, cudaStream_t s);
 // image metrics (metrics.cu)
 size_t metrics_scratch_doubles(size_t n, bool grad);
@@ -225,42 +238,18 @@ void launch_ssim(const void* a, const void* b, bool f64, int W, int H, int C, do
                  double* grad, cudaStream_t s);
 void launch_counters_init(Counters* c, cudaStream_t stream);
 void launch_counters_publish(const Counters* d, Counters* h_mapped, cudaStream_t stream);
-void launch_gather_bins(uint64_t n, const uint32_t* order, const int4* rects, const Counters* ctr,
-                        int4* brect, uint2* bmeta, cudaStream_t stream);
-void launch_count_tiles(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
-                        const uint32_t* done, int tiles_x, int ntile, unsigned long long* counts,
+// K6: ranges[t] = [first, last + 1) of tile t's run in the sorted tile ids; the
+// count is read from device memory.
+void launch_tile_ranges(const unsigned long long* d_count, const uint32_t* tiles, uint2* ranges,
                         cudaStream_t stream);
-void launch_emit_tile_keys(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect,
-                           const uint32_t* done, const unsigned long long* offsets,
-                           int tiles_x, int ntile, unsigned long long* keys, uint64_t capacity,
-                           cudaStream_t stream);
-// Ranges of the sorted keys; the count is read from device memory.
-void launch_tile_ranges(const unsigned long long* d_count, const unsigned long long* keys, uint2* ranges,
-                        cudaStream_t stream);
-// After K3's scan: P = offsets[m]; clamp to capacity, flag overflow, accumulate P.
-void launch_finish_scan(const unsigned long long* total, uint64_t capacity, Counters* ctr,
-                        cudaStream_t stream);
-int tile_sort_grid();
-size_t tile_sort_hist_bytes();
-unsigned long long* tile_sort(unsigned long long* a, unsigned long long* b, const unsigned long long* d_count,
-                              int tile_bits, uint32_t* hist, cudaStream_t stream, uint64_t* launches);
-// K7 over one depth chunk. first/last select state init / final output; tile_done and
-// state may be null when the frame is a single chunk.
-void launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
-                      const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
-                      const float4* colour, float3 bg,
-                      PixelState* state, uint32_t* processed, uint32_t* tile_done, uint32_t* tile_touched,
-                      bool first,
-                      bool last, Counters* counters, bool want_stats, uint32_t* work, uint32_t* wctl,
-                      bool work_ready, cudaStream_t stream);
-// Tile-major binning of one depth chunk (tile_bins.cu): counts, scan (+ the K7 work
-// list), scatter, per-tile sort; list[ranges[t]] holds Gaussian indices.
-size_t tb_sort_smem_bytes();
-void launch_tile_bins(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                      const uint32_t* touched, int tiles_x, int ntile, int pchunks, bool first, bool last, const uint32_t* order,
-                      uint32_t* cnt, uint32_t* cur, uint2* ranges, uint32_t* list, uint64_t capacity,
-                      uint32_t* work, uint32_t work_cap, uint32_t* wctl, uint32_t* sitems, uint32_t* sctl,
-                      Counters* ctr, cudaStream_t stream);
+// K7 over one depth chunk (builds the chunk's work list first). first/last select
+// state init / final output; tile_done and state may be null when the frame is a
+// single chunk.
+cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
+                             const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
+                             const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
+                             uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
+                             bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
 
 }  // namespace sgs

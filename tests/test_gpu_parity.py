@@ -269,13 +269,15 @@ def test_depth_chunking_is_bitwise_neutral():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"SGS_DEPTH_CHUNKING": "0"}, {"SGS_DEPTH_CHUNKS": "8"}, {"SGS_BIN": "tile"}, {"SGS_K7_PX": "1"}, {"SGS_K7_PX": "1", "SGS_K7_GROUP": "2"}, {"SGS_K7_GROUP": "2"}, {"SGS_DEPTH_SORT": "bucket"}, {"SGS_LANES": "1"},
+@pytest.mark.parametrize("env", [{"SGS_DEPTH_CHUNKING": "0"}, {"SGS_DEPTH_CHUNKS": "8"}, {"SGS_K7_GROUP": "2"},
+                                 {"SGS_LANES": "1"}, {"SGS_GRAPHS": "0"}, {"SGS_TIGHT_RECT": "0"},
                                  {"SGS_K1_GROUP": "1"}, {"SGS_K1_GROUP": "2"}, {"SGS_K1_GROUP": "3"},
-                                 {"SGS_K1_MINB": "1"}, {"SGS_K7_PX": "1", "SGS_K7_BATCH": "512"}])
+                                 {"SGS_K1_MINB": "1"}])
 def test_pipeline_variants_are_bitwise_equal(env):
-    """Every alternative pipeline path (tile-major binning with per-tile sorts, fused look-back binning, one-level bucket
-    depth sort, a single lane, other K1 / K7 instantiations) renders the same bits,
-    image, transmittance and E_t, as the default path, over a batch of views."""
+    """Every alternative pipeline path (no depth chunks or other chunk bounds, a single
+    lane, direct frames, the reference's 3-sigma tile rectangles, other K1 / K7
+    instantiations and multi-view K1 groups) renders the same bits, image,
+    transmittance and E_t, as the default path, over a batch of views."""
     scene = sg.synth_scene(150_000, "mixed", 91, log_scale_range=(-5.0, -3.5))
     cams = sg.orbit_cameras(5, 480, 270, 4.0, 324.0)
     # both renderers on the depth-chunked path (a 150K scene is one chunk by default)
@@ -338,12 +340,12 @@ def test_exact_mode_matches_reference_to_fp64_rounding(case):
 def _adversarial(orc, name):
     """Scenes that drive the rare paths of the frame pipeline."""
     rng = np.random.default_rng(4242)
-    if name == "ties":  # 600 splats at one depth: a fine bucket > 64 -> 64-bit CUB depth sort
+    if name == "ties":  # 600 splats at one depth: a run of equal 32-bit keys > 32 -> 64-bit depth sort
         f = orc.synth(3000, 11, "mixed", 2, ls=(-4.0, -3.0))
         f.params[:600, 0:3] = f.params[600, 0:3]  # identical positions: identical depth keys
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
         return f, cam, make_config(16, degree_override=1)
-    if name == "spike":  # 60k of 70k splats in a thin depth slab: a coarse bucket > 4096 -> retry
+    if name == "spike":  # 60k of 70k splats in a thin depth slab: long runs of equal 32-bit keys -> 64-bit sort
         f = orc.synth(70_000, 12, "sg3", 0, ls=(-5.5, -4.5))
         f.params[:60_000, 0:3] = f.params[0, 0:3] + rng.uniform(-1e-9, 1e-9, size=(60_000, 3))
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 200, 150, 180.0)
@@ -352,16 +354,24 @@ def _adversarial(orc, name):
         f = orc.synth(5000, 13, "sh", 1, ls=(-1.0, 0.2))
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.3, 0.2, 256, 256, 240.0)
         return f, cam, make_config(8)
-    if name == "longlist":  # 20k splats in a few tiles: a list above tile_bins' sort cap -> rank-major retry
+    if name == "longlist":  # 20k splats in a few tiles: lists of thousands, one sort digit everywhere
         f = orc.synth(20_000, 16, "mixed", 2, ls=(-6.0, -5.0))
         f.params[:, 0:3] = (f.params[0, 0:3] + rng.uniform(-2e-3, 2e-3, size=(20_000, 3))).astype(np.float32)
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
         return f, cam, make_config(16, degree_override=1)
-    if name == "midlist":  # 9k splats over 4 tiles: lists of thousands through the block radix sort
+    if name == "midlist":  # 9k splats over 4 tiles: whole lists of thousands walked (low opacity)
         f = orc.synth(9000, 17, "mixed", 2, ls=(-5.5, -4.5))
         f.params[:, 0:3] = (f.params[0, 0:3] + rng.uniform(-0.02, 0.02, size=(9000, 3))).astype(np.float32)
         f.params[:, 10] = -4.0  # low opacity: pixels do not terminate, whole lists are walked
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
+        return f, cam, make_config(16, degree_override=1)
+    if name == "nearties":  # 400 pairs 1e-12 apart in depth (FP64 geometry): runs of equal 32-bit keys
+        f = orc.synth(4000, 18, "mixed", 2, ls=(-4.5, -3.0))
+        src = rng.choice(4000, size=400, replace=False)
+        dst = (src + 1 + rng.integers(0, 3000, size=400)) % 4000
+        f.params[dst, 0:3] = f.params[src, 0:3]
+        f.params[dst, 2] += rng.choice([-1.0, 1.0], size=400) * 1e-12  # either side: order by depth, not index
+        cam = orc.orbit_camera([0, 0, 0], 3.5, 0.2, 0.1, 160, 120, 150.0)
         return f, cam, make_config(16, degree_override=1)
     if name == "culled":  # the camera looks away: V = 0, background only
         f = orc.synth(2000, 14, "sg1", 0, ls=(-4.0, -3.0))
@@ -375,7 +385,7 @@ def _adversarial(orc, name):
     raise KeyError(name)
 
 
-@pytest.mark.parametrize("name", ["ties", "spike", "huge", "longlist", "midlist", "culled", "tile32"])
+@pytest.mark.parametrize("name", ["ties", "spike", "nearties", "huge", "longlist", "midlist", "culled", "tile32"])
 def test_adversarial_scenes_vs_restatement(renderer, orc, name):
     f, ocam, cfg = _adversarial(orc, name)
     ref_rgb, ref_T = orc.render(f, ocam, cfg)
@@ -394,32 +404,6 @@ def test_adversarial_scenes_vs_restatement(renderer, orc, name):
         assert np.abs(rgb64 - ref_rgb).max() <= 1e-12 and np.abs(T64 - ref_T).max() <= 1e-12
     finally:
         ds.free()
-
-
-@pytest.mark.parametrize("name", ["longlist", "midlist", "huge"])
-def test_tile_major_binning_on_long_lists(orc, name):
-    """The optional tile-major binning (SGS_BIN=tile) sorts every tile list in shared
-    memory: lists of thousands go through its block radix sort, and a list above its
-    capacity (longlist: 20k entries in one tile) makes the host redo the frame
-    rank-major. Both must render the default path's bits."""
-    f, ocam, cfg = _adversarial(orc, name)
-    scene, cam = to_scene(f), to_cam(ocam)
-    os.environ["SGS_BIN"] = "tile"
-    try:
-        tile = sg.Renderer(0)
-    finally:
-        os.environ.pop("SGS_BIN")
-    base = sg.Renderer(0)
-    a_ds, b_ds = base.upload(scene), tile.upload(scene)
-    try:
-        kw = cfg_kwargs(cfg)
-        a = base.render(a_ds, cam, early_stop=cfg.early_stop_transmittance, stats=True, **kw)
-        b = tile.render(b_ds, cam, early_stop=cfg.early_stop_transmittance, stats=True, **kw)
-        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-        assert a[2].block_entries == b[2].block_entries and a[2].tile_entries == b[2].tile_entries
-    finally:
-        a_ds.free()
-        b_ds.free()
 
 
 def test_frame_graph_replay_is_bitwise_equal():
@@ -609,3 +593,55 @@ def test_camera_inside_the_scene_vs_restatement(orc, renderer, kind, deg):
             check_image(rgb, T, ref_rgb, ref_T)
     finally:
         ds.free()
+
+
+def test_refused_capture_falls_back_to_direct_frames():
+    """A frame whose capture fails inside the body (a call the capture refuses) must
+    still render -- directly, and every later frame too -- with the bits of a renderer
+    that never captures (the fallback only covered a failing EndCapture)."""
+    scene = sg.synth_scene(60_000, "mixed", 93, log_scale_range=(-5.0, -3.5))
+    cams = sg.orbit_cameras(12, 256, 160, 4.0, 190.0)
+    os.environ["SGS_GRAPHS"] = "0"
+    try:
+        plain = sg.Renderer(0)
+    finally:
+        os.environ.pop("SGS_GRAPHS")
+    os.environ["SGS_DEBUG_CAPTURE_FAIL"] = "1"
+    try:
+        refused = sg.Renderer(0)
+    finally:
+        os.environ.pop("SGS_DEBUG_CAPTURE_FAIL")
+    a_ds, b_ds = plain.upload(scene), refused.upload(scene)
+    try:
+        for _ in range(3):  # direct, capture attempt (refused -> direct), direct again
+            a = plain.render_batch(a_ds, cams, degree_override=1)
+            b = refused.render_batch(b_ds, cams, degree_override=1)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    finally:
+        a_ds.free()
+        b_ds.free()
+
+
+def test_nonfinite_parameters_vs_reference(renderer, ref):
+    """NaN / infinite colour parameters and NaN opacities: exactly the
+    pixels the reference blends them into become non-finite -- it skips every other
+    pair before touching the accumulator, and a NaN opacity passes its std::min clamp
+    and alpha test -- and every other pixel matches within the usual tolerance."""
+    rng = np.random.default_rng(77)
+    f = ref.synth(3000, 21, "mixed", 2, (-4.0, -2.8))
+    pick = rng.choice(3000, size=90, replace=False)
+    f.params[pick[:30], 11] = np.nan          # SH DC red
+    f.params[pick[30:60], 11 + 27] = np.inf   # the first SG lobe's red amplitude
+    f.params[pick[60:], 10] = np.nan          # opacity logit
+    ocam = ref.orbit_camera([0, 0, 0], 3.2, 0.4, 0.2, 120, 90, 110.0)
+    cfg = make_config(16, degree_override=2)
+    ref_rgb, ref_T = ref.render(f, ocam, cfg)
+    assert np.isnan(ref_rgb).any() and np.isnan(ref_T).any()  # the scene does reach the special paths
+    for _ in range(3):  # direct, captured, replayed
+        rgb, T = render_cfg(renderer, to_scene(f), to_cam(ocam), cfg)
+        rgb, T = rgb.astype(np.float64), T.astype(np.float64)
+        for got, want in ((rgb, ref_rgb), (T, ref_T)):
+            assert np.array_equal(np.isnan(got), np.isnan(want))
+            assert np.array_equal(np.isposinf(got), np.isposinf(want))
+            fin = np.isfinite(want)
+            assert np.abs(got[fin] - want[fin]).max() <= IMG_TOL

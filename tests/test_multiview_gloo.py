@@ -47,6 +47,18 @@ def _worker(rank, world, port, out):
         frames = torch.full((4, 3), float(rank))
         got = multiview.gather_frames(frames, dst=0)
         ok_gather = rank != 0 or all(torch.all(g == i) for i, g in enumerate(got))
+        # ragged shards (shard_views of 5 views over 2 ranks: 3 + 2), gathered to rank 1
+        b, e = multiview.shard_views(5, world, rank)
+        rag = torch.arange(b, e, dtype=torch.float32).reshape(-1, 1).repeat(1, 3)
+        got = multiview.gather_frames(rag, dst=1)
+        if rank == 1:
+            ok_gather = ok_gather and [g.shape[0] for g in got] == [3, 2] and \
+                torch.equal(torch.cat(got)[:, 0], torch.arange(5, dtype=torch.float32))
+        # src / dst are ranks within the group: group rank 1 (global rank 1) sends
+        sub = dist.new_group([0, 1])
+        src_scene = sg.synth_scene(5000, "mixed", 20260003, log_scale_range=(-5.5, -4.0)) if rank == 1 else None
+        sub_meta, sub_blob = multiview.broadcast_scene_blob(src_scene, "cpu", src=1, group=sub)
+        ok_blob = ok_blob and np.array_equal(sub_blob.numpy(), host)
         out.put((rank, ok_meta, ok_blob, bool(ok_gather), int(meta.blob_bytes)))
     finally:
         dist.destroy_process_group()

@@ -196,6 +196,24 @@ def test_error_cases_match_reference(ref, saved, tmp_path):
         assert_same(ref, p)
 
 
+def test_crafted_vertex_counts_fail_safely(tmp_path):
+    """A header whose vertex count times the property count wraps 64 bits (or just
+    exceeds the file) must fail as a truncated payload before anything is sized from
+    it -- not overrun a buffer sized from the wrapped product."""
+    props = [f"p{i}" for i in range(16)]
+    body = np.zeros((1, 16), dtype="<f4").tobytes()
+    for count in (2 ** 60 + 1, 2 ** 62, 2 ** 64 - 1, 2):  # 16 * (2^60 + 1) == 16 (mod 2^64)
+        for binary in (True, False):
+            p = tmp_path / f"crafted_{count}_{int(binary)}.ply"
+            hdr = ["ply", "format binary_little_endian 1.0" if binary else "format ascii 1.0",
+                   f"element vertex {count}"] + [f"property float {q}" for q in props] + ["end_header"]
+            payload = body if binary else (" ".join(["0"] * 16) + "\n").encode()
+            p.write_bytes(("\n".join(hdr) + "\n").encode() + payload)
+            for call in (sg.load_scene, sg.ply_info):
+                with pytest.raises(sg.IoError, match="truncated"):
+                    call(str(p))
+
+
 def test_golden_ply_fixtures():
     """Without the reference: the committed files and their reference-loaded params."""
     idx = np.load(os.path.join(GOLDEN_PLY, "expected.npz"))
