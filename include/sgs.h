@@ -125,7 +125,10 @@ typedef struct {
     uint64_t block_entries; /* E_t: list entries composited before block termination */
     uint64_t guard_hits;    /* pairs recomputed in FP64 by the compositor's guard band */
     int32_t want_timing;    /* in: 1 to record per-stage CUDA-event times */
-    int32_t reserved;
+    int32_t timing_path;    /* in: 1 to run the stats-free render path (tight tile rectangles,
+                               no E_t counting) so the stage times are those of a plain
+                               render; block_entries stays 0 and tile_entries counts the
+                               tight lists */
     float ms_preprocess, ms_depth_sort, ms_binning, ms_tile_sort, ms_composite, ms_total;
 } sgs_render_stats;
 
@@ -138,8 +141,9 @@ const char* sgs_last_error(void);
 /* Run on a caller stream (cudaStream_t as void*); NULL restores the context's own. */
 sgs_status sgs_set_stream(sgs_context* ctx, void* stream);
 sgs_status sgs_synchronize(sgs_context* ctx);
-/* Cumulative number of this library's own kernel launches on ctx (K1, K3, K4, K6,
- * K7) and of CUB library launches (radix sorts, scan), for launch accounting. */
+/* Cumulative number of this library's own kernel launches on ctx (every stage K1-K7
+ * is the library's own code) and of third-party library kernels (none: always 0),
+ * for launch accounting. */
 sgs_status sgs_launch_count(sgs_context* ctx, uint64_t* own_kernels, uint64_t* library_kernels);
 
 /* --- scenes ------------------------------------------------------------------- */

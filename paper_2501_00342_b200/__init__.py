@@ -446,20 +446,25 @@ class Renderer:
     # -- render ----------------------------------------------------------------
     def render(self, dscene: DeviceScene, cam: Camera, tile_size=16, thresholds=(2.0, 8.0),
                degree_override=-1, early_stop=1e-4, rgb=None, T=None, device_out=False,
-               stats: bool = False, timing: bool = False):
+               stats: bool = False, timing: bool = False, timing_path: bool = False):
         """One view. Host outputs (float32 numpy) unless device_out=True, in which case
         `rgb`/`T` must be device pointers (ints) supplied by the caller."""
         return self.render_batch(dscene, [cam], tile_size, thresholds, degree_override,
-                                 early_stop, rgb, T, device_out, stats, timing, _single=True)
+                                 early_stop, rgb, T, device_out, stats, timing, timing_path, _single=True)
 
     def render_batch(self, dscene: DeviceScene, cams: Sequence[Camera], tile_size=16,
                      thresholds=(2.0, 8.0), degree_override=-1, early_stop=1e-4, rgb=None, T=None,
-                     device_out=False, stats: bool = False, timing: bool = False, _single=False):
+                     device_out=False, stats: bool = False, timing: bool = False,
+                     timing_path: bool = False, _single=False):
+        """Views of one scene. stats: V / P / E_t counters; timing: per-stage device
+        times (one lane); timing_path: time the stats-free render path exactly as a plain
+        render runs it (tight tile rectangles, no E_t counting)."""
         n = len(cams)
         carr = (C.sgs_camera * max(n, 1))(*[c._c() for c in cams])
         cfg = _config(tile_size, thresholds, 0, degree_override, early_stop)
         st = C.sgs_render_stats()
         st.want_timing = 1 if timing else 0
+        st.timing_path = 1 if timing_path else 0
         if device_out:
             rgb_p, T_p = rgb, T
             mem = C.SGS_DEVICE

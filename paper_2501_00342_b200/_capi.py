@@ -100,7 +100,7 @@ class sgs_render_stats(ctypes.Structure):
         ("block_entries", ctypes.c_uint64),
         ("guard_hits", ctypes.c_uint64),
         ("want_timing", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("timing_path", ctypes.c_int32),
         ("ms_preprocess", ctypes.c_float),
         ("ms_depth_sort", ctypes.c_float),
         ("ms_binning", ctypes.c_float),

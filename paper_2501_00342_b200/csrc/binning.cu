@@ -1,15 +1,17 @@
-// binning.cu -- K3+K4 (tile binning in one pass) and K6 (tile ranges).
+// binning.cu -- K3 (per-rank tile counts), K4 (pair emission), K6 (tile ranges).
 //
 // Replaces build_tile_grid (proj/src/raster.cpp:108-130). The reference walks the
 // splats in blending order and push_backs the rank into every tile of the
-// inclusive rectangle. Here, for a depth chunk of ranks [rb, re), ONE kernel
-// (bin_emit_kernel) counts each rank's live tiles, turns the counts into output
-// offsets with a warp-level decoupled look-back scan across the grid (so a warp of 32
-// consecutive ranks owns one contiguous output range), and emits the (tile id,
-// Gaussian index) pairs, tiles row-major as the reference's (ty, tx) double loop
-// visits them. The pairs leave in rank order; K5 (radix.cu, stable on the tile id)
-// then yields every tile's run in rank order -- the reference's TileGrid list -- and
-// K6 finds each tile's [first, last + 1).
+// inclusive rectangle. Here, for a depth chunk of ranks [rb, re):
+//   K3  counts[r - rb] = live tiles of rank r's rectangle, and each CTA's sum;
+//   K4  each CTA turns the counts into output offsets itself -- the sum of the CTA
+//       sums before it (read from L2 by all its threads) plus a block scan of its
+//       own counts (warp shuffles) -- and emits the (tile id, Gaussian index) pairs,
+//       tiles row-major as the reference's (ty, tx) double loop visits them, so a
+//       warp of 32 consecutive ranks owns one contiguous output range. No CTA waits
+//       for another. The pairs leave in rank order; K5 (radix.cu, stable on the tile
+//       id) yields every tile's run in rank order -- the reference's TileGrid list --
+//   K6  ranges[tile] = [first, last + 1) of the tile's run.
 // A tile whose every pixel has terminated (transmittance below the threshold) in
 // an earlier chunk receives no further pairs: the reference never reads past that
 // point of its list (raster.cpp:177-179), so the image is unchanged.
@@ -21,8 +23,13 @@ namespace sgs {
 namespace {
 
 // The finished-tile flags of the frame as a bitmap in shared memory (tiles up to
-// kMaxBitmapTiles; larger grids read the byte flags from global memory).
+// kMaxBitmapTiles; larger grids read the global bitmap).
 constexpr int kMaxBitmapTiles = 1 << 18;
+constexpr int kBinThreads = 1024;
+// Splats covering more than kCoop tiles are emitted cooperatively by the whole warp
+// (ballot-compacted over the live tiles) so one large splat does not serialise a
+// lane while 31 idle.
+constexpr uint32_t kCoop = 32;
 
 __device__ __forceinline__ void load_done_bitmap(const uint32_t* __restrict__ done, int ntile, uint32_t* bits) {
     const int words = (ntile + 31) / 32;
@@ -44,66 +51,88 @@ __device__ __forceinline__ uint32_t live_tiles(const int4 rc, const DoneView& do
     return c;
 }
 
-// K3+K4: one pass per chunk counts each rank's live tiles, scans the counts across
-// the grid with a decoupled look-back (CTAs take logical block numbers from a
-// ticket, so every predecessor a CTA waits on is already resident), and emits the
-// pairs at the scanned offsets, adding each tile id's K5 digits to block histograms.
-// The last block records the chunk's P (total, overflow flag) and opens the sort's
-// epoch.
-// status[b] = flag << 62 | value: flag 1 = block aggregate, 2 = inclusive prefix.
-constexpr unsigned long long kFlagAgg = 1ULL << 62;
-constexpr unsigned long long kFlagPre = 2ULL << 62;
-constexpr unsigned long long kValMask = (1ULL << 62) - 1;
-constexpr int kBinThreads = 1024;
-// Splats covering more than kCoop tiles are emitted cooperatively by the whole warp
-// (ballot-compacted over the live tiles) so one large splat does not serialise a
-// lane while 31 idle.
-constexpr uint32_t kCoop = 32;
-
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ DoneView done_view(const uint32_t* done_bits, int ntile, uint32_t* smem) {
+    DoneView done{done_bits};
+    if (done_bits && ntile <= kMaxBitmapTiles) {
+        load_done_bitmap(done_bits, ntile, smem);  // ends with __syncthreads
+        done.bits = smem;
+    }
+    return done;
 }
 
+// K3: counts[k] = live tiles of rank rb + k; csum[blk] = the CTA's total.
+__global__ void __launch_bounds__(kBinThreads) bin_count_kernel(uint64_t rb, uint64_t re,
+                                                                const uint2* __restrict__ bmeta,
+                                                                const int4* __restrict__ brect,
+                                                                const uint32_t* __restrict__ done_bits, int tiles_x,
+                                                                int ntile, uint32_t* __restrict__ counts,
+                                                                unsigned long long* __restrict__ csum) {
+    extern __shared__ uint32_t bitmap[];
+    __shared__ unsigned long long s_warp[kBinThreads / 32];
+    const DoneView done = done_view(done_bits, ntile, bitmap);
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * kBinThreads + threadIdx.x;
+    const uint64_t r = rb + k;
+    uint32_t c = 0;
+    if (r < re) {
+        c = bmeta[r].y;
+        if (done_bits) {
+            const int4 rc = brect[r];  // issued with the bmeta load (stale when c == 0, unused)
+            if (c) c = live_tiles(rc, done, tiles_x);
+        }
+        counts[k] = c;
+    }
+    unsigned long long s = c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = s_warp[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) csum[blockIdx.x] = s;
+    }
+}
+
+// K4: offsets from the CTA sums before this CTA and a block scan of its counts; the
+// last CTA records the chunk's P (total, overflow flag, clamped count for K5-K7).
 __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     uint64_t rb, uint64_t re, const uint2* __restrict__ bmeta, const int4* __restrict__ brect,
-    const uint32_t* __restrict__ done_bytes, int tiles_x, int ntile, uint32_t* __restrict__ tk,
-    uint32_t* __restrict__ tv, uint64_t capacity, unsigned long long* __restrict__ status, const TileDigits td,
-    SortCtl* __restrict__ ctl, Counters* __restrict__ ctr) {
-    extern __shared__ uint32_t done_bits[];
-    __shared__ uint32_t s_blk;
-    __shared__ uint32_t s_hist[4 * 256];
-    for (int k = threadIdx.x; k < td.passes * 256; k += kBinThreads) s_hist[k] = 0;
+    const uint32_t* __restrict__ done_bits, int tiles_x, int ntile, const uint32_t* __restrict__ counts,
+    const unsigned long long* __restrict__ csum, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
+    uint64_t capacity, Counters* __restrict__ ctr) {
+    extern __shared__ uint32_t bitmap[];
     __shared__ unsigned long long s_warp[kBinThreads / 32];
     __shared__ unsigned long long s_base;
-    const unsigned nblk = gridDim.x;
-    if (threadIdx.x == 0) s_blk = atomicAdd(reinterpret_cast<unsigned int*>(&status[nblk]), 1u);
-    DoneView done{done_bytes};
-    if (done_bytes && ntile <= kMaxBitmapTiles) {
-        load_done_bitmap(done_bytes, ntile, done_bits);  // ends with __syncthreads
-        done.bits = done_bits;
-    } else {
-        __syncthreads();
-    }
-    const uint32_t blk = s_blk;
+    const DoneView done = done_view(done_bits, ntile, bitmap);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t r = rb + static_cast<uint64_t>(blk) * kBinThreads + threadIdx.x;
-    uint32_t g = 0, area = 0;
-    int4 rc = make_int4(0, -1, 0, -1);
-    unsigned long long c = 0;
-    if (r < re) {
-        const uint2 m = bmeta[r];
-        g = m.x;
-        area = m.y;
-        if (area) {
-            rc = brect[r];
-            c = done_bytes ? live_tiles(rc, done, tiles_x) : area;
+    const uint32_t blk = blockIdx.x;
+    // sum of the CTA totals before this one
+    unsigned long long before = 0;
+    for (uint32_t p = threadIdx.x; p < blk; p += kBinThreads) before += csum[p];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    if (lane == 0) s_warp[warp] = before;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long v = s_warp[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+            s_base = v;
+            if (blk == gridDim.x - 1) {
+                const unsigned long long p = v + csum[blk];
+                ctr->tile_entries += p;
+                if (p > ctr->max_chunk_entries) ctr->max_chunk_entries = p;
+                if (p > capacity) ctr->key_overflow = 1;
+                ctr->chunk_entries = p < capacity ? p : capacity;
+            }
         }
     }
+    __syncthreads();
+    const uint64_t k = static_cast<uint64_t>(blk) * kBinThreads + threadIdx.x;
+    const uint64_t r = rb + k;
+    const uint32_t c = r < re ? counts[k] : 0u;
     // block-exclusive scan of the counts
     unsigned long long inc = c;
 #pragma unroll
@@ -111,6 +140,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
         const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= static_cast<unsigned>(o)) inc += y;
     }
+    __syncthreads();  // (s_warp reuse)
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
     if (warp == 0) {
@@ -121,61 +151,20 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
             const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
             if (lane >= static_cast<unsigned>(o)) wi += y;
         }
-        s_warp[lane] = wi - w;  // exclusive warp offsets
-        // wi (lane 31) = block total: publish it, look back over the predecessors a
-        // warp-wide window of 32 at a time, publish the inclusive prefix
-        const unsigned long long total = __shfl_sync(0xffffffffu, wi, 31);
-        if (blk == 0) {
-            if (lane == 0) st_release(&status[0], kFlagPre | total);
-        } else if (lane == 0) {
-            st_release(&status[blk], kFlagAgg | total);
-        }
-        unsigned long long excl = 0;
-        if (blk > 0) {
-            int64_t hi = static_cast<int64_t>(blk) - 1;  // window [hi - 31, hi], lane i reads hi - i
-            for (;;) {
-                const int64_t pb = hi - static_cast<int64_t>(lane);
-                unsigned long long v = pb >= 0 ? 0ULL : kFlagPre;  // before block 0: prefix 0
-                // every lane of the warp runs this loop until all 32 flags are set
-                for (;;) {
-                    if (v == 0) v = ld_acquire(&status[pb]);
-                    if (__all_sync(0xffffffffu, v != 0)) break;
-                }
-                const unsigned pre = __ballot_sync(0xffffffffu, (v & kFlagPre) != 0);
-                const int stop_lane = pre ? __ffs(pre) - 1 : 31;
-                unsigned long long part = static_cast<int>(lane) <= stop_lane ? (v & kValMask) : 0ULL;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-                excl += part;
-                if (pre) break;
-                hi -= 32;
-            }
-            if (lane == 0) st_release(&status[blk], kFlagPre | (excl + total));
-        }
-        if (lane == 0) {
-            s_base = excl;
-            if (blk == nblk - 1) {
-                // the chunk's P: total, overflow flag, clamped count for K5-K7
-                const unsigned long long p = excl + total;
-                ctr->tile_entries += p;
-                if (p > ctr->max_chunk_entries) ctr->max_chunk_entries = p;
-                if (p > capacity) ctr->key_overflow = 1;
-                ctr->chunk_entries = p < capacity ? p : capacity;
-                ctl->epoch += 1;  // (the K5 passes of this chunk run after this kernel)
-            }
-        }
+        s_warp[lane] = wi - w;
     }
     __syncthreads();
-    // emit one (tile, index) pair at slot pos (dropped past the capacity: the frame is redone)
-    auto put = [&](unsigned long long pos, uint32_t tile, uint32_t gi) {
-        if (pos < capacity) {
-            tk[pos] = tile;
-            tv[pos] = gi;
-            for (int p = 0; p < td.passes; ++p)
-                atomicAdd(&s_hist[p * 256 + ((tile >> td.shift[p]) & ((1u << td.bits[p]) - 1u))], 1u);
-        }
-    };
     const unsigned long long off = s_base + s_warp[warp] + inc - c;
+    // a rank with no live tile is skipped before its rectangle is read (in late chunks
+    // most ranks only cover finished tiles)
+    uint32_t g = 0, area = 0;
+    int4 rc = make_int4(0, -1, 0, -1);
+    if (c) {
+        const uint2 m = bmeta[r];
+        g = m.x;
+        area = m.y;
+        rc = brect[r];
+    }
     const uint32_t w = static_cast<uint32_t>(rc.y - rc.x + 1);
     if (area && area <= kCoop) {
         uint32_t o = 0;
@@ -183,7 +172,10 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
             const uint32_t tile = static_cast<uint32_t>(rc.z + static_cast<int>(j / w)) * tiles_x +
                                   static_cast<uint32_t>(rc.x + static_cast<int>(j % w));
             if (done(tile)) continue;
-            put(off + o, tile, g);
+            if (off + o < capacity) {
+                tk[off + o] = tile;
+                tv[off + o] = g;
+            }
             ++o;
         }
     }
@@ -209,13 +201,13 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
             }
             const unsigned m = __ballot_sync(0xffffffffu, live);
             const unsigned long long pos = o + __popc(m & ((1u << lane) - 1u));
-            if (live) put(pos, tile, gg);
+            if (live && pos < capacity) {
+                tk[pos] = tile;
+                tv[pos] = gg;
+            }
             o += __popc(m);
         }
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < td.passes * 256; k += kBinThreads)
-        if (s_hist[k]) atomicAdd(&ctl->hist[k >> 8][k & 255], s_hist[k]);
 }
 
 // Per-frame counters without the copy engines: the init is a kernel, and the final
@@ -244,11 +236,13 @@ __global__ void tile_ranges_kernel(const unsigned long long* __restrict__ count,
     }
 }
 
-}  // namespace
-
-static size_t bitmap_smem(const uint32_t* done, int ntile) {
+size_t bitmap_smem(const uint32_t* done, int ntile) {
     return done && ntile <= kMaxBitmapTiles ? static_cast<size_t>((ntile + 31) / 32) * 4 : 0;
 }
+
+uint64_t bin_blocks(uint64_t ranks) { return ranks ? (ranks + kBinThreads - 1) / kBinThreads : 1; }
+
+}  // namespace
 
 void launch_tile_ranges(const unsigned long long* d_count, const uint32_t* tiles, uint2* ranges,
                         cudaStream_t stream) {
@@ -268,23 +262,26 @@ TileDigits tile_digits(int tile_bits) {
     return td;
 }
 
-size_t bin_emit_status_bytes(uint64_t ranks) {
-    return ((ranks + kBinThreads - 1) / kBinThreads + 1) * sizeof(unsigned long long);
+size_t bin_scratch_bytes(uint64_t ranks) {
+    const uint64_t nb = bin_blocks(ranks);
+    return (nb * kBinThreads * sizeof(uint32_t) + 255) / 256 * 256 + nb * sizeof(unsigned long long);
 }
 
-cudaError_t launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                            int tiles_x, int ntile, uint32_t* tk, uint32_t* tv, uint64_t capacity,
-                            unsigned long long* status, const TileDigits& td, SortCtl* ctl, Counters* ctr,
-                            cudaStream_t stream) {
+cudaError_t launch_binning(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
+                           int tiles_x, int ntile, uint32_t* tk, uint32_t* tv, uint64_t capacity, void* scratch,
+                           Counters* ctr, cudaStream_t stream, uint64_t* launches) {
     const uint64_t n = re > rb ? re - rb : 0;
-    const unsigned grid = static_cast<unsigned>(n ? (n + kBinThreads - 1) / kBinThreads : 1);
-    cudaError_t e = cudaMemsetAsync(status, 0, (grid + 1) * sizeof(unsigned long long), stream);
-    if (e == cudaSuccess)  // the K5 tickets and histograms this chunk's pairs fill
-        e = cudaMemsetAsync(&ctl->ticket[0], 0, sizeof(SortCtl) - offsetof(SortCtl, ticket), stream);
-    if (e != cudaSuccess) return e;
-    bin_emit_kernel<<<grid, kBinThreads, bitmap_smem(done, ntile), stream>>>(rb, re, bmeta, brect, done, tiles_x,
-                                                                             ntile, tk, tv, capacity, status, td,
-                                                                             ctl, ctr);
+    const uint64_t nb = bin_blocks(n);
+    uint32_t* counts = static_cast<uint32_t*>(scratch);
+    unsigned long long* csum = reinterpret_cast<unsigned long long*>(
+        static_cast<char*>(scratch) + (nb * kBinThreads * sizeof(uint32_t) + 255) / 256 * 256);
+    const size_t smem = bitmap_smem(done, ntile);
+    bin_count_kernel<<<static_cast<unsigned>(nb), kBinThreads, smem, stream>>>(rb, re, bmeta, brect, done, tiles_x,
+                                                                               ntile, counts, csum);
+    bin_emit_kernel<<<static_cast<unsigned>(nb), kBinThreads, smem, stream>>>(rb, re, bmeta, brect, done, tiles_x,
+                                                                              ntile, counts, csum, tk, tv, capacity,
+                                                                              ctr);
+    *launches += 2;
     return cudaGetLastError();
 }
 

@@ -102,11 +102,11 @@ struct Lane {
     cudaStream_t plain = nullptr, ranked = nullptr;
     cudaEvent_t swap = nullptr;
     DevBuf keys_a, order, rec, colour, rects, brect, bmeta;
-    DevBuf bin_status;  // K3+K4 look-back status
+    DevBuf bin_status;  // K3/K4 scratch: per-rank counts, per-CTA sums
     DevBuf work;        // K7 work list (+ control words)
     // (tile id, Gaussian index) pairs, ping-pong for K5; also K2's sort scratch
     DevBuf tk_a, tv_a, tk_b, tv_b;
-    DevBuf sort_ctl, sort_status;  // radix sort control block and per-tile status
+    DevBuf sort_ctl, sort_hist;  // radix sort: global digit counts, per-slice histograms
     DevBuf ranges, tile_done, pix_state, pix_walked;
     // host-output frames: kOutSlots device buffers per lane drained by the lane's copy
     // stream, so the lane renders its next views while earlier ones cross PCIe
@@ -270,8 +270,8 @@ enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
 // run_frame_once results besides sgs_status
 constexpr int kRetryWide = 100;  // a run of equal 32-bit depth keys: redo with 64-bit keys
 constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, redo
-// the radix sort's status words hold prefix counts in 30 bits
-constexpr uint64_t kMaxSortKeys = (1ULL << 30) - 1;
+// the radix sort's counters are 32-bit (kept one bit clear)
+constexpr uint64_t kMaxSortKeys = (1ULL << 31) - 1;
 
 // Depth chunking: the first chunk holds the
 // nearest ceil(N / div0) ranks; tiles whose pixels all terminate inside it are
@@ -310,7 +310,7 @@ std::vector<uint64_t> frame_graph_key(const sgs_context* ctx, const Lane& L) {
                             static_cast<uint64_t>(j.cfg.tile_size), static_cast<uint64_t>(j.cfg.has_override),
                             static_cast<uint64_t>(j.cfg.override_degree), bits(j.cfg.degree_threshold_lo),
                             bits(j.cfg.degree_threshold_hi), bits(j.cfg.early_stop_transmittance),
-                            j.stats ? 1u : 0u, j.wide ? 1u : 0u,
+                            (j.stats ? 1u : 0u) | (j.stats && j.stats->timing_path ? 2u : 0u), j.wide ? 1u : 0u,
                             static_cast<uint64_t>(j.mode), L.tkey_cap, g_alloc_generation.load(),
                             ctx->chunking ? 1u : 0u, ctx->chunk_divs_set ? 1u : 0u};
     for (uint64_t d : ctx->chunk_divs) k.push_back(d);
@@ -415,8 +415,10 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     const CamParams cp = make_cam(cam);
     CfgParams kp = make_cfg(cfg, cam);
     // render frames without stats bin each splat into the tiles its cut ellipse reaches
-    // (E_t, a stat, is defined over the reference's lists, so stats frames keep them)
-    kp.tight_rect = ctx->tight_rect && mode == kRender && !j.stats ? 1 : 0;
+    // (E_t, a stat, is defined over the reference's lists, so stats frames keep them --
+    // unless they only time the plain render path)
+    const bool count_stats = j.stats && !j.stats->timing_path;
+    kp.tight_rect = ctx->tight_rect && mode == kRender && !count_stats ? 1 : 0;
     const uint64_t ntile = static_cast<uint64_t>(kp.tiles_x) * static_cast<uint64_t>(kp.tiles_y);
     const uint64_t npx = static_cast<uint64_t>(cam->width) * static_cast<uint64_t>(cam->height);
     const bool timing = j.stats && j.stats->want_timing;
@@ -430,28 +432,21 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     SGS_CUDA(L.colour.ensure(n1 * sizeof(float4)));
     SGS_CUDA(L.brect.ensure(n1 * sizeof(int4)));
     SGS_CUDA(L.bmeta.ensure(n1 * sizeof(uint2)));
-    SGS_CUDA(L.bin_status.ensure(bin_emit_status_bytes(n1)));
+    SGS_CUDA(L.bin_status.ensure(bin_scratch_bytes(n1)));
     SGS_CUDA(L.ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
     // tile pairs (grow-only; P above the capacity makes the frame regrow and redo);
     // at least n1, as K2 sorts in these arrays too
     if (L.tkey_cap == 0) L.tkey_cap = std::max<uint64_t>(16 * n, 1 << 20);
     L.tkey_cap = std::min<uint64_t>(std::max<uint64_t>(L.tkey_cap, n1), kMaxSortKeys);
-    if (n1 > kMaxSortKeys) return fail(SGS_ERR_INVALID_ARGUMENT, "more than 2^30 Gaussians in one frame");
+    if (n1 > kMaxSortKeys) return fail(SGS_ERR_INVALID_ARGUMENT, "more than 2^31 - 1 Gaussians in one frame");
     SGS_CUDA(L.tk_a.ensure(L.tkey_cap * 4));
     SGS_CUDA(L.tv_a.ensure(L.tkey_cap * 4));
     SGS_CUDA(L.tk_b.ensure(L.tkey_cap * 4));
     SGS_CUDA(L.tv_b.ensure(L.tkey_cap * 4));
-    if (L.sort_ctl.bytes < sizeof(SortCtl)) {
-        SGS_CUDA(L.sort_ctl.ensure(sizeof(SortCtl)));
-        SGS_CUDA(cudaMemsetAsync(L.sort_ctl.ptr, 0, L.sort_ctl.bytes, s));
-    }
-    const size_t status_bytes = sort_status_words(L.tkey_cap) * 4;
-    if (L.sort_status.bytes < status_bytes) {  // (tagged per sort: zeroed once, never cleared)
-        SGS_CUDA(L.sort_status.ensure(status_bytes));
-        SGS_CUDA(cudaMemsetAsync(L.sort_status.ptr, 0, L.sort_status.bytes, s));
-    }
+    SGS_CUDA(L.sort_ctl.ensure(sizeof(SortCtl)));
+    SGS_CUDA(L.sort_hist.ensure(radix_hist_words() * 4));
     SortCtl* const sctl = L.sort_ctl.as<SortCtl>();
-    uint32_t* const sstatus = L.sort_status.as<uint32_t>();
+    uint32_t* const shist = L.sort_hist.as<uint32_t>();
     float* d_rgb = j.d_rgb;
     float* d_T = j.d_T;
     const int slot = L.out_slot;
@@ -526,7 +521,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         const uint32_t* order = L.order.as<uint32_t>();
         SGS_CUDA(launch_depth_sort(n, L.keys_a.as<unsigned long long>(), L.d_ctr, j.wide, L.tk_a.as<uint32_t>(),
                                    L.tv_a.as<uint32_t>(), L.tk_b.as<uint32_t>(), L.tv_b.as<uint32_t>(), sctl,
-                                   sstatus, L.rects.as<int4>(), L.order.as<uint32_t>(), L.brect.as<int4>(),
+                                   shist, L.rects.as<int4>(), L.order.as<uint32_t>(), L.brect.as<int4>(),
                                    L.bmeta.as<uint2>(), s, &ctx->own_launches));
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 
@@ -560,23 +555,23 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             const uint32_t* done = c > 0 ? L.tile_done.as<uint32_t>() : nullptr;
             if (timing) SGS_CUDA(cudaEventRecord(L.ev[3], s));
             // K3 + K4: (tile, index) pairs of the chunk's ranks, in rank order
-            SGS_CUDA(launch_bin_emit(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
-                                     static_cast<int>(ntile), L.tk_a.as<uint32_t>(), L.tv_a.as<uint32_t>(),
-                                     L.tkey_cap, L.bin_status.as<unsigned long long>(), td, sctl, L.d_ctr, s));
-            ctx->own_launches += 1;
+            SGS_CUDA(launch_binning(rb, re, L.bmeta.as<uint2>(), L.brect.as<int4>(), done, kp.tiles_x,
+                                    static_cast<int>(ntile), L.tk_a.as<uint32_t>(), L.tv_a.as<uint32_t>(),
+                                    L.tkey_cap, L.bin_status.ptr, L.d_ctr, s, &ctx->own_launches));
             if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
-            // K5: stable onesweep passes on the tile id (device-sized)
+            // K5: stable radix passes on the tile id (device-sized)
+            SGS_CUDA(cudaMemsetAsync(sctl, 0, sizeof(SortCtl), s));
             uint32_t* tk = L.tk_a.as<uint32_t>();
             uint32_t* tv = L.tv_a.as<uint32_t>();
             uint32_t* tk2 = L.tk_b.as<uint32_t>();
             uint32_t* tv2 = L.tv_b.as<uint32_t>();
             for (int p = 0; p < td.passes; ++p) {
-                SGS_CUDA(launch_onesweep_pass(tk, tv, tk2, tv2, d_pc, 0, td.shift[p], td.bits[p], sctl, p, sstatus,
-                                              s));
+                SGS_CUDA(launch_radix_pass(tk, tv, tk2, tv2, d_pc, 0, td.shift[p], td.bits[p], sctl, p, shist,
+                                           false, s));
                 std::swap(tk, tk2);
                 std::swap(tv, tv2);
             }
-            ctx->own_launches += td.passes;
+            ctx->own_launches += 2 * td.passes;
             // K6
             SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
             launch_tile_ranges(d_pc, tk, L.ranges.as<uint2>(), s);
@@ -602,7 +597,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
                                           L.colour.as<float4>(), bg, L.pix_state.as<PixelState>(),
                                           L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
                                           L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1,
-                                          L.d_ctr, j.stats != nullptr, L.work.as<uint32_t>(),
+                                          L.d_ctr, count_stats, L.work.as<uint32_t>(),
                                           L.work.as<uint32_t>() + 6 * work_cap, s));
                 ctx->own_launches += 2;  // (+ the work list kernel)
             }
@@ -658,7 +653,7 @@ int check_frame(Lane& L) {
     if (j.mode == kProjectOnly) return SGS_OK;
     if (hc.tie_overflow && !j.wide) return kRetryWide;
     if (hc.key_overflow) {
-        if (L.tkey_cap >= kMaxSortKeys) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^30 tile entries in one chunk");
+        if (L.tkey_cap >= kMaxSortKeys) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^31 - 1 tile entries in one chunk");
         L.tkey_cap = std::min<uint64_t>(hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024, kMaxSortKeys);
         return kRetryGrow;
     }
@@ -1191,7 +1186,7 @@ void sgs_destroy(sgs_context* ctx) {
     for (Lane& L : ctx->lane) {
         if (L.stream) cudaStreamSynchronize(L.stream);
         for (DevBuf* b : {&L.keys_a, &L.order, &L.rec, &L.colour, &L.rects, &L.brect, &L.bmeta, &L.bin_status,
-                          &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_ctl, &L.sort_status, &L.ranges,
+                          &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_ctl, &L.sort_hist, &L.ranges,
                           &L.tile_done, &L.pix_state, &L.pix_walked})
             b->release();
         if (L.d_ctr) cudaFree(L.d_ctr);

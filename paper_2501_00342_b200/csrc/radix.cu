@@ -1,21 +1,17 @@
 // radix.cu -- the library's own device radix sort (no CUB on any path), and the
 // depth-order stage K2 built on it.
 //
-// Onesweep LSD radix sort of (u32 key, u32 value) pairs: ONE kernel per digit pass.
-// A persistent grid takes 4096-key tiles in ticket order; each CTA ranks its tile
-// stably in shared memory (warp match.any + per-warp digit counters), publishes the
-// tile's digit counts, finds the counts of all earlier tiles by a decoupled
-// look-back over per-tile status words (a warp checks 32 predecessors at once, every
-// thread of the CTA then sums its digit over the window), and scatters the tile
-// through shared memory so each digit run leaves as one contiguous write. The global
-// digit histograms of every pass come from the kernel that produced the keys (K1's
-// depth keys via depth_key32_kernel; the binning's tile ids in bin_emit_kernel), so
-// a pass count of p costs p launches and no scan kernels.
-//
-// Status words carry an (epoch, pass) tag -- the epoch is bumped by the producer of
-// each sort -- so the per-tile status never needs clearing between sorts; a count of keys
-// is read from device memory, so a frame sorts a device-sized list with no host
-// round trip.
+// Stable LSD radix sort of (u32 key, u32 value) pairs, two kernels per digit pass
+// and no scan kernel: the keys are cut into G = 296 contiguous slices (2 CTAs per
+// SM); the upsweep writes each slice's digit histogram and adds it to the pass's
+// global digit counts; the downsweep CTA of slice g computes its own output offsets
+// -- the exclusive scan of the global counts plus the column sums of the slices
+// before it (at most 295 rows of 256 counters, read from L2 by 256 threads) -- and
+// walks its slice in order, 2048 keys per step, ranking equal digits within a warp
+// by match.any + popc and across warps by a shared-memory prefix, so the scatter is
+// stable. No CTA waits for another (nothing spins), so the passes overlap freely
+// with the other lanes' kernels. The count of keys is read from device memory: a
+// frame sorts a device-sized list with no host round trip.
 //
 // K2 (raster.cpp:93-101, stable order by (double depth, index)): the 64-bit
 // orderable depth keys are reduced to 32 bits as (key - kmin) >> s (s so the range
@@ -23,7 +19,7 @@
 // stay in index order), and the rare runs of equal 32-bit keys are re-sorted by the
 // full (key, index) in depth_rank_kernel, which also writes the ranks and the
 // rank-ordered binning inputs. A run longer than kRunCap makes the host redo the
-// frame with the full 64-bit sort (8 passes of the same kernel).
+// frame with the full 64-bit sort (8 passes).
 #include <algorithm>
 #include <cstddef>
 
@@ -32,41 +28,17 @@
 namespace sgs {
 namespace {
 
-constexpr int kOsThreads = 512;
-constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsItems = 8;
-constexpr int kOsTile = kOsThreads * kOsItems;  // keys per tile
-constexpr uint32_t kStAgg = 1u;  // tile status: aggregate counts published
-constexpr uint32_t kStPre = 2u;  // inclusive prefix counts published
+constexpr int kRsThreads = 512;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsPer = 4;                       // keys per thread per step
+constexpr int kRsStep = kRsThreads * kRsPer;    // keys per CTA step
+constexpr int kSlices = 2 * 148;                // G: slices = CTAs of every pass
 
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ uint64_t slice_begin(uint64_t n, int g) {
+    const uint64_t per = (n + kSlices - 1) / kSlices;
+    const uint64_t v = per * static_cast<uint64_t>(g);
+    return v < n ? v : n;
 }
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
-// Dynamic shared memory of one onesweep CTA.
-struct OsSmem {
-    uint32_t wcnt[kOsWarps][257];  // per-warp digit counters -> per-warp digit offsets
-    uint32_t tot[256];             // tile digit counts
-    uint32_t toff[256];            // tile digit exclusive offsets
-    uint32_t gofs[256];            // global position of local position 0 of digit d
-    uint32_t gbase[256];           // global digit offsets (exclusive scan of the histogram)
-    uint32_t excl[256];            // counts of digit d in all earlier tiles
-    uint32_t key[kOsTile];
-    uint32_t val[kOsTile];
-    uint32_t warp_tmp[kOsWarps];
-    uint32_t tile;
-    int32_t win_lo, win_pre;  // look-back window [win_lo, win_hi]; win_pre: its lowest tile holds a prefix
-};
 
 // Exclusive scan of v[0, 256) by the first 256 threads (warps 0..7) into out.
 __device__ __forceinline__ void scan256(const uint32_t* v, uint32_t* out, uint32_t* warp_tmp) {
@@ -87,143 +59,110 @@ __device__ __forceinline__ void scan256(const uint32_t* v, uint32_t* out, uint32
     __syncthreads();
 }
 
+// hist[g * 256 + d] = keys of slice g with digit d; tot[d] += the same (tot zeroed
+// by the sort's memset).
+__global__ void __launch_bounds__(kRsThreads) radix_upsweep_kernel(const uint32_t* __restrict__ keys,
+                                                                    const unsigned long long* __restrict__ dcount,
+                                                                    uint64_t hcount, int shift, int bits,
+                                                                    uint32_t* __restrict__ hist,
+                                                                    uint32_t* __restrict__ tot) {
+    __shared__ uint32_t h[256];
+    const int g = blockIdx.x;
+    const uint64_t n = dcount ? *dcount : hcount;
+    const uint32_t mask = (1u << bits) - 1u;
+    if (threadIdx.x < 256) h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t b = slice_begin(n, g), e = slice_begin(n, g + 1);
+    for (uint64_t i = b + threadIdx.x; i < e; i += kRsThreads) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+    __syncthreads();
+    if (threadIdx.x < 256) {
+        const uint32_t c = h[threadIdx.x];
+        hist[g * 256 + threadIdx.x] = c;
+        if (c) atomicAdd(&tot[threadIdx.x], c);
+    }
+}
+
 template <bool kIota>
-__global__ void __launch_bounds__(kOsThreads, 2) onesweep_kernel(
+__global__ void __launch_bounds__(kRsThreads) radix_downsweep_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, const unsigned long long* __restrict__ dcount, uint64_t hcount, int shift, int bits,
-    SortCtl* __restrict__ ctl, int pass, uint32_t* __restrict__ status) {
-    extern __shared__ __align__(16) unsigned char os_raw[];
-    OsSmem& S = *reinterpret_cast<OsSmem*>(os_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ tot) {
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t wcnt[kRsWarps][257];
+    __shared__ uint32_t total[256];
+    __shared__ uint32_t warp_tmp[kRsWarps];
+    const int g = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t n = dcount ? *dcount : hcount;
-    const uint32_t radix = 1u << bits, mask = radix - 1;
-    const uint32_t ntiles = static_cast<uint32_t>((n + kOsTile - 1) / kOsTile);
-    // (epoch, pass) tag of this pass's status words; the low 2 bits of a word are its state
-    const uint32_t tag = ((ctl->epoch << 3) | static_cast<uint32_t>(pass)) & 0x3FFFFFFFu;
-    // status layout per tile: [0] tag | state word, [1..256] aggregate, [257..512] inclusive prefix
-    constexpr int kStride = 1 + 2 * 256;
-    if (tid < 256) S.tot[tid] = tid < static_cast<int>(radix) ? ctl->hist[pass][tid] : 0u;
+    const uint32_t mask = (1u << bits) - 1u;
+    // this slice's first output slot per digit: keys of smaller digits anywhere, plus
+    // keys of this digit in the slices before g
+    if (threadIdx.x < 256) total[threadIdx.x] = tot[threadIdx.x];
     __syncthreads();
-    scan256(S.tot, S.gbase, S.warp_tmp);
-    for (;;) {
-        if (tid == 0) S.tile = atomicAdd(&ctl->ticket[pass], 1u);
-        for (int k = tid; k < kOsWarps * 257; k += kOsThreads) (&S.wcnt[0][0])[k] = 0;
+    scan256(total, base, warp_tmp);
+    if (threadIdx.x < 256) {
+        uint32_t acc = 0;
+        int p = 0;
+        for (; p + 4 <= g; p += 4)
+            acc += hist[(p + 0) * 256 + threadIdx.x] + hist[(p + 1) * 256 + threadIdx.x] +
+                   hist[(p + 2) * 256 + threadIdx.x] + hist[(p + 3) * 256 + threadIdx.x];
+        for (; p < g; ++p) acc += hist[p * 256 + threadIdx.x];
+        base[threadIdx.x] += acc;
+    }
+    const uint64_t b = slice_begin(n, g), e = slice_begin(n, g + 1);
+    for (uint64_t t0 = b; t0 < e; t0 += kRsStep) {
+        for (int k = threadIdx.x; k < kRsWarps * 257; k += kRsThreads) (&wcnt[0][0])[k] = 0;
         __syncthreads();
-        const uint32_t tile = S.tile;
-        if (tile >= ntiles) break;
-        const uint64_t t0 = static_cast<uint64_t>(tile) * kOsTile;
-        // load: warp w owns keys [t0 + w * 32 kOsItems, +32 kOsItems) in rounds of 32, so
-        // the stable order inside the tile is (warp, round, lane) = memory order
-        uint32_t key[kOsItems], val[kOsItems], dg[kOsItems], rk[kOsItems];
-        const uint64_t w0 = t0 + static_cast<uint64_t>(warp) * (32 * kOsItems) + lane;
+        // warp w ranks the consecutive keys [t0 + w * 32 kRsPer, +32 kRsPer) in kRsPer
+        // rounds of 32: the stable order inside a step is (warp, round, lane)
+        uint32_t key[kRsPer], val[kRsPer], dg[kRsPer], rk[kRsPer];
+        const uint64_t w0 = t0 + static_cast<uint64_t>(warp) * (32 * kRsPer) + lane;
 #pragma unroll
-        for (int j = 0; j < kOsItems; ++j) {
+        for (int j = 0; j < kRsPer; ++j) {
             const uint64_t i = w0 + j * 32;
-            const bool ok = i < n;
+            const bool ok = i < e;
             key[j] = ok ? kin[i] : 0u;
             val[j] = kIota ? static_cast<uint32_t>(i) : (ok ? vin[i] : 0u);
             dg[j] = ok ? (key[j] >> shift) & mask : 256u;
         }
 #pragma unroll
-        for (int j = 0; j < kOsItems; ++j) {
+        for (int j = 0; j < kRsPer; ++j) {
             const unsigned peers = __match_any_sync(0xffffffffu, dg[j]);
             const unsigned below = peers & ((1u << lane) - 1u);
-            const uint32_t before = S.wcnt[warp][dg[j]];
+            const uint32_t before = wcnt[warp][dg[j]];
             rk[j] = before + __popc(below);
             __syncwarp();
-            if (below == 0) S.wcnt[warp][dg[j]] = before + __popc(peers);
+            if (below == 0) wcnt[warp][dg[j]] = before + __popc(peers);
             __syncwarp();
         }
         __syncthreads();
-        if (tid < 256) {
+        if (threadIdx.x < 256) {
             uint32_t run = 0;
 #pragma unroll
-            for (int w = 0; w < kOsWarps; ++w) {
-                const uint32_t c = S.wcnt[w][tid];
-                S.wcnt[w][tid] = run;
+            for (int w = 0; w < kRsWarps; ++w) {
+                const uint32_t c = wcnt[w][threadIdx.x];
+                wcnt[w][threadIdx.x] = run;
                 run += c;
             }
-            S.tot[tid] = run;
-            S.excl[tid] = 0;
+            total[threadIdx.x] = run;
         }
         __syncthreads();
-        scan256(S.tot, S.toff, S.warp_tmp);
-        // publish the tile's aggregate (tile 0: its prefix)
-        uint32_t* st = status + static_cast<size_t>(tile) * kStride;
-        if (tid < 256) {
-            st[1 + tid] = S.tot[tid];
-            if (tile == 0) st[257 + tid] = S.tot[tid];
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release_u32(st, tag << 2 | (tile == 0 ? kStPre : kStAgg));
-        // decoupled look-back: warp 0 finds, 32 predecessors at a time, the window that
-        // ends at the nearest tile with a published prefix; every thread adds its digit
-        if (tile > 0) {
-            int64_t hi = static_cast<int64_t>(tile) - 1;
-            for (;;) {
-                if (warp == 0) {
-                    const int64_t p = hi - lane;
-                    uint32_t s = p >= 0 ? 0u : (tag << 2 | kStPre);
-                    for (;;) {
-                        if (p >= 0 && (s >> 2) != tag) s = ld_acquire_u32(status + static_cast<size_t>(p) * kStride);
-                        const bool ready = p < 0 || ((s >> 2) == tag && (s & 3u) != 0u);
-                        if (__all_sync(0xffffffffu, ready)) break;
-                    }
-                    const unsigned pre = __ballot_sync(0xffffffffu, p >= 0 && (s & 3u) == kStPre);
-                    const int stop = pre ? __ffs(pre) - 1 : 31;
-                    if (lane == 0) {
-                        const int64_t lo = hi - stop;
-                        S.win_lo = static_cast<int32_t>(lo < 0 ? 0 : lo);
-                        S.win_pre = pre ? 1 : 0;
-                    }
-                }
-                __syncthreads();
-                const int64_t lo = S.win_lo;
-                const bool has_pre = S.win_pre != 0;
-                if (tid < 256) {
-                    uint32_t acc = 0;
-                    for (int64_t p = hi; p >= lo; --p) {
-                        const uint32_t* sp = status + static_cast<size_t>(p) * kStride;
-                        acc += ld_cg_u32(sp + ((has_pre && p == lo) ? 257 : 1) + tid);
-                    }
-                    S.excl[tid] += acc;
-                }
-                __syncthreads();
-                if (has_pre || lo == 0) break;
-                hi = lo - 1;
-            }
-            if (tid < 256) st[257 + tid] = S.excl[tid] + S.tot[tid];
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) st_release_u32(st, tag << 2 | kStPre);
-        }
-        if (tid < 256) S.gofs[tid] = S.gbase[tid] + S.excl[tid] - S.toff[tid];
-        // local scatter into digit order, then contiguous digit runs to global memory
 #pragma unroll
-        for (int j = 0; j < kOsItems; ++j) {
+        for (int j = 0; j < kRsPer; ++j) {
             if (dg[j] < 256u) {
-                const uint32_t lp = S.toff[dg[j]] + S.wcnt[warp][dg[j]] + rk[j];
-                S.key[lp] = key[j];
-                S.val[lp] = val[j];
+                const uint32_t pos = base[dg[j]] + wcnt[warp][dg[j]] + rk[j];
+                kout[pos] = key[j];
+                vout[pos] = val[j];
             }
         }
         __syncthreads();
-        const uint32_t m = static_cast<uint32_t>(n - t0 < static_cast<uint64_t>(kOsTile) ? n - t0 : kOsTile);
-        for (uint32_t i = tid; i < m; i += kOsThreads) {
-            const uint32_t k = S.key[i];
-            const uint32_t pos = S.gofs[(k >> shift) & mask] + i;
-            kout[pos] = k;
-            vout[pos] = S.val[i];
-        }
-        __syncthreads();
+        if (threadIdx.x < 256) base[threadIdx.x] += total[threadIdx.x];
     }
 }
 
 // ---------------------------------------------------------------------------
 // K2 producers and the rank writer.
 
-constexpr int kHistThreads = 512;
 constexpr int kRunCap = 32;  // longest run of equal 32-bit depth keys fixed up in place
 
 __device__ __forceinline__ int key32_shift(const Counters* ctr) {
@@ -233,19 +172,20 @@ __device__ __forceinline__ int key32_shift(const Counters* ctr) {
     return bits > 32 ? bits - 32 : 0;
 }
 
-// k32[i] = culled ? ~0 : min((key - kmin) >> s, ~0 - 1), and the 4 digit histograms;
-// block 0 opens the sort's epoch.
-__global__ void __launch_bounds__(kHistThreads) depth_key32_kernel(uint64_t n, const unsigned long long* __restrict__ key,
-                                                                   const Counters* __restrict__ ctr,
-                                                                   uint32_t* __restrict__ k32, SortCtl* __restrict__ ctl) {
-    __shared__ uint32_t h[4 * 256];
-    for (int k = threadIdx.x; k < 4 * 256; k += kHistThreads) h[k] = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->epoch += 1;
+// k32[i] = culled ? ~0 : min((key - kmin) >> s, ~0 - 1), and the first pass's upsweep
+// (slice histograms of digit 0, global counts into ctl->hist[pass0]).
+__global__ void __launch_bounds__(kRsThreads) depth_key32_kernel(uint64_t n, const unsigned long long* __restrict__ key,
+                                                                 const Counters* __restrict__ ctr,
+                                                                 uint32_t* __restrict__ k32, uint32_t* __restrict__ hist,
+                                                                 uint32_t* __restrict__ tot) {
+    __shared__ uint32_t h[256];
+    if (threadIdx.x < 256) h[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long kmin = ctr->kmin;
     const int sh = key32_shift(ctr);
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kHistThreads + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * kHistThreads) {
+    const int g = blockIdx.x;
+    const uint64_t b = slice_begin(n, g), e = slice_begin(n, g + 1);
+    for (uint64_t i = b + threadIdx.x; i < e; i += kRsThreads) {
         const unsigned long long k = key[i];
         uint32_t v = 0xFFFFFFFFu;
         if (k != ~0ULL) {
@@ -253,33 +193,38 @@ __global__ void __launch_bounds__(kHistThreads) depth_key32_kernel(uint64_t n, c
             v = d < 0xFFFFFFFEULL ? static_cast<uint32_t>(d) : 0xFFFFFFFEu;
         }
         k32[i] = v;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) atomicAdd(&h[p * 256 + ((v >> (8 * p)) & 255u)], 1u);
+        atomicAdd(&h[v & 255u], 1u);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 4 * 256; k += kHistThreads)
-        if (h[k]) atomicAdd(&ctl->hist[k >> 8][k & 255], h[k]);
+    if (threadIdx.x < 256) {
+        const uint32_t c = h[threadIdx.x];
+        hist[g * 256 + threadIdx.x] = c;
+        if (c) atomicAdd(&tot[threadIdx.x], c);
+    }
 }
 
 // Wide path: the low (half 0) or high (half 1, gathered through the sorted values)
-// 32 bits of the raw 64-bit keys, and their digit histograms (passes 4*half ..).
-__global__ void __launch_bounds__(kHistThreads) depth_key_half_kernel(uint64_t n, const unsigned long long* __restrict__ key,
-                                                                      const uint32_t* __restrict__ idx, int half,
-                                                                      uint32_t* __restrict__ k32, SortCtl* __restrict__ ctl) {
-    __shared__ uint32_t h[4 * 256];
-    for (int k = threadIdx.x; k < 4 * 256; k += kHistThreads) h[k] = 0;
-    if (half == 0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->epoch += 1;
+// 32 bits of the raw 64-bit keys, with the upsweep of their first digit.
+__global__ void __launch_bounds__(kRsThreads) depth_key_half_kernel(uint64_t n, const unsigned long long* __restrict__ key,
+                                                                    const uint32_t* __restrict__ idx, int half,
+                                                                    uint32_t* __restrict__ k32, uint32_t* __restrict__ hist,
+                                                                    uint32_t* __restrict__ tot) {
+    __shared__ uint32_t h[256];
+    if (threadIdx.x < 256) h[threadIdx.x] = 0;
     __syncthreads();
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kHistThreads + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * kHistThreads) {
+    const int g = blockIdx.x;
+    const uint64_t b = slice_begin(n, g), e = slice_begin(n, g + 1);
+    for (uint64_t i = b + threadIdx.x; i < e; i += kRsThreads) {
         const uint32_t v = half ? static_cast<uint32_t>(key[idx[i]] >> 32) : static_cast<uint32_t>(key[i]);
         k32[i] = v;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) atomicAdd(&h[p * 256 + ((v >> (8 * p)) & 255u)], 1u);
+        atomicAdd(&h[v & 255u], 1u);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 4 * 256; k += kHistThreads)
-        if (h[k]) atomicAdd(&ctl->hist[4 * half + (k >> 8)][k & 255], h[k]);
+    if (threadIdx.x < 256) {
+        const uint32_t c = h[threadIdx.x];
+        hist[g * 256 + threadIdx.x] = c;
+        if (c) atomicAdd(&tot[threadIdx.x], c);
+    }
 }
 
 __device__ __forceinline__ bool less_ki(unsigned long long ka, uint32_t ia, unsigned long long kb, uint32_t ib) {
@@ -349,71 +294,62 @@ __global__ void depth_rank_kernel(uint64_t n, const uint32_t* __restrict__ sk, c
     for (uint32_t a = 0; a < m; ++a) put_rank(r + a, ii[a], true, rects, order, brect, bmeta);
 }
 
-size_t onesweep_smem() { return sizeof(OsSmem); }
-
 }  // namespace
 
-size_t sort_status_words(uint64_t capacity) {
-    return static_cast<size_t>((capacity + kOsTile - 1) / kOsTile + 1) * (1 + 2 * 256);
-}
+size_t radix_hist_words() { return static_cast<size_t>(kSlices) * 256; }
 
-int onesweep_grid() { return 148 * 2; }
-
-cudaError_t launch_onesweep_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
-                                 const unsigned long long* dcount, uint64_t hcount, int shift, int bits,
-                                 SortCtl* ctl, int pass, uint32_t* status, cudaStream_t stream) {
-    static const cudaError_t attr = [] {
-        cudaError_t e = cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(onesweep_smem()));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(onesweep_smem()));
-        return e;
-    }();
-    if (attr != cudaSuccess) return attr;
+cudaError_t launch_radix_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                              const unsigned long long* dcount, uint64_t hcount, int shift, int bits, SortCtl* ctl,
+                              int pass, uint32_t* hist, bool histogram_ready, cudaStream_t stream) {
+    uint32_t* tot = ctl->hist[pass];
+    if (!histogram_ready) {
+        radix_upsweep_kernel<<<kSlices, kRsThreads, 0, stream>>>(kin, dcount, hcount, shift, bits, hist, tot);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     if (vin)
-        onesweep_kernel<false><<<onesweep_grid(), kOsThreads, onesweep_smem(), stream>>>(
-            kin, vin, kout, vout, dcount, hcount, shift, bits, ctl, pass, status);
+        radix_downsweep_kernel<false><<<kSlices, kRsThreads, 0, stream>>>(kin, vin, kout, vout, dcount, hcount,
+                                                                        shift, bits, hist, tot);
     else
-        onesweep_kernel<true><<<onesweep_grid(), kOsThreads, onesweep_smem(), stream>>>(
-            kin, nullptr, kout, vout, dcount, hcount, shift, bits, ctl, pass, status);
+        radix_downsweep_kernel<true><<<kSlices, kRsThreads, 0, stream>>>(kin, nullptr, kout, vout, dcount, hcount,
+                                                                       shift, bits, hist, tot);
     return cudaGetLastError();
 }
 
-// K2: depth order of n splats. Narrow: key32 + 4 passes + rank fix-up (6 launches);
-// wide: low half 4 passes, high half 4 passes, ranks (11 launches).
+// K2: depth order of n splats. Narrow: key32 (+ first upsweep), 4 passes, ranks with
+// the run fix-up (9 launches); wide: low half 4 passes, high half 4 passes, ranks.
 cudaError_t launch_depth_sort(uint64_t n, const unsigned long long* key, Counters* ctr, bool wide, uint32_t* ka,
-                              uint32_t* va, uint32_t* kb, uint32_t* vb, SortCtl* ctl, uint32_t* status,
+                              uint32_t* va, uint32_t* kb, uint32_t* vb, SortCtl* ctl, uint32_t* hist,
                               const int4* rects, uint32_t* order, int4* brect, uint2* bmeta, cudaStream_t stream,
                               uint64_t* launches) {
     if (n == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(&ctl->ticket[0], 0, sizeof(SortCtl) - offsetof(SortCtl, ticket), stream);
     if (e != cudaSuccess) return e;
-    const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>((n + kHistThreads - 1) / kHistThreads, 148 * 4));
-    // 4 passes over 8-bit digits: (ka, iota) -> (kb, vb) -> (ka, va) -> (kb, vb) -> (ka, va)
+    // 4 passes over 8-bit digits: (ka, iota) -> (kb, vb) -> (ka, va) -> (kb, vb) -> (ka, va);
+    // the first pass's histograms come from the key producer
     auto four = [&](int pass0, bool iota_first) -> cudaError_t {
         cudaError_t ee = cudaSuccess;
         for (int p = 0; p < 4 && ee == cudaSuccess; ++p) {
             const bool even = (p & 1) == 0;
-            ee = launch_onesweep_pass(even ? ka : kb, (p == 0 && iota_first) ? nullptr : (even ? va : vb),
-                                      even ? kb : ka, even ? vb : va, nullptr, n, 8 * p, 8, ctl, pass0 + p, status,
-                                      stream);
+            ee = launch_radix_pass(even ? ka : kb, (p == 0 && iota_first) ? nullptr : (even ? va : vb),
+                                   even ? kb : ka, even ? vb : va, nullptr, n, 8 * p, 8, ctl, pass0 + p, hist,
+                                   p == 0, stream);
         }
         return ee;
     };
     if (!wide) {
-        depth_key32_kernel<<<hgrid, kHistThreads, 0, stream>>>(n, key, ctr, ka, ctl);
+        depth_key32_kernel<<<kSlices, kRsThreads, 0, stream>>>(n, key, ctr, ka, hist, ctl->hist[0]);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = four(0, true)) != cudaSuccess) return e;
-        *launches += 6;
+        *launches += 9;
     } else {
-        depth_key_half_kernel<<<hgrid, kHistThreads, 0, stream>>>(n, key, nullptr, 0, ka, ctl);
+        depth_key_half_kernel<<<kSlices, kRsThreads, 0, stream>>>(n, key, nullptr, 0, ka, hist, ctl->hist[0]);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = four(0, true)) != cudaSuccess) return e;
-        depth_key_half_kernel<<<hgrid, kHistThreads, 0, stream>>>(n, key, va, 1, ka, ctl);
+        depth_key_half_kernel<<<kSlices, kRsThreads, 0, stream>>>(n, key, va, 1, ka, hist, ctl->hist[4]);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = four(4, false)) != cudaSuccess) return e;
-        *launches += 11;
+        *launches += 17;
     }
     depth_rank_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, ka, va, key, wide ? 1 : 0, ctr,
                                                                                   rects, order, brect, bmeta);

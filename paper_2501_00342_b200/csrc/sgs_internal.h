@@ -181,13 +181,11 @@ const void* k1_record_func(const K1Record* r);
 cudaError_t k1_record_patch(cudaGraphExec_t exec, cudaGraphNode_t node, K1Record* r, const CamParams& cam);
 // per-scene 3D covariance cache: 3 planes of n double2 (projection.cuh)
 void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream);
-// Device control block of one radix sort (radix.cu), one per lane. The epoch tags the
-// per-tile status words (never cleared); tickets and histograms are zeroed by a memset
-// from `ticket` on before the producer of the keys accumulates the histograms.
+// Device control block of one radix sort (radix.cu), one per lane: the global digit
+// counts of every pass, zeroed by a memset before the producer of the keys.
 struct SortCtl {
-    uint32_t epoch;
-    uint32_t ticket[8];      // per pass: tile tickets
-    uint32_t hist[8][256];   // per pass: global digit histogram (filled by the key producer)
+    uint32_t ticket[8];      // (reserved)
+    uint32_t hist[8][256];   // per pass: global digit counts
 };
 // The digit split of a tile-id sort: passes of <= 8 bits, LSD first.
 struct TileDigits {
@@ -195,27 +193,29 @@ struct TileDigits {
     int shift[4];
     int bits[4];
 };
-size_t sort_status_words(uint64_t capacity);
-cudaError_t launch_onesweep_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
-                                 const unsigned long long* dcount, uint64_t hcount, int shift, int bits,
-                                 SortCtl* ctl, int pass, uint32_t* status, cudaStream_t stream);
+// Per-slice digit histograms of one pass (radix_hist_words() u32).
+size_t radix_hist_words();
+// One stable pass on bits [shift, shift + bits) of (key, value) pairs; vin null: the
+// values are the input positions. The count is *dcount if dcount, else hcount.
+// histogram_ready: hist / ctl->hist[pass] were filled by the key producer.
+cudaError_t launch_radix_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                              const unsigned long long* dcount, uint64_t hcount, int shift, int bits, SortCtl* ctl,
+                              int pass, uint32_t* hist, bool histogram_ready, cudaStream_t stream);
 // K2: the depth order of n splats: order[r], and the rank-ordered binning inputs
 // brect[r] / bmeta[r] = (index, tiles of its rectangle). ka/va/kb/vb: 4 scratch arrays
 // of n u32. Narrow (32-bit keys + exact run fix-up) unless `wide` (full 64-bit keys).
 cudaError_t launch_depth_sort(uint64_t n, const unsigned long long* key, Counters* ctr, bool wide, uint32_t* ka,
-                              uint32_t* va, uint32_t* kb, uint32_t* vb, SortCtl* ctl, uint32_t* status,
+                              uint32_t* va, uint32_t* kb, uint32_t* vb, SortCtl* ctl, uint32_t* hist,
                               const int4* rects, uint32_t* order, int4* brect, uint2* bmeta, cudaStream_t stream,
                               uint64_t* launches);
-// K3+K4 fused (binning.cu): for the ranks [rb, re) of a depth chunk, count each
-// rank's live tiles, scan the counts by decoupled look-back, and emit the (tile id,
-// Gaussian index) pairs into tk / tv in rank order; the tile ids' digit histograms of
-// the K5 passes go to ctl->hist, the chunk's P to ctr (chunk_entries), and the sort
-// epoch is opened. status: bin_emit_status_bytes zeroed bytes.
-size_t bin_emit_status_bytes(uint64_t ranks);
-cudaError_t launch_bin_emit(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
-                            int tiles_x, int ntile, uint32_t* tk, uint32_t* tv, uint64_t capacity,
-                            unsigned long long* status, const TileDigits& td, SortCtl* ctl, Counters* ctr,
-                            cudaStream_t stream);
+// K3 + K4 (binning.cu): for the ranks [rb, re) of a depth chunk, count each rank's
+// live tiles, then emit the (tile id, Gaussian index) pairs into tk / tv in rank order
+// at offsets each CTA scans itself; the chunk's P goes to ctr (chunk_entries).
+// scratch: bin_scratch_bytes(ranks) bytes.
+size_t bin_scratch_bytes(uint64_t ranks);
+cudaError_t launch_binning(uint64_t rb, uint64_t re, const uint2* bmeta, const int4* brect, const uint32_t* done,
+                           int tiles_x, int ntile, uint32_t* tk, uint32_t* tv, uint64_t capacity, void* scratch,
+                           Counters* ctr, cudaStream_t stream, uint64_t* launches);
 TileDigits tile_digits(int tile_bits);
 // backward (backward.cu)
 size_t bwd_splat_bytes();
