@@ -101,12 +101,13 @@ struct Lane {
     cudaStream_t stream = nullptr;  // the lane's current stream: plain or ranked
     cudaStream_t plain = nullptr, ranked = nullptr;
     cudaEvent_t swap = nullptr;
-    DevBuf keys_a, order, rec, colour, rects, brect, bmeta;
+    DevBuf keys_a, keys_b, order, rec, colour, rects, brect, bmeta;
+    DevBuf buckets;     // K2 coarse histogram / offsets
     DevBuf bin_status;  // K3/K4 scratch: per-rank counts, per-CTA sums
     DevBuf work;        // K7 work list (+ control words)
     // (tile id, Gaussian index) pairs, ping-pong for K5; also K2's sort scratch
     DevBuf tk_a, tv_a, tk_b, tv_b;
-    DevBuf sort_ctl, sort_hist;  // radix sort: global digit counts, per-slice histograms
+    DevBuf sort_hist;  // radix sort: per-slice digit histograms
     DevBuf ranges, tile_done, pix_state, pix_walked;
     // host-output frames: kOutSlots device buffers per lane drained by the lane's copy
     // stream, so the lane renders its next views while earlier ones cross PCIe
@@ -443,9 +444,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     SGS_CUDA(L.tv_a.ensure(L.tkey_cap * 4));
     SGS_CUDA(L.tk_b.ensure(L.tkey_cap * 4));
     SGS_CUDA(L.tv_b.ensure(L.tkey_cap * 4));
-    SGS_CUDA(L.sort_ctl.ensure(sizeof(SortCtl)));
     SGS_CUDA(L.sort_hist.ensure(radix_hist_words() * 4));
-    SortCtl* const sctl = L.sort_ctl.as<SortCtl>();
     uint32_t* const shist = L.sort_hist.as<uint32_t>();
     float* d_rgb = j.d_rgb;
     float* d_T = j.d_T;
@@ -517,12 +516,25 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             return SGS_OK;
         }
 
-        // K2: ranks and the rank-ordered binning inputs (radix.cu)
+        // K2: ranks and the rank-ordered binning inputs (depth_sort.cu; the 64-bit radix
+        // sort of radix.cu after a tie overflow)
         const uint32_t* order = L.order.as<uint32_t>();
-        SGS_CUDA(launch_depth_sort(n, L.keys_a.as<unsigned long long>(), L.d_ctr, j.wide, L.tk_a.as<uint32_t>(),
-                                   L.tv_a.as<uint32_t>(), L.tk_b.as<uint32_t>(), L.tv_b.as<uint32_t>(), sctl,
-                                   shist, L.rects.as<int4>(), L.order.as<uint32_t>(), L.brect.as<int4>(),
-                                   L.bmeta.as<uint2>(), s, &ctx->own_launches));
+        if (!j.wide) {
+            const int log2c = depth_coarse_log2(n);
+            const size_t half = align_up(depth_two_level_scratch(log2c), 256);
+            SGS_CUDA(L.buckets.ensure(2 * half));
+            SGS_CUDA(L.keys_b.ensure(n1 * 8));
+            SGS_CUDA(launch_depth_two_level(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2c,
+                                            L.buckets.as<uint32_t>(), L.buckets.as<uint32_t>() + half / 4,
+                                            L.keys_b.as<unsigned long long>(), L.order.as<uint32_t>(),
+                                            L.rects.as<int4>(), L.brect.as<int4>(), L.bmeta.as<uint2>(), s,
+                                            &ctx->own_launches));
+        } else {
+            SGS_CUDA(launch_depth_sort_wide(n, L.keys_a.as<unsigned long long>(), L.d_ctr, L.tk_a.as<uint32_t>(),
+                                            L.tv_a.as<uint32_t>(), L.tk_b.as<uint32_t>(), L.tv_b.as<uint32_t>(),
+                                            shist, L.rects.as<int4>(), L.order.as<uint32_t>(),
+                                            L.brect.as<int4>(), L.bmeta.as<uint2>(), s, &ctx->own_launches));
+        }
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 
         // depth chunks over ranks (bounds known on the host: culled splats sort last and
@@ -560,18 +572,16 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
                                     L.tkey_cap, L.bin_status.ptr, L.d_ctr, s, &ctx->own_launches));
             if (timing) SGS_CUDA(cudaEventRecord(L.ev[4], s));
             // K5: stable radix passes on the tile id (device-sized)
-            SGS_CUDA(cudaMemsetAsync(sctl, 0, sizeof(SortCtl), s));
             uint32_t* tk = L.tk_a.as<uint32_t>();
             uint32_t* tv = L.tv_a.as<uint32_t>();
             uint32_t* tk2 = L.tk_b.as<uint32_t>();
             uint32_t* tv2 = L.tv_b.as<uint32_t>();
             for (int p = 0; p < td.passes; ++p) {
-                SGS_CUDA(launch_radix_pass(tk, tv, tk2, tv2, d_pc, 0, td.shift[p], td.bits[p], sctl, p, shist,
-                                           false, s));
+                SGS_CUDA(launch_radix_pass(tk, tv, tk2, tv2, d_pc, 0, td.shift[p], td.bits[p], shist, false, s));
                 std::swap(tk, tk2);
                 std::swap(tv, tv2);
             }
-            ctx->own_launches += 2 * td.passes;
+            ctx->own_launches += 3 * td.passes;
             // K6
             SGS_CUDA(cudaMemsetAsync(L.ranges.ptr, 0, ntile * sizeof(uint2), s));
             launch_tile_ranges(d_pc, tk, L.ranges.as<uint2>(), s);
@@ -1185,8 +1195,8 @@ void sgs_destroy(sgs_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (Lane& L : ctx->lane) {
         if (L.stream) cudaStreamSynchronize(L.stream);
-        for (DevBuf* b : {&L.keys_a, &L.order, &L.rec, &L.colour, &L.rects, &L.brect, &L.bmeta, &L.bin_status,
-                          &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_ctl, &L.sort_hist, &L.ranges,
+        for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.buckets, &L.order, &L.rec, &L.colour, &L.rects, &L.brect, &L.bmeta, &L.bin_status,
+                          &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_hist, &L.ranges,
                           &L.tile_done, &L.pix_state, &L.pix_walked})
             b->release();
         if (L.d_ctr) cudaFree(L.d_ctr);

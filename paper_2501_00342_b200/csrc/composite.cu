@@ -361,8 +361,7 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
                     const float4 B = R[j][1];
                     float m0, m1;
                     mahal2x2<kSameRow>(A, B.x, fcx0, fcy0, fcx1, fcy1, m0, m1);
-                    // (NaN-aware: a NaN m2 is decided by the FP64 path, as the reference blends it)
-                    guard |= !(m0 > B.y || m0 < B.z) || !(m1 > B.y || m1 < B.z);
+                    guard |= (m0 <= B.y && m0 >= B.z) || (m1 <= B.y && m1 >= B.z);
                     a0[k] = m0 < B.z ? fast_alpha(m0, B.w) : 0.0f;
                     a1[k] = m1 < B.z ? fast_alpha(m1, B.w) : 0.0f;
                 }

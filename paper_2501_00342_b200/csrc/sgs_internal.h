@@ -181,12 +181,6 @@ const void* k1_record_func(const K1Record* r);
 cudaError_t k1_record_patch(cudaGraphExec_t exec, cudaGraphNode_t node, K1Record* r, const CamParams& cam);
 // per-scene 3D covariance cache: 3 planes of n double2 (projection.cuh)
 void launch_cov3d(const ScenePlanes& sp, double2* cov, cudaStream_t stream);
-// Device control block of one radix sort (radix.cu), one per lane: the global digit
-// counts of every pass, zeroed by a memset before the producer of the keys.
-struct SortCtl {
-    uint32_t ticket[8];      // (reserved)
-    uint32_t hist[8][256];   // per pass: global digit counts
-};
 // The digit split of a tile-id sort: passes of <= 8 bits, LSD first.
 struct TileDigits {
     int passes;
@@ -197,17 +191,25 @@ struct TileDigits {
 size_t radix_hist_words();
 // One stable pass on bits [shift, shift + bits) of (key, value) pairs; vin null: the
 // values are the input positions. The count is *dcount if dcount, else hcount.
-// histogram_ready: hist / ctl->hist[pass] were filled by the key producer.
+// histogram_ready: hist was filled by the key producer.
 cudaError_t launch_radix_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
-                              const unsigned long long* dcount, uint64_t hcount, int shift, int bits, SortCtl* ctl,
-                              int pass, uint32_t* hist, bool histogram_ready, cudaStream_t stream);
-// K2: the depth order of n splats: order[r], and the rank-ordered binning inputs
-// brect[r] / bmeta[r] = (index, tiles of its rectangle). ka/va/kb/vb: 4 scratch arrays
-// of n u32. Narrow (32-bit keys + exact run fix-up) unless `wide` (full 64-bit keys).
-cudaError_t launch_depth_sort(uint64_t n, const unsigned long long* key, Counters* ctr, bool wide, uint32_t* ka,
-                              uint32_t* va, uint32_t* kb, uint32_t* vb, SortCtl* ctl, uint32_t* hist,
-                              const int4* rects, uint32_t* order, int4* brect, uint2* bmeta, cudaStream_t stream,
-                              uint64_t* launches);
+                              const unsigned long long* dcount, uint64_t hcount, int shift, int bits,
+                              uint32_t* hist, bool histogram_ready, cudaStream_t stream);
+// K2 (depth_sort.cu): the depth order of n splats -- order[r], and the rank-ordered
+// binning inputs brect[r] / bmeta[r] = (index, tiles of its rectangle) -- by a
+// two-level bucket sort. Scratch: ghist / cur depth_two_level_scratch bytes each,
+// part_key n u64. Raises tie_overflow on a degenerate depth distribution.
+int depth_coarse_log2(uint64_t n);
+size_t depth_two_level_scratch(int log2c);
+cudaError_t launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters* ctr, int log2c,
+                                   uint32_t* ghist, uint32_t* cur, unsigned long long* part_key, uint32_t* order,
+                                   const int4* rects, int4* brect, uint2* bmeta, cudaStream_t stream,
+                                   uint64_t* launches);
+// K2's fallback (radix.cu): the full 64-bit radix sort. ka/va/kb/vb: n u32 each.
+cudaError_t launch_depth_sort_wide(uint64_t n, const unsigned long long* key, Counters* ctr, uint32_t* ka,
+                                   uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
+                                   const int4* rects, uint32_t* order, int4* brect, uint2* bmeta,
+                                   cudaStream_t stream, uint64_t* launches);
 // K3 + K4 (binning.cu): for the ranks [rb, re) of a depth chunk, count each rank's
 // live tiles, then emit the (tile id, Gaussian index) pairs into tk / tv in rank order
 // at offsets each CTA scans itself; the chunk's P goes to ctr (chunk_entries).
