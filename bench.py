@@ -309,13 +309,18 @@ def main():
     total_frames = world * vpr * args.steps
     value = total_frames / (dev_ms / 1e3)
 
-    # ---------------- per-stage breakdown + counters (separate pass) ----------------
-    _, _, st = renderer.render_batch(dscene, my_cams[:4], degree_override=1,
-                                     rgb=frames.data_ptr(), T=trans.data_ptr(), device_out=True,
-                                     stats=True, timing=True)
+    # ---------------- per-stage breakdown (the timed path) + counters ----------------
+    # Stage times: frames of the timed path itself (tight tile rectangles, no E_t
+    # counting), one lane, CUDA events around each stage on the lane's stream.
+    # Counters: stats frames, whose E_t / P are defined over the reference's lists.
     nv = 4
+    _, _, st = renderer.render_batch(dscene, my_cams[:nv], degree_override=1,
+                                     rgb=frames.data_ptr(), T=trans.data_ptr(), device_out=True,
+                                     timing=True, timing_path=True)
     stage_ms = {k: v / nv for k, v in st.ms.items()}
-    V, P, E_t = st.visible / nv, st.tile_entries / nv, st.block_entries / nv
+    _, _, sc = renderer.render_batch(dscene, my_cams[:nv], degree_override=1,
+                                     rgb=frames.data_ptr(), T=trans.data_ptr(), device_out=True, stats=True)
+    V, P, E_t = sc.visible / nv, sc.tile_entries / nv, sc.block_entries / nv
     hbm, peak_kind = peaks()
     comp_bytes = composite_algorithmic_bytes(E_t)
     comp_ms = stage_ms["composite"]
@@ -414,21 +419,24 @@ def main():
             "config": {"workload": WORKLOAD, "gaussians": N_GAUSS, "width": W, "height": H,
                        "views_per_gpu_per_step": vpr, "parallelism": f"views x{world}",
                        "l2": "inputs larger than L2 (scene blob %.0f MB > 126 MB)" % (meta.blob_bytes / 1e6)},
-            "roofline": {"bound": "hbm", "kernel": "preprocess (K1): longest single launch, the frame's "
-                                                "HBM-dominant kernel", "achieved": k1_gbs,
-                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": k1_gbs / hbm,
-                         "traffic": prof.get("k1_dram_bytes_per_launch"),
-                         "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms},
-            "composite_roofline": {"bound": "issue (SM instruction issue; HBM fraction beside it)",
-                                   "kernel": "composite (K7), all depth-chunk launches of a frame",
-                                   "issue": k7_issue, "hbm_achieved": comp_gbs, "hbm_peak": hbm,
-                                   "hbm_frac": comp_gbs / hbm,
-                                   "traffic": prof.get("composite_dram_bytes_per_frame"),
-                                   "algorithmic_bytes_per_frame": comp_bytes, "ms_per_frame": comp_ms},
+            # the dominant kernel: K7, over the depth-chunk launches of one frame of the
+            # timed path; HBM fraction per the contract, SM-issue fraction beside it (K7
+            # evaluates ~1e8 (pixel, splat) pairs over ~86 MB: issue-bound by design)
+            "roofline": {"bound": "hbm", "kernel": "composite (K7): all depth-chunk launches of a frame",
+                         "achieved": comp_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": comp_gbs / hbm, "traffic": prof.get("composite_dram_bytes_per_frame"),
+                         "algorithmic_bytes_per_frame": comp_bytes, "bytes_formula": "52 E_t + 16 W H",
+                         "ms_per_frame": comp_ms, "issue": k7_issue},
+            "k1_roofline": {"bound": "hbm", "kernel": "preprocess (K1), one launch per frame",
+                            "achieved": k1_gbs, "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm,
+                            "traffic": prof.get("k1_dram_bytes_per_launch"),
+                            "algorithmic_bytes_per_launch": k1_bytes, "bytes_formula": "4 N (11 + n_c) + 88 V",
+                            "launch_ms": k1_ms},
             "frame_roofline": {"achieved": frame_gbs, "peak": hbm, "unit": "GB/s",
                                "frac": frame_gbs / hbm, "bytes_per_frame": frame_bytes},
             "stage_ms_per_frame": stage_ms, "dominant_stage": dominant,
-            "counters_per_frame": {"V": V, "P": P, "E_t": E_t, "guard_hits": st.guard_hits / nv},
+            "counters_per_frame": {"V": V, "P": P, "E_t": E_t, "guard_hits": sc.guard_hits / nv,
+                                   "P_tight": st.tile_entries / nv},
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -436,7 +444,7 @@ def main():
                              "d2h_bytes_per_step": vpr * H * W * 12,
                              "note": "image only, the reference Python render's default output"},
             "gpu_launches": int(launches1[0] - launches0[0]),
-            "library_launches": int(launches1[1] - launches0[1]),
+            "library_launches": int(launches1[1] - launches0[1]),  # third-party kernels: none
             "clocks": clocks,
             "scene_setup_s": setup_s, "scene_broadcast_ms": bcast_ms, "frame_gather_ms": gather_ms,
         }
