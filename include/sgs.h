@@ -284,6 +284,40 @@ sgs_status sgs_ply_read(const char* path, sgs_ply_info* info, double* params, ui
  * builds from sgs_ply_read's parameters, bit for bit). */
 sgs_status sgs_scene_load_ply(sgs_context* ctx, const char* path, sgs_ply_info* info, sgs_scene** out);
 
+/* --- multi-GPU ------------------------------------------------ *
+ * Replaces the reference's per-view loops (tools/main.cpp:207-216, :280-287) and its
+ * std::thread parallel_for (common.hpp:53-77) across GPUs: one rank per GPU over
+ * NCCL, the scene replicated by one broadcast, the views block-partitioned, the
+ * frames gathered to a root with grouped send/recv overlapped with rendering. Every
+ * sgs_group_* call below is collective: each rank makes it (one process per GPU, or
+ * one host thread per rank of an sgs_group_create set). NCCL is loaded at run time;
+ * without it these calls return SGS_ERR_NCCL. */
+typedef struct sgs_group sgs_group;
+#define SGS_GROUP_ID_BYTES 128
+/* A fresh NCCL unique id (ncclGetUniqueId), made on one rank and shipped to all. */
+sgs_status sgs_group_unique_id(uint8_t* id /* SGS_GROUP_ID_BYTES */);
+/* Rank `rank` of `nranks` on ctx's device (ncclCommInitRank; one process per GPU). */
+sgs_status sgs_group_init_rank(sgs_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id,
+                               sgs_group** out);
+/* Every rank of one process (ncclCommInitAll over devices[0..ndev)), each with its
+ * own context: out[r] is rank r. Drive each rank's collective calls from its own
+ * host thread. */
+sgs_status sgs_group_create(int32_t ndev, const int32_t* devices, sgs_group** out /* ndev */);
+void sgs_group_destroy(sgs_group* group);
+/* The rank's render context (owned by the group when made by sgs_group_create). */
+sgs_status sgs_group_context(sgs_group* group, sgs_context** ctx);
+/* The root uploads desc (ignored elsewhere); its device layout and blob reach every
+ * rank by NCCL broadcast; *out is the rank's device scene (free with sgs_scene_free). */
+sgs_status sgs_group_broadcast_scene(sgs_group* group, const sgs_scene_desc* desc, int32_t root,
+                                     sgs_scene** out);
+/* Views [0, n) of cams (the same on every rank), rank r rendering its contiguous
+ * block; the root receives every frame: rgb + i*H*W*3 and T + i*H*W (T may be NULL)
+ * in out_memory (device buffers on the root's device, or host). Other ranks ignore
+ * rgb / T. stats (optional) accumulates the rank's own views. */
+sgs_status sgs_group_render_views(sgs_group* group, const sgs_scene* scene, const sgs_camera* cams, int32_t n,
+                                  const sgs_render_config* cfg, int32_t root, float* rgb, float* T,
+                                  int32_t out_memory, sgs_render_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

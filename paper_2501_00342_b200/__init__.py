@@ -335,11 +335,22 @@ class Renderer:
         _check(self._lib.sgs_create(device, ctypes.byref(h)))
         self.handle = h
         self.device = device
+        self._owned = True
+
+    @classmethod
+    def _wrap(cls, handle: int, device: int) -> "Renderer":
+        """A Renderer over a context someone else owns (an sgs_group's)."""
+        r = cls.__new__(cls)
+        r._lib = _lib()
+        r.handle = ctypes.c_void_p(handle)
+        r.device = device
+        r._owned = False
+        return r
 
     def close(self):
-        if self.handle:
+        if self.handle and self._owned:
             self._lib.sgs_destroy(self.handle)
-            self.handle = ctypes.c_void_p()
+        self.handle = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -354,7 +365,8 @@ class Renderer:
         _check(self._lib.sgs_synchronize(self.handle))
 
     def launch_count(self):
-        """(own kernel launches, CUB library launches) issued on this context so far."""
+        """(own kernel launches, third-party library launches -- none) issued on this
+        context so far."""
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         _check(self._lib.sgs_launch_count(self.handle, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value

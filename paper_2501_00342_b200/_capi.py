@@ -180,7 +180,17 @@ SIGNATURES = {
                       ctypes.c_int32, ctypes.POINTER(ctypes.c_double), _P]),
     "sgs_ply_read": (_S, [ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), _P, ctypes.c_uint64]),
     "sgs_scene_load_ply": (_S, [_P, ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), ctypes.POINTER(_P)]),
+    "sgs_group_unique_id": (_S, [_P]),
+    "sgs_group_init_rank": (_S, [_P, ctypes.c_int32, ctypes.c_int32, _P, ctypes.POINTER(_P)]),
+    "sgs_group_create": (_S, [ctypes.c_int32, _P, _P]),
+    "sgs_group_destroy": (None, [_P]),
+    "sgs_group_context": (_S, [_P, ctypes.POINTER(_P)]),
+    "sgs_group_broadcast_scene": (_S, [_P, ctypes.POINTER(sgs_scene_desc), ctypes.c_int32, ctypes.POINTER(_P)]),
+    "sgs_group_render_views": (_S, [_P, _P, ctypes.POINTER(sgs_camera), ctypes.c_int32,
+                                    ctypes.POINTER(sgs_render_config), ctypes.c_int32, _P, _P, ctypes.c_int32,
+                                    ctypes.POINTER(sgs_render_stats)]),
 }
+GROUP_ID_BYTES = 128
 
 _lib = None
 

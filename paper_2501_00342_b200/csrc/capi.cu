@@ -1116,6 +1116,23 @@ std::vector<int32_t> ply_slot_table(const PlyTable& t, int color_planes, int* mu
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Helpers for group.cu (sgs_internal.h).
+namespace sgs {
+sgs_status fail_status(sgs_status code, const std::string& msg) { return fail(code, msg); }
+int context_device(const sgs_context* ctx) { return ctx->device; }
+void context_stream(const sgs_context* ctx, cudaStream_t* stream) { *stream = ctx->stream; }
+sgs_status scene_bind_owned(sgs_context* ctx, const sgs_scene_meta* meta, void* blob, uint64_t bytes,
+                            sgs_scene** out) {
+    sgs_status st = sgs_scene_bind(ctx, meta, blob, bytes, out);
+    if (st == SGS_OK) {  // the scene frees the blob with itself
+        (*out)->owned.ptr = blob;
+        (*out)->owned.bytes = bytes;
+    }
+    return st;
+}
+}  // namespace sgs
+
 // ===========================================================================
 extern "C" {
 

@@ -10,6 +10,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 
 #include <cuda_runtime.h>
 
@@ -253,5 +254,13 @@ cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const 
                              uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
                              bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream);
 int composite_pixel_chunks(int tile_size);
+
+// capi.cu helpers for group.cu: the last-error text, a context's device and render
+// stream, and binding a device blob the scene then owns (freed with it).
+sgs_status fail_status(sgs_status code, const std::string& msg);
+int context_device(const sgs_context* ctx);
+void context_stream(const sgs_context* ctx, cudaStream_t* stream);
+sgs_status scene_bind_owned(sgs_context* ctx, const sgs_scene_meta* meta, void* blob, uint64_t bytes,
+                            sgs_scene** out);
 
 }  // namespace sgs

