@@ -102,9 +102,10 @@ class RenderGroup:
     """One rank of an sgs_group (include/sgs.h): every method is collective -- each
     rank calls it, with the same arguments (the scene only on the root)."""
 
-    def __init__(self, handle: int, renderer):
+    def __init__(self, handle: int, renderer, rank: int):
         self.handle = ctypes.c_void_p(handle)
         self.renderer = renderer  # the rank's render context
+        self.rank = rank
 
     @staticmethod
     def unique_id() -> bytes:
@@ -122,7 +123,7 @@ class RenderGroup:
         h = ctypes.c_void_p()
         idb = (ctypes.c_uint8 * C.GROUP_ID_BYTES).from_buffer_copy(uid)
         _check(_lib().sgs_group_init_rank(renderer.handle, nranks, rank, idb, ctypes.byref(h)))
-        return cls(h.value, renderer)
+        return cls(h.value, renderer, rank)
 
     @classmethod
     def create(cls, devices: Sequence[int]) -> List["RenderGroup"]:
@@ -134,10 +135,10 @@ class RenderGroup:
         hs = (ctypes.c_void_p * n)()
         _check(_lib().sgs_group_create(n, devs, hs))
         out = []
-        for d, h in zip(devices, hs):
+        for r, (d, h) in enumerate(zip(devices, hs)):
             ctx = ctypes.c_void_p()
             _check(_lib().sgs_group_context(h, ctypes.byref(ctx)))
-            out.append(cls(h, Renderer._wrap(ctx.value, d)))
+            out.append(cls(h, Renderer._wrap(ctx.value, d), r))
         return out
 
     def close(self):
@@ -162,10 +163,11 @@ class RenderGroup:
         return DeviceScene(self.renderer, h.value)
 
     def render_views(self, dscene, cams, root: int = 0, tile_size=16, thresholds=(2.0, 8.0), degree_override=-1,
-                     early_stop=1e-4, rgb=None, T=None, device_out=False):
+                     early_stop=1e-4, rgb=None, T=None, device_out=False, with_T=True):
         """Views [0, len(cams)): this rank renders its block; the root receives every
-        frame (numpy host arrays, or device pointers with device_out=True). Returns
-        (rgb, T) on the root, (None, None) elsewhere."""
+        frame (numpy host arrays, or device pointers with device_out=True). with_T
+        (the same on every rank; T=False on the root means the same) says whether
+        transmittance frames travel. Returns (rgb, T) on the root."""
         import numpy as np
 
         from . import _check, _config, _lib
@@ -173,8 +175,16 @@ class RenderGroup:
         n = len(cams)
         carr = (C.sgs_camera * max(n, 1))(*[c._c() for c in cams])
         cfg = _config(tile_size, thresholds, 0, degree_override, early_stop)
+        with_T = with_T and T is not False
+        if self.rank != root:  # off the root only T's null-ness matters: 1 stands for "T travels"
+            _check(_lib().sgs_group_render_views(self.handle, dscene.handle, carr, n, ctypes.byref(cfg), root,
+                                                 None, 1 if with_T else None,
+                                                 C.SGS_DEVICE if device_out else C.SGS_HOST, None))
+            return None, None
         if device_out:
-            rgb_p, T_p, mem = rgb, T, C.SGS_DEVICE
+            if with_T and not T:
+                raise ValueError("with_T on the root needs a device T buffer")
+            rgb_p, T_p, mem = rgb, T if with_T else None, C.SGS_DEVICE
         else:
             H, W = (cams[0].height, cams[0].width) if n else (0, 0)
             if rgb is None:
@@ -182,7 +192,7 @@ class RenderGroup:
             if T is None:
                 T = np.empty((n, H, W, 1), dtype=np.float32)
             rgb_p = rgb.ctypes.data
-            T_p = T.ctypes.data if T is not False else None
+            T_p = T.ctypes.data if with_T else None
             mem = C.SGS_HOST
         _check(_lib().sgs_group_render_views(self.handle, dscene.handle, carr, n, ctypes.byref(cfg), root,
                                              rgb_p, T_p, mem, None))
