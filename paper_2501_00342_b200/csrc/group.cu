@@ -14,11 +14,13 @@
 // sgs_group_* call is collective: each rank makes it with the same arguments (the
 // scene description only on the root).
 //
-// NCCL is resolved at run time (dlopen "libnccl.so.2": the system 2.27 or the one
-// torch loaded), so the library itself has no link-time NCCL dependency.
+// NCCL is resolved at run time -- the one already in the process (torch's), else
+// SGS_NCCL_PATH, else the system's libnccl.so.2 -- so the library itself has no
+// link-time NCCL dependency and never loads a second NCCL beside torch's.
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -49,9 +51,15 @@ const Nccl& nccl() {
     static Nccl n;
     static std::once_flag once;
     std::call_once(once, [] {
+        // an NCCL the process already loaded (e.g. torch's), else SGS_NCCL_PATH, else the
+        // system's: never a second copy under the same soname
+        n.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!n.lib) {
+            if (const char* path = std::getenv("SGS_NCCL_PATH")) n.lib = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+        }
         for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            n.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
             if (n.lib) break;
+            n.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
         }
         if (!n.lib) {
             n.error = std::string("NCCL not found: ") + dlerror();

@@ -98,6 +98,15 @@ def gather_frames(frames, dst: int = 0, group=None):
     return [r[: k] for r, k in zip(recv, sizes)] if rank == dst else None
 
 
+def _load_nccl_first():
+    """The library binds the NCCL already in the process; when torch is installed,
+    import it first so that is torch's (one NCCL per process)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 class RenderGroup:
     """One rank of an sgs_group (include/sgs.h): every method is collective -- each
     rank calls it, with the same arguments (the scene only on the root)."""
@@ -111,6 +120,7 @@ class RenderGroup:
     def unique_id() -> bytes:
         from . import _check, _lib
 
+        _load_nccl_first()
         buf = (ctypes.c_uint8 * C.GROUP_ID_BYTES)()
         _check(_lib().sgs_group_unique_id(buf))
         return bytes(buf)
@@ -120,6 +130,7 @@ class RenderGroup:
         """Rank `rank` of `nranks`, one process per GPU (ncclCommInitRank)."""
         from . import _check, _lib
 
+        _load_nccl_first()
         h = ctypes.c_void_p()
         idb = (ctypes.c_uint8 * C.GROUP_ID_BYTES).from_buffer_copy(uid)
         _check(_lib().sgs_group_init_rank(renderer.handle, nranks, rank, idb, ctypes.byref(h)))
@@ -130,6 +141,7 @@ class RenderGroup:
         """Every rank in this process (ncclCommInitAll); drive each from its own thread."""
         from . import Renderer, _check, _lib
 
+        _load_nccl_first()
         n = len(devices)
         devs = (ctypes.c_int32 * n)(*devices)
         hs = (ctypes.c_void_p * n)()
