@@ -125,7 +125,6 @@ struct Lane {
     FrameConsts* h_consts = nullptr;  // pinned staging copy
     cudaEvent_t ev[8] = {};
     cudaEvent_t done = nullptr;  // the frame's counters have reached h_ctr
-    cudaEvent_t k1ev = nullptr;  // multi-view K1 hand-off (start_group)
     // the frame in flight (valid while busy)
     struct Job {
         const sgs_scene* scene = nullptr;
@@ -168,7 +167,6 @@ struct sgs_context {
     int lanes = 8;                     // lanes of the one-view-per-K1 schedule (SGS_LANES, 1..kLanes; 8 measured best)
     int host_lanes = 6;                // lanes for host-frame batches (SGS_HOST_LANES; fewer frames in flight
                                        // hand the copy engines their first frames sooner)
-    int k1_group = 1;                  // views per multi-view K1 (SGS_K1_GROUP, 2..4; measured: no gain)
     Counters* h_ctr_init = nullptr;    // pinned initial counters block (err/kmin = ~0)
     bool chunking = true;
     std::vector<uint64_t> chunk_divs;  // depth-chunk boundaries N/div (SGS_DEPTH_CHUNKS; else by N)
@@ -292,9 +290,6 @@ std::vector<uint64_t> default_chunk_divs(uint64_t n) {
 // size lives on the device), ending with a 128-B D2H of the counters and L.done.
 // finish_frame() reads the counters, reports errors and -- rarely -- regrows the
 // tile-key arena or switches to the 64-bit depth sort and enqueues the frame again.
-// part: kAll = the whole frame; kPre = arenas, counters, constants (up to K1);
-// kPost = everything after K1 (a multi-view K1 ran in between, start_group).
-enum EnqueuePart { kAll = 0, kPre = 1, kPost = 2 };
 
 // Everything the captured frame depends on besides the per-frame constants (camera,
 // outputs) and the K1 camera: a frame whose key differs is enqueued directly; the
@@ -405,7 +400,7 @@ sgs_status launch_frame_graph(sgs_context* ctx, Lane& L, const CamParams& cp, Bo
     return SGS_OK;
 }
 
-sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
+sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
     Lane::Job& j = L.job;
     cudaStream_t s = L.stream;
     const sgs_scene* scene = j.scene;
@@ -459,7 +454,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
     }
 
     const bool host_out = mode == kRender && (j.h_rgb || j.h_T);
-    if (part != kPost) {
+    {
         if (mode == kRender) {
             // the pinned staging block is per lane; the lane's previous frame has
             // completed (finish_frame waits for it before the lane is reused)
@@ -469,13 +464,13 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
             L.h_consts->out_T = d_T;
         }
     }
-    if (host_out && part != kPre) {
+    if (host_out) {
         // the slot's previous frame must have left the device before K7 rewrites it
         SGS_CUDA(cudaStreamWaitEvent(s, L.copied[slot], 0));
         L.out_slot = (slot + 1) % Lane::kOutSlots;
     }
     sgs_context::TraceRec* tr = nullptr;
-    if (ctx->trace && mode == kRender && part != kPre) {
+    if (ctx->trace && mode == kRender) {
         ctx->trace_recs.push_back(sgs_context::TraceRec{static_cast<int>(&L - ctx->lane), {}});
         tr = &ctx->trace_recs.back();
         for (auto& e : tr->ev) SGS_CUDA(cudaEventCreate(&e));
@@ -494,14 +489,13 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         // (test hook: a stream synchronize is illegal inside a capture, as the driver
         // refusing it mid-body would be)
         if (capturing && ctx->debug_capture_fail) SGS_CUDA(cudaStreamSynchronize(s));
-        if (part != kPost) {
+        {
             launch_counters_init(L.d_ctr, s);
             if (mode == kRender)
                 SGS_CUDA(cudaMemcpyAsync(L.d_consts, L.h_consts, sizeof(FrameConsts), cudaMemcpyHostToDevice, s));
         }
-        if (part == kPre) return SGS_OK;
         // K1
-        if (part == kAll) {
+        {
             if (timing) SGS_CUDA(cudaEventRecord(L.ev[0], s));  // brackets K1 alone
             launch_preprocess(scene->planes, cp, kp, L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(),
                               L.rects.as<int4>(), L.colour.as<float4>(), L.d_ctr, j.d_debug,
@@ -629,7 +623,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L, int part = kAll) {
         }
         return SGS_OK;
     };
-    const bool graph = ctx->graphs && mode == kRender && part == kAll && !timing && !tr && !j.d_debug;
+    const bool graph = ctx->graphs && mode == kRender && !timing && !tr && !j.d_debug;
     if (!graph) {
         sgs_status st = body();
         if (st != SGS_OK) return st;
@@ -735,71 +729,6 @@ sgs_status start_frame(sgs_context* ctx, Lane& L, const sgs_scene* scene, const 
     if (st != SGS_OK) {
         cudaStreamSynchronize(L.stream);
         L.busy = false;
-    }
-    return st;
-}
-
-// Start views [0, g) of `cams` on lanes[0..g) (all idle) with ONE multi-view K1
-// (SURVEY.md §8f row 1): every lane stages its arenas and counters, the lead lane
-// waits for them, projects all g views reading each Gaussian once, and the other
-// lanes continue from K2 after it. A lane that needs a retry later re-runs its own
-// frame alone (finish_frame -> enqueue_frame).
-sgs_status start_group(sgs_context* ctx, Lane* const* lanes, int g, const sgs_scene* scene, const sgs_camera* cams,
-                       const sgs_render_config* cfg, float* const* d_rgb, float* const* d_T, float* const* h_rgb,
-                       float* const* h_T, sgs_render_stats* stats) {
-    if (cfg->tile_size < 1) return fail(SGS_ERR_INVALID_ARGUMENT, "tile_size must be >= 1");
-    for (int k = 0; k < g; ++k) {
-        sgs_status st = validate_camera(&cams[k]);
-        if (st != SGS_OK) return st;
-    }
-    sgs_status st = SGS_OK;
-    int started = 0;
-    for (int k = 0; k < g && st == SGS_OK; ++k) {
-        Lane& L = *lanes[k];
-        Lane::Job& j = L.job;
-        j = Lane::Job{};
-        j.scene = scene;
-        j.cam = cams[k];
-        j.cfg = *cfg;
-        j.d_rgb = d_rgb[k];
-        j.d_T = d_T[k];
-        j.h_rgb = h_rgb[k];
-        j.h_T = h_T[k];
-        j.stats = stats;
-        j.mode = kRender;
-        L.busy = true;
-        ++started;
-        st = enqueue_frame(ctx, L, kPre);
-    }
-    Lane& lead = *lanes[0];
-    if (st == SGS_OK) {
-        for (int k = 1; k < g && st == SGS_OK; ++k) {
-            cudaError_t e = cudaEventRecord(lanes[k]->k1ev, lanes[k]->stream);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(lead.stream, lanes[k]->k1ev, 0);
-            if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
-        }
-    }
-    if (st == SGS_OK) {
-        K1Views views{};
-        views.nv = g;
-        for (int k = 0; k < g; ++k) {
-            Lane& L = *lanes[k];
-            views.v[k] = K1Out{L.keys_a.as<unsigned long long>(), L.rec.as<SplatRec>(), L.rects.as<int4>(),
-                               L.colour.as<float4>(), L.d_ctr, make_cam(&cams[k])};
-        }
-        launch_preprocess_views(scene->planes, make_cfg(cfg, &cams[0]), views, nullptr, lead.stream);
-        cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess && scene->meta.count) ctx->own_launches += 1;
-        if (e == cudaSuccess) e = cudaEventRecord(lead.k1ev, lead.stream);
-        for (int k = 1; k < g && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(lanes[k]->stream, lead.k1ev, 0);
-        if (e != cudaSuccess) st = fail(SGS_ERR_CUDA, cudaGetErrorString(e));
-    }
-    for (int k = 0; k < g && st == SGS_OK; ++k) st = enqueue_frame(ctx, *lanes[k], kPost);
-    if (st != SGS_OK) {
-        for (int k = 0; k < started; ++k) {
-            cudaStreamSynchronize(lanes[k]->stream);
-            lanes[k]->busy = false;
-        }
     }
     return st;
 }
@@ -1174,7 +1103,6 @@ sgs_status sgs_create(int device, sgs_context** out) {
         SGS_CUDA(cudaMallocHost(&L.h_consts, sizeof(FrameConsts)));
         for (auto& ev : L.ev) SGS_CUDA(cudaEventCreate(&ev));
         SGS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
-        SGS_CUDA(cudaEventCreateWithFlags(&L.k1ev, cudaEventDisableTiming));
         SGS_CUDA(cudaStreamCreateWithFlags(&L.copy_stream, cudaStreamNonBlocking));
         for (int k = 0; k < Lane::kOutSlots; ++k) {
             SGS_CUDA(cudaEventCreateWithFlags(&L.rendered[k], cudaEventDisableTiming));
@@ -1188,8 +1116,6 @@ sgs_status sgs_create(int device, sgs_context** out) {
     if (const char* e = std::getenv("SGS_DEBUG_CAPTURE_FAIL")) ctx->debug_capture_fail = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_LANES")) ctx->lanes = std::min(std::max(std::atoi(e), 1), kLanes);
     if (const char* e = std::getenv("SGS_HOST_LANES")) ctx->host_lanes = std::min(std::max(std::atoi(e), 1), kLanes);
-    if (const char* e = std::getenv("SGS_K1_GROUP"))
-        ctx->k1_group = std::min(std::max(std::atoi(e), 1), std::min(kMaxK1Views, kLanes / 2));
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKING")) ctx->chunking = std::atoi(e) != 0;
     if (const char* e = std::getenv("SGS_DEPTH_CHUNKS")) {  // e.g. "16,4": boundaries at N/16, N/4
         ctx->chunk_divs.clear();
@@ -1223,7 +1149,6 @@ void sgs_destroy(sgs_context* ctx) {
         for (auto& ev : L.ev)
             if (ev) cudaEventDestroy(ev);
         if (L.done) cudaEventDestroy(L.done);
-        if (L.k1ev) cudaEventDestroy(L.k1ev);
         if (L.copy_stream) {
             cudaStreamSynchronize(L.copy_stream);
             cudaStreamDestroy(L.copy_stream);
@@ -1432,52 +1357,24 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
     };
     sgs_status st = select_lane_streams(ctx, host && n > 1);
     if (st != SGS_OK) return st;
-    int lanes = 0;
-    const int group = timing ? 1 : ctx->k1_group;
-    if (group > 1 && n > 1) {
-        // groups of `group` views share one multi-view K1; two lane sets alternate so
-        // one group's K1 overlaps the previous group's sorts and compositing
-        constexpr int kSets = 2;
-        lanes = kSets * group;
-        st = fork_lanes(ctx, lanes);
-        if (st != SGS_OK) return st;
-        int gi = 0;
-        for (int i = 0; i < n && st == SGS_OK; i += group, ++gi) {
-            const int g = std::min(group, n - i);
-            Lane* ls[kMaxK1Views];
-            float *drgb[kMaxK1Views], *dT[kMaxK1Views], *hrgb[kMaxK1Views], *hT[kMaxK1Views];
-            for (int k = 0; k < g && st == SGS_OK; ++k) {
-                ls[k] = &ctx->lane[(gi % kSets) * group + k];
-                st = finish_frame(ctx, *ls[k]);
-                outs(i + k, &drgb[k], &dT[k], &hrgb[k], &hT[k]);
-            }
-            if (st == SGS_OK) st = start_group(ctx, ls, g, scene, &cams[i], cfg, drgb, dT, hrgb, hT, stats);
-        }
-        for (int s2 = 0; s2 < kSets; ++s2)  // settle the views still in flight, in order
-            for (int k = 0; k < group; ++k) {
-                sgs_status sk = finish_frame(ctx, ctx->lane[((gi + s2) % kSets) * group + k]);
-                if (st == SGS_OK) st = sk;
-            }
-    } else {
-        // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
-        lanes = std::min<int>(timing ? 1 : (host ? ctx->host_lanes : ctx->lanes), n);
-        st = fork_lanes(ctx, lanes);
-        if (st != SGS_OK) return st;
-        // view i runs on lane i % lanes; a lane's previous view is settled (checked,
-        // retried if needed) before the lane is reused, so views complete in order
-        for (int i = 0; i < n && st == SGS_OK; ++i) {
-            Lane& L = ctx->lane[i % lanes];
-            st = finish_frame(ctx, L);
-            if (st != SGS_OK) break;
-            float *drgb, *dT, *hrgb, *hT;
-            outs(i, &drgb, &dT, &hrgb, &hT);
-            st = start_frame(ctx, L, scene, &cams[i], cfg, drgb, dT, hrgb, hT, stats, nullptr, kRender);
-        }
-        for (int k = 0; k < lanes; ++k) {  // settle the views still in flight, in order
-            Lane& L = ctx->lane[(n + k) % lanes];
-            sgs_status sk = finish_frame(ctx, L);
-            if (st == SGS_OK) st = sk;
-        }
+    // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
+    const int lanes = std::min<int>(timing ? 1 : (host ? ctx->host_lanes : ctx->lanes), n);
+    st = fork_lanes(ctx, lanes);
+    if (st != SGS_OK) return st;
+    // view i runs on lane i % lanes; a lane's previous view is settled (checked,
+    // retried if needed) before the lane is reused, so views complete in order
+    for (int i = 0; i < n && st == SGS_OK; ++i) {
+        Lane& L = ctx->lane[i % lanes];
+        st = finish_frame(ctx, L);
+        if (st != SGS_OK) break;
+        float *drgb, *dT, *hrgb, *hT;
+        outs(i, &drgb, &dT, &hrgb, &hT);
+        st = start_frame(ctx, L, scene, &cams[i], cfg, drgb, dT, hrgb, hT, stats, nullptr, kRender);
+    }
+    for (int k = 0; k < lanes; ++k) {  // settle the views still in flight, in order
+        Lane& L = ctx->lane[(n + k) % lanes];
+        sgs_status sk = finish_frame(ctx, L);
+        if (st == SGS_OK) st = sk;
     }
     sgs_status sj = join_lanes(ctx, lanes);
     // host frames are complete (or abandoned, on an error) once the copies drained

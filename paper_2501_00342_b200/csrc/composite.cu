@@ -175,7 +175,7 @@ __device__ __forceinline__ void mahal2x2(const float4& A, float Bx, float fcx0, 
     }
 }
 
-template <int kGroup, int MINB, bool kSameRow>
+template <int kGroup, int MINB, bool kSameRow, int kBatch>
 __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
@@ -189,7 +189,6 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
     // Slot kBatch of each buffer is a null record (never contributes) that pads the
     // compacted lists to whole groups.
-    constexpr int kBatch = 256;
     constexpr int kPer = kBatch / kThreads2;
     constexpr int kWarps = kThreads2 / 32;
     extern __shared__ float4 k7_smem[];
@@ -530,12 +529,27 @@ int composite_pixel_chunks(int ts) {
 }
 
 namespace {
-template <int G, bool ROW>
-cudaError_t k7_attr(size_t smem) {
-    static const cudaError_t e = cudaFuncSetAttribute(composite2_kernel<G, 4, ROW>,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      static_cast<int>(smem));
-    return e;
+constexpr size_t k7_smem_bytes(int batch) {
+    return static_cast<size_t>(2 * (batch + 1) * 4 + batch) * sizeof(float4) +
+           static_cast<size_t>(kThreads2 / 32) * (batch + 8) * sizeof(uint16_t);
+}
+
+template <int G, int M, bool ROW, int B>
+cudaError_t launch_k7(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg, int nchunks,
+                      const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
+                      const float4* colour, float3 bg, PixelState* state, uint32_t* processed, uint32_t* tile_done,
+                      uint32_t* tile_touched, bool first, bool last, Counters* counters, bool want_stats,
+                      uint32_t* work, uint32_t* wctl, uint32_t cap, cudaStream_t stream) {
+    constexpr size_t smem = k7_smem_bytes(B);
+    static const cudaError_t attr = cudaFuncSetAttribute(composite2_kernel<G, M, ROW, B>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         static_cast<int>(smem));
+    if (attr != cudaSuccess) return attr;
+    // persistent grid: M resident CTAs of 128 threads per SM
+    composite2_kernel<G, M, ROW, B><<<148u * M, kThreads2, smem, stream>>>(
+        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed, tile_done,
+        tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 6, cap);
+    return cudaGetLastError();
 }
 }  // namespace
 
@@ -551,31 +565,28 @@ cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const 
     if (e != cudaSuccess) return e;
     build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
                                                              last ? 1 : 0, ntile, nchunks, cap, work, wctl);
-    static const int group = [] {
-        const char* e = std::getenv("SGS_K7_GROUP");
-        return e && std::atoi(e) == 2 ? 2 : 4;
+    static const int variant = [] {
+        const char* v = std::getenv("SGS_K7_VARIANT");
+        return v ? std::atoi(v) : 0;
     }();
-    // persistent grid: 4 resident CTAs of 128 threads per SM
-    const unsigned grid = 148u * 4u;
-    constexpr int kB = 256;
-    const size_t smem = static_cast<size_t>(2 * (kB + 1) * 4 + kB) * sizeof(float4) +
-                        static_cast<size_t>(kThreads2 / 32) * (kB + 8) * sizeof(uint16_t);
-#define SGS_K7X2(G, ROW)                                                                                     \
-    do {                                                                                                     \
-        if ((e = k7_attr<G, ROW>(smem)) != cudaSuccess) return e;                                            \
-        composite2_kernel<G, 4, ROW><<<grid, kThreads2, smem, stream>>>(                                     \
-            fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,        \
-            tile_done, tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl,  \
-            wctl + 6, cap);                                                                                  \
-    } while (0)
-    const bool row = cfg.tile_size == 16;
-    if (group == 2) {
-        if (row) SGS_K7X2(2, true); else SGS_K7X2(2, false);
-    } else {
-        if (row) SGS_K7X2(4, true); else SGS_K7X2(4, false);
+#define SGS_K7(G, M, B)                                                                                        \
+    (cfg.tile_size == 16                                                                                      \
+         ? launch_k7<G, M, true, B>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,      \
+                                    processed, tile_done, tile_touched, first, last, counters, want_stats,     \
+                                    work, wctl, cap, stream)                                                  \
+         : launch_k7<G, M, false, B>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,     \
+                                     processed, tile_done, tile_touched, first, last, counters, want_stats,    \
+                                     work, wctl, cap, stream))
+    switch (variant) {
+        case 1: return SGS_K7(4, 5, 128);
+        case 2: return SGS_K7(4, 6, 128);
+        case 3: return SGS_K7(2, 6, 128);
+        case 4: return SGS_K7(2, 8, 128);
+        case 5: return SGS_K7(2, 4, 256);
+        case 6: return SGS_K7(4, 5, 256);
+        default: return SGS_K7(4, 4, 256);
     }
-#undef SGS_K7X2
-    return cudaGetLastError();
+#undef SGS_K7
 }
 
 }  // namespace sgs

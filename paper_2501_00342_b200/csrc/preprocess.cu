@@ -581,12 +581,6 @@ void launch_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& vi
         launch_k1<F64, KIND, 1, true, 1>(sp, cfg, views, debug, stream);
         return;
     }
-    switch (views.nv) {
-        case 2: launch_k1<F64, KIND, kDefaultMinB, false, 2>(sp, cfg, views, nullptr, stream); return;
-        case 3: launch_k1<F64, KIND, kDefaultMinB, false, 3>(sp, cfg, views, nullptr, stream); return;
-        case 4: launch_k1<F64, KIND, kDefaultMinB, false, 4>(sp, cfg, views, nullptr, stream); return;
-        default: break;
-    }
     switch (k1_minb()) {
         case 1: launch_k1<F64, KIND, 1, false, 1>(sp, cfg, views, nullptr, stream); break;
         case 3: launch_k1<F64, KIND, 3, false, 1>(sp, cfg, views, nullptr, stream); break;

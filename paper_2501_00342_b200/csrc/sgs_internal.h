@@ -156,9 +156,12 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
                        float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream);
-// K1 over up to kMaxK1Views cameras of one batch: every Gaussian is read once and
-// projected into each view's arenas.
-constexpr int kMaxK1Views = 4;
+// K1's outputs for one view. (A multi-view K1 -- every Gaussian read once, projected
+// into up to 4 views' arenas, SURVEY.md §8f row 1 -- was built and measured: 152 us
+// per view at NV=1, 154 at NV=2, 167 at NV=4, batch throughput 0.719 vs 0.724 ms per
+// frame, because with the covariance cached K1 is bound by its per-view FP64 work and
+// writes, not by the shared scene read. It is not kept.)
+constexpr int kMaxK1Views = 1;
 struct K1Out {
     unsigned long long* keys;
     SplatRec* rec;

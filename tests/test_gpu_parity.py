@@ -246,12 +246,11 @@ def test_depth_chunking_is_bitwise_neutral():
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"SGS_DEPTH_CHUNKING": "0"}, {"SGS_DEPTH_CHUNKS": "8"}, {"SGS_K7_GROUP": "2"},
                                  {"SGS_LANES": "1"}, {"SGS_GRAPHS": "0"}, {"SGS_TIGHT_RECT": "0"},
-                                 {"SGS_K1_GROUP": "1"}, {"SGS_K1_GROUP": "2"}, {"SGS_K1_GROUP": "3"},
-                                 {"SGS_K1_MINB": "1"}])
+                                 {"SGS_K1_MINB": "1"}, {"SGS_K7_VARIANT": "2"}])
 def test_pipeline_variants_are_bitwise_equal(env):
     """Every alternative pipeline path (no depth chunks or other chunk bounds, a single
     lane, direct frames, the reference's 3-sigma tile rectangles, other K1 / K7
-    instantiations and multi-view K1 groups) renders the same bits, image,
+    instantiations) renders the same bits, image,
     transmittance and E_t, as the default path, over a batch of views."""
     scene = sg.synth_scene(150_000, "mixed", 91, log_scale_range=(-5.0, -3.5))
     cams = sg.orbit_cameras(5, 480, 270, 4.0, 324.0)
