@@ -216,6 +216,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-frames", type=int, default=3, help="CPU-baseline sample frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in render timing")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL frame gather")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo: host-path check only)")
@@ -422,6 +423,25 @@ def main():
         torch.cuda.synchronize()
         gather_ms = max_over_ranks(g0.elapsed_time(g1))
 
+    # ---------------- the drop-in C++ call (rank 0, N=1 only) ----------------
+    # sgsplat::render(scene, camera, cfg) -- the reference's own C++ API (raster.hpp:56)
+    # served by libsgsplat_b200.so -- under the reference's bench protocol (3 warm-ups,
+    # median of K; tools/main.cpp:232-243): the caller's AoS scene packed and uploaded,
+    # the frame rendered and returned as the double Image, every call
+    e2e_dropin = None
+    if rank == 0 and world == 1 and not args.no_dropin:
+        exe = os.path.join(ROOT, "build", "dropin_bench")
+        try:
+            o = subprocess.run([exe, str(N_GAUSS), "5"], capture_output=True, text=True, timeout=600)
+            d = json.loads(o.stdout.strip().splitlines()[-1])
+            e2e_dropin = {"value": d["fps"], "unit": "frames/s", "median_ms": d["median_ms"],
+                          "h2d_bytes_per_step": N_GAUSS * 35 * 4, "d2h_bytes_per_step": W * H * 16,
+                          "protocol": "sgsplat::render(const Scene&, const Camera&, const RenderConfig&) via "
+                                      "libsgsplat_b200.so, 3 warm-ups then the median of 5 (main.cpp:232-243); "
+                                      "one view, host Scene in, double Image (RGB + T) out"}
+        except Exception as exc:
+            e2e_dropin = {"value": None, "error": str(exc)[:200]}
+
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -470,6 +490,7 @@ def main():
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
+            "e2e_dropin": e2e_dropin,
             "e2e_rgb_only": {"value": e2e_rgb_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                              "d2h_bytes_per_step": vpr * H * W * 12,
                              "note": "image only, the reference Python render's default output"},

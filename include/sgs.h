@@ -146,6 +146,11 @@ sgs_status sgs_synchronize(sgs_context* ctx);
  * for launch accounting. */
 sgs_status sgs_launch_count(sgs_context* ctx, uint64_t* own_kernels, uint64_t* library_kernels);
 
+/* Page-locked host memory (cudaHostAlloc) for callers that stage scenes or frames
+ * through host buffers: transfers from / to it run at DMA speed. */
+sgs_status sgs_host_alloc(uint64_t bytes, void** out);
+void sgs_host_free(void* p);
+
 /* --- scenes ------------------------------------------------------------------- */
 /* Validates the desc (homogeneous by construction; scene.cpp:7-25 rules on degree)
  * and fills the device layout it will use. */

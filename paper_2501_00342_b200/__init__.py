@@ -190,13 +190,15 @@ class Scene:
     def total_params(self) -> int:
         return self.num_gaussians * (0 if self.num_gaussians == 0 else 11 + self.param_count_per_gaussian())
 
-    def _desc(self):
-        params = np.ascontiguousarray(self.params, dtype=np.float64)
+    def _desc(self, f32: bool = False):
+        """The C-ABI description; f32: the parameters as float32 rows (the upload then
+        scatters them into the planes on the device)."""
+        params = np.ascontiguousarray(self.params, dtype=np.float32 if f32 else np.float64)
         d = C.sgs_scene_desc()
         d.count = params.shape[0]
         d.kind = KINDS[self.kind]
         d.sh_degree = self.sh_degree
-        d.dtype = C.SGS_F64
+        d.dtype = C.SGS_F32 if f32 else C.SGS_F64
         d.params = params.ctypes.data if params.size else None
         axes = np.asarray(self.shared_axes, dtype=np.float64).reshape(9)
         bg = np.asarray(self.background, dtype=np.float64).reshape(3)
@@ -372,8 +374,11 @@ class Renderer:
         return a.value, b.value
 
     # -- scenes ---------------------------------------------------------------
-    def upload(self, scene: Scene) -> DeviceScene:
-        d, keep = scene._desc()
+    def upload(self, scene: Scene, f32: bool = False) -> DeviceScene:
+        """scene into HBM. f32: ship float32 rows that a kernel scatters into the planes
+        (for f32-exact parameters -- synthetic scenes and PLY checkpoints are -- the
+        same blob as the default float64 path)."""
+        d, keep = scene._desc(f32)
         h = ctypes.c_void_p()
         _check(self._lib.sgs_scene_upload(self.handle, ctypes.byref(d), ctypes.byref(h)))
         return DeviceScene(self, h.value)

@@ -180,6 +180,8 @@ SIGNATURES = {
                       ctypes.c_int32, ctypes.POINTER(ctypes.c_double), _P]),
     "sgs_ply_read": (_S, [ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), _P, ctypes.c_uint64]),
     "sgs_scene_load_ply": (_S, [_P, ctypes.c_char_p, ctypes.POINTER(sgs_ply_info), ctypes.POINTER(_P)]),
+    "sgs_host_alloc": (_S, [ctypes.c_uint64, ctypes.POINTER(_P)]),
+    "sgs_host_free": (None, [_P]),
     "sgs_group_unique_id": (_S, [_P]),
     "sgs_group_init_rank": (_S, [_P, ctypes.c_int32, ctypes.c_int32, _P, ctypes.POINTER(_P)]),
     "sgs_group_create": (_S, [ctypes.c_int32, _P, _P]),

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ply_internal.h"
@@ -71,6 +72,24 @@ struct DevBuf {
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Host loops over Gaussians (scene checks and packing) on every core: fn(begin, end).
+template <typename Fn>
+void parallel_for(size_t n, Fn&& fn) {
+    const size_t hw = std::max<unsigned>(std::thread::hardware_concurrency(), 1u);
+    const size_t nt = std::min<size_t>(hw, n / 65536 + 1);
+    if (nt <= 1) {
+        fn(size_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t per = (n + nt - 1) / nt;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t b = t * per, e = std::min(n, b + per);
+        if (b < e) pool.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& th : pool) th.join();
+}
 
 int color_param_count_impl(int kind, int degree) {
     switch (kind) {
@@ -861,8 +880,9 @@ void fill_blob(const sgs_scene_desc* d, const sgs_scene_meta& m, std::vector<cha
     const int cpc = color_param_count_impl(m.kind, m.sh_degree);
     const size_t stride = 11 + static_cast<size_t>(cpc);
     char* base = host.data();
+    parallel_for(n, [&](size_t i0, size_t i1) {
     std::vector<float> c(static_cast<size_t>(L.color_planes) * 4);
-    for (size_t i = 0; i < n; ++i) {
+    for (size_t i = i0; i < i1; ++i) {
         const size_t o = i * stride;
         if (m.geometry_f64) {
             for (int k = 0; k < 11; ++k) reinterpret_cast<double*>(base + L.geo_off[k])[i] = param_at(d, o + k);
@@ -915,7 +935,10 @@ void fill_blob(const sgs_scene_desc* d, const sgs_scene_meta& m, std::vector<cha
             for (int k = 0; k < cpc; ++k) c64[static_cast<size_t>(k) * n + i] = param_at(d, co + k);
         }
     }
+    });
 }
+
+cudaError_t upload_rows_f32(sgs_context* ctx, const sgs_scene_desc* desc, const sgs_scene_meta& m, void* blob);
 
 sgs_status upload_common(sgs_context* ctx, const sgs_scene_desc* desc, void* blob, uint64_t bytes,
                          bool own, sgs_scene** out) {
@@ -942,9 +965,16 @@ sgs_status upload_common(sgs_context* ctx, const sgs_scene_desc* desc, void* blo
         }
         sc->blob = blob;
     }
-    std::vector<char> host;
-    fill_blob(desc, m, host);
-    cudaError_t e = cudaMemcpy(sc->blob, host.data(), host.size(), cudaMemcpyHostToDevice);
+    cudaError_t e = cudaSuccess;
+    if (desc->dtype == SGS_F32 && m.count) {
+        // float32 rows go to the device as they are and a kernel scatters them into the
+        // planes (the PLY loader's path with an identity column map)
+        e = upload_rows_f32(ctx, desc, m, sc->blob);
+    } else {
+        std::vector<char> host;
+        fill_blob(desc, m, host);
+        e = cudaMemcpy(sc->blob, host.data(), host.size(), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         delete sc;
         return fail(SGS_ERR_CUDA, std::string("scene upload: ") + cudaGetErrorString(e));
@@ -1041,6 +1071,44 @@ std::vector<int32_t> ply_slot_table(const PlyTable& t, int color_planes, int* mu
             break;
     }
     return tab;
+}
+
+// An SGS_F32 description's rows (count x (11 + colour params) floats, Scene::param
+// order) into the planes of blob: one copy of the rows, then ply_rows_kernel with the
+// identity column map (SG1 lobe axes normalised in FP64 as at every upload).
+cudaError_t upload_rows_f32(sgs_context* ctx, const sgs_scene_desc* desc, const sgs_scene_meta& m, void* blob) {
+    PlyTable t;
+    t.count = m.count;
+    t.info.kind = m.kind;
+    t.info.sh_degree = m.sh_degree;
+    const int stride = 11 + color_param_count_impl(m.kind, m.sh_degree);
+    t.src.resize(static_cast<size_t>(stride));
+    for (int k = 0; k < stride; ++k) t.src[static_cast<size_t>(k)] = k;
+    const Layout L = make_layout(m);
+    int mu_col = -1;
+    const std::vector<int32_t> tab = ply_slot_table(t, L.color_planes, &mu_col);
+    const size_t nfloat = static_cast<size_t>(m.count) * static_cast<size_t>(stride);
+    DevBuf d_rows, d_tab;
+    cudaStream_t s = ctx->stream;
+    cudaError_t e = d_rows.ensure(nfloat * sizeof(float));
+    if (e == cudaSuccess) e = d_tab.ensure(tab.size() * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(blob, 0, m.blob_bytes, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_rows.ptr, desc->params, nfloat * sizeof(float), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        char* base = static_cast<char*>(blob);
+        ply_rows_kernel<<<static_cast<unsigned>((m.count + 255) / 256), 256, 0, s>>>(
+            m.count, d_rows.as<float>(), stride, static_cast<int>(tab.size()), d_tab.as<int32_t>(), mu_col,
+            reinterpret_cast<float4*>(base + L.geo_off[0]), reinterpret_cast<float4*>(base + L.geo_off[1]),
+            reinterpret_cast<float4*>(base + L.geo_off[2]), reinterpret_cast<float4*>(base + L.color_off));
+        e = cudaGetLastError();
+        if (e == cudaSuccess) ctx->own_launches += 1;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    d_rows.release();
+    d_tab.release();
+    return e;
 }
 
 }  // namespace
@@ -1201,6 +1269,17 @@ sgs_status sgs_launch_count(sgs_context* ctx, uint64_t* own_kernels, uint64_t* l
 
 int32_t sgs_color_param_count(int32_t kind, int32_t sh_degree) { return color_param_count_impl(kind, sh_degree); }
 
+sgs_status sgs_host_alloc(uint64_t bytes, void** out) {
+    if (!out) return fail(SGS_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    SGS_CUDA(cudaHostAlloc(out, std::max<uint64_t>(bytes, 1), cudaHostAllocDefault));
+    return SGS_OK;
+}
+
+void sgs_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 sgs_status sgs_scene_plan(const sgs_scene_desc* d, sgs_scene_meta* m) {
     if (!d || !m) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
     if (d->kind < SGS_SH || d->kind > SGS_MIXED) return fail(SGS_ERR_INVALID_ARGUMENT, "unknown color model kind");
@@ -1221,14 +1300,18 @@ sgs_status sgs_scene_plan(const sgs_scene_desc* d, sgs_scene_meta* m) {
     if (d->dtype == SGS_F64) {
         const size_t stride = 11 + static_cast<size_t>(color_param_count_impl(d->kind, deg));
         const double* p = static_cast<const double*>(d->params);
-        for (size_t i = 0; i < d->count && !f64; ++i)
-            for (int k = 0; k < 11; ++k) {
-                const double v = p[i * stride + k];
-                if (static_cast<double>(static_cast<float>(v)) != v) {
-                    f64 = 1;
-                    break;
+        std::atomic<int> any{0};
+        parallel_for(d->count, [&](size_t i0, size_t i1) {
+            for (size_t i = i0; i < i1 && !any.load(std::memory_order_relaxed); ++i)
+                for (int k = 0; k < 11; ++k) {
+                    const double v = p[i * stride + k];
+                    if (static_cast<double>(static_cast<float>(v)) != v) {
+                        any.store(1, std::memory_order_relaxed);
+                        break;
+                    }
                 }
-            }
+        });
+        f64 = any.load();
     }
     m->geometry_f64 = f64;
     // colour: the float planes feed the FP32 compositor; FP64 copies are added when
@@ -1238,14 +1321,18 @@ sgs_status sgs_scene_plan(const sgs_scene_desc* d, sgs_scene_meta* m) {
         const int cpc = color_param_count_impl(d->kind, deg);
         const size_t stride = 11 + static_cast<size_t>(cpc);
         const double* p = static_cast<const double*>(d->params);
-        for (size_t i = 0; i < d->count && !cf64; ++i)
-            for (int k = 0; k < cpc; ++k) {
-                const double v = p[i * stride + 11 + k];
-                if (static_cast<double>(static_cast<float>(v)) != v) {
-                    cf64 = 1;
-                    break;
+        std::atomic<int> any{0};
+        parallel_for(d->count, [&](size_t i0, size_t i1) {
+            for (size_t i = i0; i < i1 && !any.load(std::memory_order_relaxed); ++i)
+                for (int k = 0; k < cpc; ++k) {
+                    const double v = p[i * stride + 11 + k];
+                    if (static_cast<double>(static_cast<float>(v)) != v) {
+                        any.store(1, std::memory_order_relaxed);
+                        break;
+                    }
                 }
-            }
+        });
+        cf64 = any.load();
     }
     m->color_f64 = cf64;
     for (int k = 0; k < 9; ++k) m->shared_axes[k] = d->shared_axes[k];

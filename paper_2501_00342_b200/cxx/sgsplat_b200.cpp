@@ -15,10 +15,14 @@
 #include "sgsplat/raster.hpp"
 #include "sgsplat/synth.hpp"
 
+#include <algorithm>
+#include <atomic>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <sstream>
+#include <thread>
 
 namespace sgsplat {
 
@@ -115,6 +119,109 @@ struct DeviceScene {
     ~DeviceScene() { sgs_scene_free(s); }
 };
 
+// ---- the render() fast path -------------------------------------------------
+// Host loops over Gaussians / pixels on every core: fn(begin, end).
+template <typename Fn>
+void parallel_for(std::size_t n, Fn&& fn) {
+    const std::size_t hw = std::max<unsigned>(std::thread::hardware_concurrency(), 1u);
+    const std::size_t nt = std::min<std::size_t>(hw, n / 32768 + 1);
+    if (nt <= 1) {
+        fn(std::size_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const std::size_t per = (n + nt - 1) / nt;
+    for (std::size_t t = 0; t < nt; ++t) {
+        const std::size_t b = t * per, e = std::min(n, b + per);
+        if (b < e) pool.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+// Pinned host staging reused by every render() call (grow-only): scene rows up, frames
+// down, both at DMA speed.
+struct PinnedBuf {
+    void* p = nullptr;
+    std::size_t bytes = 0;
+    void* get(std::size_t need) {
+        if (need > bytes) {
+            sgs_host_free(p);
+            p = nullptr;
+            bytes = 0;
+            if (sgs_host_alloc(need, &p) != SGS_OK) throw std::bad_alloc();
+            bytes = need;
+        }
+        return p;
+    }
+};
+std::mutex g_stage_mu;  // render() calls share the staging (the reference is reentrant:
+PinnedBuf g_rows, g_frame;  // concurrent calls serialise here, results stay per call)
+
+// The colour parameters of one Gaussian in canonical order (one variant visit).
+template <typename T>
+void pack_color(const ColorModel& model, T* out) {
+    std::visit(
+        [&](const auto& m) {
+            using M = std::decay_t<decltype(m)>;
+            int k = 0;
+            if constexpr (std::is_same_v<M, SHOnlyModel>) {
+                for (const Vec3& c : m.sh.coeffs)
+                    for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(c[j]);
+            } else if constexpr (std::is_same_v<M, DiffuseSGModel>) {
+                for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(m.diffuse[j]);
+                for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(m.alpha[j]);
+                out[k++] = static_cast<T>(m.log_lambda);
+                for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(m.mu[j]);
+            } else if constexpr (std::is_same_v<M, DiffuseOrthoSGModel>) {
+                for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(m.diffuse[j]);
+                for (int l = 0; l < 3; ++l) {
+                    for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(m.alpha[static_cast<std::size_t>(l)][j]);
+                    out[k++] = static_cast<T>(m.log_lambda[static_cast<std::size_t>(l)]);
+                }
+            } else {
+                for (const Vec3& c : m.sh.coeffs)
+                    for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(c[j]);
+                for (int l = 0; l < 3; ++l) {
+                    for (int j = 0; j < 3; ++j) out[k++] = static_cast<T>(m.alpha[static_cast<std::size_t>(l)][j]);
+                    out[k++] = static_cast<T>(m.log_lambda[static_cast<std::size_t>(l)]);
+                }
+            }
+        },
+        model);
+}
+
+bool f32_exact(double v) { return static_cast<double>(static_cast<float>(v)) == v; }
+
+// The scene as float32 rows in pinned memory, packed on every core; false when some
+// parameter is not f32-exact (the caller then takes the float64 path).
+bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride, float* rows) {
+    std::atomic<bool> exact{true};
+    parallel_for(gs.size(), [&](std::size_t b, std::size_t e) {
+        std::vector<double> c(stride - kGeometryParams);
+        bool ok = true;
+        for (std::size_t i = b; i < e && ok; ++i) {
+            const GaussianPrimitive& g = gs[i];
+            double p[kGeometryParams];
+            for (int k = 0; k < 3; ++k) p[k] = g.position[k];
+            for (int k = 0; k < 4; ++k) p[3 + k] = g.rotation[k];
+            for (int k = 0; k < 3; ++k) p[7 + k] = g.log_scale[k];
+            p[10] = g.opacity_logit;
+            pack_color(g.color, c.data());
+            float* r = rows + i * stride;
+            for (int k = 0; k < kGeometryParams; ++k) {
+                ok = ok && f32_exact(p[k]);
+                r[k] = static_cast<float>(p[k]);
+            }
+            for (std::size_t k = 0; k < c.size(); ++k) {
+                ok = ok && f32_exact(c[k]);
+                r[kGeometryParams + k] = static_cast<float>(c[k]);
+            }
+        }
+        if (!ok) exact.store(false);
+    });
+    return exact.load();
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------- raster
@@ -153,7 +260,43 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
     if (cfg.tile_size < 1) throw InvalidArgument("tile_size must be >= 1");
     scene.check_homogeneous();
     cam.validate();
-    DeviceScene ds(scene.gaussians, scene.shared_axes, scene.background);
+    std::unique_lock<std::mutex> stage(g_stage_mu);
+    // the scene: float32 rows packed on every core into pinned memory, scattered into
+    // the device planes by a kernel (sgs_scene_upload of an SGS_F32 description) --
+    // exactly the planes of the float64 path whenever every value is f32-exact
+    // (synthetic scenes and PLY checkpoints are); otherwise the float64 path
+    std::unique_ptr<DeviceScene> slow;
+    sgs_scene* dscene = nullptr;
+    const std::vector<GaussianPrimitive>& gs = scene.gaussians;
+    const std::size_t stride = gs.empty() ? 0 : kGeometryParams + param_count(gs.front().color);
+    bool fast = !gs.empty();
+    if (fast) {
+        float* rows = static_cast<float*>(g_rows.get(gs.size() * stride * sizeof(float)));
+        fast = pack_rows_f32(gs, stride, rows);
+        if (fast) {
+            sgs_scene_desc d{};
+            d.count = gs.size();
+            d.kind = static_cast<int32_t>(kind_of(gs.front().color));
+            d.sh_degree = stored_degree(gs.front().color);
+            d.dtype = SGS_F32;
+            d.params = rows;
+            for (int r = 0; r < 3; ++r)
+                for (int c2 = 0; c2 < 3; ++c2) d.shared_axes[r * 3 + c2] = scene.shared_axes(r, c2);
+            for (int c2 = 0; c2 < 3; ++c2) d.background[c2] = scene.background[c2];
+            check(sgs_scene_upload(context(), &d, &dscene));
+        }
+    }
+    if (!fast) {
+        slow = std::make_unique<DeviceScene>(scene.gaussians, scene.shared_axes, scene.background);
+        dscene = slow->s;
+    }
+    struct Free {
+        sgs_scene* s;
+        bool own;
+        ~Free() {
+            if (own) sgs_scene_free(s);
+        }
+    } free_fast{dscene, fast};
     const sgs_camera c = to_c(cam);
     const sgs_render_config k = to_c(cfg);
     const std::size_t npx = static_cast<std::size_t>(cam.width) * static_cast<std::size_t>(cam.height);
@@ -167,13 +310,22 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
         return e && std::atoi(e) != 0;
     }();
     if (exact) {
-        check(sgs_render_f64(context(), ds.s, &c, &k, out.image.data.data(), out.transmittance.data.data(), SGS_HOST));
+        check(sgs_render_f64(context(), dscene, &c, &k, out.image.data.data(), out.transmittance.data.data(),
+                             SGS_HOST));
         return out;
     }
-    std::vector<float> rgb(npx * 3), T(npx);
-    check(sgs_render(context(), ds.s, &c, &k, rgb.data(), T.data(), SGS_HOST, nullptr));
-    for (std::size_t i = 0; i < npx * 3; ++i) out.image.data[i] = rgb[i];
-    for (std::size_t i = 0; i < npx; ++i) out.transmittance.data[i] = T[i];
+    // float32 frame into pinned memory, widened to the double Image on every core
+    float* rgb = static_cast<float*>(g_frame.get(npx * 4 * sizeof(float)));
+    float* T = rgb + npx * 3;
+    check(sgs_render(context(), dscene, &c, &k, rgb, T, SGS_HOST, nullptr));
+    parallel_for(npx, [&](std::size_t b, std::size_t e) {
+        for (std::size_t i = b; i < e; ++i) {
+            out.image.data[3 * i] = rgb[3 * i];
+            out.image.data[3 * i + 1] = rgb[3 * i + 1];
+            out.image.data[3 * i + 2] = rgb[3 * i + 2];
+            out.transmittance.data[i] = T[i];
+        }
+    });
     return out;
 }
 

@@ -269,3 +269,26 @@ def _device_bytes(ptr, n):
 
     torch.cuda.synchronize()
     return torch.as_tensor(_DevView(ptr, n), device="cuda").clone()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,deg", [("sh", 3), ("sg1", 0), ("sg3", 0), ("mixed", 2)])
+def test_f32_row_upload_matches_host_packing(kind, deg):
+    """sgs_scene_upload of an SGS_F32 description (rows scattered into the planes on
+    the device, the drop-in render's path) == the float64 description packed on the
+    host: identical blob bytes."""
+    import torch
+
+    r = sg.Renderer(0)
+    s = sg.synth_scene(20_000, kind, 77, sh_degree=deg)
+    if kind == "sg1":  # un-normalised lobe axes: the FP64 normalisation runs on the device
+        s.params[:, 11 + 7:11 + 10] *= 3.0
+    a, b = r.upload(s), r.upload(s, f32=True)
+    try:
+        assert bytes(a.meta) == bytes(b.meta)
+        pa, na = a.blob()
+        pb, nb = b.blob()
+        assert torch.equal(_device_bytes(pa, na), _device_bytes(pb, nb))
+    finally:
+        a.free()
+        b.free()
