@@ -168,6 +168,15 @@ sgs_status sgs_scene_upload_into(sgs_context* ctx, const sgs_scene_desc* desc,
 /* Bind an already-populated blob (e.g. received by ncclBroadcast) without copying. */
 sgs_status sgs_scene_bind(sgs_context* ctx, const sgs_scene_meta* meta, void* device_blob,
                           uint64_t bytes, sgs_scene** out);
+/* The blob of a bound scene changed in place (e.g. a torch tensor the caller owns):
+ * recompute what the library caches from it (the 3D covariances). Without this, later
+ * renders would use the covariances of the old contents. */
+sgs_status sgs_scene_refresh(sgs_context* ctx, sgs_scene* scene);
+/* New parameters for an existing device scene with the same layout (count, model,
+ * degree, float32/float64 planes): repacked into its blob, caches refreshed; plane
+ * addresses do not change, so captured frame graphs stay valid. A different layout
+ * is SGS_ERR_INVALID_ARGUMENT (upload a new scene). */
+sgs_status sgs_scene_update(sgs_context* ctx, sgs_scene* scene, const sgs_scene_desc* desc);
 sgs_status sgs_scene_get_meta(const sgs_scene* scene, sgs_scene_meta* meta);
 sgs_status sgs_scene_blob(const sgs_scene* scene, void** device_blob, uint64_t* bytes);
 sgs_status sgs_scene_set_background(sgs_scene* scene, const double* rgb);

@@ -312,6 +312,18 @@ class DeviceScene:
         _check(_lib().sgs_scene_blob(self.handle, ctypes.byref(p), ctypes.byref(n)))
         return p.value, n.value
 
+    def refresh(self):
+        """The blob changed in place (a caller-owned tensor): recompute the cached 3D
+        covariances (sgs_scene_refresh) before the next render."""
+        _check(_lib().sgs_scene_refresh(self._r.handle, self.handle))
+
+    def update(self, scene: "Scene", f32: bool = False):
+        """New parameters with the same layout, repacked into this scene's blob
+        (sgs_scene_update; plane addresses and captured frame graphs stay valid)."""
+        d, keep = scene._desc(f32)
+        _check(_lib().sgs_scene_update(self._r.handle, self.handle, ctypes.byref(d)))
+        del keep
+
     def set_background(self, rgb):
         bg = np.ascontiguousarray(rgb, dtype=np.float64)
         _check(_lib().sgs_scene_set_background(self.handle, bg.ctypes.data))

@@ -142,6 +142,8 @@ SIGNATURES = {
                                    ctypes.POINTER(_P)]),
     "sgs_scene_bind": (_S, [_P, ctypes.POINTER(sgs_scene_meta), _P, ctypes.c_uint64,
                             ctypes.POINTER(_P)]),
+    "sgs_scene_refresh": (_S, [_P, _P]),
+    "sgs_scene_update": (_S, [_P, _P, ctypes.POINTER(sgs_scene_desc)]),
     "sgs_scene_get_meta": (_S, [_P, ctypes.POINTER(sgs_scene_meta)]),
     "sgs_scene_blob": (_S, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_uint64)]),
     "sgs_scene_set_background": (_S, [_P, _P]),

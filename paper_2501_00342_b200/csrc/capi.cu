@@ -202,6 +202,7 @@ struct sgs_context {
     };
     std::vector<TraceRec> trace_recs;
     DevBuf metrics;  // PSNR / SSIM scratch (inputs staged from host, maps, partial sums)
+    DevBuf rows;     // float32 scene rows of an SGS_F32 upload (grow-only)
     DevBuf bwd;      // backward scratch (FP64 splats, ranks, per-entry partials, staging)
     uint64_t own_launches = 0, lib_launches = 0;
 };
@@ -1088,7 +1089,8 @@ cudaError_t upload_rows_f32(sgs_context* ctx, const sgs_scene_desc* desc, const 
     int mu_col = -1;
     const std::vector<int32_t> tab = ply_slot_table(t, L.color_planes, &mu_col);
     const size_t nfloat = static_cast<size_t>(m.count) * static_cast<size_t>(stride);
-    DevBuf d_rows, d_tab;
+    DevBuf& d_rows = ctx->rows;
+    DevBuf d_tab;
     cudaStream_t s = ctx->stream;
     cudaError_t e = d_rows.ensure(nfloat * sizeof(float));
     if (e == cudaSuccess) e = d_tab.ensure(tab.size() * sizeof(int32_t));
@@ -1106,7 +1108,6 @@ cudaError_t upload_rows_f32(sgs_context* ctx, const sgs_scene_desc* desc, const 
         if (e == cudaSuccess) ctx->own_launches += 1;
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    d_rows.release();
     d_tab.release();
     return e;
 }
@@ -1235,6 +1236,7 @@ void sgs_destroy(sgs_context* ctx) {
         if (L.swap) cudaEventDestroy(L.swap);
     }
     ctx->metrics.release();
+    ctx->rows.release();
     ctx->bwd.release();
     if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -1382,6 +1384,37 @@ sgs_status sgs_scene_bind(sgs_context* ctx, const sgs_scene_meta* meta, void* de
     }
     *out = sc;
     return SGS_OK;
+}
+
+sgs_status sgs_scene_refresh(sgs_context* ctx, sgs_scene* scene) {
+    if (!ctx || !scene) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    return bind_and_cache(scene, ctx->stream);
+}
+
+sgs_status sgs_scene_update(sgs_context* ctx, sgs_scene* scene, const sgs_scene_desc* desc) {
+    if (!ctx || !scene || !desc) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    sgs_scene_meta m{};
+    sgs_status st = sgs_scene_plan(desc, &m);
+    if (st != SGS_OK) return st;
+    const sgs_scene_meta& o = scene->meta;
+    if (m.count != o.count || m.kind != o.kind || m.sh_degree != o.sh_degree || m.geometry_f64 != o.geometry_f64 ||
+        m.color_f64 != o.color_f64 || m.blob_bytes != o.blob_bytes)
+        return fail(SGS_ERR_INVALID_ARGUMENT, "scene update changes the device layout");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    cudaError_t e = cudaSuccess;
+    if (desc->dtype == SGS_F32 && m.count) {
+        e = upload_rows_f32(ctx, desc, m, scene->blob);
+    } else {
+        std::vector<char> host;
+        fill_blob(desc, m, host);
+        e = cudaMemcpy(scene->blob, host.data(), host.size(), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) return fail(SGS_ERR_CUDA, std::string("scene update: ") + cudaGetErrorString(e));
+    scene->meta = m;  // (axes and background may change)
+    return bind_and_cache(scene, ctx->stream);
 }
 
 sgs_status sgs_scene_get_meta(const sgs_scene* scene, sgs_scene_meta* meta) {

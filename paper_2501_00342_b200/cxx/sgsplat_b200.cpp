@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <memory>
 #include <cstdlib>
 #include <cstring>
@@ -156,6 +158,9 @@ struct PinnedBuf {
 };
 std::mutex g_stage_mu;  // render() calls share the staging (the reference is reentrant:
 PinnedBuf g_rows, g_frame;  // concurrent calls serialise here, results stay per call)
+// The device scene every render() call repacks its scene into (sgs_scene_update: same
+// planes, no device allocation per call) while the layout stays the same.
+sgs_scene* g_scene = nullptr;
 
 // The colour parameters of one Gaussian in canonical order (one variant visit).
 template <typename T>
@@ -193,14 +198,23 @@ void pack_color(const ColorModel& model, T* out) {
 bool f32_exact(double v) { return static_cast<double>(static_cast<float>(v)) == v; }
 
 // The scene as float32 rows in pinned memory, packed on every core; false when some
-// parameter is not f32-exact (the caller then takes the float64 path).
-bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride, float* rows) {
-    std::atomic<bool> exact{true};
+// parameter is not f32-exact (the caller then takes the float64 path). *mixed: some
+// Gaussian's colour model or stored degree differs from the first one's
+// (Scene::check_homogeneous then raises the reference's error).
+bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride, float* rows, bool* mixed) {
+    std::atomic<bool> exact{true}, hetero{false};
+    const ColorModelKind kind0 = kind_of(gs.front().color);
+    const int deg0 = stored_degree(gs.front().color);
     parallel_for(gs.size(), [&](std::size_t b, std::size_t e) {
         std::vector<double> c(stride - kGeometryParams);
         bool ok = true;
         for (std::size_t i = b; i < e && ok; ++i) {
             const GaussianPrimitive& g = gs[i];
+            if (kind_of(g.color) != kind0 || stored_degree(g.color) != deg0) {
+                hetero.store(true);
+                ok = false;
+                break;
+            }
             double p[kGeometryParams];
             for (int k = 0; k < 3; ++k) p[k] = g.position[k];
             for (int k = 0; k < 4; ++k) p[3 + k] = g.rotation[k];
@@ -219,6 +233,7 @@ bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride,
         }
         if (!ok) exact.store(false);
     });
+    *mixed = hetero.load();
     return exact.load();
 }
 
@@ -258,22 +273,49 @@ std::optional<Splat2D> project(const GaussianPrimitive& g, const Camera& cam, co
 
 RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& cfg) {
     if (cfg.tile_size < 1) throw InvalidArgument("tile_size must be >= 1");
-    scene.check_homogeneous();
-    cam.validate();
+    // project_scene's checks (raster.cpp:82-85): the scene's homogeneity -- folded into
+    // the packing below -- then the camera
     std::unique_lock<std::mutex> stage(g_stage_mu);
+    // SGS_DROPIN_TRACE=1: per-phase wall times of each call on stderr
+    static const bool trace = [] {
+        const char* e = std::getenv("SGS_DROPIN_TRACE");
+        return e && std::atoi(e) != 0;
+    }();
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
+    auto t1 = t0, t2 = t0;
     // the scene: float32 rows packed on every core into pinned memory, scattered into
     // the device planes by a kernel (sgs_scene_upload of an SGS_F32 description) --
     // exactly the planes of the float64 path whenever every value is f32-exact
     // (synthetic scenes and PLY checkpoints are); otherwise the float64 path
     std::unique_ptr<DeviceScene> slow;
+    RenderResult out;
+    std::thread alloc;
+    struct Join {
+        std::thread& t;
+        ~Join() {
+            if (t.joinable()) t.join();
+        }
+    } join_alloc{alloc};
     sgs_scene* dscene = nullptr;
     const std::vector<GaussianPrimitive>& gs = scene.gaussians;
     const std::size_t stride = gs.empty() ? 0 : kGeometryParams + param_count(gs.front().color);
     bool fast = !gs.empty();
     if (fast) {
         float* rows = static_cast<float*>(g_rows.get(gs.size() * stride * sizeof(float)));
-        fast = pack_rows_f32(gs, stride, rows);
+        bool mixed = false;
+        fast = pack_rows_f32(gs, stride, rows, &mixed);
+        if (mixed) scene.check_homogeneous();  // throws the reference's InvalidArgument
+        cam.validate();
+        t1 = now();
         if (fast) {
+            // the result images (66 MB at 1080p, zeroed by their constructor) are
+            // allocated while the rows cross PCIe
+            alloc = std::thread([&] {
+                out.image = Image(cam.width, cam.height, 3);
+                out.transmittance = Image(cam.width, cam.height, 1);
+            });
             sgs_scene_desc d{};
             d.count = gs.size();
             d.kind = static_cast<int32_t>(kind_of(gs.front().color));
@@ -283,26 +325,30 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
             for (int r = 0; r < 3; ++r)
                 for (int c2 = 0; c2 < 3; ++c2) d.shared_axes[r * 3 + c2] = scene.shared_axes(r, c2);
             for (int c2 = 0; c2 < 3; ++c2) d.background[c2] = scene.background[c2];
-            check(sgs_scene_upload(context(), &d, &dscene));
+            if (!(g_scene && sgs_scene_update(context(), g_scene, &d) == SGS_OK)) {
+                sgs_scene_free(g_scene);
+                g_scene = nullptr;
+                check(sgs_scene_upload(context(), &d, &g_scene));
+            }
+            dscene = g_scene;
         }
     }
+    t2 = now();
     if (!fast) {
+        scene.check_homogeneous();
+        cam.validate();
         slow = std::make_unique<DeviceScene>(scene.gaussians, scene.shared_axes, scene.background);
         dscene = slow->s;
     }
-    struct Free {
-        sgs_scene* s;
-        bool own;
-        ~Free() {
-            if (own) sgs_scene_free(s);
-        }
-    } free_fast{dscene, fast};
     const sgs_camera c = to_c(cam);
     const sgs_render_config k = to_c(cfg);
     const std::size_t npx = static_cast<std::size_t>(cam.width) * static_cast<std::size_t>(cam.height);
-    RenderResult out;
-    out.image = Image(cam.width, cam.height, 3);
-    out.transmittance = Image(cam.width, cam.height, 1);
+    if (alloc.joinable()) {
+        alloc.join();
+    } else {
+        out.image = Image(cam.width, cam.height, 3);
+        out.transmittance = Image(cam.width, cam.height, 1);
+    }
     // SGS_EXACT=1: the reference's FP64 compositing (sgs_render_f64); default: the
     // FP32 throughput path (exact decisions, image within 1e-5)
     static const bool exact = [] {
@@ -317,7 +363,9 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
     // float32 frame into pinned memory, widened to the double Image on every core
     float* rgb = static_cast<float*>(g_frame.get(npx * 4 * sizeof(float)));
     float* T = rgb + npx * 3;
+    const auto t3 = now();
     check(sgs_render(context(), dscene, &c, &k, rgb, T, SGS_HOST, nullptr));
+    const auto t4 = now();
     parallel_for(npx, [&](std::size_t b, std::size_t e) {
         for (std::size_t i = b; i < e; ++i) {
             out.image.data[3 * i] = rgb[3 * i];
@@ -326,6 +374,9 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
             out.transmittance.data[i] = T[i];
         }
     });
+    if (trace)
+        std::fprintf(stderr, "dropin: pack %.2f upload %.2f image-alloc %.2f render %.2f widen %.2f ms\n",
+                     ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, now()));
     return out;
 }
 

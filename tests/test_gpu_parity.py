@@ -740,3 +740,43 @@ def test_frame_counters_vs_oracle(orc, chunks):
         assert st.tile_entries < want["P"]  # finished tiles receive no later entries
     print(f"E_t device {st.block_entries} oracle {want['E_t']} diff {st.block_entries - want['E_t']}")
     assert abs(st.block_entries - want["E_t"]) <= 1e-4 * want["E_t"]
+
+
+def test_scene_refresh_and_update():
+    """A bound, caller-owned blob changed in place is stale until sgs_scene_refresh
+    recomputes the cached covariances; sgs_scene_update repacks new
+    parameters of the same layout into an existing scene (frame graphs replay on it);
+    a different layout is refused."""
+    import torch
+
+    a = sg.synth_scene(40_000, "mixed", 501, log_scale_range=(-5.0, -3.5))
+    b = sg.synth_scene(40_000, "mixed", 502, log_scale_range=(-5.0, -3.5))
+    cams = sg.orbit_cameras(6, 256, 160, 4.0, 190.0)
+    r = sg.Renderer(0)
+    fresh_b = r.upload(b)
+    want = r.render_batch(fresh_b, cams, degree_override=1)
+    # in-place blob change + refresh
+    meta, host_a = sg.Renderer.pack(a)
+    _, host_b = sg.Renderer.pack(b)
+    blob = torch.from_numpy(host_a).cuda()
+    bound = r.bind(meta, blob.data_ptr(), meta.blob_bytes, keepalive=blob)
+    for _ in range(3):  # direct, captured, replayed
+        r.render_batch(bound, cams, degree_override=1)
+    blob.copy_(torch.from_numpy(host_b))
+    torch.cuda.synchronize()
+    bound.refresh()
+    got = r.render_batch(bound, cams, degree_override=1)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    # update in place (float64 and float32 rows), graphs replaying on the same planes
+    up = r.upload(a)
+    for _ in range(3):
+        r.render_batch(up, cams, degree_override=1)
+    for f32 in (False, True):
+        up.update(b, f32=f32)
+        got = r.render_batch(up, cams, degree_override=1)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+        up.update(a, f32=f32)
+    with pytest.raises(sg.InvalidArgumentError):
+        up.update(sg.synth_scene(1000, "mixed", 503))
+    for d in (fresh_b, bound, up):
+        d.free()
