@@ -177,7 +177,11 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
     if (m == 0) return;
     const int tid = threadIdx.x;
     if (m > kL2Cap) {
+        // too many keys for one CTA: the host redoes the frame with the 64-bit sort.
+        // Until then the rest of this frame still runs, so these ranks get empty
+        // binning inputs (no tiles) instead of whatever the arena held before.
         if (tid == 0) atomicAdd(&ctr->tie_overflow, 1ULL);
+        for (uint32_t e = tid; e < m; e += kL2Threads) bmeta[s + e] = make_uint2(order[s + e], 0u);
         return;
     }
     const unsigned long long kmin = ctr->kmin;
