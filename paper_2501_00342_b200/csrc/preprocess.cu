@@ -61,7 +61,13 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 // Thread-private staging: each thread copies its own Gaussian's slots (coalesced
 // across the warp, slot-major so smem reads are conflict free) and later reads
-// only them, so no CTA barrier is needed.
+// only them, so no CTA barrier is needed. Measured against 1D bulk copies
+// (cp.async.bulk + mbarriers, the TMA engine) of the same slots at config C: one
+// elected thread per CTA moving 4-KB slots with CTA-wide full / empty mbarriers,
+// 166 us per launch; lane 0 of every warp moving its 512-B slot parts with per-warp
+// mbarriers, 174 us; this per-thread cp.async pipeline, 158 us. K1 is bound by the
+// latency of its per-Gaussian FP64 chain at 16 warps per SM, not by issuing loads,
+// and the bulk variants' refills wait on slower consumers.
 template <bool F64>
 __device__ __forceinline__ void stage_item(const ScenePlanes& sp, const K1Stage& st, uint64_t i, float4* buf,
                                            int tid) {
@@ -81,61 +87,6 @@ __device__ __forceinline__ void stage_item(const ScenePlanes& sp, const K1Stage&
     b += st.sh_pre * kK1Threads;
     for (int p = 0; p < st.lobe_pre; ++p)
         cp_async16(&b[p * kK1Threads + tid], &sp.color[static_cast<uint64_t>(st.lobe_base + p) * sp.n + i]);
-}
-
-// Bulk staging (float32 geometry): the CTA's 256 consecutive Gaussians of a step are
-// one contiguous range in every plane, so a single elected thread moves each slot
-// with one 1D bulk copy (cp.async.bulk, the TMA engine) of up to 4 KB, completion
-// counted in bytes on the buffer's "full" mbarrier; every thread arrives on the
-// buffer's "empty" mbarrier once it no longer reads it, and the elected thread waits
-// on that before refilling the buffer. SASS: UBLKCP + SYNCS instead of 2560 LDGSTS
-// per CTA step.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-// Elected thread: every slot of the step starting at Gaussian `base` into buf.
-__device__ __forceinline__ void stage_bulk(const ScenePlanes& sp, const K1Stage& st, uint64_t base, float4* buf,
-                                           uint64_t* full) {
-    const uint64_t cnt = sp.n - base < static_cast<uint64_t>(kK1Threads) ? sp.n - base : kK1Threads;
-    const uint32_t bytes = static_cast<uint32_t>(cnt * sizeof(float4));
-    mbar_expect_tx(full, bytes * static_cast<uint32_t>(st.slots));
-    bulk_g2s(buf, sp.g4[0] + base, bytes, full);
-    float4* b = buf + kK1Threads;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) bulk_g2s(b + k * kK1Threads, sp.cov[k] + base, bytes, full);
-    b += 3 * kK1Threads;
-    for (int p = 0; p < st.sh_pre; ++p) bulk_g2s(b + p * kK1Threads, sp.color + static_cast<uint64_t>(p) * sp.n + base, bytes, full);
-    b += st.sh_pre * kK1Threads;
-    for (int p = 0; p < st.lobe_pre; ++p)
-        bulk_g2s(b + p * kK1Threads, sp.color + static_cast<uint64_t>(st.lobe_base + p) * sp.n + base, bytes, full);
 }
 
 template <bool F64>
@@ -499,26 +450,9 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
     const int tid = threadIdx.x;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kK1Threads;
     const int buf_stride = stg.slots * kK1Threads;
-    const uint64_t block0 = static_cast<uint64_t>(blockIdx.x) * kK1Threads;
-    uint64_t i = block0 + tid;
-    // float32 geometry: bulk copies (mbarriers after the two buffers: full[2], empty[2]);
-    // float64 geometry (interleaved 8-byte planes): per-thread cp.async
-    constexpr bool kBulk = !F64;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(k1_smem + 2 * buf_stride);
-    if constexpr (kBulk) {
-        if (tid == 0) {
-            mbar_init(&bars[0], 1);
-            mbar_init(&bars[1], 1);
-            mbar_init(&bars[2], kK1Threads);
-            mbar_init(&bars[3], kK1Threads);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        if (tid == 0 && block0 < sp.n) stage_bulk(sp, stg, block0, k1_smem, &bars[0]);
-    } else {
-        if (i < sp.n) stage_item<F64>(sp, stg, i, k1_smem, tid);
-        cp_async_commit();
-    }
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * kK1Threads + tid;
+    if (i < sp.n) stage_item<F64>(sp, stg, i, k1_smem, tid);
+    cp_async_commit();
     uint32_t nvis[NV];
     unsigned long long kmin[NV], kmax[NV];
 #pragma unroll
@@ -527,27 +461,13 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
         kmin[v] = ~0ULL;
         kmax[v] = 0ULL;
     }
-    for (int it = 0; block0 + static_cast<uint64_t>(it) * stride < sp.n; ++it, i += stride) {
-        const int b = it & 1;
-        if constexpr (kBulk) {
-            // refill the other buffer with the next step once every thread is done with
-            // its previous use (step it - 1), then wait for this step's bytes
-            const uint64_t next = block0 + static_cast<uint64_t>(it + 1) * stride;
-            if (tid == 0 && next < sp.n) {
-                if (it >= 1) mbar_wait(&bars[2 + (b ^ 1)], static_cast<uint32_t>(((it - 1) >> 1) & 1));
-                stage_bulk(sp, stg, next, k1_smem + (b ^ 1) * buf_stride, &bars[b ^ 1]);
-            }
-            mbar_wait(&bars[b], static_cast<uint32_t>((it >> 1) & 1));
-        } else {
-            if (i + stride < sp.n) stage_item<F64>(sp, stg, i + stride, k1_smem + ((it + 1) & 1) * buf_stride, tid);
-            cp_async_commit();
-            cp_async_wait1();
-        }
-        if (i >= sp.n) {
-            if constexpr (kBulk) mbar_arrive(&bars[2 + b]);
-            continue;
-        }
-        const float4* buf = k1_smem + b * buf_stride;
+    for (int it = 0; static_cast<uint64_t>(blockIdx.x) * kK1Threads + static_cast<uint64_t>(it) * stride < sp.n;
+         ++it, i += stride) {
+        if (i + stride < sp.n) stage_item<F64>(sp, stg, i + stride, k1_smem + ((it + 1) & 1) * buf_stride, tid);
+        cp_async_commit();
+        cp_async_wait1();
+        if (i >= sp.n) continue;
+        const float4* buf = k1_smem + (it & 1) * buf_stride;
         Geo g;
         geo_from_stage<F64>(buf, stg.geo_slots, tid, g);
 #pragma unroll
@@ -570,7 +490,6 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
                 kmax[v] = max(kmax[v], key);
             }
         }
-        if constexpr (kBulk) mbar_arrive(&bars[2 + b]);  // this step's buffer is no longer read
     }
     // visible count and depth-key range per view: one atomic each per warp
 #pragma unroll
@@ -636,7 +555,7 @@ template <bool F64, int KIND, int MINB, bool DEBUG, int NV>
 void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
                cudaStream_t stream) {
     const K1Stage st = make_stage(sp, cfg);
-    const size_t smem = static_cast<size_t>(2) * st.slots * kK1Threads * sizeof(float4) + 4 * sizeof(uint64_t);
+    const size_t smem = static_cast<size_t>(2) * st.slots * kK1Threads * sizeof(float4);
     auto kern = preprocess_kernel<F64, KIND, MINB, DEBUG, NV>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int dev = 0, sms = 148, per_sm = 1;
