@@ -367,17 +367,9 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
         const double guard =
             2.0 * 5.9604644775390625e-08 * csum * (9.0 * radius * radius + 3.0 * radius * ts) +
             1e-6;
-        // colour (FP32), direction from the FP64 offset
-        const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
-        const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
-        const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
-        // A non-finite colour or a NaN opacity must reach exactly the pixels the
-        // reference blends it into (it skips the others before touching acc; a NaN
-        // opacity passes std::min and the alpha test): such a splat gets an infinite
-        // guard band, so every one of its pairs is decided and blended one at a time
-        // by the compositor's FP64 path, and it keeps its 3-sigma tile rectangle.
-        const bool special = !(isfinite(col.x) && isfinite(col.y) && isfinite(col.z)) || isnan(opacity);
-        // combined cutoff: alpha < 1/255 <=> m2 > 2 ln(255 op) (op > 0)
+        // combined cutoff: alpha < 1/255 <=> m2 > 2 ln(255 op) (op > 0); a NaN opacity
+        // keeps the support cutoff (the reference blends it: NaN passes std::min and the
+        // alpha test)
         const double acut = opacity > 0.0 ? 2.0 * log(255.0 * opacity) : -1.0;
         const double cut = isnan(opacity) ? kSupportMahalanobisSq
                                           : (acut < kSupportMahalanobisSq ? acut : kSupportMahalanobisSq);
@@ -392,10 +384,11 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
         r.cc = static_cast<float>(conc);
         r.lop = opacity > 0.0 ? __log2f(static_cast<float>(opacity)) : -1e30f;
         r.cut = static_cast<float>(cut);
-        r.guard = special ? INFINITY : (guard < 1e30 ? static_cast<float>(guard) : FLT_MAX);
-        r.ext_x = special ? INFINITY : sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
-        r.ext_y = special ? INFINITY : sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
-        if (cfg.tight_rect && !special && x1 >= x0 && y1 >= y0) {
+        r.guard = guard < 1e30 ? static_cast<float>(guard) : FLT_MAX;
+        r.ext_x = sqrtf(static_cast<float>(K * pg.a)) * (1.0f + 1e-5f) + 1e-3f;
+        r.ext_y = sqrtf(static_cast<float>(K * pg.c)) * (1.0f + 1e-5f) + 1e-3f;
+        const int4 rect3s = make_int4(x0, x1, y0, y1);  // the reference's 3-sigma rectangle
+        if (cfg.tight_rect && x1 >= x0 && y1 >= y0) {
             // Render frames list a splat only in the tiles its cut ellipse's box reaches:
             // every pixel outside it has m2 > cut and is skipped by the reference, so the
             // image is unchanged (the parity dumps and stats frames keep the reference's
@@ -413,7 +406,21 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
             if (cut + guard < 0.0) x1 = x0 - 1;
         }
         o.rects[i] = make_int4(x0, x1, y0, y1);
+        // colour (FP32), direction from the FP64 offset
+        const float4* sb = buf + (stg.geo_slots + 3) * kK1Threads;
+        const PlaneFetch pf{sb, sb + stg.sh_pre * kK1Threads, sp.color, sp.n, i, tid, stg.sh_pre, stg.lobe_base};
+        const float4 col = eval_colour<KIND>(sp, pf, deg, fdx, fdy, fdz);
         o.colour[i] = col;
+        // A non-finite colour or a NaN opacity must reach exactly the pixels the
+        // reference blends it into (it skips the others before touching acc): such a
+        // (rare) splat gets an infinite guard band, so every one of its pairs is decided
+        // and blended one at a time by the compositor's FP64 path, and its 3-sigma
+        // rectangle.
+        if (!(isfinite(col.x) && isfinite(col.y) && isfinite(col.z)) || isnan(opacity)) {
+            r.guard = INFINITY;
+            r.ext_x = r.ext_y = INFINITY;
+            o.rects[i] = rect3s;
+        }
         if constexpr (DEBUG) {
             dbg.color[0] = col.x;
             dbg.color[1] = col.y;
