@@ -565,28 +565,16 @@ cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const 
     if (e != cudaSuccess) return e;
     build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
                                                              last ? 1 : 0, ntile, nchunks, cap, work, wctl);
-    static const int variant = [] {
-        const char* v = std::getenv("SGS_K7_VARIANT");
-        return v ? std::atoi(v) : 0;
-    }();
-#define SGS_K7(G, M, B)                                                                                        \
-    (cfg.tile_size == 16                                                                                      \
-         ? launch_k7<G, M, true, B>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,      \
-                                    processed, tile_done, tile_touched, first, last, counters, want_stats,     \
-                                    work, wctl, cap, stream)                                                  \
-         : launch_k7<G, M, false, B>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,     \
-                                     processed, tile_done, tile_touched, first, last, counters, want_stats,    \
-                                     work, wctl, cap, stream))
-    switch (variant) {
-        case 1: return SGS_K7(4, 5, 128);
-        case 2: return SGS_K7(4, 6, 128);
-        case 3: return SGS_K7(2, 6, 128);
-        case 4: return SGS_K7(2, 8, 128);
-        case 5: return SGS_K7(2, 4, 256);
-        case 6: return SGS_K7(4, 5, 256);
-        default: return SGS_K7(4, 4, 256);
-    }
-#undef SGS_K7
+    // Measured alternatives (SURVEY-C 32-view batch, ms/frame): 5 or 6 CTAs per SM with
+    // 128-record batches 0.595 / 0.588, 2-record groups at 4 or 6 CTAs 0.610 / 0.605,
+    // 8 CTAs (64 registers, spills) 0.618 -- against 0.592 for this default.
+    if (cfg.tile_size == 16)
+        return launch_k7<4, 4, true, 256>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,
+                                          processed, tile_done, tile_touched, first, last, counters, want_stats,
+                                          work, wctl, cap, stream);
+    return launch_k7<4, 4, false, 256>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,
+                                       processed, tile_done, tile_touched, first, last, counters, want_stats, work,
+                                       wctl, cap, stream);
 }
 
 }  // namespace sgs
