@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=3, help="CPU-baseline sample frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in render timing")
+    ap.add_argument("--group", action="store_true",
+                    help="use the C-ABI multi-GPU group path even at N=1 (a world-1 check of it)")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL frame gather")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo: host-path check only)")
@@ -254,20 +256,22 @@ def main():
     renderer.set_stream(stream.cuda_stream)
     # N>1 over NCCL: the C-ABI's own multi-GPU group (sgs_group_*); --backend gloo keeps
     # the torch.distributed host path (a single-GPU check of the multi-rank logic)
-    use_group = world > 1 and args.backend == "nccl"
+    use_group = (world > 1 and args.backend == "nccl") or args.group
     group = None
     if use_group:
         holder = [multiview.RenderGroup.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(holder, src=0)
+        if world > 1:
+            dist.broadcast_object_list(holder, src=0)
         group = multiview.RenderGroup.init_rank(renderer, world, rank, holder[0])
 
     # --- scene: synthesised on rank 0, its device layout NCCL-broadcast to the others
     t_b0 = time.perf_counter()
     scene = sg.synth_scene(N_GAUSS, "mixed", SEED, log_scale_range=LOG_SCALE) if rank == 0 else None
     bcast_ms = None
-    if world > 1:
+    if world > 1 or use_group:
         torch.cuda.synchronize()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
         tb = time.perf_counter()
         if use_group:
             dscene = group.broadcast_scene(scene, root=0)
