@@ -68,6 +68,9 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // mbarriers, 174 us; this per-thread cp.async pipeline, 158 us. K1 is bound by the
 // latency of its per-Gaussian FP64 chain at 16 warps per SM, not by issuing loads,
 // and the bulk variants' refills wait on slower consumers.
+// Staging only geometry + covariance and reading the colour planes at use (32-view
+// batch, config C): 0.637 ms/frame at 2 CTAs/SM, 0.606 at 3, 0.614 at 4, against
+// 0.594 for the full stage at 2 (and 0.621 for the full stage at 3).
 template <bool F64>
 __device__ __forceinline__ void stage_item(const ScenePlanes& sp, const K1Stage& st, uint64_t i, float4* buf,
                                            int tid) {
