@@ -128,6 +128,7 @@ struct Lane {
     DevBuf tk_a, tv_a, tk_b, tv_b;
     DevBuf sort_hist;  // radix sort: per-slice digit histograms
     DevBuf ranges, tile_done, pix_state, pix_walked;
+    DevBuf tile_emax;  // stats frames: deepest entry per (tile, pixel chunk) (E_t)
     // host-output frames: kOutSlots device buffers per lane drained by the lane's copy
     // stream, so the lane renders its next views while earlier ones cross PCIe
     static constexpr int kOutSlots = 3;
@@ -562,10 +563,12 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
                 const uint64_t b = (n + div - 1) / div;
                 if (b > bounds.back() && b < n) bounds.push_back(b);
             }
-            SGS_CUDA(L.tile_done.ensure((ntile + 31) / 32 * 4 * 2));  // done + touched bitmaps
+            // done, touched and part-done bitmaps
+            const size_t flag_bytes = composite_flag_words(static_cast<uint32_t>(ntile)) * 4;
+            SGS_CUDA(L.tile_done.ensure(flag_bytes));
             SGS_CUDA(L.pix_state.ensure(npx * sizeof(PixelState)));
             SGS_CUDA(L.pix_walked.ensure(npx * sizeof(uint32_t)));
-            SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, (ntile + 31) / 32 * 4 * 2, s));
+            SGS_CUDA(cudaMemsetAsync(L.tile_done.ptr, 0, flag_bytes, s));
         }
         bounds.push_back(n);
         const int nchunks = static_cast<int>(bounds.size()) - 1;
@@ -573,7 +576,8 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
                                       static_cast<float>(scene->meta.background[1]),
                                       static_cast<float>(scene->meta.background[2]));
         const TileDigits td = tile_digits(std::max(1, ceil_log2(ntile)));
-        const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_pixel_chunks(cfg->tile_size));
+        const uint64_t work_cap = ntile * static_cast<uint64_t>(composite_work_items(cfg->tile_size));
+        if (count_stats) SGS_CUDA(L.tile_emax.ensure(ntile * composite_pixel_chunks(cfg->tile_size) * 4));
         SGS_CUDA(L.work.ensure((7 * work_cap + 8) * sizeof(uint32_t)));  // 6 length classes, 8 control words, background items
         const unsigned long long* d_pc = &L.d_ctr->chunk_entries;
         for (int c = 0; c < nchunks; ++c) {
@@ -619,11 +623,11 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
             if (mode == kRender) {
                 SGS_CUDA(launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, 1, L.rec.as<SplatRec>(),
                                           L.colour.as<float4>(), bg, L.pix_state.as<PixelState>(),
-                                          L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(),
-                                          L.tile_done.as<uint32_t>() + (ntile + 31) / 32, c == 0, c == nchunks - 1,
-                                          L.d_ctr, count_stats, L.work.as<uint32_t>(),
+                                          L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(), c == 0,
+                                          c == nchunks - 1, L.d_ctr, count_stats, L.tile_emax.as<uint32_t>(),
+                                          L.work.as<uint32_t>(),
                                           L.work.as<uint32_t>() + 6 * work_cap, s));
-                ctx->own_launches += 2;  // (+ the work list kernel)
+                ctx->own_launches += count_stats && c == nchunks - 1 ? 3 : 2;  // (+ work list, E_t sum)
             }
             if (timing) {
                 SGS_CUDA(cudaEventRecord(L.ev[6], s));
@@ -1209,7 +1213,7 @@ void sgs_destroy(sgs_context* ctx) {
         if (L.stream) cudaStreamSynchronize(L.stream);
         for (DevBuf* b : {&L.keys_a, &L.keys_b, &L.buckets, &L.order, &L.rec, &L.colour, &L.rects, &L.brect, &L.bmeta, &L.bin_status,
                           &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_hist, &L.ranges,
-                          &L.tile_done, &L.pix_state, &L.pix_walked})
+                          &L.tile_done, &L.pix_state, &L.pix_walked, &L.tile_emax})
             b->release();
         if (L.d_ctr) cudaFree(L.d_ctr);
         if (L.h_ctr) cudaFreeHost(L.h_ctr);

@@ -6,20 +6,21 @@
 // skip alpha < 1/255, accumulate c * alpha * T, T *= 1 - alpha, stop after the
 // splat that pushed T below the threshold, then add T * background.
 //
-// composite2_kernel: 128 threads per (tile, 256-pixel chunk), two horizontally
-// adjacent pixels per thread, warp w owning one 8x8 quadrant of a 16x16 tile.
+// composite_kernel: independent warps, each compositing one 64-pixel part of a
+// tile (an 8x8 quadrant of a 16x16 tile), two horizontally adjacent pixels per
+// thread.
 //
-// Layout. The tile's list streams through shared memory in batches of 256 64-B
-// records (cp.async gathers, double-buffered). Each warp compacts the batch to the
-// records whose support box reaches its live pixels (ballot + popc).
+// Layout. The tile's list streams through the warp's shared memory in batches of 64
+// 64-B records (cp.async gathers, double-buffered). The warp compacts each batch to
+// the records whose support box reaches its live pixels (ballot + popc).
 //
 // Latency. A pixel's walk is inherently sequential, so long lists (tiles on the
 // silhouette whose pixels never saturate) sit on the critical path. The walk goes
 // in groups of kGroup records: the m2 / alpha of the group are computed
 // independently (ILP), then a branch-free blend chain applies them in order; a
 // skipped pair, or any pair after the pixel terminated, blends with alpha = 0,
-// which leaves T and the colour bit-identical. __syncthreads_count ends the tile
-// once every pixel has terminated.
+// which leaves T and the colour bit-identical. The warp leaves its part once every
+// pixel in it has terminated.
 //
 // Exactness. The two skip tests are one per-splat cutoff: alpha < 1/255 <=>
 // m2 > 2 ln(255 op), so "skip" <=> m2 > cut = min(9, 2 ln(255 op)) (FP64 in K1).
@@ -134,16 +135,35 @@ __device__ __forceinline__ void write_background(int W, int H, const CfgParams& 
 }
 
 // ---------------------------------------------------------------------------
-// K7, two pixels per thread (the default). One CTA of 128 threads per (tile,
-// 256-pixel chunk); on 16x16 tiles warp w owns one 8x8 quadrant and a thread the two
-// horizontally adjacent pixels (2c, 2c+1) of one row, so a record's dy terms
+// K7. Every warp is an independent compositor: it takes its own (tile, 64-pixel part)
+// items from the work list -- on 16x16 tiles one 8x8 quadrant -- and streams the
+// tile's list through its own double-buffered shared-memory ring, so no warp ever
+// waits for another (the CTA only groups four warps for residency). A thread owns
+// two horizontally adjacent pixels (2c, 2c+1) of one row, so a record's dy terms
 // (dy, 2b dy, c dy^2) and its shared-memory reads serve both pixels. m2 is formed
-// per pixel with the same operations and rounding for both pixels, and
-// the blend chain drops the per-step termination bookkeeping: transmittance only
-// decreases, so "the pixel stopped before this splat" is T < stop, tested in the
-// chain; the splat that stopped it is found afterwards by replaying the group's T
-// products (bit-identical), which happens once per pixel.
-constexpr int kThreads2 = 128;
+// per pixel with the same operations and rounding for both pixels, and the blend
+// chain drops the per-step termination bookkeeping: transmittance only decreases, so
+// "the pixel stopped before this splat" is T < stop, tested in the chain; the splat
+// that stopped it is found afterwards by replaying the group's T products
+// (bit-identical), which happens once per pixel. Each record is staged once per warp
+// that needs it (4x the L2 reads of a CTA-shared stage, ~200 MB/frame at config C,
+// and ~3% more instructions), in exchange for no CTA barrier anywhere in the walk.
+constexpr int kThreads = 128;  // four independent warps per CTA
+constexpr int kWB = 64;        // records per warp batch (two per lane)
+constexpr int kSubPx = 64;     // pixels per warp item (two per lane)
+constexpr int kSubsPerChunk = kChunkPx / kSubPx;
+
+// One warp's staging: 64-B records, double-buffered (cp.async). After arrival each
+// lane rewrites its records in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard,
+// cut - guard, log2 op), [2] (r, g, b, gaussian index bits), and the filter box into
+// box. Slot kWB of each buffer is a null record (never contributes) that pads the
+// compacted lists to whole groups.
+struct WarpStage {
+    float4 raw[2][kWB + 1][4];
+    float4 box[kWB];
+    uint16_t idx[kWB + 8];
+};
+static_assert(sizeof(WarpStage) % 16 == 0, "warp stage alignment");
 
 struct Pix {
     float T, r, g, b;
@@ -175,35 +195,41 @@ __device__ __forceinline__ void mahal2x2(const float4& A, float Bx, float fcx0, 
     }
 }
 
-template <int kGroup, int MINB, bool kSameRow, int kBatch>
-__global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
+// Flags of a depth-chunked frame: tiles finished (binning skips them); per part
+// (bit tile * 4 + part: depth chunking runs on tiles of at most 256 pixels, so a tile
+// has at most 4 parts) whether its pixel state was written by an earlier chunk and
+// whether it is final. A part's two bits are read and written only by the warp
+// compositing it (and by the work-list kernel between launches): the parts of one
+// tile run concurrently.
+struct TileFlags {
+    uint32_t* done;
+    uint32_t* touched;
+    uint32_t* sub_done;
+};
+
+__device__ __forceinline__ bool part_bit(const uint32_t* bits, uint32_t tile, uint32_t part) {
+    const uint32_t b = tile * 4u + part;
+    return (bits[b >> 5] >> (b & 31)) & 1u;
+}
+
+template <int kGroup, int MINB, bool kSameRow>
+__global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
     const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
-    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, uint32_t* __restrict__ tile_done,
-    uint32_t* __restrict__ tile_touched, int first, int last, Counters* __restrict__ ctr, int want_stats,
-    const uint32_t* __restrict__ work, const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next,
-    uint32_t work_cap) {
-    // 64-B records, double-buffered (cp.async). After arrival each thread rewrites its
-    // record in place as [0] (lmx, lmy, ca, 2cb), [1] (cc, cut + guard, cut - guard,
-    // log2 op), [2] (r, g, b, gaussian index bits), and the warp-filter box into sF.
-    // Slot kBatch of each buffer is a null record (never contributes) that pads the
-    // compacted lists to whole groups.
-    constexpr int kPer = kBatch / kThreads2;
-    constexpr int kWarps = kThreads2 / 32;
+    PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, const TileFlags flags, int first, int last,
+    Counters* __restrict__ ctr, int want_stats, uint32_t* __restrict__ tile_emax, const uint32_t* __restrict__ work,
+    const uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_next, uint32_t work_cap) {
     extern __shared__ float4 k7_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpStage& S = reinterpret_cast<WarpStage*>(k7_smem)[warp];
     float* const out_rgb = fc->out_rgb;  // the frame's outputs (FrameConsts)
     float* const out_T = fc->out_T;
-    float4(*sRaw)[kBatch + 1][4] = reinterpret_cast<float4(*)[kBatch + 1][4]>(k7_smem);
-    float4* sF = k7_smem + 2 * (kBatch + 1) * 4;
-    uint16_t(*sIdx)[kBatch + 8] = reinterpret_cast<uint16_t(*)[kBatch + 8]>(sF + kBatch);
-    __shared__ unsigned long long s_red[2][kWarps];
-    __shared__ uint32_t s_item;
-
-    if (threadIdx.x < 8) {
-        const int b = threadIdx.x >> 2, c = threadIdx.x & 3;
-        sRaw[b][kBatch][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane < 8) {
+        const int b = lane >> 2, c = lane & 3;
+        S.raw[b][kWB][c] = c == 1 ? make_float4(0.f, -1.f, -2.f, -1e30f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    __syncwarp();
     uint32_t n_class[kWorkClasses], n_items = 0;
 #pragma unroll
     for (int c = 0; c < kWorkClasses; ++c) n_items += (n_class[c] = work_count[c]);
@@ -212,33 +238,32 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     // splat has alpha >= 1/255), and keeps T < stop false for a pixel that has not
     // blended anything yet.
     const float stop = cfg.early_stop > 1.0f ? 1.0f : cfg.early_stop;
+    const int nsub = kSubsPerChunk * nchunks;
+    const int ts = cfg.tile_size;
     for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(work_next, 1u);
-    __syncthreads();
-    const uint32_t item = s_item;
-    __syncthreads();
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(work_next, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
     const uint32_t witem = work_item(work, n_class, work_cap, item);
-    const int ts = cfg.tile_size;
-    const int tile = static_cast<int>(witem / nchunks);
-    const int chunk = static_cast<int>(witem - static_cast<uint32_t>(tile) * nchunks);
+    const int tile = static_cast<int>(witem / nsub);
+    const int sub = static_cast<int>(witem - static_cast<uint32_t>(tile) * nsub);
     const uint2 range = ranges[tile];
     const uint32_t start = range.x, end = range.y;
-    const bool touched = !first && ((tile_touched[tile >> 5] >> (tile & 31)) & 1u);
+    const bool touched = !first && part_bit(flags.touched, tile, sub);
     const int tx = tile % cfg.tiles_x, ty = tile / cfg.tiles_x;
     const int px0 = tx * ts, py0 = ty * ts;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int lx0, ly0, lx1, ly1;
     bool in0, in1;
     if (ts == 16) {
-        // warp w owns the 8x8 quadrant (w & 1, w >> 1): a square strip meets fewer
+        // part q is the 8x8 quadrant (q & 1, q >> 1): a square strip meets fewer
         // splat boxes per pixel than a 16x4 one
-        lx0 = (warp & 1) * 8 + (lane & 3) * 2;
+        lx0 = (sub & 1) * 8 + (lane & 3) * 2;
         lx1 = lx0 + 1;
-        ly0 = ly1 = (warp >> 1) * 8 + (lane >> 2);
+        ly0 = ly1 = (sub >> 1) * 8 + (lane >> 2);
         in0 = in1 = true;
     } else {
-        const int p = chunk * 256 + 2 * static_cast<int>(threadIdx.x);
+        const int p = sub * kSubPx + 2 * lane;
         lx0 = p % ts;
         ly0 = p / ts;
         lx1 = (p + 1) % ts;
@@ -269,35 +294,33 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
     bool live0 = v0 && !(P0.T < stop), live1 = v1 && !(P1.T < stop);
     uint32_t processed0 = live0 ? end - start : 0u, processed1 = live1 ? end - start : 0u;
     int term0 = -1, term1 = -1;  // compacted-walk position of the stopping splat in this batch
-
     uint32_t guard_hits = 0;
-    uint16_t* idx = sIdx[warp];
 
-    const int t = threadIdx.x;
-    uint32_t g_next[kPer], g_cur[kPer];
+    uint32_t g_next[2], g_cur[2];
 #pragma unroll
-    for (int h = 0; h < kPer; ++h) {
-        const uint32_t k = start + t + h * kThreads2;
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t k = start + lane + h * 32;
         g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
-        if (k < end) stage_record(rec, colour, g_next[h], sRaw[0][t + h * kThreads2]);
+        if (k < end) stage_record(rec, colour, g_next[h], S.raw[0][lane + h * 32]);
     }
     asm volatile("cp.async.commit_group;\n" ::);
 #pragma unroll
-    for (int h = 0; h < kPer; ++h) {
+    for (int h = 0; h < 2; ++h) {
         g_cur[h] = g_next[h];
-        const uint32_t k = start + kBatch + t + h * kThreads2;
+        const uint32_t k = start + kWB + lane + h * 32;
         g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
     }
     int buf = 0;
 
-    for (uint32_t base = start; base < end; base += kBatch) {
+    for (uint32_t base = start; base < end; base += kWB) {
+        if (!__any_sync(0xffffffffu, live0 || live1)) break;
         asm volatile("cp.async.wait_group 0;\n" ::);
-        if (__syncthreads_count(live0 || live1) == 0) break;
+        __syncwarp();  // every lane's records landed; the previous batch is walked
 #pragma unroll
-        for (int h = 0; h < kPer; ++h) {
-            const int rt = t + h * kThreads2;
+        for (int h = 0; h < 2; ++h) {
+            const int rt = lane + h * 32;
             if (base + rt < end) {
-                float4* r = sRaw[buf][rt];
+                float4* r = S.raw[buf][rt];
                 const double2 m = *reinterpret_cast<const double2*>(&r[0]);
                 const float4 q1 = r[1];
                 const float4 q2 = r[2];
@@ -306,20 +329,20 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
                 r[0] = make_float4(lmx, lmy, q1.x, q1.y);
                 r[1] = make_float4(q1.z, q2.x + q2.y, q2.x - q2.y, q1.w);
                 r[2] = make_float4(q3.x, q3.y, q3.z, __uint_as_float(g_cur[h]));
-                sF[rt] = make_float4(lmx, lmy, q2.z, q2.w);
+                S.box[rt] = make_float4(lmx, lmy, q2.z, q2.w);
             }
-            const uint32_t kn = base + kBatch + rt;
-            if (kn < end) stage_record(rec, colour, g_next[h], sRaw[buf ^ 1][rt]);
+            const uint32_t kn = base + kWB + rt;
+            if (kn < end) stage_record(rec, colour, g_next[h], S.raw[buf ^ 1][rt]);
             g_cur[h] = g_next[h];
-            g_next[h] = kn + kBatch < end ? __ldg(&keys[static_cast<size_t>(kn + kBatch) * kstride]) : 0u;
+            g_next[h] = kn + kWB < end ? __ldg(&keys[static_cast<size_t>(kn + kWB) * kstride]) : 0u;
         }
         asm volatile("cp.async.commit_group;\n" ::);
         buf ^= 1;
-        __syncthreads();
-        const uint32_t nb = min(static_cast<uint32_t>(kBatch), end - base);
-        const float4(*R)[4] = sRaw[buf ^ 1];
+        __syncwarp();
+        const uint32_t nb = min(static_cast<uint32_t>(kWB), end - base);
+        const float4(*R)[4] = S.raw[buf ^ 1];
         int cnt = 0;
-        if (__any_sync(0xffffffffu, live0 || live1)) {
+        {
             // the warp's live-pixel box, shrinking as its pixels stop
             float wx0 = 1e30f, wx1 = -1e30f, wy0 = 1e30f, wy1 = -1e30f;
             if (live0) wx0 = fminf(wx0, fcx0), wx1 = fmaxf(wx1, fcx0), wy0 = fminf(wy0, fcy0), wy1 = fmaxf(wy1, fcy0);
@@ -331,20 +354,22 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
                 wy0 = fminf(wy0, __shfl_xor_sync(0xffffffffu, wy0, o));
                 wy1 = fmaxf(wy1, __shfl_xor_sync(0xffffffffu, wy1, o));
             }
-            for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+#pragma unroll
+            for (uint32_t j0 = 0; j0 < kWB; j0 += 32) {
                 const uint32_t j = j0 + lane;
                 bool hit = false;
                 if (j < nb) {
-                    const float4 F = sF[j];
+                    const float4 F = S.box[j];
                     hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit) idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
+                if (hit) S.idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
                 cnt += __popc(m);
             }
         }
-        if (lane < kGroup) idx[cnt + lane] = kBatch;
+        if (lane < kGroup) S.idx[cnt + lane] = kWB;
         __syncwarp();
+        const uint16_t* idx = S.idx;
         // Fast groups until one holds a pair inside the guard band; that group is
         // walked by the cold path below (outside the fast loop, so the FP64 call does
         // not weigh on the fast loop's registers), then the fast loop resumes.
@@ -435,12 +460,11 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
             processed1 = base + idx[term1] + 1 - start;
             term1 = -2;
         }
-        // (no barrier here: the next iteration's first barrier is reached by every
-        // warp only after this walk, before anything overwrites the buffer it read)
     }
 
     asm volatile("cp.async.wait_all;\n" ::);
-    const bool all_done = __syncthreads_and(!live0 && !live1) != 0;
+    __syncwarp();  // (the next item restages buffer 0)
+    const bool all_done = !__any_sync(0xffffffffu, live0 || live1);
     const bool finalize = last || all_done;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -460,8 +484,21 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
             processed_io[pix] = (e ? walked1 : walked0) + (e ? processed1 : processed0);
         }
     }
-    if (!last && all_done && threadIdx.x == 0) atomicOr(&tile_done[tile >> 5], 1u << (tile & 31));
-    if (!finalize && !touched && threadIdx.x == 0) atomicOr(&tile_touched[tile >> 5], 1u << (tile & 31));
+    if (lane == 0) {
+        if (!last && all_done) {
+            // this part is final; the tile is finished once all its parts are
+            const uint32_t b = static_cast<uint32_t>(tile) * 4u + static_cast<uint32_t>(sub);
+            const uint32_t old = atomicOr(&flags.sub_done[b >> 5], 1u << (b & 31));
+            const int parts = min(4, (ts * ts + kSubPx - 1) / kSubPx);
+            const uint32_t need = (1u << parts) - 1u, sh = (static_cast<uint32_t>(tile) * 4u) & 31u;
+            const uint32_t before = (old >> sh) & need, after = ((old | (1u << (b & 31))) >> sh) & need;
+            if (after == need && before != need) atomicOr(&flags.done[tile >> 5], 1u << (tile & 31));
+        }
+        if (!finalize && !touched) {
+            const uint32_t b = static_cast<uint32_t>(tile) * 4u + static_cast<uint32_t>(sub);
+            atomicOr(&flags.touched[b >> 5], 1u << (b & 31));
+        }
+    }
     if (want_stats) {
         unsigned long long e = 0;
         if (finalize && v0) e = max(e, static_cast<unsigned long long>(walked0 + processed0));
@@ -473,52 +510,58 @@ __global__ void __launch_bounds__(kThreads2, MINB) composite2_kernel(
             h += __shfl_xor_sync(0xffffffffu, h, o);
         }
         if (lane == 0) {
-            s_red[0][warp] = e;
-            s_red[1][warp] = h;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long em = 0, hs = 0;
-            for (int w = 0; w < kWarps; ++w) {
-                em = max(em, s_red[0][w]);
-                hs += s_red[1][w];
-            }
-            if (em) atomicAdd(&ctr->block_entries, em);
-            if (hs) atomicAdd(&ctr->guard_hits, hs);
+            // E_t counts the deepest entry of each (tile, 256-pixel chunk)
+            if (e) atomicMax(&tile_emax[static_cast<size_t>(tile) * nchunks + sub / kSubsPerChunk],
+                             static_cast<uint32_t>(e));
+            if (h) atomicAdd(&ctr->guard_hits, h);
         }
     }
-    __syncthreads();
     }  // persistent loop
     // background-only items (tiles that never received an entry): T = 1, rgb = bg
-    write_background<kThreads2>(W, H, cfg, nchunks, work_count, out_rgb, out_T, bg);
+    write_background<kThreads>(W, H, cfg, nchunks, work_count, out_rgb, out_T, bg);
 }
 
 // Work buffer: kWorkClasses regions of cap items, one per list-length class (the
-// persistent CTAs take the longest lists first); then kWorkCtl control words (the
+// persistent warps take the longest lists first); then kWorkCtl control words (the
 // class counts, the compositor's cursor [6], the background count [7]); then the
-// background-only items.
-// Work list of a depth chunk: (tile, pixel chunk) items that still need K7 -- every
-// unfinished tile in the last chunk (it writes the final pixels), otherwise only
-// tiles with entries in this chunk. Tiles with long lists are queued from the front
-// of `work`, the rest from the back, so the persistent CTAs start on the longest.
-__global__ void build_work_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ tile_done,
-                                  const uint32_t* __restrict__ tile_touched, int first, int last, uint32_t ntile,
-                                  int nchunks, uint32_t cap, uint32_t* __restrict__ work,
+// background-only (tile, pixel chunk) items.
+// Work list of a depth chunk: (tile, 64-pixel part) items that still need K7 -- every
+// unfinished part in the last chunk (it writes the final pixels), otherwise only
+// parts of tiles with entries in this chunk.
+__global__ void build_work_kernel(const uint2* __restrict__ ranges, const TileFlags flags, int first, int last,
+                                  uint32_t ntile, int nchunks, int tile_px, uint32_t cap, uint32_t* __restrict__ work,
                                   uint32_t* __restrict__ wctl) {
+    const uint32_t nsub = static_cast<uint32_t>(kSubsPerChunk * nchunks);
     const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= ntile * static_cast<uint32_t>(nchunks)) return;
-    const uint32_t tile = it / nchunks;
-    if (!first && ((tile_done[tile >> 5] >> (tile & 31)) & 1u)) return;
+    if (it >= ntile * nsub) return;
+    const uint32_t tile = it / nsub, sub = it - tile * nsub;
+    if (static_cast<int>(sub) * kSubPx >= tile_px) return;  // a part without pixels
+    // (a later depth chunk: at most 4 parts per tile)
+    if (!first && ((flags.done[tile >> 5] >> (tile & 31)) & 1u)) return;
+    if (!first && part_bit(flags.sub_done, tile, sub)) return;  // final already
     const uint2 r = ranges[tile];
     const uint32_t len = r.y - r.x;
     if (!last && len == 0) return;
-    if (len == 0 && (first || !((tile_touched[tile >> 5] >> (tile & 31)) & 1u))) {
-        // never received an entry: background pixels, written by the tail loop
-        wctl[kWorkCtl + atomicAdd(&wctl[7], 1u)] = it;
+    // A part that is neither final nor touched was never composited: then no part of
+    // the tile was (all parts of a tile are queued in the same chunks, and each ends
+    // final or touched), and without entries the tile is background.
+    if (len == 0 && (first || !part_bit(flags.touched, tile, sub))) {
+        // never received an entry: background pixels, written by the tail loop (one
+        // item per 256-pixel chunk)
+        if (sub % kSubsPerChunk == 0) wctl[kWorkCtl + atomicAdd(&wctl[7], 1u)] = tile * nchunks + sub / kSubsPerChunk;
         return;
     }
     const int c = work_class(len);
     work[static_cast<size_t>(c) * cap + atomicAdd(&wctl[c], 1u)] = it;
+}
+
+// Stats frames: E_t = the sum of the per-(tile, chunk) deepest entries.
+__global__ void emax_sum_kernel(const uint32_t* __restrict__ emax, uint32_t n, Counters* __restrict__ ctr) {
+    unsigned long long s = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s += emax[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(&ctr->block_entries, s);
 }
 
 }  // namespace
@@ -528,27 +571,24 @@ int composite_pixel_chunks(int ts) {
     return static_cast<int>((tile_px + kChunkPx - 1) / kChunkPx);
 }
 
-namespace {
-constexpr size_t k7_smem_bytes(int batch) {
-    return static_cast<size_t>(2 * (batch + 1) * 4 + batch) * sizeof(float4) +
-           static_cast<size_t>(kThreads2 / 32) * (batch + 8) * sizeof(uint16_t);
-}
+int composite_work_items(int ts) { return kSubsPerChunk * composite_pixel_chunks(ts); }
 
-template <int G, int M, bool ROW, int B>
+namespace {
+template <int G, int M, bool ROW>
 cudaError_t launch_k7(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg, int nchunks,
                       const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
-                      const float4* colour, float3 bg, PixelState* state, uint32_t* processed, uint32_t* tile_done,
-                      uint32_t* tile_touched, bool first, bool last, Counters* counters, bool want_stats,
-                      uint32_t* work, uint32_t* wctl, uint32_t cap, cudaStream_t stream) {
-    constexpr size_t smem = k7_smem_bytes(B);
-    static const cudaError_t attr = cudaFuncSetAttribute(composite2_kernel<G, M, ROW, B>,
+                      const float4* colour, float3 bg, PixelState* state, uint32_t* processed, const TileFlags& flags,
+                      bool first, bool last, Counters* counters, bool want_stats, uint32_t* emax, uint32_t* work,
+                      uint32_t* wctl, uint32_t cap, cudaStream_t stream) {
+    constexpr size_t smem = (kThreads / 32) * sizeof(WarpStage);
+    static const cudaError_t attr = cudaFuncSetAttribute(composite_kernel<G, M, ROW>,
                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
-    // persistent grid: M resident CTAs of 128 threads per SM
-    composite2_kernel<G, M, ROW, B><<<148u * M, kThreads2, smem, stream>>>(
-        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed, tile_done,
-        tile_touched, first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, work, wctl, wctl + 6, cap);
+    // persistent grid: M resident CTAs of four warps per SM
+    composite_kernel<G, M, ROW><<<148u * M, kThreads, smem, stream>>>(
+        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed, flags,
+        first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, emax, work, wctl, wctl + 6, cap);
     return cudaGetLastError();
 }
 }  // namespace
@@ -556,25 +596,35 @@ cudaError_t launch_k7(const FrameConsts* fc, const CamParams& cam, const CfgPara
 cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                              const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
                              const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
-                             uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
-                             bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream) {
+                             uint32_t* tile_flags, bool first, bool last, Counters* counters, bool want_stats,
+                             uint32_t* tile_emax, uint32_t* work, uint32_t* wctl, cudaStream_t stream) {
     const int nchunks = composite_pixel_chunks(cfg.tile_size);
     const uint32_t ntile = static_cast<uint32_t>(cfg.tiles_x) * static_cast<uint32_t>(cfg.tiles_y);
-    const uint32_t cap = ntile * static_cast<uint32_t>(nchunks);
+    const uint32_t cap = ntile * static_cast<uint32_t>(composite_work_items(cfg.tile_size));
+    const uint32_t words = (ntile + 31) / 32;
+    const uint32_t part_words = (4 * ntile + 31) / 32;
+    const TileFlags flags{tile_flags, tile_flags + words, tile_flags + words + part_words};
     cudaError_t e = cudaMemsetAsync(wctl, 0, kWorkCtl * sizeof(uint32_t), stream);
     if (e != cudaSuccess) return e;
-    build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, tile_done, tile_touched, first ? 1 : 0,
-                                                             last ? 1 : 0, ntile, nchunks, cap, work, wctl);
-    // Measured alternatives (SURVEY-C 32-view batch, ms/frame): 5 or 6 CTAs per SM with
-    // 128-record batches 0.595 / 0.588, 2-record groups at 4 or 6 CTAs 0.610 / 0.605,
-    // 8 CTAs (64 registers, spills) 0.618 -- against 0.592 for this default.
+    if (want_stats && first) {
+        e = cudaMemsetAsync(tile_emax, 0, static_cast<size_t>(ntile) * nchunks * sizeof(uint32_t), stream);
+        if (e != cudaSuccess) return e;
+    }
+    build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, flags, first ? 1 : 0, last ? 1 : 0, ntile,
+                                                             nchunks, cfg.tile_size * cfg.tile_size, cap, work, wctl);
     if (cfg.tile_size == 16)
-        return launch_k7<4, 4, true, 256>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,
-                                          processed, tile_done, tile_touched, first, last, counters, want_stats,
-                                          work, wctl, cap, stream);
-    return launch_k7<4, 4, false, 256>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state,
-                                       processed, tile_done, tile_touched, first, last, counters, want_stats, work,
-                                       wctl, cap, stream);
+        e = launch_k7<4, 4, true>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,
+                                  flags, first, last, counters, want_stats, tile_emax, work, wctl, cap, stream);
+    else
+        e = launch_k7<4, 4, false>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,
+                                   flags, first, last, counters, want_stats, tile_emax, work, wctl, cap, stream);
+    if (e != cudaSuccess) return e;
+    if (want_stats && last)
+        emax_sum_kernel<<<64, 256, 0, stream>>>(tile_emax, ntile * static_cast<uint32_t>(nchunks), counters);
+    return cudaGetLastError();
 }
+
+// words of the per-tile flag block launch_composite reads (done | touched | part-done)
+size_t composite_flag_words(uint32_t ntile) { return (ntile + 31) / 32 + 2 * ((4 * static_cast<size_t>(ntile) + 31) / 32); }
 
 }  // namespace sgs

@@ -254,8 +254,11 @@ void launch_tile_ranges(const unsigned long long* d_count, const uint32_t* tiles
 cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
                              const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
                              const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
-                             uint32_t* tile_done, uint32_t* tile_touched, bool first, bool last, Counters* counters,
-                             bool want_stats, uint32_t* work, uint32_t* wctl, cudaStream_t stream);
+                             uint32_t* tile_flags, bool first, bool last, Counters* counters, bool want_stats,
+                             uint32_t* tile_emax, uint32_t* work, uint32_t* wctl, cudaStream_t stream);
+// K7 work items per tile (64-pixel parts) and the per-tile flag block's size in words
+int composite_work_items(int tile_size);
+size_t composite_flag_words(uint32_t ntile);
 int composite_pixel_chunks(int tile_size);
 
 // capi.cu helpers for group.cu: the last-error text, a context's device and render
