@@ -165,19 +165,18 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
         area = m.y;
         rc = brect[r];
     }
-    const uint32_t w = static_cast<uint32_t>(rc.y - rc.x + 1);
     if (area && area <= kCoop) {
-        uint32_t o = 0;
-        for (uint32_t j = 0; j < area; ++j) {
-            const uint32_t tile = static_cast<uint32_t>(rc.z + static_cast<int>(j / w)) * tiles_x +
-                                  static_cast<uint32_t>(rc.x + static_cast<int>(j % w));
-            if (done(tile)) continue;
-            if (off + o < capacity) {
-                tk[off + o] = tile;
-                tv[off + o] = g;
+        unsigned long long o = off;
+        for (int ty = rc.z; ty <= rc.w; ++ty)
+            for (int tx = rc.x; tx <= rc.y; ++tx) {
+                const uint32_t tile = static_cast<uint32_t>(ty * tiles_x + tx);
+                if (done(tile)) continue;
+                if (o < capacity) {
+                    tk[o] = tile;
+                    tv[o] = g;
+                }
+                ++o;
             }
-            ++o;
-        }
     }
     unsigned big = __ballot_sync(0xffffffffu, area > kCoop);
     while (big) {
