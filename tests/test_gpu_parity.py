@@ -215,9 +215,12 @@ def test_device_output_and_stats(renderer):
         ds.free()
 
 
-def test_depth_chunking_is_bitwise_neutral():
-    """Termination-aware binning (two depth chunks, finished tiles skip the second)
-    must not change a single bit of the image, the transmittance or E_t."""
+@pytest.mark.parametrize("ts", [16, 13, 8])
+def test_depth_chunking_is_bitwise_neutral(ts):
+    """Termination-aware binning (depth chunks, finished tiles skip the later ones)
+    must not change a single bit of the image, the transmittance or E_t -- also on
+    tiles of three parts (13: the compositor's 64-pixel parts, the last one partial)
+    and of one (8)."""
     scene = sg.synth_scene(200_000, "mixed", 77, log_scale_range=(-5.0, -3.5))
     cams = sg.orbit_cameras(3, 480, 270, 4.0, 324.0)
     os.environ["SGS_DEPTH_CHUNKING"] = "0"
@@ -233,11 +236,17 @@ def test_depth_chunking_is_bitwise_neutral():
     a_ds, b_ds = plain.upload(scene), chunked.upload(scene)
     try:
         for cam in cams:
-            a = plain.render(a_ds, cam, degree_override=1, stats=True)
-            b = chunked.render(b_ds, cam, degree_override=1, stats=True)
+            a = plain.render(a_ds, cam, tile_size=ts, degree_override=1, stats=True)
+            b = chunked.render(b_ds, cam, tile_size=ts, degree_override=1, stats=True)
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
             assert a[2].block_entries == b[2].block_entries
             assert b[2].tile_entries < a[2].tile_entries  # finished tiles skipped
+            # and the stats-free render path (tight rectangles, frame graphs)
+            for _ in range(3):
+                c = plain.render(a_ds, cam, tile_size=ts, degree_override=1)
+                d = chunked.render(b_ds, cam, tile_size=ts, degree_override=1)
+                assert np.array_equal(c[0], a[0]) and np.array_equal(d[0], a[0])
+                assert np.array_equal(c[1], a[1]) and np.array_equal(d[1], a[1])
     finally:
         a_ds.free()
         b_ds.free()
