@@ -298,6 +298,14 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
             if (t.joinable()) t.join();
         }
     } join_alloc{alloc};
+    // the result images (66 MB at 1080p, zeroed by their constructor: page faults and
+    // stores on one core) are allocated while the rows are packed and cross PCIe; an
+    // invalid size is left to cam.validate() below
+    if (cam.width >= 1 && cam.height >= 1)
+        alloc = std::thread([&] {
+            out.image = Image(cam.width, cam.height, 3);
+            out.transmittance = Image(cam.width, cam.height, 1);
+        });
     sgs_scene* dscene = nullptr;
     const std::vector<GaussianPrimitive>& gs = scene.gaussians;
     const std::size_t stride = gs.empty() ? 0 : kGeometryParams + param_count(gs.front().color);
@@ -310,12 +318,6 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
         cam.validate();
         t1 = now();
         if (fast) {
-            // the result images (66 MB at 1080p, zeroed by their constructor) are
-            // allocated while the rows cross PCIe
-            alloc = std::thread([&] {
-                out.image = Image(cam.width, cam.height, 3);
-                out.transmittance = Image(cam.width, cam.height, 1);
-            });
             sgs_scene_desc d{};
             d.count = gs.size();
             d.kind = static_cast<int32_t>(kind_of(gs.front().color));
