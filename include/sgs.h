@@ -177,6 +177,17 @@ sgs_status sgs_scene_refresh(sgs_context* ctx, sgs_scene* scene);
  * addresses do not change, so captured frame graphs stay valid. A different layout
  * is SGS_ERR_INVALID_ARGUMENT (upload a new scene). */
 sgs_status sgs_scene_update(sgs_context* ctx, sgs_scene* scene, const sgs_scene_desc* desc);
+/* sgs_scene_update with the float32 rows produced block by block, so packing them
+ * overlaps their copy to the device: fill(user, rows, first, count) writes rows
+ * [first, first + count) -- 11 + colour-parameter floats each, Scene::param order --
+ * into a pinned staging block the library owns, which is copied while the caller fills
+ * the next one. desc->dtype must be SGS_F32; desc->params is not read. A nonzero
+ * return from fill ends the call with SGS_ERR_INVALID_ARGUMENT before the scene is
+ * touched (it keeps its previous contents). The C++ drop-in's render() feeds it from
+ * the caller's Scene. */
+typedef int32_t (*sgs_row_fill_fn)(void* user, float* rows, uint64_t first, uint64_t count);
+sgs_status sgs_scene_update_rows(sgs_context* ctx, sgs_scene* scene, const sgs_scene_desc* desc,
+                                 sgs_row_fill_fn fill, void* user);
 sgs_status sgs_scene_get_meta(const sgs_scene* scene, sgs_scene_meta* meta);
 sgs_status sgs_scene_blob(const sgs_scene* scene, void** device_blob, uint64_t* bytes);
 sgs_status sgs_scene_set_background(sgs_scene* scene, const double* rgb);

@@ -324,6 +324,27 @@ class DeviceScene:
         _check(_lib().sgs_scene_update(self._r.handle, self.handle, ctypes.byref(d)))
         del keep
 
+    def update_rows(self, scene: "Scene", fill=None):
+        """update() through sgs_scene_update_rows: float32 rows produced block by block
+        (each block copied to the device while the next is filled). fill(first, count)
+        returns the rows [first, first + count) as float32 (count, stride), or None to
+        abort (the scene then keeps its contents); by default they come from `scene`."""
+        d, _ = scene._desc(True)
+        d.params = None
+        stride = 11 + param_count(scene.kind, scene.sh_degree)
+        src = np.asarray(scene.params)
+
+        def produce(_user, rows, first, count):
+            blk = src[first:first + count].astype(np.float32) if fill is None else fill(first, count)
+            if blk is None:
+                return 1
+            blk = np.ascontiguousarray(blk, dtype=np.float32).reshape(count, stride)
+            ctypes.memmove(rows, blk.ctypes.data, blk.nbytes)
+            return 0
+
+        cb = C.ROW_FILL(produce)
+        _check(_lib().sgs_scene_update_rows(self._r.handle, self.handle, ctypes.byref(d), cb, None))
+
     def set_background(self, rgb):
         bg = np.ascontiguousarray(rgb, dtype=np.float64)
         _check(_lib().sgs_scene_set_background(self.handle, bg.ctypes.data))

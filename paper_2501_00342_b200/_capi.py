@@ -125,6 +125,8 @@ class sgs_splat(ctypes.Structure):
 
 _P = ctypes.c_void_p
 _S = ctypes.c_int  # sgs_status
+# sgs_row_fill_fn: int32 fill(void* user, float* rows, uint64 first, uint64 count)
+ROW_FILL = ctypes.CFUNCTYPE(ctypes.c_int32, _P, ctypes.POINTER(ctypes.c_float), ctypes.c_uint64, ctypes.c_uint64)
 
 # name -> (restype, argtypes); the full list of entry points declared in include/sgs.h
 SIGNATURES = {
@@ -144,6 +146,7 @@ SIGNATURES = {
                             ctypes.POINTER(_P)]),
     "sgs_scene_refresh": (_S, [_P, _P]),
     "sgs_scene_update": (_S, [_P, _P, ctypes.POINTER(sgs_scene_desc)]),
+    "sgs_scene_update_rows": (_S, [_P, _P, ctypes.POINTER(sgs_scene_desc), ROW_FILL, _P]),
     "sgs_scene_get_meta": (_S, [_P, ctypes.POINTER(sgs_scene_meta)]),
     "sgs_scene_blob": (_S, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_uint64)]),
     "sgs_scene_set_background": (_S, [_P, _P]),

@@ -204,6 +204,11 @@ struct sgs_context {
     std::vector<TraceRec> trace_recs;
     DevBuf metrics;  // PSNR / SSIM scratch (inputs staged from host, maps, partial sums)
     DevBuf rows;     // float32 scene rows of an SGS_F32 upload (grow-only)
+    // sgs_scene_update_rows: two pinned staging blocks (filled by the caller while the
+    // other crosses PCIe) and the copy-done events
+    void* stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     DevBuf bwd;      // backward scratch (FP64 splats, ranks, per-entry partials, staging)
     uint64_t own_launches = 0, lib_launches = 0;
 };
@@ -1081,7 +1086,18 @@ std::vector<int32_t> ply_slot_table(const PlyTable& t, int color_planes, int* mu
 // An SGS_F32 description's rows (count x (11 + colour params) floats, Scene::param
 // order) into the planes of blob: one copy of the rows, then ply_rows_kernel with the
 // identity column map (SG1 lobe axes normalised in FP64 as at every upload).
+cudaError_t rows_to_planes(sgs_context* ctx, const sgs_scene_meta& m, void* blob);
+
 cudaError_t upload_rows_f32(sgs_context* ctx, const sgs_scene_desc* desc, const sgs_scene_meta& m, void* blob) {
+    const size_t nfloat = static_cast<size_t>(m.count) * static_cast<size_t>(11 + color_param_count_impl(m.kind, m.sh_degree));
+    cudaError_t e = ctx->rows.ensure(nfloat * sizeof(float));
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->rows.ptr, desc->params, nfloat * sizeof(float), cudaMemcpyHostToDevice, ctx->stream);
+    return e == cudaSuccess ? rows_to_planes(ctx, m, blob) : e;
+}
+
+// The float32 rows in ctx->rows into the planes of blob.
+cudaError_t rows_to_planes(sgs_context* ctx, const sgs_scene_meta& m, void* blob) {
     PlyTable t;
     t.count = m.count;
     t.info.kind = m.kind;
@@ -1092,14 +1108,11 @@ cudaError_t upload_rows_f32(sgs_context* ctx, const sgs_scene_desc* desc, const 
     const Layout L = make_layout(m);
     int mu_col = -1;
     const std::vector<int32_t> tab = ply_slot_table(t, L.color_planes, &mu_col);
-    const size_t nfloat = static_cast<size_t>(m.count) * static_cast<size_t>(stride);
     DevBuf& d_rows = ctx->rows;
     DevBuf d_tab;
     cudaStream_t s = ctx->stream;
-    cudaError_t e = d_rows.ensure(nfloat * sizeof(float));
-    if (e == cudaSuccess) e = d_tab.ensure(tab.size() * sizeof(int32_t));
+    cudaError_t e = d_tab.ensure(tab.size() * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMemsetAsync(blob, 0, m.blob_bytes, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_rows.ptr, desc->params, nfloat * sizeof(float), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) {
@@ -1241,6 +1254,10 @@ void sgs_destroy(sgs_context* ctx) {
     }
     ctx->metrics.release();
     ctx->rows.release();
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->stage[b]) cudaFreeHost(ctx->stage[b]);
+        if (ctx->stage_ev[b]) cudaEventDestroy(ctx->stage_ev[b]);
+    }
     ctx->bwd.release();
     if (ctx->h_ctr_init) cudaFreeHost(ctx->h_ctr_init);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -1419,6 +1436,62 @@ sgs_status sgs_scene_update(sgs_context* ctx, sgs_scene* scene, const sgs_scene_
     if (e != cudaSuccess) return fail(SGS_ERR_CUDA, std::string("scene update: ") + cudaGetErrorString(e));
     scene->meta = m;  // (axes and background may change)
     return bind_and_cache(scene, ctx->stream);
+}
+
+sgs_status sgs_scene_update_rows(sgs_context* ctx, sgs_scene* scene, const sgs_scene_desc* desc,
+                                 sgs_row_fill_fn fill, void* user) {
+    if (!ctx || !scene || !desc || !fill) return fail(SGS_ERR_INVALID_ARGUMENT, "null argument");
+    if (desc->dtype != SGS_F32) return fail(SGS_ERR_INVALID_ARGUMENT, "streamed rows are float32 (SGS_F32)");
+    sgs_scene_desc d = *desc;
+    float unused = 0.0f;
+    if (!d.params) d.params = &unused;  // (the rows come from fill)
+    sgs_scene_meta m{};
+    sgs_status st = sgs_scene_plan(&d, &m);
+    if (st != SGS_OK) return st;
+    const sgs_scene_meta& o = scene->meta;
+    if (m.count != o.count || m.kind != o.kind || m.sh_degree != o.sh_degree || m.geometry_f64 != o.geometry_f64 ||
+        m.color_f64 != o.color_f64 || m.blob_bytes != o.blob_bytes)
+        return fail(SGS_ERR_INVALID_ARGUMENT, "scene update changes the device layout");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    SGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const uint64_t stride = 11 + static_cast<uint64_t>(color_param_count_impl(m.kind, m.sh_degree));
+    if (m.count) {
+        // ~64 MB blocks: a few fills per scene, each copy hidden behind the next fill
+        constexpr size_t kBlockBytes = size_t{64} << 20;
+        const uint64_t per = std::max<uint64_t>(1, kBlockBytes / (stride * sizeof(float)));
+        const size_t block_bytes = static_cast<size_t>(std::min<uint64_t>(per, m.count) * stride * sizeof(float));
+        if (ctx->stage_bytes < block_bytes) {
+            for (int b = 0; b < 2; ++b) {
+                if (ctx->stage[b]) SGS_CUDA(cudaFreeHost(ctx->stage[b]));
+                ctx->stage[b] = nullptr;
+            }
+            ctx->stage_bytes = 0;
+            for (int b = 0; b < 2; ++b) SGS_CUDA(cudaHostAlloc(&ctx->stage[b], block_bytes, cudaHostAllocDefault));
+            ctx->stage_bytes = block_bytes;
+        }
+        for (int b = 0; b < 2; ++b)
+            if (!ctx->stage_ev[b]) SGS_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[b], cudaEventDisableTiming));
+        SGS_CUDA(ctx->rows.ensure(m.count * stride * sizeof(float)));
+        float* d_rows = ctx->rows.as<float>();
+        uint64_t k = 0;
+        for (uint64_t first = 0; first < m.count; first += per, ++k) {
+            const uint64_t cnt = std::min<uint64_t>(per, m.count - first);
+            float* buf = static_cast<float*>(ctx->stage[k & 1]);
+            if (k >= 2) SGS_CUDA(cudaEventSynchronize(ctx->stage_ev[k & 1]));  // its previous copy left
+            if (fill(user, buf, first, cnt) != 0) {
+                SGS_CUDA(cudaStreamSynchronize(s));  // (the scene's blob was not touched)
+                return fail(SGS_ERR_INVALID_ARGUMENT, "scene update aborted by the row producer");
+            }
+            SGS_CUDA(cudaMemcpyAsync(d_rows + first * stride, buf, cnt * stride * sizeof(float),
+                                     cudaMemcpyHostToDevice, s));
+            SGS_CUDA(cudaEventRecord(ctx->stage_ev[k & 1], s));
+        }
+        const cudaError_t e = rows_to_planes(ctx, m, scene->blob);
+        if (e != cudaSuccess) return fail(SGS_ERR_CUDA, std::string("scene update: ") + cudaGetErrorString(e));
+    }
+    scene->meta = m;  // (axes and background may change)
+    return bind_and_cache(scene, s);
 }
 
 sgs_status sgs_scene_get_meta(const sgs_scene* scene, sgs_scene_meta* meta) {

@@ -201,14 +201,15 @@ bool f32_exact(double v) { return static_cast<double>(static_cast<float>(v)) == 
 // parameter is not f32-exact (the caller then takes the float64 path). *mixed: some
 // Gaussian's colour model or stored degree differs from the first one's
 // (Scene::check_homogeneous then raises the reference's error).
-bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride, float* rows, bool* mixed) {
+bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t first, std::size_t count,
+                   std::size_t stride, float* rows, bool* mixed) {
     std::atomic<bool> exact{true}, hetero{false};
     const ColorModelKind kind0 = kind_of(gs.front().color);
     const int deg0 = stored_degree(gs.front().color);
-    parallel_for(gs.size(), [&](std::size_t b, std::size_t e) {
+    parallel_for(count, [&](std::size_t b, std::size_t e) {
         std::vector<double> c(stride - kGeometryParams);
         bool ok = true;
-        for (std::size_t i = b; i < e && ok; ++i) {
+        for (std::size_t i = first + b; i < first + e && ok; ++i) {
             const GaussianPrimitive& g = gs[i];
             if (kind_of(g.color) != kind0 || stored_degree(g.color) != deg0) {
                 hetero.store(true);
@@ -221,7 +222,7 @@ bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride,
             for (int k = 0; k < 3; ++k) p[7 + k] = g.log_scale[k];
             p[10] = g.opacity_logit;
             pack_color(g.color, c.data());
-            float* r = rows + i * stride;
+            float* r = rows + (i - first) * stride;
             for (int k = 0; k < kGeometryParams; ++k) {
                 ok = ok && f32_exact(p[k]);
                 r[k] = static_cast<float>(p[k]);
@@ -236,6 +237,22 @@ bool pack_rows_f32(const std::vector<GaussianPrimitive>& gs, std::size_t stride,
     *mixed = hetero.load();
     return exact.load();
 }
+
+// sgs_scene_update_rows' row producer: packs the caller's Scene block by block while
+// the library copies the previous block to the device.
+struct RowFill {
+    const std::vector<GaussianPrimitive>* gs;
+    std::size_t stride;
+    bool mixed = false, inexact = false;
+    static int32_t call(void* user, float* rows, uint64_t first, uint64_t count) {
+        RowFill& f = *static_cast<RowFill*>(user);
+        bool mixed = false;
+        const bool exact = pack_rows_f32(*f.gs, first, count, f.stride, rows, &mixed);
+        f.mixed = f.mixed || mixed;
+        f.inexact = f.inexact || !exact;
+        return mixed || !exact ? 1 : 0;
+    }
+};
 
 }  // namespace
 
@@ -311,27 +328,41 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
     const std::size_t stride = gs.empty() ? 0 : kGeometryParams + param_count(gs.front().color);
     bool fast = !gs.empty();
     if (fast) {
-        float* rows = static_cast<float*>(g_rows.get(gs.size() * stride * sizeof(float)));
-        bool mixed = false;
-        fast = pack_rows_f32(gs, stride, rows, &mixed);
-        if (mixed) scene.check_homogeneous();  // throws the reference's InvalidArgument
-        cam.validate();
-        t1 = now();
-        if (fast) {
-            sgs_scene_desc d{};
-            d.count = gs.size();
-            d.kind = static_cast<int32_t>(kind_of(gs.front().color));
-            d.sh_degree = stored_degree(gs.front().color);
-            d.dtype = SGS_F32;
-            d.params = rows;
-            for (int r = 0; r < 3; ++r)
-                for (int c2 = 0; c2 < 3; ++c2) d.shared_axes[r * 3 + c2] = scene.shared_axes(r, c2);
-            for (int c2 = 0; c2 < 3; ++c2) d.background[c2] = scene.background[c2];
-            if (!(g_scene && sgs_scene_update(context(), g_scene, &d) == SGS_OK)) {
+        sgs_scene_desc d{};
+        d.count = gs.size();
+        d.kind = static_cast<int32_t>(kind_of(gs.front().color));
+        d.sh_degree = stored_degree(gs.front().color);
+        d.dtype = SGS_F32;
+        for (int r = 0; r < 3; ++r)
+            for (int c2 = 0; c2 < 3; ++c2) d.shared_axes[r * 3 + c2] = scene.shared_axes(r, c2);
+        for (int c2 = 0; c2 < 3; ++c2) d.background[c2] = scene.background[c2];
+        bool streamed = false;
+        if (g_scene) {
+            // the resident scene takes the new rows in place, packed block by block
+            // while the previous block crosses PCIe
+            RowFill f{&gs, stride};
+            const sgs_status st = sgs_scene_update_rows(context(), g_scene, &d, &RowFill::call, &f);
+            if (f.mixed) scene.check_homogeneous();  // throws the reference's InvalidArgument
+            streamed = st == SGS_OK;
+            if (f.inexact) fast = false;  // (g_scene kept its contents) the float64 path
+            // otherwise a different layout: packed and uploaded below as a new scene
+        }
+        if (fast && !streamed) {
+            float* rows = static_cast<float*>(g_rows.get(gs.size() * stride * sizeof(float)));
+            bool mixed = false;
+            fast = pack_rows_f32(gs, 0, gs.size(), stride, rows, &mixed);
+            if (mixed) scene.check_homogeneous();
+            if (fast) {
+                cam.validate();  // (before the upload, as the reference checks it first)
+                d.params = rows;
                 sgs_scene_free(g_scene);
                 g_scene = nullptr;
                 check(sgs_scene_upload(context(), &d, &g_scene));
             }
+        }
+        t1 = now();
+        if (fast) {
+            cam.validate();
             dscene = g_scene;
         }
     }
@@ -377,7 +408,7 @@ RenderResult render(const Scene& scene, const Camera& cam, const RenderConfig& c
         }
     });
     if (trace)
-        std::fprintf(stderr, "dropin: pack %.2f upload %.2f image-alloc %.2f render %.2f widen %.2f ms\n",
+        std::fprintf(stderr, "dropin: scene (pack + upload) %.2f tail %.2f image-wait %.2f render %.2f widen %.2f ms\n",
                      ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, now()));
     return out;
 }

@@ -791,6 +791,47 @@ def test_scene_refresh_and_update():
         d.free()
 
 
+def test_scene_update_rows_streamed():
+    """sgs_scene_update_rows (float32 rows packed block by block while the previous
+    block crosses PCIe; the C++ drop-in's render() path): several blocks land exactly
+    as sgs_scene_update's; a producer that aborts mid-way leaves the scene as it was;
+    a different layout is refused before the producer runs."""
+    a = sg.synth_scene(1_200_000, "mixed", 511, log_scale_range=(-5.0, -3.5))  # > 2 blocks of 64 MB
+    b = sg.synth_scene(1_200_000, "mixed", 512, log_scale_range=(-5.0, -3.5))
+    cams = sg.orbit_cameras(3, 320, 200, 4.0, 240.0)
+    r = sg.Renderer(0)
+    fresh_b = r.upload(b, f32=True)
+    want_b = r.render_batch(fresh_b, cams, degree_override=1)
+    up = r.upload(a, f32=True)
+    want_a = r.render_batch(up, cams, degree_override=1)
+    for _ in range(2):
+        r.render_batch(up, cams, degree_override=1)  # graphs captured on these planes
+    calls = []
+
+    def fill_b(first, count):
+        calls.append((first, count))
+        return b.params[first:first + count].astype(np.float32)
+
+    up.update_rows(b, fill_b)
+    assert len(calls) >= 3 and calls[0][0] == 0 and sum(c for _, c in calls) == 1_200_000
+    got = r.render_batch(up, cams, degree_override=1)
+    assert np.array_equal(got[0], want_b[0]) and np.array_equal(got[1], want_b[1])
+    # an aborting producer: the scene keeps b
+    with pytest.raises(sg.InvalidArgumentError):
+        up.update_rows(a, lambda first, count: None if first > 0 else a.params[:count].astype(np.float32))
+    got = r.render_batch(up, cams, degree_override=1)
+    assert np.array_equal(got[0], want_b[0]) and np.array_equal(got[1], want_b[1])
+    up.update_rows(a)  # the default producer
+    got = r.render_batch(up, cams, degree_override=1)
+    assert np.array_equal(got[0], want_a[0]) and np.array_equal(got[1], want_a[1])
+    ran = []
+    with pytest.raises(sg.InvalidArgumentError):
+        up.update_rows(sg.synth_scene(1000, "mixed", 513), lambda f, c: ran.append(f))
+    assert not ran
+    for d in (fresh_b, up):
+        d.free()
+
+
 @pytest.mark.slow
 def test_sg3_renders_faster_than_sh3():
     """The reference's acceptance criterion 3 (acceptance.cpp:79-134):
