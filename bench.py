@@ -58,6 +58,11 @@ def frame_algorithmic_bytes(v, p, e_t, n=N_GAUSS, n_c=24, w=W, h=H):
     return 4 * n * (11 + n_c) + 100 * v + 36 * p + 52 * e_t + 16 * w * h
 
 
+# HBM3e spec (B200_PROFILING.md: 7.7 TB/s HGX): the second denominator SURVEY.md
+# 8(d) asks for beside the measured copy bandwidth
+HBM_SPEC_GBS = 7700.0
+
+
 def composite_algorithmic_bytes(e_t, w=W, h=H):
     """K7: 4-B list entry + 48-B splat record per processed entry + 16 B/px out."""
     return 52 * e_t + 16 * w * h
@@ -480,14 +485,16 @@ def main():
                          "achieved": comp_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": comp_gbs / hbm, "traffic": prof.get("composite_dram_bytes_per_frame"),
                          "algorithmic_bytes_per_frame": comp_bytes, "bytes_formula": "52 E_t + 16 W H",
-                         "ms_per_frame": comp_ms, "issue": k7_issue},
+                         "ms_per_frame": comp_ms, "issue": k7_issue,
+                         "spec_peak": HBM_SPEC_GBS, "spec_frac": comp_gbs / HBM_SPEC_GBS},
             "k1_roofline": {"bound": "hbm", "kernel": "preprocess (K1), one launch per frame",
                             "achieved": k1_gbs, "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm,
                             "traffic": prof.get("k1_dram_bytes_per_launch"),
                             "algorithmic_bytes_per_launch": k1_bytes, "bytes_formula": "4 N (11 + n_c) + 88 V",
-                            "launch_ms": k1_ms},
+                            "launch_ms": k1_ms, "spec_peak": HBM_SPEC_GBS, "spec_frac": k1_gbs / HBM_SPEC_GBS},
             "frame_roofline": {"achieved": frame_gbs, "peak": hbm, "unit": "GB/s",
-                               "frac": frame_gbs / hbm, "bytes_per_frame": frame_bytes},
+                               "frac": frame_gbs / hbm, "bytes_per_frame": frame_bytes,
+                               "spec_peak": HBM_SPEC_GBS, "spec_frac": frame_gbs / HBM_SPEC_GBS},
             "stage_ms_per_frame": stage_ms, "dominant_stage": dominant,
             "counters_per_frame": {"V": V, "P": P, "E_t": E_t, "guard_hits": sc.guard_hits / nv,
                                    "P_tight": st.tile_entries / nv},
