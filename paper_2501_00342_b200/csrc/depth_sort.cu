@@ -73,10 +73,8 @@ __global__ void __launch_bounds__(kL1Threads) coarse_scatter_kernel(
     uint64_t n, const unsigned long long* __restrict__ key, const Counters* __restrict__ ctr, int log2c,
     uint32_t* __restrict__ cur, unsigned long long* __restrict__ part_key, uint32_t* __restrict__ part_idx,
     uint2* __restrict__ bmeta) {
-    extern __shared__ uint32_t sh[];
+    extern __shared__ uint32_t cnt[];  // per-bucket counts, then this CTA's first slot per bucket
     const uint32_t C = 1u << log2c;
-    uint32_t* cnt = sh;
-    uint32_t* gbase = sh + (C + 1);
     for (uint32_t b = threadIdx.x; b <= C; b += kL1Threads) cnt[b] = 0;
     const unsigned long long kmin = ctr->kmin;
     const int shift = bucket_shift(ctr, log2c);
@@ -96,13 +94,13 @@ __global__ void __launch_bounds__(kL1Threads) coarse_scatter_kernel(
     }
     __syncthreads();
     for (uint32_t b = threadIdx.x; b <= C; b += kL1Threads)
-        if (cnt[b]) gbase[b] = atomicAdd(&cur[b], cnt[b]);
+        if (cnt[b]) cnt[b] = atomicAdd(&cur[b], cnt[b]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kL1Per; ++j) {
         const uint64_t i = base + j * kL1Threads;
         if (i >= n) continue;
-        const uint32_t pos = gbase[bk[j]] + lo[j];
+        const uint32_t pos = cnt[bk[j]] + lo[j];
         part_idx[pos] = static_cast<uint32_t>(i);
         if (bk[j] == C)
             bmeta[pos] = make_uint2(static_cast<uint32_t>(i), 0u);
@@ -296,7 +294,7 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
 }
 
 
-// Exclusive scan of in[0, m) into out (one CTA; m = C + 1 <= 16385).
+// Exclusive scan of in[0, m) into out (one CTA; m = C + 1 <= 32769).
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_kernel(const uint32_t* __restrict__ in,
                                                                   uint32_t* __restrict__ out, uint32_t m) {
@@ -336,7 +334,7 @@ __global__ void __launch_bounds__(kScanThreads) bucket_scan_kernel(const uint32_
 
 int depth_coarse_log2(uint64_t n) {
     int l = 0;
-    while (l < 14 && (1ULL << l) * 1024 < n) ++l;
+    while (l < 15 && (1ULL << l) * 1024 < n) ++l;
     return l;
 }
 
@@ -349,11 +347,22 @@ cudaError_t launch_depth_two_level(uint64_t n, const unsigned long long* key, Co
     if (n == 0) return cudaSuccess;
     const uint32_t C = 1u << log2c;
     const uint32_t G = static_cast<uint32_t>((n + kL1Tile - 1) / kL1Tile);
+    // shared memory of the level-1 kernels: C + 1 counters, past the default 48 KB above
+    // 8M Gaussians (C = 32768 at most: 128 KB)
+    static const cudaError_t l1attr = [] {
+        constexpr int kMaxL1Smem = ((1 << 15) + 1) * 4;
+        cudaError_t a = cudaFuncSetAttribute(coarse_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMaxL1Smem);
+        if (a == cudaSuccess)
+            a = cudaFuncSetAttribute(coarse_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxL1Smem);
+        return a;
+    }();
+    if (l1attr != cudaSuccess) return l1attr;
     cudaError_t e = cudaMemsetAsync(ghist, 0, (C + 1) * 4, stream);
     if (e != cudaSuccess) return e;
     coarse_hist_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, ghist);
     bucket_scan_kernel<<<1, kScanThreads, 0, stream>>>(ghist, cur, C + 1);
-    coarse_scatter_kernel<<<G, kL1Threads, (C + 1) * 8, stream>>>(n, key, ctr, log2c, cur, part_key, order, bmeta);
+    coarse_scatter_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, cur, part_key, order, bmeta);
     constexpr int kL2Smem = kL2Cap * 12;
     static const cudaError_t attr =
         cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);

@@ -684,6 +684,32 @@ def test_full_size_vs_reference(renderer, ref, cfgname):
 
 
 @pytest.mark.slow
+def test_large_scene_vs_reference(renderer, ref):
+    """A scene past 8M Gaussians: K2's coarse level at its largest (32768 buckets,
+    128 KB of shared counters per CTA -- the sizes that once failed to launch above
+    4M) against the reference's own build: bit-exact depth order, tile ranges and
+    lists, image within tolerance."""
+    scene = sg.synth_scene(9_000_000, "mixed", 20260009, log_scale_range=(-6.0, -4.5))
+    cam = sg.orbit_camera([0, 0, 0], 4.0, 0.5, 0.3, 480, 270, 324.0)
+    f = _flat(scene)
+    ocam = OrcCamera.from_buffer_copy(bytes(cam._c()))
+    cfg = make_config(degree_override=1)
+    ds = renderer.upload(scene)
+    try:
+        got = renderer.tile_grid(ds, cam, degree_override=1)
+        want = ref.tile_grid(f, ocam, cfg)
+        assert np.array_equal(got[0], want[0]), "depth order"
+        assert np.array_equal(got[1], want[1]), "tile ranges"
+        assert np.array_equal(got[2], want[2]), "tile lists"
+        ref_rgb, ref_T = ref.render(f, ocam, cfg)
+        for _ in range(3):  # direct, captured, replayed
+            rgb, T = renderer.render(ds, cam, degree_override=1)
+            check_image(rgb, T, ref_rgb, ref_T)
+    finally:
+        ds.free()
+
+
+@pytest.mark.slow
 def test_benchmarked_batch_vs_reference(ref):
     """The path bench.py times: a 32-view render_batch of config C/E (3M Gaussians,
     views 0..31 of the 256-camera ring) with the default lanes, frame graphs and tight
