@@ -458,7 +458,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
     SGS_CUDA(L.ranges.ensure(std::max<uint64_t>(ntile, 1) * sizeof(uint2)));
     // tile pairs (grow-only; P above the capacity makes the frame regrow and redo);
     // at least n1, as K2 sorts in these arrays too
-    if (L.tkey_cap == 0) L.tkey_cap = std::max<uint64_t>(16 * n, 1 << 20);
+    if (L.tkey_cap == 0) L.tkey_cap = std::max<uint64_t>(2 * n, 1 << 20);  // (regrown from the observed P)
     L.tkey_cap = std::min<uint64_t>(std::max<uint64_t>(L.tkey_cap, n1), kMaxSortKeys);
     if (n1 > kMaxSortKeys) return fail(SGS_ERR_INVALID_ARGUMENT, "more than 2^31 - 1 Gaussians in one frame");
     SGS_CUDA(L.tk_a.ensure(L.tkey_cap * 4));
