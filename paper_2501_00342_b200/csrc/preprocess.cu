@@ -447,15 +447,12 @@ __device__ __forceinline__ void k1_view(const ScenePlanes& sp, const CfgParams& 
 
 // K1: persistent CTAs walk the Gaussians with a two-stage cp.async pipeline (the
 // next Gaussian's geometry, covariance and colour planes land in shared memory
-// while this one is projected), so the FP64 chain overlaps the HBM latency. With
-// NV > 1 views (a batch's cameras) every Gaussian is read once
-// and projected into each view's arenas.
+// while this one is projected), so the FP64 chain overlaps the HBM latency.
 // MINB (min resident CTAs per SM) trades registers for occupancy; selected at run
 // time by SGS_K1_MINB for tuning (default kDefaultMinB, see profiles/).
-template <bool F64, int KIND, int MINB, bool DEBUG, int NV>
+template <bool F64, int KIND, int MINB, bool DEBUG>
 __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
-    const ScenePlanes sp, const CfgParams cfg, const K1Stage stg, const K1Views views,
-    DebugSplat* __restrict__ debug) {
+    const ScenePlanes sp, const CfgParams cfg, const K1Stage stg, const K1Out o, DebugSplat* __restrict__ debug) {
     extern __shared__ float4 k1_smem[];
     const int tid = threadIdx.x;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kK1Threads;
@@ -463,14 +460,8 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
     uint64_t i = static_cast<uint64_t>(blockIdx.x) * kK1Threads + tid;
     if (i < sp.n) stage_item<F64>(sp, stg, i, k1_smem, tid);
     cp_async_commit();
-    uint32_t nvis[NV];
-    unsigned long long kmin[NV], kmax[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        nvis[v] = 0;
-        kmin[v] = ~0ULL;
-        kmax[v] = 0ULL;
-    }
+    uint32_t nvis = 0;
+    unsigned long long kmin = ~0ULL, kmax = 0ULL;
     for (int it = 0; static_cast<uint64_t>(blockIdx.x) * kK1Threads + static_cast<uint64_t>(it) * stride < sp.n;
          ++it, i += stride) {
         if (i + stride < sp.n) stage_item<F64>(sp, stg, i + stride, k1_smem + ((it + 1) & 1) * buf_stride, tid);
@@ -480,42 +471,34 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
         const float4* buf = k1_smem + (it & 1) * buf_stride;
         Geo g;
         geo_from_stage<F64>(buf, stg.geo_slots, tid, g);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const K1Out& o = views.v[v];
-            unsigned long long key = ~0ULL;
-            uint32_t count = 0;
-            bool visible = false;
-            DebugSplat dbg;
-            if constexpr (DEBUG) {
-                memset(&dbg, 0, sizeof(dbg));
-                dbg.degree = -1;
-            }
-            k1_view<KIND, DEBUG>(sp, cfg, stg, o, buf, tid, i, g, dbg, key, count, visible);
-            o.keys[i] = key;
-            if constexpr (DEBUG) debug[i] = dbg;
-            if (visible) {
-                ++nvis[v];
-                kmin[v] = min(kmin[v], key);
-                kmax[v] = max(kmax[v], key);
-            }
+        unsigned long long key = ~0ULL;
+        uint32_t count = 0;
+        bool visible = false;
+        DebugSplat dbg;
+        if constexpr (DEBUG) {
+            memset(&dbg, 0, sizeof(dbg));
+            dbg.degree = -1;
+        }
+        k1_view<KIND, DEBUG>(sp, cfg, stg, o, buf, tid, i, g, dbg, key, count, visible);
+        o.keys[i] = key;
+        if constexpr (DEBUG) debug[i] = dbg;
+        if (visible) {
+            ++nvis;
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
         }
     }
-    // visible count and depth-key range per view: one atomic each per warp
+    // visible count and depth-key range: one atomic each per warp
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            nvis[v] += __shfl_xor_sync(0xffffffffu, nvis[v], o);
-            kmin[v] = min(kmin[v], __shfl_xor_sync(0xffffffffu, kmin[v], o));
-            kmax[v] = max(kmax[v], __shfl_xor_sync(0xffffffffu, kmax[v], o));
-        }
-        if ((tid & 31) == 0 && nvis[v]) {
-            Counters* ctr = views.v[v].ctr;
-            atomicAdd(&ctr->visible, static_cast<unsigned long long>(nvis[v]));
-            atomicMin(&ctr->kmin, kmin[v]);
-            atomicMax(&ctr->kmax, kmax[v]);
-        }
+    for (int s = 16; s > 0; s >>= 1) {
+        nvis += __shfl_xor_sync(0xffffffffu, nvis, s);
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, s));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, s));
+    }
+    if ((tid & 31) == 0 && nvis) {
+        atomicAdd(&o.ctr->visible, static_cast<unsigned long long>(nvis));
+        atomicMin(&o.ctr->kmin, kmin);
+        atomicMax(&o.ctr->kmax, kmax);
     }
 }
 
@@ -553,7 +536,7 @@ struct K1Record {
     ScenePlanes sp;
     CfgParams cfg;
     K1Stage st;
-    K1Views views;
+    K1Out out;
     DebugSplat* debug = nullptr;
 };
 
@@ -561,12 +544,12 @@ namespace {
 
 thread_local K1Record t_last_k1;
 
-template <bool F64, int KIND, int MINB, bool DEBUG, int NV>
-void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
+template <bool F64, int KIND, int MINB, bool DEBUG>
+void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Out& out, DebugSplat* debug,
                cudaStream_t stream) {
     const K1Stage st = make_stage(sp, cfg);
     const size_t smem = static_cast<size_t>(2) * st.slots * kK1Threads * sizeof(float4);
-    auto kern = preprocess_kernel<F64, KIND, MINB, DEBUG, NV>;
+    auto kern = preprocess_kernel<F64, KIND, MINB, DEBUG>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -575,8 +558,8 @@ void launch_k1(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views
     const uint64_t need = (sp.n + kK1Threads - 1) / kK1Threads;
     const uint64_t grid = std::min<uint64_t>(need, static_cast<uint64_t>(sms) * std::max(per_sm, 1));
     t_last_k1 = K1Record{reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(grid)), dim3(kK1Threads),
-                         smem, sp, cfg, st, views, debug};
-    kern<<<static_cast<unsigned>(grid), kK1Threads, smem, stream>>>(sp, cfg, st, views, debug);
+                         smem, sp, cfg, st, out, debug};
+    kern<<<static_cast<unsigned>(grid), kK1Threads, smem, stream>>>(sp, cfg, st, out, debug);
 }
 
 constexpr int kDefaultMinB = 2;
@@ -591,28 +574,28 @@ int k1_minb() {
 }
 
 template <bool F64, int KIND>
-void launch_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
-                  cudaStream_t stream) {
+void launch_minb(const ScenePlanes& sp, const CfgParams& cfg, const K1Out& out, DebugSplat* debug,
+                 cudaStream_t stream) {
     if (debug) {
-        launch_k1<F64, KIND, 1, true, 1>(sp, cfg, views, debug, stream);
+        launch_k1<F64, KIND, 1, true>(sp, cfg, out, debug, stream);
         return;
     }
     switch (k1_minb()) {
-        case 1: launch_k1<F64, KIND, 1, false, 1>(sp, cfg, views, nullptr, stream); break;
-        case 3: launch_k1<F64, KIND, 3, false, 1>(sp, cfg, views, nullptr, stream); break;
-        case 4: launch_k1<F64, KIND, 4, false, 1>(sp, cfg, views, nullptr, stream); break;
-        default: launch_k1<F64, KIND, 2, false, 1>(sp, cfg, views, nullptr, stream); break;
+        case 1: launch_k1<F64, KIND, 1, false>(sp, cfg, out, nullptr, stream); break;
+        case 3: launch_k1<F64, KIND, 3, false>(sp, cfg, out, nullptr, stream); break;
+        case 4: launch_k1<F64, KIND, 4, false>(sp, cfg, out, nullptr, stream); break;
+        default: launch_k1<F64, KIND, 2, false>(sp, cfg, out, nullptr, stream); break;
     }
 }
 
 template <bool F64>
-void launch_kind(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
+void launch_kind(const ScenePlanes& sp, const CfgParams& cfg, const K1Out& out, DebugSplat* debug,
                  cudaStream_t stream) {
     switch (sp.kind) {
-        case SGS_SH: launch_views<F64, SGS_SH>(sp, cfg, views, debug, stream); break;
-        case SGS_SG1: launch_views<F64, SGS_SG1>(sp, cfg, views, debug, stream); break;
-        case SGS_SG3: launch_views<F64, SGS_SG3>(sp, cfg, views, debug, stream); break;
-        default: launch_views<F64, SGS_MIXED>(sp, cfg, views, debug, stream); break;
+        case SGS_SH: launch_minb<F64, SGS_SH>(sp, cfg, out, debug, stream); break;
+        case SGS_SG1: launch_minb<F64, SGS_SG1>(sp, cfg, out, debug, stream); break;
+        case SGS_SG3: launch_minb<F64, SGS_SG3>(sp, cfg, out, debug, stream); break;
+        default: launch_minb<F64, SGS_MIXED>(sp, cfg, out, debug, stream); break;
     }
 }
 
@@ -656,19 +639,12 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
                        float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream) {
-    K1Views views{};
-    views.nv = 1;
-    views.v[0] = K1Out{depth_keys, rec, rects, colour, counters, cam};
-    launch_preprocess_views(sp, cfg, views, debug, stream);
-}
-
-void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
-                             cudaStream_t stream) {
     if (sp.n == 0) return;
+    const K1Out out{depth_keys, rec, rects, colour, counters, cam};
     if (sp.geometry_f64)
-        launch_kind<true>(sp, cfg, views, debug, stream);
+        launch_kind<true>(sp, cfg, out, debug, stream);
     else
-        launch_kind<false>(sp, cfg, views, debug, stream);
+        launch_kind<false>(sp, cfg, out, debug, stream);
 }
 
 K1Record* k1_last_launch_clone() { return new K1Record(t_last_k1); }
@@ -678,8 +654,8 @@ void k1_record_free(K1Record* r) { delete r; }
 const void* k1_record_func(const K1Record* r) { return r->func; }
 
 cudaError_t k1_record_patch(cudaGraphExec_t exec, cudaGraphNode_t node, K1Record* r, const CamParams& cam) {
-    r->views.v[0].cam = cam;
-    void* args[] = {&r->sp, &r->cfg, &r->st, &r->views, &r->debug};
+    r->out.cam = cam;
+    void* args[] = {&r->sp, &r->cfg, &r->st, &r->out, &r->debug};
     cudaKernelNodeParams p{};
     p.func = const_cast<void*>(r->func);
     p.gridDim = r->grid;

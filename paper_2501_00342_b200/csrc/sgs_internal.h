@@ -116,15 +116,12 @@ struct Counters {
     unsigned long long tile_entries;
     unsigned long long kmin;  // min / max orderable depth key of the visible splats
     unsigned long long kmax;
-    unsigned long long tie_runs;      // 32-bit depth-key collisions re-sorted by K2b
-    unsigned long long tie_overflow;  // runs too long for K2b (host falls back to 64-bit)
+    unsigned long long reserved0;
+    unsigned long long tie_overflow;  // a K2 bucket too large for its local sort (host redoes the frame with 64-bit keys)
     unsigned long long key_overflow;  // a chunk needed more tile keys than allocated
     unsigned long long max_chunk_entries;  // largest chunk P (sizes the retry)
     unsigned long long chunk_entries;  // P of the chunk in flight (clamped to capacity)
-    unsigned long long culled_cursor;  // K2 scatter slot for culled splats
-    unsigned long long big_buckets;    // K2 buckets queued for the warp sort
-    unsigned long long list_overflow;  // a tile list exceeded the tile-major sort's capacity
-    unsigned long long pad;
+    unsigned long long reserved1[4];
 };
 static_assert(sizeof(Counters) == 128, "counters block");
 
@@ -156,12 +153,11 @@ void launch_preprocess(const ScenePlanes& sp, const CamParams& cam, const CfgPar
                        unsigned long long* depth_keys, SplatRec* rec, int4* rects,
                        float4* colour, Counters* counters, DebugSplat* debug,
                        cudaStream_t stream);
-// K1's outputs for one view. (A multi-view K1 -- every Gaussian read once, projected
+// K1's outputs for its view. (A multi-view K1 -- every Gaussian read once, projected
 // into up to 4 views' arenas, SURVEY.md §8f row 1 -- was built and measured: 152 us
 // per view at NV=1, 154 at NV=2, 167 at NV=4, batch throughput 0.719 vs 0.724 ms per
 // frame, because with the covariance cached K1 is bound by its per-view FP64 work and
 // writes, not by the shared scene read. It is not kept.)
-constexpr int kMaxK1Views = 1;
 struct K1Out {
     unsigned long long* keys;
     SplatRec* rec;
@@ -170,12 +166,6 @@ struct K1Out {
     Counters* ctr;
     CamParams cam;
 };
-struct K1Views {
-    int nv;
-    K1Out v[kMaxK1Views];
-};
-void launch_preprocess_views(const ScenePlanes& sp, const CfgParams& cfg, const K1Views& views, DebugSplat* debug,
-                             cudaStream_t stream);
 // The last K1 launch of this thread (function, configuration, arguments), so a frame
 // graph can patch the camera of its captured K1 node (capi.cu launch_frame_graph).
 struct K1Record;
