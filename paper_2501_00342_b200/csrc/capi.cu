@@ -157,7 +157,6 @@ struct Lane {
         sgs_render_stats* stats = nullptr;
         DebugSplat* d_debug = nullptr;
         int mode = 0;
-        bool wide = false;  // K2 on the full 64-bit keys (a long run of equal 32-bit keys)
         float ms_bin = 0, ms_tsort = 0, ms_comp = 0;
     } job;
     bool busy = false;
@@ -293,7 +292,6 @@ int ceil_log2(uint64_t v) {
 
 enum FrameMode { kRender = 0, kProjectOnly = 1, kTileGrid = 2 };
 // run_frame_once results besides sgs_status
-constexpr int kRetryWide = 100;  // a run of equal 32-bit depth keys: redo with 64-bit keys
 constexpr int kRetryGrow = 101;  // the tile-key arena was too small: grown, redo
 // the radix sort's counters are 32-bit (kept one bit clear)
 constexpr uint64_t kMaxSortKeys = (1ULL << 31) - 1;
@@ -315,7 +313,7 @@ std::vector<uint64_t> default_chunk_divs(uint64_t n) {
 // Enqueue lane L's job on L.stream without a host round trip (every data-dependent
 // size lives on the device), ending with a 128-B D2H of the counters and L.done.
 // finish_frame() reads the counters, reports errors and -- rarely -- regrows the
-// tile-key arena or switches to the 64-bit depth sort and enqueues the frame again.
+// tile-key arena and enqueues the frame again.
 
 // Everything the captured frame depends on besides the per-frame constants (camera,
 // outputs) and the K1 camera: a frame whose key differs is enqueued directly; the
@@ -332,7 +330,7 @@ std::vector<uint64_t> frame_graph_key(const sgs_context* ctx, const Lane& L) {
                             static_cast<uint64_t>(j.cfg.tile_size), static_cast<uint64_t>(j.cfg.has_override),
                             static_cast<uint64_t>(j.cfg.override_degree), bits(j.cfg.degree_threshold_lo),
                             bits(j.cfg.degree_threshold_hi), bits(j.cfg.early_stop_transmittance),
-                            (j.stats ? 1u : 0u) | (j.stats && j.stats->timing_path ? 2u : 0u), j.wide ? 1u : 0u,
+                            (j.stats ? 1u : 0u) | (j.stats && j.stats->timing_path ? 2u : 0u),
                             static_cast<uint64_t>(j.mode), L.tkey_cap, g_alloc_generation.load(),
                             ctx->chunking ? 1u : 0u, ctx->chunk_divs_set ? 1u : 0u};
     for (uint64_t d : ctx->chunk_divs) k.push_back(d);
@@ -536,24 +534,19 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
             return SGS_OK;
         }
 
-        // K2: ranks and the rank-ordered binning inputs (depth_sort.cu; the 64-bit radix
-        // sort of radix.cu after a tie overflow)
+        // K2: ranks and the rank-ordered binning inputs (depth_sort.cu)
         const uint32_t* order = L.order.as<uint32_t>();
-        if (!j.wide) {
+        {
             const int log2c = depth_coarse_log2(n);
             const size_t half = align_up(depth_two_level_scratch(log2c), 256);
-            SGS_CUDA(L.buckets.ensure(2 * half));
+            SGS_CUDA(L.buckets.ensure(3 * half));  // histogram, offsets, big-bucket list
             SGS_CUDA(L.keys_b.ensure(n1 * 8));
             SGS_CUDA(launch_depth_two_level(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2c,
                                             L.buckets.as<uint32_t>(), L.buckets.as<uint32_t>() + half / 4,
+                                            L.buckets.as<uint32_t>() + 2 * (half / 4),
                                             L.keys_b.as<unsigned long long>(), L.order.as<uint32_t>(),
-                                            L.rects.as<int4>(), L.brect.as<int4>(), L.bmeta.as<uint2>(), s,
-                                            &ctx->own_launches));
-        } else {
-            SGS_CUDA(launch_depth_sort_wide(n, L.keys_a.as<unsigned long long>(), L.d_ctr, L.tk_a.as<uint32_t>(),
-                                            L.tv_a.as<uint32_t>(), L.tk_b.as<uint32_t>(), L.tv_b.as<uint32_t>(),
-                                            shist, L.rects.as<int4>(), L.order.as<uint32_t>(),
-                                            L.brect.as<int4>(), L.bmeta.as<uint2>(), s, &ctx->own_launches));
+                                            L.tk_a.as<uint32_t>(), L.rects.as<int4>(), L.brect.as<int4>(),
+                                            L.bmeta.as<uint2>(), s, &ctx->own_launches));
         }
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 
@@ -600,7 +593,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
             uint32_t* tk2 = L.tk_b.as<uint32_t>();
             uint32_t* tv2 = L.tv_b.as<uint32_t>();
             for (int p = 0; p < td.passes; ++p) {
-                SGS_CUDA(launch_radix_pass(tk, tv, tk2, tv2, d_pc, 0, td.shift[p], td.bits[p], shist, false, s));
+                SGS_CUDA(launch_radix_pass(tk, tv, tk2, tv2, d_pc, td.shift[p], td.bits[p], shist, s));
                 std::swap(tk, tk2);
                 std::swap(tv, tv2);
             }
@@ -676,15 +669,14 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
     return SGS_OK;
 }
 
-// Wait for lane L's frame and check it: SGS_OK / an error status, or kRetryWide /
-// kRetryGrow when the frame must be enqueued again.
+// Wait for lane L's frame and check it: SGS_OK / an error status, or kRetryGrow when
+// the frame must be enqueued again.
 int check_frame(Lane& L) {
     Lane::Job& j = L.job;
     SGS_CUDA(cudaEventSynchronize(L.done));
     const Counters& hc = *L.h_ctr;
     if (hc.err != ~0ULL) return device_error(hc.err, j.scene, &j.cfg);
     if (j.mode == kProjectOnly) return SGS_OK;
-    if (hc.tie_overflow && !j.wide) return kRetryWide;
     if (hc.key_overflow) {
         if (L.tkey_cap >= kMaxSortKeys) return fail(SGS_ERR_OUT_OF_MEMORY, "more than 2^31 - 1 tile entries in one chunk");
         L.tkey_cap = std::min<uint64_t>(hc.max_chunk_entries + hc.max_chunk_entries / 4 + 1024, kMaxSortKeys);
@@ -718,8 +710,7 @@ sgs_status finish_frame(sgs_context* ctx, Lane& L) {
     if (!L.busy) return SGS_OK;
     for (int attempt = 0; attempt < 4; ++attempt) {
         const int rc = check_frame(L);
-        if (rc == kRetryWide || rc == kRetryGrow) {
-            if (rc == kRetryWide) L.job.wide = true;
+        if (rc == kRetryGrow) {
             sgs_status st = enqueue_frame(ctx, L);
             if (st != SGS_OK) {
                 L.busy = false;

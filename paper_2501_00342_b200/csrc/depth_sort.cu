@@ -6,8 +6,11 @@
 // ones, in index order; they own no tiles. Measured against a 4-pass LSD radix sort
 // of 32-bit keys (radix.cu) with an exact fix-up of equal-key runs: 171 against
 // 230 us per frame at config C -- one scattered partition plus shared-memory sorts
-// move less than four global passes. The 64-bit radix sort is the fallback for
-// degenerate depth distributions.
+// move less than four global passes. Dense depth clusters stay on this path: a fine
+// bucket past the warp sort's 64 keys sends its coarse bucket to a shared-memory
+// bitonic sort, and a coarse bucket past 4096 keys to big_bucket_kernel (runs sorted
+// in shared memory, merged in global memory), so no depth distribution forces a
+// slower sort on the whole frame.
 
 #include "sgs_internal.h"
 
@@ -148,6 +151,35 @@ __device__ void block_exclusive_scan(uint32_t* v, int m, uint32_t* warp_tot) {
     __syncthreads();
 }
 
+// Sort (key, index) pairs [0, m) of shared memory in place by (key, index), m <= kL2Cap:
+// a CTA-wide bitonic network over the next power of two (padding with (~0, ~0), which
+// sorts last). Every thread of the CTA calls it.
+__device__ void cta_bitonic_sort(unsigned long long* key, uint32_t* idx, uint32_t m) {
+    uint32_t P = 1;
+    while (P < m) P <<= 1;
+    for (uint32_t e = m + threadIdx.x; e < P; e += blockDim.x) {
+        key[e] = ~0ULL;
+        idx[e] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= P; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P / 2; i += blockDim.x) {
+                const uint32_t a = (i / stride) * 2 * stride + (i % stride), b = a + stride;
+                const bool up = (a & size) == 0;
+                if (less_ki(key[b], idx[b], key[a], idx[a]) == up) {
+                    const unsigned long long tk = key[a];
+                    const uint32_t ti = idx[a];
+                    key[a] = key[b];
+                    idx[a] = idx[b];
+                    key[b] = tk;
+                    idx[b] = ti;
+                }
+            }
+            __syncthreads();
+        }
+}
+
 // visible splats always have their rect written by K1: both gathers issue together
 __device__ __forceinline__ void put_rank(uint32_t r, uint32_t g, const int4* __restrict__ rects,
                                          uint32_t* __restrict__ order, int4* __restrict__ brect,
@@ -162,24 +194,21 @@ __device__ __forceinline__ void put_rank(uint32_t r, uint32_t g, const int4* __r
 __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
     Counters* __restrict__ ctr, int log2c, const int4* __restrict__ rects,
-    int4* __restrict__ brect, uint2* __restrict__ bmeta) {
+    int4* __restrict__ brect, uint2* __restrict__ bmeta, uint32_t* __restrict__ big_list) {
     extern __shared__ unsigned long long sKey[];  // kL2Cap keys, then kL2Cap indices
     uint32_t* sIdx = reinterpret_cast<uint32_t*>(sKey + kL2Cap);
     __shared__ uint32_t sCur[1 << kL2MaxFineLog2];
     __shared__ uint32_t sBig[kL2Cap / (kSmall + 1) + 1];
     __shared__ uint32_t sWarp[kL2Threads / 32];
     __shared__ uint32_t sNBig;
+    __shared__ uint32_t sFull;  // a fine bucket too large for the warp sort: sort the whole bucket
     const uint32_t b = blockIdx.x;
     const uint32_t s = b ? cend[b - 1] : 0u;
     const uint32_t m = cend[b] - s;
     if (m == 0) return;
     const int tid = threadIdx.x;
-    if (m > kL2Cap) {
-        // too many keys for one CTA: the host redoes the frame with the 64-bit sort.
-        // Until then the rest of this frame still runs, so these ranks get empty
-        // binning inputs (no tiles) instead of whatever the arena held before.
-        if (tid == 0) atomicAdd(&ctr->tie_overflow, 1ULL);
-        for (uint32_t e = tid; e < m; e += kL2Threads) bmeta[s + e] = make_uint2(order[s + e], 0u);
+    if (m > kL2Cap) {  // more keys than shared memory holds: big_bucket_kernel sorts it
+        if (tid == 0) big_list[atomicAdd(&ctr->big_buckets, 1ULL)] = b;
         return;
     }
     const unsigned long long kmin = ctr->kmin;
@@ -190,7 +219,7 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
     const int shiftF = shiftC - F;
     const uint32_t nf = 1u << F, fmask = nf - 1;
     for (uint32_t f = tid; f < nf; f += kL2Threads) sCur[f] = 0;
-    if (tid == 0) sNBig = 0;
+    if (tid == 0) sNBig = 0, sFull = 0;
     unsigned long long k[kL2Per];
     uint32_t ix[kL2Per];
 #pragma unroll
@@ -219,7 +248,7 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
         const uint32_t fs = f ? sCur[f - 1] : 0u, fe = sCur[f], mf = fe - fs;
         if (mf <= 1) continue;
         if (mf > kBucketCap) {
-            atomicAdd(&ctr->tie_overflow, 1ULL);
+            sFull = 1;
             continue;
         }
         if (mf > kSmall) {
@@ -240,6 +269,11 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
         }
     }
     __syncthreads();
+    if (sFull) {  // (dense depths: a fine bucket past the warp sort) the whole bucket at once
+        cta_bitonic_sort(sKey, sIdx, m);
+        for (uint32_t e = tid; e < m; e += kL2Threads) put_rank(s + e, sIdx[e], rects, order, brect, bmeta);
+        return;
+    }
     const int lane = tid & 31;
     for (uint32_t q = tid >> 5; q < sNBig; q += kL2Threads / 32) {
         const uint32_t f = sBig[q];
@@ -294,6 +328,79 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
 }
 
 
+// Coarse buckets with more than kL2Cap keys (dense depth clusters, very large scenes):
+// one CTA per bucket sorts its (key, index) pairs by (key, index) in global memory --
+// 4096-pair runs sorted in shared memory, then merged pairwise, each pair placed by
+// binary search (keys are unique with the index) -- and writes the ranks. The runs
+// ping-pong through tmp_key / tmp_idx (K1's depth keys and the tile-pair arena, both
+// free while K2 runs).
+__device__ __forceinline__ uint32_t count_less(const unsigned long long* key, const uint32_t* idx, uint32_t lo,
+                                               uint32_t hi, unsigned long long k, uint32_t i) {
+    uint32_t a = lo, b = hi;
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (less_ki(key[mid], idx[mid], k, i))
+            a = mid + 1;
+        else
+            b = mid;
+    }
+    return a - lo;
+}
+
+__global__ void __launch_bounds__(kL2Threads) big_bucket_kernel(
+    const uint32_t* __restrict__ cend, unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
+    unsigned long long* __restrict__ tmp_key, uint32_t* __restrict__ tmp_idx, const Counters* __restrict__ ctr,
+    const uint32_t* __restrict__ big_list, const int4* __restrict__ rects, int4* __restrict__ brect,
+    uint2* __restrict__ bmeta) {
+    extern __shared__ unsigned long long sKey[];
+    uint32_t* sIdx = reinterpret_cast<uint32_t*>(sKey + kL2Cap);
+    const uint32_t nbig = static_cast<uint32_t>(ctr->big_buckets);
+    for (uint32_t q = blockIdx.x; q < nbig; q += gridDim.x) {
+        const uint32_t b = big_list[q];
+        const uint32_t s = b ? cend[b - 1] : 0u;
+        const uint32_t m = cend[b] - s;
+        unsigned long long* srcK = part_key + s;
+        uint32_t* srcI = order + s;
+        unsigned long long* dstK = tmp_key + s;
+        uint32_t* dstI = tmp_idx + s;
+        // runs of kL2Cap, sorted in shared memory
+        for (uint32_t r0 = 0; r0 < m; r0 += kL2Cap) {
+            const uint32_t rm = min(static_cast<uint32_t>(kL2Cap), m - r0);
+            for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
+                sKey[e] = srcK[r0 + e];
+                sIdx[e] = srcI[r0 + e];
+            }
+            __syncthreads();
+            cta_bitonic_sort(sKey, sIdx, rm);
+            for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
+                dstK[r0 + e] = sKey[e];
+                dstI[r0 + e] = sIdx[e];
+            }
+            __syncthreads();
+        }
+        // pairwise merges: an element's place is its index in its run plus the number
+        // of smaller elements in the other run
+        for (uint32_t w = kL2Cap; w < m; w <<= 1) {
+            unsigned long long* tk = srcK;
+            uint32_t* ti = srcI;
+            srcK = dstK, srcI = dstI, dstK = tk, dstI = ti;
+            for (uint32_t e = threadIdx.x; e < m; e += kL2Threads) {
+                const uint32_t base = e / (2 * w) * (2 * w);
+                const uint32_t mid = min(base + w, m), end = min(base + 2 * w, m);
+                const unsigned long long k = srcK[e];
+                const uint32_t i = srcI[e];
+                const uint32_t pos = e < mid ? e + count_less(srcK, srcI, mid, end, k, i)
+                                             : e - w + count_less(srcK, srcI, base, mid, k, i);
+                dstK[pos] = k;
+                dstI[pos] = i;
+            }
+            __syncthreads();
+        }
+        for (uint32_t e = threadIdx.x; e < m; e += kL2Threads) put_rank(s + e, dstI[e], rects, order, brect, bmeta);
+        __syncthreads();
+    }
+}
+
 // Exclusive scan of in[0, m) into out (one CTA; m = C + 1 <= 32769).
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_kernel(const uint32_t* __restrict__ in,
@@ -338,12 +445,12 @@ int depth_coarse_log2(uint64_t n) {
     return l;
 }
 
-size_t depth_two_level_scratch(int log2c) { return static_cast<size_t>((1u << log2c) + 1) * 4; }
+size_t depth_two_level_scratch(int log2c) { return static_cast<size_t>((1u << log2c) + 1) * 4; }  // (per region)
 
-cudaError_t launch_depth_two_level(uint64_t n, const unsigned long long* key, Counters* ctr, int log2c,
-                                   uint32_t* ghist, uint32_t* cur, unsigned long long* part_key, uint32_t* order,
-                                   const int4* rects, int4* brect, uint2* bmeta, cudaStream_t stream,
-                                   uint64_t* launches) {
+cudaError_t launch_depth_two_level(uint64_t n, unsigned long long* key, Counters* ctr, int log2c,
+                                   uint32_t* ghist, uint32_t* cur, uint32_t* big_list, unsigned long long* part_key,
+                                   uint32_t* order, uint32_t* tmp_idx, const int4* rects, int4* brect, uint2* bmeta,
+                                   cudaStream_t stream, uint64_t* launches) {
     if (n == 0) return cudaSuccess;
     const uint32_t C = 1u << log2c;
     const uint32_t G = static_cast<uint32_t>((n + kL1Tile - 1) / kL1Tile);
@@ -364,11 +471,19 @@ cudaError_t launch_depth_two_level(uint64_t n, const unsigned long long* key, Co
     bucket_scan_kernel<<<1, kScanThreads, 0, stream>>>(ghist, cur, C + 1);
     coarse_scatter_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, cur, part_key, order, bmeta);
     constexpr int kL2Smem = kL2Cap * 12;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
+    static const cudaError_t attr = [] {
+        cudaError_t a = cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
+        if (a == cudaSuccess)
+            a = cudaFuncSetAttribute(big_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
+        return a;
+    }();
     if (attr != cudaSuccess) return attr;
-    local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, ctr, log2c, rects, brect, bmeta);
-    *launches += 4;
+    local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, ctr, log2c, rects, brect, bmeta,
+                                                           big_list);
+    // (the coarse keys are dead once partitioned: K1's key array is the merge scratch)
+    big_bucket_kernel<<<148, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, key, tmp_idx, ctr, big_list, rects,
+                                                             brect, bmeta);
+    *launches += 5;
     return cudaGetLastError();
 }
 

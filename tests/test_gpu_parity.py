@@ -323,12 +323,12 @@ def test_exact_mode_matches_reference_to_fp64_rounding(case):
 def _adversarial(orc, name):
     """Scenes that drive the rare paths of the frame pipeline."""
     rng = np.random.default_rng(4242)
-    if name == "ties":  # 600 splats at one depth: a run of equal 32-bit keys > 32 -> 64-bit depth sort
+    if name == "ties":  # 600 splats at one depth: a fine bucket past the warp sort -> K2's whole-bucket bitonic sort
         f = orc.synth(3000, 11, "mixed", 2, ls=(-4.0, -3.0))
         f.params[:600, 0:3] = f.params[600, 0:3]  # identical positions: identical depth keys
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 160, 120, 140.0)
         return f, cam, make_config(16, degree_override=1)
-    if name == "spike":  # 60k of 70k splats in a thin depth slab: long runs of equal 32-bit keys -> 64-bit sort
+    if name == "spike":  # 60k of 70k splats in a thin depth slab: a coarse bucket past 4096 keys -> big_bucket_kernel
         f = orc.synth(70_000, 12, "sg3", 0, ls=(-5.5, -4.5))
         f.params[:60_000, 0:3] = f.params[0, 0:3] + rng.uniform(-1e-9, 1e-9, size=(60_000, 3))
         cam = orc.orbit_camera([0, 0, 0], 3.0, 0.0, 0.0, 200, 150, 180.0)
