@@ -710,6 +710,40 @@ def test_large_scene_vs_reference(renderer, ref):
 
 
 @pytest.mark.slow
+def test_dense_depth_wall_vs_reference(renderer, ref):
+    """A real-scene depth distribution the synthetic ball lacks: 400K of 1.2M splats on
+    a wall facing the camera (depths within 1e-3), plus 2000 at one exact depth --
+    coarse depth buckets far past 4096 keys (big_bucket_kernel's shared-memory runs and
+    global merges) and fine buckets past the warp sort (the whole-bucket bitonic sort)
+    -- against the reference's own build: bit-exact order and lists, image in tolerance."""
+    scene = sg.synth_scene(1_200_000, "mixed", 20260011, log_scale_range=(-6.0, -4.5))
+    rng = np.random.default_rng(11)
+    p = scene.params
+    p[:400_000, 0] = rng.uniform(-5e-4, 5e-4, 400_000)  # the orbit camera at angle 0 looks down -x
+    p[:400_000, 1] = rng.uniform(-0.8, 0.8, 400_000)
+    p[:400_000, 2] = rng.uniform(-0.8, 0.8, 400_000)
+    p[400_000:402_000, 0:3] = p[400_000, 0:3]
+    p[:, 0:3] = p[:, 0:3].astype(np.float32)
+    cam = sg.orbit_camera([0, 0, 0], 4.0, 0.0, 0.0, 640, 360, 480.0)  # looking down the wall's normal
+    f = _flat(scene)
+    ocam = OrcCamera.from_buffer_copy(bytes(cam._c()))
+    cfg = make_config(degree_override=1)
+    ds = renderer.upload(scene)
+    try:
+        got = renderer.tile_grid(ds, cam, degree_override=1)
+        want = ref.tile_grid(f, ocam, cfg)
+        assert np.array_equal(got[0], want[0]), "depth order"
+        assert np.array_equal(got[1], want[1]), "tile ranges"
+        assert np.array_equal(got[2], want[2]), "tile lists"
+        ref_rgb, ref_T = ref.render(f, ocam, cfg)
+        for _ in range(3):  # direct, captured, replayed
+            rgb, T = renderer.render(ds, cam, degree_override=1)
+            check_image(rgb, T, ref_rgb, ref_T)
+    finally:
+        ds.free()
+
+
+@pytest.mark.slow
 def test_benchmarked_batch_vs_reference(ref):
     """The path bench.py times: a 32-view render_batch of config C/E (3M Gaussians,
     views 0..31 of the 256-camera ring) with the default lanes, frame graphs and tight
