@@ -8,8 +8,8 @@
 // 230 us per frame at config C -- one scattered partition plus shared-memory sorts
 // move less than four global passes. Dense depth clusters stay on this path: a fine
 // bucket past the warp sort's 64 keys sends its coarse bucket to a shared-memory
-// bitonic sort, and a coarse bucket past 4096 keys to big_bucket_kernel (runs sorted
-// in shared memory, merged in global memory), so no depth distribution forces a
+// bitonic sort, and its CTA sorts a coarse bucket past 4096 keys in global memory
+// (runs sorted in shared memory, then merged), so no depth distribution forces a
 // slower sort on the whole frame.
 
 #include "sgs_internal.h"
@@ -191,10 +191,72 @@ __device__ __forceinline__ void put_rank(uint32_t r, uint32_t g, const int4* __r
     brect[r] = rc;
 }
 
+// A coarse bucket with more than kL2Cap keys (dense depth clusters, very large
+// scenes), sorted by its CTA by (key, index) in global memory: 4096-pair runs sorted in
+// shared memory, then merged pairwise, each pair placed by binary search (keys are
+// unique with the index); then its ranks. The runs ping-pong through tmp_key / tmp_idx
+// (K1's depth keys and the tile-pair arena, both free while K2 runs).
+__device__ __forceinline__ uint32_t count_less(const unsigned long long* key, const uint32_t* idx, uint32_t lo,
+                                               uint32_t hi, unsigned long long k, uint32_t i) {
+    uint32_t a = lo, b = hi;
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (less_ki(key[mid], idx[mid], k, i))
+            a = mid + 1;
+        else
+            b = mid;
+    }
+    return a - lo;
+}
+
+__device__ __noinline__ void sort_big_bucket(uint32_t s, uint32_t m, unsigned long long* part_key, uint32_t* order,
+                                             unsigned long long* tmp_key, uint32_t* tmp_idx,
+                                             unsigned long long* sKey, uint32_t* sIdx, const int4* rects,
+                                             int4* brect, uint2* bmeta) {
+    unsigned long long* srcK = part_key + s;
+    uint32_t* srcI = order + s;
+    unsigned long long* dstK = tmp_key + s;
+    uint32_t* dstI = tmp_idx + s;
+    for (uint32_t r0 = 0; r0 < m; r0 += kL2Cap) {
+        const uint32_t rm = min(static_cast<uint32_t>(kL2Cap), m - r0);
+        for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
+            sKey[e] = srcK[r0 + e];
+            sIdx[e] = srcI[r0 + e];
+        }
+        __syncthreads();
+        cta_bitonic_sort(sKey, sIdx, rm);
+        for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
+            dstK[r0 + e] = sKey[e];
+            dstI[r0 + e] = sIdx[e];
+        }
+        __syncthreads();
+    }
+    // pairwise merges: an element's place is its index in its run plus the number of
+    // smaller elements in the other run
+    for (uint32_t w = kL2Cap; w < m; w <<= 1) {
+        unsigned long long* tk = srcK;
+        uint32_t* ti = srcI;
+        srcK = dstK, srcI = dstI, dstK = tk, dstI = ti;
+        for (uint32_t e = threadIdx.x; e < m; e += kL2Threads) {
+            const uint32_t base = e / (2 * w) * (2 * w);
+            const uint32_t mid = min(base + w, m), end = min(base + 2 * w, m);
+            const unsigned long long k = srcK[e];
+            const uint32_t i = srcI[e];
+            const uint32_t pos = e < mid ? e + count_less(srcK, srcI, mid, end, k, i)
+                                         : e - w + count_less(srcK, srcI, base, mid, k, i);
+            dstK[pos] = k;
+            dstI[pos] = i;
+        }
+        __syncthreads();
+    }
+    for (uint32_t e = threadIdx.x; e < m; e += kL2Threads) put_rank(s + e, dstI[e], rects, order, brect, bmeta);
+}
+
 __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
-    const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ cend, unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
     Counters* __restrict__ ctr, int log2c, const int4* __restrict__ rects,
-    int4* __restrict__ brect, uint2* __restrict__ bmeta, uint32_t* __restrict__ big_list) {
+    int4* __restrict__ brect, uint2* __restrict__ bmeta, unsigned long long* __restrict__ tmp_key,
+    uint32_t* __restrict__ tmp_idx) {
     extern __shared__ unsigned long long sKey[];  // kL2Cap keys, then kL2Cap indices
     uint32_t* sIdx = reinterpret_cast<uint32_t*>(sKey + kL2Cap);
     __shared__ uint32_t sCur[1 << kL2MaxFineLog2];
@@ -207,8 +269,8 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
     const uint32_t m = cend[b] - s;
     if (m == 0) return;
     const int tid = threadIdx.x;
-    if (m > kL2Cap) {  // more keys than shared memory holds: big_bucket_kernel sorts it
-        if (tid == 0) big_list[atomicAdd(&ctr->big_buckets, 1ULL)] = b;
+    if (m > kL2Cap) {  // more keys than shared memory holds
+        sort_big_bucket(s, m, part_key, order, tmp_key, tmp_idx, sKey, sIdx, rects, brect, bmeta);
         return;
     }
     const unsigned long long kmin = ctr->kmin;
@@ -328,79 +390,6 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
 }
 
 
-// Coarse buckets with more than kL2Cap keys (dense depth clusters, very large scenes):
-// one CTA per bucket sorts its (key, index) pairs by (key, index) in global memory --
-// 4096-pair runs sorted in shared memory, then merged pairwise, each pair placed by
-// binary search (keys are unique with the index) -- and writes the ranks. The runs
-// ping-pong through tmp_key / tmp_idx (K1's depth keys and the tile-pair arena, both
-// free while K2 runs).
-__device__ __forceinline__ uint32_t count_less(const unsigned long long* key, const uint32_t* idx, uint32_t lo,
-                                               uint32_t hi, unsigned long long k, uint32_t i) {
-    uint32_t a = lo, b = hi;
-    while (a < b) {
-        const uint32_t mid = (a + b) >> 1;
-        if (less_ki(key[mid], idx[mid], k, i))
-            a = mid + 1;
-        else
-            b = mid;
-    }
-    return a - lo;
-}
-
-__global__ void __launch_bounds__(kL2Threads) big_bucket_kernel(
-    const uint32_t* __restrict__ cend, unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
-    unsigned long long* __restrict__ tmp_key, uint32_t* __restrict__ tmp_idx, const Counters* __restrict__ ctr,
-    const uint32_t* __restrict__ big_list, const int4* __restrict__ rects, int4* __restrict__ brect,
-    uint2* __restrict__ bmeta) {
-    extern __shared__ unsigned long long sKey[];
-    uint32_t* sIdx = reinterpret_cast<uint32_t*>(sKey + kL2Cap);
-    const uint32_t nbig = static_cast<uint32_t>(ctr->big_buckets);
-    for (uint32_t q = blockIdx.x; q < nbig; q += gridDim.x) {
-        const uint32_t b = big_list[q];
-        const uint32_t s = b ? cend[b - 1] : 0u;
-        const uint32_t m = cend[b] - s;
-        unsigned long long* srcK = part_key + s;
-        uint32_t* srcI = order + s;
-        unsigned long long* dstK = tmp_key + s;
-        uint32_t* dstI = tmp_idx + s;
-        // runs of kL2Cap, sorted in shared memory
-        for (uint32_t r0 = 0; r0 < m; r0 += kL2Cap) {
-            const uint32_t rm = min(static_cast<uint32_t>(kL2Cap), m - r0);
-            for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
-                sKey[e] = srcK[r0 + e];
-                sIdx[e] = srcI[r0 + e];
-            }
-            __syncthreads();
-            cta_bitonic_sort(sKey, sIdx, rm);
-            for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
-                dstK[r0 + e] = sKey[e];
-                dstI[r0 + e] = sIdx[e];
-            }
-            __syncthreads();
-        }
-        // pairwise merges: an element's place is its index in its run plus the number
-        // of smaller elements in the other run
-        for (uint32_t w = kL2Cap; w < m; w <<= 1) {
-            unsigned long long* tk = srcK;
-            uint32_t* ti = srcI;
-            srcK = dstK, srcI = dstI, dstK = tk, dstI = ti;
-            for (uint32_t e = threadIdx.x; e < m; e += kL2Threads) {
-                const uint32_t base = e / (2 * w) * (2 * w);
-                const uint32_t mid = min(base + w, m), end = min(base + 2 * w, m);
-                const unsigned long long k = srcK[e];
-                const uint32_t i = srcI[e];
-                const uint32_t pos = e < mid ? e + count_less(srcK, srcI, mid, end, k, i)
-                                             : e - w + count_less(srcK, srcI, base, mid, k, i);
-                dstK[pos] = k;
-                dstI[pos] = i;
-            }
-            __syncthreads();
-        }
-        for (uint32_t e = threadIdx.x; e < m; e += kL2Threads) put_rank(s + e, dstI[e], rects, order, brect, bmeta);
-        __syncthreads();
-    }
-}
-
 // Exclusive scan of in[0, m) into out (one CTA; m = C + 1 <= 32769).
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_kernel(const uint32_t* __restrict__ in,
@@ -448,8 +437,8 @@ int depth_coarse_log2(uint64_t n) {
 size_t depth_two_level_scratch(int log2c) { return static_cast<size_t>((1u << log2c) + 1) * 4; }  // (per region)
 
 cudaError_t launch_depth_two_level(uint64_t n, unsigned long long* key, Counters* ctr, int log2c,
-                                   uint32_t* ghist, uint32_t* cur, uint32_t* big_list, unsigned long long* part_key,
-                                   uint32_t* order, uint32_t* tmp_idx, const int4* rects, int4* brect, uint2* bmeta,
+                                   uint32_t* ghist, uint32_t* cur, unsigned long long* part_key, uint32_t* order,
+                                   uint32_t* tmp_idx, const int4* rects, int4* brect, uint2* bmeta,
                                    cudaStream_t stream, uint64_t* launches) {
     if (n == 0) return cudaSuccess;
     const uint32_t C = 1u << log2c;
@@ -471,19 +460,13 @@ cudaError_t launch_depth_two_level(uint64_t n, unsigned long long* key, Counters
     bucket_scan_kernel<<<1, kScanThreads, 0, stream>>>(ghist, cur, C + 1);
     coarse_scatter_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, cur, part_key, order, bmeta);
     constexpr int kL2Smem = kL2Cap * 12;
-    static const cudaError_t attr = [] {
-        cudaError_t a = cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
-        if (a == cudaSuccess)
-            a = cudaFuncSetAttribute(big_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
-        return a;
-    }();
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
     if (attr != cudaSuccess) return attr;
+    // (the keys are dead once partitioned: K1's key array is the big buckets' scratch)
     local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, ctr, log2c, rects, brect, bmeta,
-                                                           big_list);
-    // (the coarse keys are dead once partitioned: K1's key array is the merge scratch)
-    big_bucket_kernel<<<148, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, key, tmp_idx, ctr, big_list, rects,
-                                                             brect, bmeta);
-    *launches += 5;
+                                                           key, tmp_idx);
+    *launches += 4;
     return cudaGetLastError();
 }
 
