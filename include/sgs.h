@@ -339,7 +339,10 @@ sgs_status sgs_group_broadcast_scene(sgs_group* group, const sgs_scene_desc* des
  * block; the root receives every frame: rgb + i*H*W*3 and T + i*H*W (T may be NULL)
  * in out_memory (device buffers on the root's device, or host). Other ranks ignore
  * rgb and the value of T, but T's null-ness must match the root's (it says whether
- * transmittance frames travel). stats (optional) accumulates the rank's own views. */
+ * transmittance frames travel). stats (optional) accumulates the rank's own views.
+ * The views must share one image size (SGS_ERR_INVALID_ARGUMENT otherwise). Like any
+ * collective, an error on one rank leaves the others waiting in NCCL: callers abort
+ * the group (sgs_group_destroy on every rank) after a failure. */
 sgs_status sgs_group_render_views(sgs_group* group, const sgs_scene* scene, const sgs_camera* cams, int32_t n,
                                   const sgs_render_config* cfg, int32_t root, float* rgb, float* T,
                                   int32_t out_memory, sgs_render_stats* stats);

@@ -288,6 +288,9 @@ sgs_status sgs_group_render_views(sgs_group* g, const sgs_scene* scene, const sg
     if (n == 0) return SGS_OK;
     SGS_GCUDA(cudaSetDevice(g->device));
     const int W = cams[0].width, H = cams[0].height;
+    for (int v = 1; v < n; ++v)  // (frames are gathered at one stride)
+        if (cams[v].width != W || cams[v].height != H)
+            return sgs::fail_status(SGS_ERR_INVALID_ARGUMENT, "group views must share one image size");
     const size_t npx = static_cast<size_t>(W) * static_cast<size_t>(H);
     const bool want_T = T != nullptr;
     const size_t fr_rgb = npx * 3 * sizeof(float), fr_T = want_T ? npx * sizeof(float) : 0;

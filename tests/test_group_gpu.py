@@ -83,3 +83,14 @@ def test_group_errors():
     r = sg.Renderer(0)
     with pytest.raises(sg.InvalidArgumentError):
         RenderGroup.init_rank(r, 2, 2, bytes(128))
+    # views of different sizes cannot share the gather stride
+    scene, cams = _scene_cams()
+    (g,) = RenderGroup.create([0])
+    try:
+        ds = g.broadcast_scene(scene, root=0)
+        mixed = cams[:2] + sg.orbit_cameras(1, 160, 90, 4.0, 108.0)
+        with pytest.raises(sg.InvalidArgumentError):
+            g.render_views(ds, mixed, root=0, degree_override=1)
+        ds.free()
+    finally:
+        g.close()
