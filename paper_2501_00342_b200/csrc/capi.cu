@@ -55,7 +55,7 @@ struct DevBuf {
         if (ptr) cudaFree(ptr);
         ptr = nullptr;
         bytes = 0;
-        size_t grow = need + need / 4 + 256;
+        size_t grow = need + need / 16 + 256;  // (a little slack for sizes that creep up)
         cudaError_t e = cudaMalloc(&ptr, grow);
         if (e == cudaSuccess) bytes = grow;
         return e;
@@ -702,6 +702,38 @@ int check_frame(Lane& L) {
         }
     }
     return SGS_OK;
+}
+
+uint64_t lane_bytes(const Lane& L) {
+    uint64_t b = 0;
+    for (const DevBuf* d : {&L.keys_a, &L.keys_b, &L.buckets, &L.order, &L.rec, &L.colour, &L.rects, &L.brect,
+                            &L.bmeta, &L.bin_status, &L.work, &L.tk_a, &L.tv_a, &L.tk_b, &L.tv_b, &L.sort_hist,
+                            &L.ranges, &L.tile_done, &L.pix_state, &L.pix_walked, &L.tile_emax})
+        b += d->bytes;
+    return b;
+}
+
+// How many of the first `lanes` lanes can hold a frame's arenas -- about 170 B per
+// Gaussian (K1's keys, records, rectangles and colours, K2's partition and ranks, the
+// binning inputs, 2N tile pairs) and 32 B per pixel -- in the free HBM, less a tenth
+// kept for the caller (at least one lane; sizes only ever grow, so lanes holding
+// arenas count what they already have). A 60M-Gaussian scene takes ~10 GB per lane.
+int lanes_that_fit(const sgs_context* ctx, uint64_t n, uint64_t npx, int lanes) {
+    const uint64_t per_lane = n * 170 + npx * 32 + (uint64_t{64} << 20);
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return lanes;
+    }
+    uint64_t budget = free_b - free_b / 10;
+    int k = 0;
+    for (; k < lanes; ++k) {
+        const uint64_t held = lane_bytes(ctx->lane[k]);
+        const uint64_t need = per_lane > held ? per_lane - held : 0;
+        if (k > 0 && need > budget) break;
+        budget -= std::min(budget, need);
+    }
+    return std::max(k, 1);
 }
 
 // Settle lane L's frame: check it, re-enqueue on a retry verdict, until it is done.
@@ -1544,8 +1576,10 @@ sgs_status sgs_render_batch(sgs_context* ctx, const sgs_scene* scene, const sgs_
     };
     sgs_status st = select_lane_streams(ctx, host && n > 1);
     if (st != SGS_OK) return st;
-    // per-stage timing reads events mid-frame: one lane keeps the stages unmixed
-    const int lanes = std::min<int>(timing ? 1 : (host ? ctx->host_lanes : ctx->lanes), n);
+    // per-stage timing reads events mid-frame: one lane keeps the stages unmixed; very
+    // large scenes get as many lanes as their arenas fit in HBM
+    const int lanes = lanes_that_fit(ctx, scene->meta.count, npx,
+                                     std::min<int>(timing ? 1 : (host ? ctx->host_lanes : ctx->lanes), n));
     st = fork_lanes(ctx, lanes);
     if (st != SGS_OK) return st;
     // view i runs on lane i % lanes; a lane's previous view is settled (checked,
