@@ -209,6 +209,7 @@ struct sgs_context {
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     DevBuf bwd;      // backward scratch (FP64 splats, ranks, per-entry partials, staging)
+    uint64_t hbm_bytes = 0;  // the device's memory
     uint64_t own_launches = 0, lib_launches = 0;
 };
 
@@ -720,6 +721,8 @@ uint64_t lane_bytes(const Lane& L) {
 // arenas count what they already have). A 60M-Gaussian scene takes ~10 GB per lane.
 int lanes_that_fit(const sgs_context* ctx, uint64_t n, uint64_t npx, int lanes) {
     const uint64_t per_lane = n * 170 + npx * 32 + (uint64_t{64} << 20);
+    // (the free-memory query costs time: only large scenes ask)
+    if (lanes <= 1 || per_lane * static_cast<uint64_t>(lanes) <= ctx->hbm_bytes / 4) return lanes;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
         cudaGetLastError();
@@ -1187,6 +1190,11 @@ sgs_status sgs_create(int device, sgs_context** out) {
     SGS_CUDA(cudaSetDevice(device));
     auto* ctx = new sgs_context();
     ctx->device = device;
+    {
+        cudaDeviceProp prop{};
+        SGS_CUDA(cudaGetDeviceProperties(&prop, device));
+        ctx->hbm_bytes = prop.totalGlobalMem;
+    }
     SGS_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     SGS_CUDA(cudaMallocHost(&ctx->h_ctr_init, sizeof(Counters)));
