@@ -183,8 +183,9 @@ sgs_status sgs_scene_update(sgs_context* ctx, sgs_scene* scene, const sgs_scene_
  * into a pinned staging block the library owns, which is copied while the caller fills
  * the next one. desc->dtype must be SGS_F32; desc->params is not read. A nonzero
  * return from fill ends the call with SGS_ERR_INVALID_ARGUMENT before the scene is
- * touched (it keeps its previous contents). The C++ drop-in's render() feeds it from
- * the caller's Scene. */
+ * touched (it keeps its previous contents). fill runs on the calling thread while the
+ * context is locked: it must not call into the library with this context. The C++
+ * drop-in's render() feeds it from the caller's Scene. */
 typedef int32_t (*sgs_row_fill_fn)(void* user, float* rows, uint64_t first, uint64_t count);
 sgs_status sgs_scene_update_rows(sgs_context* ctx, sgs_scene* scene, const sgs_scene_desc* desc,
                                  sgs_row_fill_fn fill, void* user);
