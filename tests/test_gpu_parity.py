@@ -684,6 +684,31 @@ def test_full_size_vs_reference(renderer, ref, cfgname):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("ts", [8, 13, 32])
+def test_config_b_other_tile_sizes_vs_reference(renderer, ref, ts):
+    """Config B (1M Gaussians, 1080p, depth-chunked) on tiles of one compositor part
+    (8), three parts with a partial one (13) and sixteen parts in four pixel chunks (32,
+    unchunked): bit-exact order and lists, images within tolerance on the render path."""
+    scene, cam, override = _full_config("B")
+    f = _flat(scene)
+    ocam = OrcCamera.from_buffer_copy(bytes(cam._c()))
+    cfg = make_config(tile_size=ts, degree_override=override)
+    ds = renderer.upload(scene)
+    try:
+        got = renderer.tile_grid(ds, cam, tile_size=ts, degree_override=override)
+        want = ref.tile_grid(f, ocam, cfg)
+        assert np.array_equal(got[0], want[0]), "depth order"
+        assert np.array_equal(got[1], want[1]), "tile ranges"
+        assert np.array_equal(got[2], want[2]), "tile lists"
+        ref_rgb, ref_T = ref.render(f, ocam, cfg)
+        for _ in range(3):  # direct, captured, replayed
+            rgb, T = renderer.render(ds, cam, tile_size=ts, degree_override=override)
+            check_image(rgb, T, ref_rgb, ref_T)
+    finally:
+        ds.free()
+
+
+@pytest.mark.slow
 def test_large_scene_vs_reference(renderer, ref):
     """A scene past 8M Gaussians: K2's coarse level at its largest (32768 buckets,
     128 KB of shared counters per CTA -- the sizes that once failed to launch above
