@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) radix_downsweep_kernel(
             dg[j] = w0 + j * 32 < e ? (ck[j] >> shift) & mask : 256u;
         }
         if (t0 + kStep < e) load(t0 + kStep);  // the next step's keys, in flight during this one
-        // rank: equal digits within a warp by match.any, in (round, lane) order
+        // rank: equal digits within a warp by ballots, in (round, lane) order
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             // lanes holding the same digit (the past-the-end sentinel 256 included): one
