@@ -541,12 +541,12 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
             const int log2c = depth_coarse_log2(n);
             const size_t half = align_up(depth_two_level_scratch(log2c), 256);
             SGS_CUDA(L.buckets.ensure(2 * half));  // histogram, offsets
-            SGS_CUDA(L.keys_b.ensure(n1 * 8));
+            SGS_CUDA(L.keys_b.ensure(n1 * 16));  // K2's (key, index) partition
             SGS_CUDA(launch_depth_two_level(n, L.keys_a.as<unsigned long long>(), L.d_ctr, log2c,
                                             L.buckets.as<uint32_t>(), L.buckets.as<uint32_t>() + half / 4,
-                                            L.keys_b.as<unsigned long long>(), L.order.as<uint32_t>(),
-                                            L.tk_a.as<uint32_t>(), L.rects.as<int4>(), L.brect.as<int4>(),
-                                            L.bmeta.as<uint2>(), s, &ctx->own_launches));
+                                            L.keys_b.ptr, L.order.as<uint32_t>(), L.tk_a.as<uint32_t>(),
+                                            L.rects.as<int4>(), L.brect.as<int4>(), L.bmeta.as<uint2>(), s,
+                                            &ctx->own_launches));
         }
         if (timing) SGS_CUDA(cudaEventRecord(L.ev[2], s));
 

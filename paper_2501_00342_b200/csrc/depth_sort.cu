@@ -39,6 +39,15 @@ constexpr int kL2Cap = 4096;
 constexpr int kL2Per = kL2Cap / kL2Threads;
 constexpr int kL2MaxFineLog2 = 11;
 
+// A visible splat in K2's partition: its key and index side by side (one 16-B store
+// per scattered element instead of two partial-sector ones).
+__device__ __forceinline__ void put_part(uint4* part, uint32_t pos, unsigned long long k, uint32_t i) {
+    part[pos] = make_uint4(static_cast<uint32_t>(k), static_cast<uint32_t>(k >> 32), i, 0u);
+}
+__device__ __forceinline__ unsigned long long part_key(const uint4 v) {
+    return static_cast<unsigned long long>(v.x) | (static_cast<unsigned long long>(v.y) << 32);
+}
+
 __device__ __forceinline__ unsigned long long shr64(unsigned long long v, int s) { return s < 64 ? v >> s : 0ULL; }
 
 __device__ __forceinline__ uint32_t coarse_of(unsigned long long k, unsigned long long kmin, int shift, uint32_t C) {
@@ -70,11 +79,11 @@ __global__ void __launch_bounds__(kL1Threads) coarse_hist_kernel(uint64_t n, con
 }
 
 // cur = exclusive offsets of the coarse buckets, advanced to their ends. Visible
-// keys go to (part_key, part_idx); culled ones straight to their final ranks
+// keys go to the partition as (key, index) pairs; culled ones straight to their final ranks
 // [V, N) with (index, 0 tiles) metadata.
 __global__ void __launch_bounds__(kL1Threads) coarse_scatter_kernel(
     uint64_t n, const unsigned long long* __restrict__ key, const Counters* __restrict__ ctr, int log2c,
-    uint32_t* __restrict__ cur, unsigned long long* __restrict__ part_key, uint32_t* __restrict__ part_idx,
+    uint32_t* __restrict__ cur, uint4* __restrict__ part, uint32_t* __restrict__ order,
     uint2* __restrict__ bmeta) {
     extern __shared__ uint32_t cnt[];  // per-bucket counts, then this CTA's first slot per bucket
     const uint32_t C = 1u << log2c;
@@ -104,11 +113,12 @@ __global__ void __launch_bounds__(kL1Threads) coarse_scatter_kernel(
         const uint64_t i = base + j * kL1Threads;
         if (i >= n) continue;
         const uint32_t pos = cnt[bk[j]] + lo[j];
-        part_idx[pos] = static_cast<uint32_t>(i);
-        if (bk[j] == C)
+        if (bk[j] == C) {
+            order[pos] = static_cast<uint32_t>(i);
             bmeta[pos] = make_uint2(static_cast<uint32_t>(i), 0u);
-        else
-            part_key[pos] = k[j];
+        } else {
+            put_part(part, pos, k[j], static_cast<uint32_t>(i));
+        }
     }
 }
 
@@ -209,19 +219,22 @@ __device__ __forceinline__ uint32_t count_less(const unsigned long long* key, co
     return a - lo;
 }
 
-__device__ __noinline__ void sort_big_bucket(uint32_t s, uint32_t m, unsigned long long* part_key, uint32_t* order,
+__device__ __noinline__ void sort_big_bucket(uint32_t s, uint32_t m, uint4* part, uint32_t* order,
                                              unsigned long long* tmp_key, uint32_t* tmp_idx,
                                              unsigned long long* sKey, uint32_t* sIdx, const int4* rects,
                                              int4* brect, uint2* bmeta) {
-    unsigned long long* srcK = part_key + s;
-    uint32_t* srcI = order + s;
+    // the runs ping-pong between tmp and the bucket's own 16m-byte stretch of the
+    // partition (8m bytes of keys, then 4m of indices) once it has been read
+    unsigned long long* srcK = reinterpret_cast<unsigned long long*>(part + s);
+    uint32_t* srcI = reinterpret_cast<uint32_t*>(srcK + m);
     unsigned long long* dstK = tmp_key + s;
     uint32_t* dstI = tmp_idx + s;
     for (uint32_t r0 = 0; r0 < m; r0 += kL2Cap) {
         const uint32_t rm = min(static_cast<uint32_t>(kL2Cap), m - r0);
         for (uint32_t e = threadIdx.x; e < rm; e += kL2Threads) {
-            sKey[e] = srcK[r0 + e];
-            sIdx[e] = srcI[r0 + e];
+            const uint4 v = part[s + r0 + e];
+            sKey[e] = part_key(v);
+            sIdx[e] = v.z;
         }
         __syncthreads();
         cta_bitonic_sort(sKey, sIdx, rm);
@@ -253,7 +266,7 @@ __device__ __noinline__ void sort_big_bucket(uint32_t s, uint32_t m, unsigned lo
 }
 
 __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
-    const uint32_t* __restrict__ cend, unsigned long long* __restrict__ part_key, uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ cend, uint4* __restrict__ part, uint32_t* __restrict__ order,
     Counters* __restrict__ ctr, int log2c, const int4* __restrict__ rects,
     int4* __restrict__ brect, uint2* __restrict__ bmeta, unsigned long long* __restrict__ tmp_key,
     uint32_t* __restrict__ tmp_idx) {
@@ -270,7 +283,7 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
     if (m == 0) return;
     const int tid = threadIdx.x;
     if (m > kL2Cap) {  // more keys than shared memory holds
-        sort_big_bucket(s, m, part_key, order, tmp_key, tmp_idx, sKey, sIdx, rects, brect, bmeta);
+        sort_big_bucket(s, m, part, order, tmp_key, tmp_idx, sKey, sIdx, rects, brect, bmeta);
         return;
     }
     const unsigned long long kmin = ctr->kmin;
@@ -287,8 +300,9 @@ __global__ void __launch_bounds__(kL2Threads) local_sort_kernel(
 #pragma unroll
     for (int j = 0; j < kL2Per; ++j) {
         const uint32_t e = tid + j * kL2Threads;
-        k[j] = e < m ? part_key[s + e] : 0ULL;
-        ix[j] = e < m ? order[s + e] : 0u;
+        const uint4 v = e < m ? part[s + e] : make_uint4(0u, 0u, 0u, 0u);
+        k[j] = part_key(v);
+        ix[j] = v.z;
     }
     __syncthreads();
 #pragma unroll
@@ -437,7 +451,7 @@ int depth_coarse_log2(uint64_t n) {
 size_t depth_two_level_scratch(int log2c) { return static_cast<size_t>((1u << log2c) + 1) * 4; }  // (per region)
 
 cudaError_t launch_depth_two_level(uint64_t n, unsigned long long* key, Counters* ctr, int log2c,
-                                   uint32_t* ghist, uint32_t* cur, unsigned long long* part_key, uint32_t* order,
+                                   uint32_t* ghist, uint32_t* cur, void* part_buf, uint32_t* order,
                                    uint32_t* tmp_idx, const int4* rects, int4* brect, uint2* bmeta,
                                    cudaStream_t stream, uint64_t* launches) {
     if (n == 0) return cudaSuccess;
@@ -458,13 +472,14 @@ cudaError_t launch_depth_two_level(uint64_t n, unsigned long long* key, Counters
     if (e != cudaSuccess) return e;
     coarse_hist_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, ghist);
     bucket_scan_kernel<<<1, kScanThreads, 0, stream>>>(ghist, cur, C + 1);
-    coarse_scatter_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, cur, part_key, order, bmeta);
+    uint4* part = static_cast<uint4*>(part_buf);
+    coarse_scatter_kernel<<<G, kL1Threads, (C + 1) * 4, stream>>>(n, key, ctr, log2c, cur, part, order, bmeta);
     constexpr int kL2Smem = kL2Cap * 12;
     static const cudaError_t attr =
         cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL2Smem);
     if (attr != cudaSuccess) return attr;
     // (the keys are dead once partitioned: K1's key array is the big buckets' scratch)
-    local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part_key, order, ctr, log2c, rects, brect, bmeta,
+    local_sort_kernel<<<C, kL2Threads, kL2Smem, stream>>>(cur, part, order, ctr, log2c, rects, brect, bmeta,
                                                            key, tmp_idx);
     *launches += 4;
     return cudaGetLastError();

@@ -189,12 +189,12 @@ cudaError_t launch_radix_pass(const uint32_t* kin, const uint32_t* vin, uint32_t
 // K2 (depth_sort.cu): the depth order of n splats -- order[r], and the rank-ordered
 // binning inputs brect[r] / bmeta[r] = (index, tiles of its rectangle) -- by a
 // two-level bucket sort. Scratch: ghist / cur depth_two_level_scratch bytes each,
-// part_key n u64, tmp_idx n u32; key (K1's, dead once partitioned) doubles as the
+// part 16 n bytes, tmp_idx n u32; key (K1's, dead once partitioned) doubles as the
 // big buckets' merge scratch.
 int depth_coarse_log2(uint64_t n);
 size_t depth_two_level_scratch(int log2c);
 cudaError_t launch_depth_two_level(uint64_t n, unsigned long long* key, Counters* ctr, int log2c,
-                                   uint32_t* ghist, uint32_t* cur, unsigned long long* part_key, uint32_t* order,
+                                   uint32_t* ghist, uint32_t* cur, void* part, uint32_t* order,
                                    uint32_t* tmp_idx, const int4* rects, int4* brect, uint2* bmeta,
                                    cudaStream_t stream, uint64_t* launches);
 // K3 + K4 (binning.cu): for the ranks [rb, re) of a depth chunk, count each rank's
