@@ -502,6 +502,8 @@ __global__ void __launch_bounds__(kK1Threads, MINB) preprocess_kernel(
     }
 }
 
+constexpr int kMaxStageSlots = 10;
+
 K1Stage make_stage(const ScenePlanes& sp, const CfgParams& cfg) {
     K1Stage st{};
     st.geo_slots = sp.geometry_f64 ? 2 : 1;
@@ -524,6 +526,15 @@ K1Stage make_stage(const ScenePlanes& sp, const CfgParams& cfg) {
         default: st.lobe_pre = 4; break;
     }
     st.slots = st.geo_slots + 3 + st.sh_pre + st.lobe_pre;
+    // At most kMaxStageSlots slots are staged; the SH planes beyond are read at use. A
+    // degree-3 SH scene would otherwise stage 16 (128 KB per CTA, one CTA per SM): config
+    // D's K1 0.265 -> 0.212 ms and batch 0.684 -> 0.629 ms/frame with 10 (13: 0.224 /
+    // 0.644; 8 also trims config C's stage: 0.605 against 0.586).
+    if (st.slots > kMaxStageSlots) {
+        const int cut = std::min(st.sh_pre, st.slots - kMaxStageSlots);
+        st.sh_pre -= cut;
+        st.slots -= cut;
+    }
     return st;
 }
 
