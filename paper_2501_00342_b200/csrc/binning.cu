@@ -26,6 +26,7 @@ namespace {
 // kMaxBitmapTiles; larger grids read the global bitmap).
 constexpr int kMaxBitmapTiles = 1 << 18;
 constexpr int kBinThreads = 1024;
+static_assert(kBinThreads == 1024, "the CTA scans and sums reduce over exactly 32 warps");
 // Splats covering more than kCoop tiles are emitted cooperatively by the whole warp
 // (ballot-compacted over the live tiles) so one large splat does not serialise a
 // lane while 31 idle.
