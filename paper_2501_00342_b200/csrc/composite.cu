@@ -533,26 +533,49 @@ __global__ void build_work_kernel(const uint2* __restrict__ ranges, const TileFl
                                   uint32_t* __restrict__ wctl) {
     const uint32_t nsub = static_cast<uint32_t>(kSubsPerChunk * nchunks);
     const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= ntile * nsub) return;
-    const uint32_t tile = it / nsub, sub = it - tile * nsub;
-    if (static_cast<int>(sub) * kSubPx >= tile_px) return;  // a part without pixels
-    // (a later depth chunk: at most 4 parts per tile)
-    if (!first && ((flags.done[tile >> 5] >> (tile & 31)) & 1u)) return;
-    if (!first && part_bit(flags.sub_done, tile, sub)) return;  // final already
-    const uint2 r = ranges[tile];
-    const uint32_t len = r.y - r.x;
-    if (!last && len == 0) return;
-    // A part that is neither final nor touched was never composited: then no part of
-    // the tile was (all parts of a tile are queued in the same chunks, and each ends
-    // final or touched), and without entries the tile is background.
-    if (len == 0 && (first || !part_bit(flags.touched, tile, sub))) {
-        // never received an entry: background pixels, written by the tail loop (one
-        // item per 256-pixel chunk)
-        if (sub % kSubsPerChunk == 0) wctl[kWorkCtl + atomicAdd(&wctl[7], 1u)] = tile * nchunks + sub / kSubsPerChunk;
-        return;
+    // the list this item joins: a length class, kWorkClasses for the background list,
+    // or none (-1); every lane reaches the warp-aggregated append below
+    int dest = -1;
+    uint32_t value = 0;
+    if (it < ntile * nsub) {
+        const uint32_t tile = it / nsub, sub = it - tile * nsub;
+        bool skip = static_cast<int>(sub) * kSubPx >= tile_px;  // a part without pixels
+        // (a later depth chunk: at most 4 parts per tile)
+        skip = skip || (!first && ((flags.done[tile >> 5] >> (tile & 31)) & 1u));
+        skip = skip || (!first && part_bit(flags.sub_done, tile, sub));  // final already
+        if (!skip) {
+            const uint2 r = ranges[tile];
+            const uint32_t len = r.y - r.x;
+            if (last || len != 0) {
+                // A part that is neither final nor touched was never composited: then no
+                // part of the tile was (all parts of a tile are queued in the same chunks,
+                // and each ends final or touched), and without entries the tile is
+                // background, written by the tail loop (one item per 256-pixel chunk).
+                if (len == 0 && (first || !part_bit(flags.touched, tile, sub))) {
+                    if (sub % kSubsPerChunk == 0) {
+                        dest = kWorkClasses;
+                        value = tile * nchunks + sub / kSubsPerChunk;
+                    }
+                } else {
+                    dest = work_class(len);
+                    value = it;
+                }
+            }
+        }
     }
-    const int c = work_class(len);
-    work[static_cast<size_t>(c) * cap + atomicAdd(&wctl[c], 1u)] = it;
+    // one atomic per (warp, list): lanes bound for the same list take consecutive slots
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(0xffffffffu, dest);
+    if (dest < 0) return;
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (static_cast<int>(lane) == leader)
+        base = atomicAdd(dest == kWorkClasses ? &wctl[7] : &wctl[dest], static_cast<uint32_t>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader) + __popc(peers & ((1u << lane) - 1u));
+    if (dest == kWorkClasses)
+        wctl[kWorkCtl + base] = value;
+    else
+        work[static_cast<size_t>(dest) * cap + base] = value;
 }
 
 // Stats frames: E_t = the sum of the per-(tile, chunk) deepest entries.
