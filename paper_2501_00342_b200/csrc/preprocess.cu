@@ -85,11 +85,11 @@ __device__ __forceinline__ void stage_item(const ScenePlanes& sp, const K1Stage&
     float4* b = buf + st.geo_slots * kK1Threads;
 #pragma unroll
     for (int k = 0; k < 3; ++k) cp_async16(&b[k * kK1Threads + tid], &sp.cov[k][i]);
-    b += 3 * kK1Threads;
-    for (int p = 0; p < st.sh_pre; ++p) cp_async16(&b[p * kK1Threads + tid], &sp.color[static_cast<uint64_t>(p) * sp.n + i]);
-    b += st.sh_pre * kK1Threads;
-    for (int p = 0; p < st.lobe_pre; ++p)
-        cp_async16(&b[p * kK1Threads + tid], &sp.color[static_cast<uint64_t>(st.lobe_base + p) * sp.n + i]);
+    b += 3 * kK1Threads + tid;
+    const float4* src = sp.color + i;  // plane p of Gaussian i: src + p n
+    for (int p = 0; p < st.sh_pre; ++p, b += kK1Threads, src += sp.n) cp_async16(b, src);
+    src = sp.color + static_cast<uint64_t>(st.lobe_base) * sp.n + i;
+    for (int p = 0; p < st.lobe_pre; ++p, b += kK1Threads, src += sp.n) cp_async16(b, src);
 }
 
 template <bool F64>
