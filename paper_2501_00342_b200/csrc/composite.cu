@@ -161,7 +161,7 @@ constexpr int kSubsPerChunk = kChunkPx / kSubPx;
 struct WarpStage {
     float4 raw[2][kWB + 1][4];
     float4 box[kWB];
-    uint16_t idx[kWB + 8];
+    uint32_t idx[kWB + 8];
 };
 static_assert(sizeof(WarpStage) % 16 == 0, "warp stage alignment");
 
@@ -363,13 +363,13 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
                     hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit) S.idx[cnt + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
+                if (hit) S.idx[cnt + __popc(m & ((1u << lane) - 1u))] = j;
                 cnt += __popc(m);
             }
         }
         if (lane < kGroup) S.idx[cnt + lane] = kWB;
         __syncwarp();
-        const uint16_t* idx = S.idx;
+        const uint32_t* idx = S.idx;
         // Fast groups until one holds a pair inside the guard band; that group is
         // walked by the cold path below (outside the fast loop, so the FP64 call does
         // not weigh on the fast loop's registers), then the fast loop resumes.
