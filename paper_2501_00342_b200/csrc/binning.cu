@@ -105,9 +105,12 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(
     extern __shared__ uint32_t bitmap[];
     __shared__ unsigned long long s_warp[kBinThreads / 32];
     __shared__ unsigned long long s_base;
+    const uint32_t blk = blockIdx.x;
+    // a CTA without pairs has nothing to emit (in late chunks most ranks only cover
+    // finished tiles); the last one still records the chunk's P
+    if (csum[blk] == 0 && blk != gridDim.x - 1) return;
     const DoneView done = done_view(done_bits, ntile, bitmap);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t blk = blockIdx.x;
     // sum of the CTA totals before this one
     unsigned long long before = 0;
     for (uint32_t p = threadIdx.x; p < blk; p += kBinThreads) before += csum[p];
