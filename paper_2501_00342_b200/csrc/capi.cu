@@ -619,7 +619,7 @@ sgs_status enqueue_frame(sgs_context* ctx, Lane& L) {
             }
             // K7
             if (mode == kRender) {
-                SGS_CUDA(launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, 1, L.rec.as<SplatRec>(),
+                SGS_CUDA(launch_composite(L.d_consts, cp, kp, L.ranges.as<uint2>(), list, L.rec.as<SplatRec>(),
                                           L.colour.as<float4>(), bg, L.pix_state.as<PixelState>(),
                                           L.pix_walked.as<uint32_t>(), L.tile_done.as<uint32_t>(), c == 0,
                                           c == nchunks - 1, L.d_ctr, count_stats, L.tile_emax.as<uint32_t>(),

@@ -215,7 +215,7 @@ __device__ __forceinline__ bool part_bit(const uint32_t* bits, uint32_t tile, ui
 template <int kGroup, int MINB, bool kSameRow>
 __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
-    const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys, const int kstride,
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ keys,
     const SplatRec* __restrict__ rec, const float4* __restrict__ colour, float3 bg,
     PixelState* __restrict__ state, uint32_t* __restrict__ processed_io, const TileFlags flags, int first, int last,
     Counters* __restrict__ ctr, int want_stats, uint32_t* __restrict__ tile_emax, const uint32_t* __restrict__ work,
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const uint32_t k = start + lane + h * 32;
-        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
+        g_next[h] = k < end ? __ldg(&keys[k]) : 0u;
         if (k < end) stage_record(rec, colour, g_next[h], S.raw[0][lane + h * 32]);
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     for (int h = 0; h < 2; ++h) {
         g_cur[h] = g_next[h];
         const uint32_t k = start + kWB + lane + h * 32;
-        g_next[h] = k < end ? __ldg(&keys[static_cast<size_t>(k) * kstride]) : 0u;
+        g_next[h] = k < end ? __ldg(&keys[k]) : 0u;
     }
     int buf = 0;
 
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
             const uint32_t kn = base + kWB + rt;
             if (kn < end) stage_record(rec, colour, g_next[h], S.raw[buf ^ 1][rt]);
             g_cur[h] = g_next[h];
-            g_next[h] = kn + kWB < end ? __ldg(&keys[static_cast<size_t>(kn + kWB) * kstride]) : 0u;
+            g_next[h] = kn + kWB < end ? __ldg(&keys[kn + kWB]) : 0u;
         }
         asm volatile("cp.async.commit_group;\n" ::);
         buf ^= 1;
@@ -599,7 +599,7 @@ int composite_work_items(int ts) { return kSubsPerChunk * composite_pixel_chunks
 namespace {
 template <int G, int M, bool ROW>
 cudaError_t launch_k7(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg, int nchunks,
-                      const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
+                      const uint2* ranges, const uint32_t* keys, const SplatRec* rec,
                       const float4* colour, float3 bg, PixelState* state, uint32_t* processed, const TileFlags& flags,
                       bool first, bool last, Counters* counters, bool want_stats, uint32_t* emax, uint32_t* work,
                       uint32_t* wctl, uint32_t cap, cudaStream_t stream) {
@@ -610,14 +610,14 @@ cudaError_t launch_k7(const FrameConsts* fc, const CamParams& cam, const CfgPara
     if (attr != cudaSuccess) return attr;
     // persistent grid: M resident CTAs of four warps per SM
     composite_kernel<G, M, ROW><<<148u * M, kThreads, smem, stream>>>(
-        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed, flags,
+        fc, cam.W, cam.H, cfg, nchunks, ranges, keys, rec, colour, bg, state, processed, flags,
         first ? 1 : 0, last ? 1 : 0, counters, want_stats ? 1 : 0, emax, work, wctl, wctl + 6, cap);
     return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
-                             const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
+                             const uint2* ranges, const uint32_t* keys, const SplatRec* rec,
                              const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
                              uint32_t* tile_flags, bool first, bool last, Counters* counters, bool want_stats,
                              uint32_t* tile_emax, uint32_t* work, uint32_t* wctl, cudaStream_t stream) {
@@ -636,10 +636,10 @@ cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const 
     build_work_kernel<<<(cap + 255) / 256, 256, 0, stream>>>(ranges, flags, first ? 1 : 0, last ? 1 : 0, ntile,
                                                              nchunks, cfg.tile_size * cfg.tile_size, cap, work, wctl);
     if (cfg.tile_size == 16)
-        e = launch_k7<4, 4, true>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,
+        e = launch_k7<4, 4, true>(fc, cam, cfg, nchunks, ranges, keys, rec, colour, bg, state, processed,
                                   flags, first, last, counters, want_stats, tile_emax, work, wctl, cap, stream);
     else
-        e = launch_k7<4, 4, false>(fc, cam, cfg, nchunks, ranges, keys, kstride, rec, colour, bg, state, processed,
+        e = launch_k7<4, 4, false>(fc, cam, cfg, nchunks, ranges, keys, rec, colour, bg, state, processed,
                                    flags, first, last, counters, want_stats, tile_emax, work, wctl, cap, stream);
     if (e != cudaSuccess) return e;
     if (want_stats && last)

@@ -235,7 +235,7 @@ void launch_tile_ranges(const unsigned long long* d_count, const uint32_t* tiles
 // state init / final output; tile_done and state may be null when the frame is a
 // single chunk.
 cudaError_t launch_composite(const FrameConsts* fc, const CamParams& cam, const CfgParams& cfg,
-                             const uint2* ranges, const uint32_t* keys, int kstride, const SplatRec* rec,
+                             const uint2* ranges, const uint32_t* keys, const SplatRec* rec,
                              const float4* colour, float3 bg, PixelState* state, uint32_t* processed,
                              uint32_t* tile_flags, bool first, bool last, Counters* counters, bool want_stats,
                              uint32_t* tile_emax, uint32_t* work, uint32_t* wctl, cudaStream_t stream);
