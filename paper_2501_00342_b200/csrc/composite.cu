@@ -212,6 +212,34 @@ __device__ __forceinline__ bool part_bit(const uint32_t* bits, uint32_t tile, ui
     return (bits[b >> 5] >> (b & 31)) & 1u;
 }
 
+// True only when no point of the box [x0, x1] x [y0, y1] (tile-local pixel centres)
+// can reach the record: the minimum over the box of its FP32 quadratic form
+// m2(d) = ca dx^2 + 2cb dx dy + cc dy^2 (d = point - mean) exceeds cut + 3 guard (the
+// guard bounds the FP32 error of m2 near the cut: once for the walk's per-pixel m2,
+// once for this minimum, once to spare) and a relative 1e-4 -- so every live pixel of
+// the warp would take the record's skip branch (alpha 0, no exact re-decision) and the
+// walk may leave it out. The minimum of the convex form over a box not containing the
+// mean lies on an edge, at the edge's clamped 1-D vertex. A degenerate or non-finite
+// form never misses.
+__device__ __forceinline__ bool ellipse_misses_box(const float4 A, const float4 B, float x0, float x1, float y0,
+                                                   float y1) {
+    const float ca = A.z, cb2 = A.w, cc = B.x, thr = B.y + (B.y - B.z);  // cut + 3 guard
+    const float dx0 = x0 - A.x, dx1 = x1 - A.x, dy0 = y0 - A.y, dy1 = y1 - A.y;
+    if (dx0 <= 0.0f && dx1 >= 0.0f && dy0 <= 0.0f && dy1 >= 0.0f) return false;  // the mean is inside
+    if (!(ca > 0.0f && cc > 0.0f && thr < 1e30f)) return false;
+    const float hc = -0.5f * cb2 / cc, ha = -0.5f * cb2 / ca;
+    auto on_x = [&](float X) {  // the edge dx = X, its minimum over dy
+        const float y = fminf(fmaxf(hc * X, dy0), dy1);
+        return fmaf(fmaf(ca, X, cb2 * y), X, cc * y * y);
+    };
+    auto on_y = [&](float Y) {  // the edge dy = Y, its minimum over dx
+        const float x = fminf(fmaxf(ha * Y, dx0), dx1);
+        return fmaf(fmaf(cc, Y, cb2 * x), Y, ca * x * x);
+    };
+    const float qmin = fminf(fminf(on_x(dx0), on_x(dx1)), fminf(on_y(dy0), on_y(dy1)));
+    return qmin * 0.9999f - 1e-4f > thr;
+}
+
 template <int kGroup, int MINB, bool kSameRow>
 __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
     const FrameConsts* __restrict__ fc, const int W, const int H, const CfgParams cfg, int nchunks,
@@ -361,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, MINB) composite_kernel(
                 if (j < nb) {
                     const float4 F = S.box[j];
                     hit = F.x - F.z <= wx1 && F.x + F.z >= wx0 && F.y - F.w <= wy1 && F.y + F.w >= wy0;
+                    if (hit) hit = !ellipse_misses_box(R[j][0], R[j][1], wx0, wx1, wy0, wy1);
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
                 if (hit) S.idx[cnt + __popc(m & ((1u << lane) - 1u))] = j;
